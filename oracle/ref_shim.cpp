@@ -1,0 +1,325 @@
+// ref_shim.cpp -- extern "C" wrappers over the UNMODIFIED reference headers.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file against
+// /root/reference/proj/include (the reference sources where they lie; nothing
+// is copied) into oracle/_ref/libmobi_ref.so.  It is used (a) to pin the C
+// restatement in mobi_oracle.c bit-for-bit, (b) to mint the golden fixtures in
+// tests/golden/, and (c) as the timed CPU baseline (bench.py cpu_baseline /
+// --impl reference, kind "reference").  It is never linked into the product.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "mobi/bench/checkpoint.hpp"
+#include "mobi/bitplane.hpp"
+#include "mobi/common.hpp"
+#include "mobi/qcore.hpp"
+#include "mobi/router.hpp"
+#include "mobi/slicer.hpp"
+
+using namespace mobi;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+Matrix mat(const double* p, int64_t r, int64_t c) {
+    Matrix m(static_cast<std::size_t>(r), static_cast<std::size_t>(c));
+    if (r * c) std::memcpy(m.data(), p, sizeof(double) * static_cast<std::size_t>(r * c));
+    return m;
+}
+
+void put(const Matrix& m, double* out) {
+    if (m.size()) std::memcpy(out, m.data(), sizeof(double) * m.size());
+}
+
+qcore::QuantParams params(int64_t rows, int64_t cols, int64_t gs, int bits, const double* scale,
+                          const double* zero) {
+    qcore::QuantParams qp;
+    qp.rows = static_cast<std::size_t>(rows);
+    qp.cols = static_cast<std::size_t>(cols);
+    qp.group_size = static_cast<std::size_t>(gs);
+    qp.bits = bits;
+    std::size_t n = qp.num_groups();
+    qp.scale.assign(scale, scale + n);
+    qp.zero.assign(zero, zero + n);
+    return qp;
+}
+
+slicer::SliceStack stack_of(const uint8_t* codes, int32_t n_slices, const int32_t* slice_bits,
+                            int64_t out, int64_t in, int64_t gs, const double* scale,
+                            const double* zero) {
+    slicer::SliceStack st;
+    st.slice_bits.assign(slice_bits, slice_bits + n_slices);
+    st.base = params(out, in, gs, slice_bits[0], scale, zero);
+    const std::size_t n = static_cast<std::size_t>(out * in);
+    for (int32_t e = 0; e < n_slices; ++e) {
+        Codes c(static_cast<std::size_t>(out), static_cast<std::size_t>(in));
+        std::memcpy(c.vec().data(), codes + e * n, n);
+        st.slices.push_back(std::move(c));
+    }
+    st.clamp_mask = Codes(static_cast<std::size_t>(out), static_cast<std::size_t>(in), 0);
+    st.clamp_counts.assign(static_cast<std::size_t>(n_slices), 0);
+    return st;
+}
+
+router::RouterState router_of(int64_t d, int64_t h, int64_t nr, const double* w1, const double* b1,
+                              const double* w2, const double* b2) {
+    router::RouterState rs;
+    rs.w1 = mat(w1, d, h);
+    rs.b1.assign(b1, b1 + h);
+    rs.w2 = mat(w2, h, nr);
+    rs.b2.assign(b2, b2 + nr);
+    return rs;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// router.hpp:63
+int ref_score(const double* x, int64_t T, int64_t d, const double* w1, const double* b1, int64_t h,
+              const double* w2, const double* b2, int64_t nr, double* s) {
+    return guard([&] { put(router::score(mat(x, T, d), router_of(d, h, nr, w1, b1, w2, b2)), s); });
+}
+
+// router.hpp:93
+int ref_gate_hard(const double* s, int64_t T, int64_t nr, double delta, double* g) {
+    return guard([&] { put(router::gate_hard(mat(s, T, nr), delta), g); });
+}
+
+// router.hpp:105
+int ref_forward_elastic(const double* x, int64_t T, int64_t in, const uint8_t* codes,
+                        int32_t n_slices, const int32_t* slice_bits, const double* scale,
+                        const double* zero, int64_t out, int64_t gs, const double* gates, int hard,
+                        double* y) {
+    return guard([&] {
+        slicer::SliceStack st = stack_of(codes, n_slices, slice_bits, out, in, gs, scale, zero);
+        Matrix r = router::forward_elastic(mat(x, T, in), st, mat(gates, T, n_slices - 1),
+                                           hard ? router::GateMode::kHard : router::GateMode::kSoft);
+        put(r, y);
+    });
+}
+
+// router.hpp:167
+int ref_calibrate_threshold(const double* scores, int64_t n, double rho, double* delta) {
+    return guard([&] {
+        std::vector<double> v(scores, scores + n);
+        *delta = router::calibrate_threshold(std::move(v), rho);
+    });
+}
+
+// router.hpp:135
+int ref_avg_bits(const double* gates, int64_t T, int64_t nr, const int32_t* slice_bits,
+                 int32_t n_slices, double* result) {
+    return guard([&] {
+        *result = router::avg_bits(mat(gates, T, nr), std::vector<int>(slice_bits, slice_bits + n_slices));
+    });
+}
+
+// router.hpp:153
+int ref_ratio_from_target_bits(double target, const int32_t* slice_bits, int32_t n_slices,
+                               double* rho) {
+    return guard([&] {
+        *rho = router::ratio_from_target_bits(target, std::vector<int>(slice_bits, slice_bits + n_slices));
+    });
+}
+
+// router.hpp:47 RouterState::init with a fresh Rng(seed) (fixture generation)
+int ref_router_init(int64_t d, int64_t nr, int64_t hidden, uint64_t seed, double* w1, double* b1,
+                    double* w2, double* b2) {
+    return guard([&] {
+        Rng rng(seed);
+        router::RouterState rs = router::RouterState::init(static_cast<std::size_t>(d), static_cast<std::size_t>(nr), 1000, rng,
+                                                           static_cast<std::size_t>(hidden));
+        put(rs.w1, w1);
+        std::copy(rs.b1.begin(), rs.b1.end(), b1);
+        put(rs.w2, w2);
+        std::copy(rs.b2.begin(), rs.b2.end(), b2);
+    });
+}
+
+// qcore.hpp:122 params_from_clip (GroupStats::from_weights + ClipParams)
+int ref_params_from_clip(const double* w, int64_t rows, int64_t cols, int64_t gs,
+                         const double* gamma_lo, const double* gamma_hi, int bits, double* scale,
+                         double* zero) {
+    return guard([&] {
+        Matrix m = mat(w, rows, cols);
+        qcore::GroupStats gst = qcore::GroupStats::from_weights(m, static_cast<std::size_t>(gs));
+        qcore::ClipParams cp;
+        cp.gamma_lo.assign(gamma_lo, gamma_lo + gst.min.size());
+        cp.gamma_hi.assign(gamma_hi, gamma_hi + gst.min.size());
+        qcore::QuantParams qp = qcore::params_from_clip(m, gst, cp, bits, static_cast<std::size_t>(gs));
+        std::copy(qp.scale.begin(), qp.scale.end(), scale);
+        std::copy(qp.zero.begin(), qp.zero.end(), zero);
+    });
+}
+
+// slicer.hpp:69 decompose
+int ref_decompose(const double* w, int64_t rows, int64_t cols, int64_t gs, const double* scale,
+                  const double* zero, const int32_t* slice_bits, int32_t n_slices, uint8_t* codes,
+                  uint8_t* clamp_mask, int64_t* clamp_counts) {
+    return guard([&] {
+        qcore::QuantParams base = params(rows, cols, gs, slice_bits[0], scale, zero);
+        slicer::SliceStack st = slicer::decompose(mat(w, rows, cols), base,
+                                                  std::vector<int>(slice_bits, slice_bits + n_slices));
+        const std::size_t n = static_cast<std::size_t>(rows * cols);
+        for (int32_t e = 0; e < n_slices; ++e) std::memcpy(codes + e * n, st.slices[e].vec().data(), n);
+        if (clamp_mask) std::memcpy(clamp_mask, st.clamp_mask.vec().data(), n);
+        if (clamp_counts)
+            for (int32_t e = 0; e < n_slices; ++e) clamp_counts[e] = static_cast<int64_t>(st.clamp_counts[e]);
+    });
+}
+
+// slicer.hpp:135 reconstruct
+int ref_reconstruct(const uint8_t* codes, int64_t rows, int64_t cols, int64_t gs,
+                    const int32_t* slice_bits, int32_t n_slices, const double* scale,
+                    const double* zero, int32_t k, double* out) {
+    return guard([&] {
+        put(slicer::reconstruct(stack_of(codes, n_slices, slice_bits, rows, cols, gs, scale, zero),
+                                static_cast<std::size_t>(k)),
+            out);
+    });
+}
+
+// slicer.hpp:150 merge_codes
+int ref_merge_codes(const uint8_t* codes, int64_t rows, int64_t cols, const int32_t* slice_bits,
+                    int32_t n_slices, int32_t k, uint8_t* merged) {
+    return guard([&] {
+        std::vector<double> dummy(static_cast<std::size_t>(rows * ((cols + 127) / 128)), 1.0);
+        slicer::SliceStack st = stack_of(codes, n_slices, slice_bits, rows, cols, 128, dummy.data(), dummy.data());
+        Codes m = slicer::merge_codes(st, static_cast<std::size_t>(k));
+        std::memcpy(merged, m.vec().data(), m.size());
+    });
+}
+
+// bitplane.hpp:48 pack_bit_major; planes out[bits][rows*wpr]
+int ref_pack_bit_major(const uint8_t* codes, int64_t rows, int64_t cols, int bits, uint64_t* planes) {
+    return guard([&] {
+        Codes c(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols));
+        std::memcpy(c.vec().data(), codes, static_cast<std::size_t>(rows * cols));
+        bitplane::PackedPlanes pp = bitplane::pack_bit_major(c, bits);
+        std::size_t off = 0;
+        for (const auto& p : pp.planes) {
+            std::memcpy(planes + off, p.data(), p.size() * sizeof(uint64_t));
+            off += p.size();
+        }
+    });
+}
+
+// checkpoint.hpp:54 LayerRecord::stack() from merged bit planes -> slice codes [n_slices][rows*cols]
+int ref_layer_stack(const uint64_t* planes, int64_t rows, int64_t cols, int bits, int64_t wpr,
+                    const int32_t* slice_bits, int32_t n_slices, uint8_t* codes) {
+    return guard([&] {
+        bench::LayerRecord rec;
+        rec.rows = static_cast<std::size_t>(rows);
+        rec.cols = static_cast<std::size_t>(cols);
+        rec.group_size = 128;
+        rec.slice_bits.assign(slice_bits, slice_bits + n_slices);
+        rec.planes.out = rec.rows;
+        rec.planes.in = rec.cols;
+        rec.planes.bits = bits;
+        rec.planes.words_per_row = static_cast<std::size_t>(wpr);
+        const std::size_t np = static_cast<std::size_t>(rows * wpr);
+        for (int p = 0; p < bits; ++p) rec.planes.planes.emplace_back(planes + p * np, planes + (p + 1) * np);
+        slicer::SliceStack st = rec.stack();
+        const std::size_t n = static_cast<std::size_t>(rows * cols);
+        for (int32_t e = 0; e < n_slices; ++e) std::memcpy(codes + e * n, st.slices[e].vec().data(), n);
+    });
+}
+
+// bitplane.hpp:122 bitplane_matmul
+int ref_bitplane_matmul(const double* x, int64_t T, const uint64_t* planes, int64_t out, int64_t in,
+                        int bits, int64_t wpr, int64_t gs, const double* scale, const double* zero,
+                        const int32_t* active, int32_t n_active, double* y) {
+    return guard([&] {
+        bitplane::PackedPlanes pp;
+        pp.out = static_cast<std::size_t>(out);
+        pp.in = static_cast<std::size_t>(in);
+        pp.bits = bits;
+        pp.words_per_row = static_cast<std::size_t>(wpr);
+        const std::size_t np = static_cast<std::size_t>(out * wpr);
+        for (int p = 0; p < bits; ++p) pp.planes.emplace_back(planes + p * np, planes + (p + 1) * np);
+        auto res = bitplane::bitplane_matmul(mat(x, T, in), pp, params(out, in, gs, bits, scale, zero),
+                                             std::vector<int>(active, active + n_active));
+        put(res.out, y);
+    });
+}
+
+// bitplane.hpp:178 permute_by_slice
+int ref_permute_by_slice(const double* tokens, int64_t T, int64_t cols, const uint8_t* masks,
+                         double* permuted, int64_t* perm, int64_t* inverse, uint8_t* group_mask,
+                         int64_t* group_len, int64_t* n_groups) {
+    return guard([&] {
+        auto p = bitplane::permute_by_slice(mat(tokens, T, cols), std::vector<std::uint8_t>(masks, masks + T));
+        if (permuted) put(p.permuted, permuted);
+        for (int64_t i = 0; i < T; ++i) {
+            perm[i] = static_cast<int64_t>(p.perm[i]);
+            inverse[i] = static_cast<int64_t>(p.inverse[i]);
+        }
+        for (std::size_t g = 0; g < p.groups.size(); ++g) {
+            group_mask[g] = p.groups[g].first;
+            group_len[g] = static_cast<int64_t>(p.groups[g].second);
+        }
+        *n_groups = static_cast<int64_t>(p.groups.size());
+    });
+}
+
+// The timed CPU baseline: the reference's own per-layer inference sequence
+// score -> gate_hard(delta) -> forward_elastic (pipeline.hpp:146-183, with delta
+// given), token-sharded over `threads` std::threads (the functions are pure and
+// re-entrant).  Returns the hard gates and outputs.
+int ref_layer_forward_threaded(const double* x, int64_t T, int64_t in, const uint8_t* codes,
+                               int32_t n_slices, const int32_t* slice_bits, const double* scale,
+                               const double* zero, int64_t out, int64_t gs, int64_t h,
+                               const double* w1, const double* b1, const double* w2,
+                               const double* b2, double delta, int threads, double* gates_out,
+                               double* y) {
+    return guard([&] {
+        const int64_t nr = n_slices - 1;
+        slicer::SliceStack st = stack_of(codes, n_slices, slice_bits, out, in, gs, scale, zero);
+        router::RouterState rs = router_of(in, h, nr, w1, b1, w2, b2);
+        int nt = std::max(1, std::min<int>(threads, static_cast<int>(T)));
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(static_cast<std::size_t>(nt));
+        for (int w = 0; w < nt; ++w) {
+            pool.emplace_back([&, w] {
+                try {
+                    int64_t t0 = T * w / nt, t1 = T * (w + 1) / nt;
+                    if (t1 <= t0) return;
+                    Matrix xs = mat(x + t0 * in, t1 - t0, in);
+                    Matrix s = router::score(xs, rs);
+                    Matrix g = router::gate_hard(s, delta);
+                    Matrix ys = router::forward_elastic(xs, st, g, router::GateMode::kHard);
+                    if (gates_out) std::memcpy(gates_out + t0 * nr, g.data(), sizeof(double) * g.size());
+                    std::memcpy(y + t0 * out, ys.data(), sizeof(double) * ys.size());
+                } catch (const std::exception& e) {
+                    errs[static_cast<std::size_t>(w)] = e.what();
+                }
+            });
+        }
+        for (auto& t : pool) t.join();
+        for (auto& e : errs)
+            if (!e.empty()) throw std::invalid_argument(e);
+    });
+}
+
+}  // extern "C"
