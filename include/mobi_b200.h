@@ -1,0 +1,158 @@
+/*
+ * mobi_b200.h -- C ABI of the B200-native MoBi linear layer (the drop-in for the
+ * MoBiQuant inference hot path: route -> bucket -> nested residual GEMM -> un-permute).
+ *
+ * Plain C, plain pointers and sizes; no CUDA or torch types.  Streams are passed as
+ * `void*` (a cudaStream_t, NULL = the legacy default stream).  Device pointers are
+ * CUDA device memory on the layer's device.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj/include/mobi):
+ *   mobi_layer_create        slicer::SliceStack (slicer.hpp:25-66) + qcore::QuantParams
+ *                            (qcore.hpp:22-49) + router::RouterState (router.hpp:32-60), or
+ *                            bench::LayerRecord (bench/checkpoint.hpp:30-74) -- the reference is
+ *                            stateless, so its per-call inputs become a persistent device handle
+ *   mobi_score               router::score            (router.hpp:63-76)
+ *   mobi_route               router::score + router::gate_hard (router.hpp:63-97) + mask convention
+ *                            (bitplane.hpp:203-206) + bitplane::permute_by_slice (bitplane.hpp:178-201)
+ *   mobi_forward             score -> gate_hard(delta) -> forward_elastic(kHard) as called by
+ *                            bench::eval_at_ratio (pipeline.hpp:146-183) and trainer::calibrate_model
+ *                            (trainer.hpp:804-812)
+ *   mobi_forward_masked      router::forward_elastic (router.hpp:105-132) with given hard gates
+ *   mobi_forward_host        mobi_forward from/to host buffers (the call a CPU caller makes)
+ *   mobi_permute_by_slice    bitplane::permute_by_slice (bitplane.hpp:178-201), index part
+ *   mobi_calibrate_threshold router::calibrate_threshold (router.hpp:167-174)
+ *   mobi_layer_unpack_codes  bench::LayerRecord::stack() (checkpoint.hpp:54-73) / bitplane::unpack
+ *                            (bitplane.hpp:75-84), read back from the device layout (bit-exact check)
+ *   mobi_decompose           slicer::decompose (slicer.hpp:69-113) + qcore::params_from_clip
+ *                            (qcore.hpp:122-146), on the GPU
+ *
+ * Error convention (mirrors MOBI_CHECK, common.hpp:13-24): every entry point returns
+ * MOBI_OK, MOBI_EINVAL (the reference would throw std::invalid_argument; message names the
+ * offending dim/index like the reference's) or MOBI_ERUNTIME (CUDA/NCCL failure,
+ * std::runtime_error).  mobi_last_error() returns the thread-local message of the last failure.
+ *
+ * Threading: a layer handle is immutable after create except for its internal workspace;
+ * concurrent calls on one handle must be serialised by the caller (or use one handle per
+ * stream).  Handles on different devices are independent.
+ */
+#ifndef MOBI_B200_H
+#define MOBI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MOBI_API __attribute__((visibility("default")))
+#else
+#define MOBI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOBI_OK 0
+#define MOBI_EINVAL 1
+#define MOBI_ERUNTIME 2
+
+#define MOBI_MAX_SLICES 4 /* slice 1 + up to 3 routed residual slices -> 8 buckets */
+
+typedef struct mobi_layer* mobi_layer_t;
+
+/* Host-side description of one MoBi linear layer.  All arrays are host memory, row-major,
+ * in the reference's own layouts and dtypes (double / uint8 / uint64). */
+typedef struct {
+    int64_t out;        /* output rows of W (QuantParams::rows)                         */
+    int64_t in;         /* input dim (QuantParams::cols)                                 */
+    int64_t group_size; /* qcore::kDefaultGroupSize = 128; group = r*ceil(in/gs) + c/gs   */
+    int32_t n_slices;   /* E (SliceStack::num_slices), 2..MOBI_MAX_SLICES                */
+    const int32_t* slice_bits; /* [E], uniform widths, sum <= 8 (slice.bits = 2 2 2 2)  */
+    const double* scale; /* [out*ceil(in/gs)] base (slice-1) scales, > 0               */
+    const double* zero;  /* [out*ceil(in/gs)] base (slice-1) continuous zeros          */
+    /* slice payload, exactly one of: */
+    const uint8_t* codes;     /* [E][out][in] slice codes c_e (SliceStack::slices)      */
+    const uint64_t* planes;   /* [plane_bits][out][words_per_row] merged-code bit-planes,
+                                 MSB plane first (LayerRecord::planes, bitplane.hpp:21-36) */
+    int32_t plane_bits;
+    int64_t words_per_row;
+    /* router (RouterState): hidden width h, n_routed = E-1 */
+    int64_t router_hidden;
+    const double* w1; /* [in][h]     */
+    const double* b1; /* [h]         */
+    const double* w2; /* [h][E-1]    */
+    const double* b2; /* [E-1]       */
+} mobi_layer_desc;
+
+/* Upload, validate and repack a layer onto `device`.  The handle owns its device weights. */
+MOBI_API int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out);
+MOBI_API int mobi_layer_destroy(mobi_layer_t layer);
+/* Pre-size the internal workspace for up to max_tokens tokens (avoids allocation inside
+ * forward, required before stream capture into a CUDA graph). */
+MOBI_API int mobi_layer_reserve(mobi_layer_t layer, int64_t max_tokens);
+/* Shape queries. */
+MOBI_API int mobi_layer_info(mobi_layer_t layer, int64_t* out, int64_t* in, int32_t* n_slices,
+                    int64_t* router_hidden, int64_t* device_bytes);
+
+/* The router parameters exactly as the device uses them, widened to float (w1 is stored
+ * bf16 on the device, b1/w2/b2 fp32): lets a checker feed the oracle identical inputs. */
+MOBI_API int mobi_layer_export_router(mobi_layer_t layer, float* w1 /*[in][h]*/, float* b1, float* w2,
+                             float* b2);
+/* K6: read the device weight layout back as slice codes [E][out][in] (host). */
+MOBI_API int mobi_layer_unpack_codes(mobi_layer_t layer, uint8_t* codes_host);
+
+/* router::score: S[T][E-1] fp32 (device) from X[T][in] bf16 (device). */
+MOBI_API int mobi_score(mobi_layer_t layer, const void* x_bf16, int64_t T, float* scores, void* stream);
+
+/* score -> gate_hard(delta) -> mask_t = 1 | sum_j 1(S[t,j]-delta>0) << (j+1) -> stable bucket
+ * permutation.  All outputs device, each nullable.  perm[i] = source token of permuted row i,
+ * inverse[t] = permuted row of token t; bucket_count[m] = tokens with mask m (m < 2^(E-1)*2). */
+MOBI_API int mobi_route(mobi_layer_t layer, const void* x_bf16, int64_t T, float delta, float* scores,
+               uint8_t* masks, int32_t* perm, int32_t* inverse, int32_t* bucket_count,
+               void* stream);
+
+/* Full layer: Y[T][out] bf16 (device) = forward_elastic(X, stack, gate_hard(score(X), delta)).
+ * masks (device, nullable) receives the per-token slice masks. */
+MOBI_API int mobi_forward(mobi_layer_t layer, const void* x_bf16, int64_t T, float delta, void* y_bf16,
+                 uint8_t* masks, void* stream);
+
+/* forward_elastic with given per-token masks (device uint8, bit0 must be set; bit e-1 = slice e):
+ * isolates GEMM parity from router decisions. */
+MOBI_API int mobi_forward_masked(mobi_layer_t layer, const void* x_bf16, int64_t T, const uint8_t* masks,
+                        void* y_bf16, void* stream);
+
+/* mobi_forward from HOST buffers: x_host bf16 [T][in] -> y_host bf16 [T][out] (+ masks_host,
+ * nullable); copies go through the layer's pinned staging buffers on `stream`; synchronous. */
+MOBI_API int mobi_forward_host(mobi_layer_t layer, const void* x_host, int64_t T, float delta,
+                      void* y_host, uint8_t* masks_host, void* stream);
+
+/* bitplane::permute_by_slice index part on the GPU: masks (device, [T]) -> perm, inverse
+ * (device int32 [T]), groups (host: group_mask[<=256], group_len[<=256], *n_groups). */
+MOBI_API int mobi_permute_by_slice(const uint8_t* masks, int64_t T, int32_t* perm, int32_t* inverse,
+                          uint8_t* group_mask, int64_t* group_len, int64_t* n_groups, void* stream);
+
+/* router::calibrate_threshold over n device fp32 scores: delta = sort_desc(s)[floor(rho*n+1e-9)],
+ * or min-1 if that index is >= n.  Synchronous; result to host. */
+MOBI_API int mobi_calibrate_threshold(const float* scores, int64_t n, double rho, double* delta,
+                             void* stream);
+
+/* slicer::decompose on the GPU, with base params from params_from_clip(identity clip gamma):
+ * w (device fp64 [out][in]) -> codes (device uint8 [E][out][in]), scale/zero (device fp64
+ * [out*ceil(in/gs)]), clamp_counts (host int64 [E], nullable).  Bit-exact with the reference. */
+MOBI_API int mobi_decompose(const double* w, int64_t out, int64_t in, int64_t group_size,
+                   const int32_t* slice_bits, int32_t n_slices, double gamma, uint8_t* codes,
+                   double* scale, double* zero, int64_t* clamp_counts, void* stream);
+
+/* Number of kernels the last forward on this layer launched (for launch accounting). */
+MOBI_API int mobi_layer_last_launches(mobi_layer_t layer, int32_t* launches);
+
+MOBI_API const char* mobi_last_error(void);
+
+/* Test hook (not part of the drop-in surface): impl 1 routes the GEMM through the CUDA-core
+ * reference kernel (gemm_simt.cu) so the test-suite can cross-check the tcgen05 kernel. */
+MOBI_API int mobi_debug_set_impl(int impl);
+MOBI_API const char* mobi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOBI_B200_H */

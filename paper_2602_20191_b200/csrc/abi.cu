@@ -1,0 +1,518 @@
+// abi.cu -- host side of the C ABI (include/mobi_b200.h): validation with the reference's
+// MOBI_CHECK wording, upload + device repack of a layer, workspace management, and the
+// route -> bucket -> gather -> GEMM launch sequence.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "mobi_internal.cuh"
+
+namespace mobi {
+
+static thread_local std::string g_err;
+static int g_impl_override = 0;  // test hook: 1 = CUDA-core reference GEMM
+
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* cperm, int32_t* inverse,
+                   int32_t* hist256, cudaStream_t st);
+
+namespace {
+
+#define CHECK_ARG(cond, msg)                            \
+    do {                                                \
+        if (!(cond)) {                                  \
+            std::ostringstream o_;                      \
+            o_ << msg;                                  \
+            return set_error(MOBI_EINVAL, o_.str());    \
+        }                                               \
+    } while (0)
+
+inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+template <class T>
+int dmalloc(T** p, size_t n, mobi_layer* L) {
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+    if (e != cudaSuccess) return set_error(MOBI_ERUNTIME, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    if (L) L->device_bytes += (int64_t)(n * sizeof(T));
+    return MOBI_OK;
+}
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+uint16_t f2bf(float f) {  // round-to-nearest-even, NaN-preserving
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+float bf2f(uint16_t b) {
+    uint32_t u = (uint32_t)b << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+void free_ws(mobi_layer* L) {
+    dfree(L->s_part);
+    dfree(L->scores);
+    dfree(L->masks);
+    dfree(L->perm);
+    dfree(L->inverse);
+    dfree(L->cperm);
+    dfree(L->escale);
+    dfree(L->xperm);
+    dfree(L->tiles);
+    dfree(L->meta);
+    if (L->tmap_x) delete L->tmap_x;
+    L->tmap_x = nullptr;
+    L->ws_T = -1;
+}
+
+int ensure_ws(mobi_layer* L, int64_t T) {
+    if (T <= L->ws_T) return MOBI_OK;
+    cudaDeviceSynchronize();  // workspace may be in use by queued work
+    free_ws(L);
+    const int64_t Tc = round_up(std::max<int64_t>(T, 1), 256);
+    L->tpad_max = round_up(Tc + 2 * kMaxBuckets * (kBucketAlign - 1), kBucketAlign);
+    L->max_tiles = cdiv(Tc, kTokTile) + 2 * kMaxBuckets;
+    const int64_t htiles_max = cdiv(L->h, 64);
+    int rc;
+    if ((rc = dmalloc(&L->s_part, (size_t)(htiles_max * Tc * L->nr), nullptr))) return rc;
+    if ((rc = dmalloc(&L->scores, (size_t)(Tc * L->nr), nullptr))) return rc;
+    if ((rc = dmalloc(&L->masks, (size_t)Tc, nullptr))) return rc;
+    if ((rc = dmalloc(&L->perm, (size_t)L->tpad_max, nullptr))) return rc;
+    if ((rc = dmalloc(&L->inverse, (size_t)Tc, nullptr))) return rc;
+    if ((rc = dmalloc(&L->cperm, (size_t)Tc, nullptr))) return rc;
+    if ((rc = dmalloc(&L->escale, (size_t)L->tpad_max, nullptr))) return rc;
+    if ((rc = dmalloc(&L->xperm, (size_t)(L->tpad_max * L->in_pad), nullptr))) return rc;
+    if ((rc = dmalloc(&L->tiles, (size_t)L->max_tiles, nullptr))) return rc;
+    if ((rc = dmalloc(&L->meta, 64, nullptr))) return rc;
+    L->ws_T = Tc;
+    return MOBI_OK;
+}
+
+int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L) {
+    CHECK_ARG(d != nullptr, "mobi_layer_create: null descriptor");
+    CHECK_ARG(d->out > 0 && d->in > 0, "mobi_layer_create: empty weight " << d->out << "x" << d->in);
+    CHECK_ARG(d->group_size >= 1, "QuantParams: group_size must be >= 1");
+    CHECK_ARG(d->n_slices >= 2 && d->n_slices <= MOBI_MAX_SLICES,
+              "mobi_layer_create: " << d->n_slices << " slices; supported 2.." << MOBI_MAX_SLICES);
+    CHECK_ARG(d->slice_bits != nullptr, "decompose: slice_bits is empty");
+    int total = 0;
+    for (int e = 0; e < d->n_slices; ++e) {
+        CHECK_ARG(d->slice_bits[e] >= 1 && d->slice_bits[e] <= 8,
+                  "decompose: slice bit width " << d->slice_bits[e] << " out of [1,8]");
+        CHECK_ARG(d->slice_bits[e] == d->slice_bits[0],
+                  "merged_params: slice widths must be uniform for the merged code");
+        total += d->slice_bits[e];
+    }
+    CHECK_ARG(total <= 8, "decompose: total bits " << total << " exceed the 8-bit code budget");
+    CHECK_ARG(d->group_size >= d->in || d->group_size % 32 == 0,
+              "mobi_layer_create: group_size " << d->group_size
+                                               << " must be a multiple of 32 or cover the whole row (in=" << d->in << ")");
+    CHECK_ARG(d->scale && d->zero, "QuantParams: missing scales/zeros");
+    L->out = d->out;
+    L->in = d->in;
+    L->gs = d->group_size;
+    L->G = cdiv(d->in, d->group_size);
+    L->single_group = d->group_size >= d->in;
+    L->E = d->n_slices;
+    L->b = d->slice_bits[0];
+    L->nr = d->n_slices - 1;
+    const int64_t ng = L->out * L->G;
+    for (int64_t g = 0; g < ng; ++g) {
+        CHECK_ARG(std::isfinite(d->scale[g]) && d->scale[g] > 0.0, "QuantParams: non-positive scale at group " << g);
+        CHECK_ARG(std::isfinite(d->zero[g]), "QuantParams: non-finite zero at group " << g);
+    }
+    CHECK_ARG((d->codes != nullptr) != (d->planes != nullptr),
+              "mobi_layer_create: give exactly one of codes (SliceStack) or planes (LayerRecord)");
+    if (d->codes) {
+        const int qmax = (1 << L->b) - 1;
+        const int64_t n = L->out * L->in;
+        for (int e = 0; e < L->E; ++e)
+            for (int64_t i = 0; i < n; ++i)
+                if (d->codes[(int64_t)e * n + i] > qmax)
+                    return set_error(MOBI_EINVAL, "dequantize_centered: code " + std::to_string(d->codes[e * n + i]) +
+                                                      " out of [0," + std::to_string(qmax) + "] at (" +
+                                                      std::to_string(i / L->in) + "," + std::to_string(i % L->in) +
+                                                      ")");
+    } else {
+        CHECK_ARG(d->plane_bits == total, "bitplane: planes carry " << d->plane_bits << " bits, slices need " << total);
+        CHECK_ARG(d->words_per_row == cdiv(d->in, 64),
+                  "bitplane: words_per_row " << d->words_per_row << " != ceil(in/64) = " << cdiv(d->in, 64));
+    }
+    CHECK_ARG(d->router_hidden >= 1, "RouterState: hidden width must be >= 1");
+    CHECK_ARG(d->w1 && d->b1 && d->w2 && d->b2, "RouterState: missing router weights");
+    L->h = d->router_hidden;
+    L->out_pad = round_up(L->out, kRowTile);
+    L->in_pad = round_up(L->in, kKBlock);
+    L->kblocks = L->in_pad / kKBlock;
+    L->h_pad = round_up(L->h, 128);
+    // per-mask dequant constants (uniform b-bit slices, see mobi_internal.cuh)
+    const int P = (L->E - 1) * L->b;
+    const unsigned fm = (1u << L->b) - 1u;
+    for (int m = 0; m < 2 * kMaxBuckets; ++m) {
+        unsigned mb = 0;
+        double K = std::ldexp(1.0, P);
+        for (int e = 1; e <= L->E; ++e) {
+            if (!((m >> (e - 1)) & 1)) continue;
+            mb |= fm << ((L->E - e) * L->b);
+            if (e >= 2) K -= (double)fm * std::ldexp(1.0, P - (e - 1) * L->b);
+        }
+        L->mtab.maskword[m] = mb * 0x01010101u;
+        L->mtab.kc[m] = (float)(K / std::ldexp(1.0, P + 1));
+    }
+    L->mtab.inv_2p = (float)std::ldexp(1.0, -P);
+    return MOBI_OK;
+}
+
+int upload_layer(const mobi_layer_desc* d, mobi_layer* L) {
+    int rc;
+    const int64_t ng = L->out * L->G;
+    // weights: tiled merged codes (repacked on the device)
+    if ((rc = dmalloc(&L->codes8, (size_t)(L->out_pad * L->in_pad), L))) return rc;
+    if (d->codes) {
+        uint8_t* tmp = nullptr;
+        const size_t n = (size_t)(L->E * L->out * L->in);
+        if ((rc = dmalloc(&tmp, n, nullptr))) return rc;
+        MOBI_CUDA(cudaMemcpy(tmp, d->codes, n, cudaMemcpyHostToDevice));
+        rc = launch_pack_codes(L, tmp, 0);
+        cudaDeviceSynchronize();
+        dfree(tmp);
+        if (rc) return rc;
+    } else {
+        uint64_t* tmp = nullptr;
+        const size_t n = (size_t)(d->plane_bits * L->out * d->words_per_row);
+        if ((rc = dmalloc(&tmp, n, nullptr))) return rc;
+        MOBI_CUDA(cudaMemcpy(tmp, d->planes, n * 8, cudaMemcpyHostToDevice));
+        rc = launch_pack_planes(L, tmp, d->plane_bits, d->words_per_row, 0);
+        cudaDeviceSynchronize();
+        dfree(tmp);
+        if (rc) return rc;
+    }
+    std::vector<float> s(ng), sz(ng);
+    for (int64_t g = 0; g < ng; ++g) {
+        s[g] = (float)d->scale[g];
+        sz[g] = (float)(d->scale[g] * d->zero[g]);
+    }
+    if ((rc = dmalloc(&L->gscale, (size_t)ng, L))) return rc;
+    if ((rc = dmalloc(&L->gsz, (size_t)ng, L))) return rc;
+    MOBI_CUDA(cudaMemcpy(L->gscale, s.data(), ng * 4, cudaMemcpyHostToDevice));
+    MOBI_CUDA(cudaMemcpy(L->gsz, sz.data(), ng * 4, cudaMemcpyHostToDevice));
+    // router: w1 transposed to [h_pad][in_pad] bf16 (K-major B operand), zero padded
+    std::vector<uint16_t> w1t((size_t)(L->h_pad * L->in_pad), 0);
+    for (int64_t k = 0; k < L->in; ++k)
+        for (int64_t j = 0; j < L->h; ++j) w1t[(size_t)(j * L->in_pad + k)] = f2bf((float)d->w1[k * L->h + j]);
+    std::vector<float> b1((size_t)L->h_pad, 0.f), w2((size_t)(L->h_pad * L->nr), 0.f), b2((size_t)L->nr);
+    for (int64_t j = 0; j < L->h; ++j) {
+        b1[j] = (float)d->b1[j];
+        for (int k = 0; k < L->nr; ++k) w2[j * L->nr + k] = (float)d->w2[j * L->nr + k];
+    }
+    for (int k = 0; k < L->nr; ++k) b2[k] = (float)d->b2[k];
+    if ((rc = dmalloc(&L->w1t, w1t.size(), L))) return rc;
+    if ((rc = dmalloc(&L->b1, b1.size(), L))) return rc;
+    if ((rc = dmalloc(&L->w2, w2.size(), L))) return rc;
+    if ((rc = dmalloc(&L->b2, b2.size(), L))) return rc;
+    MOBI_CUDA(cudaMemcpy(L->w1t, w1t.data(), w1t.size() * 2, cudaMemcpyHostToDevice));
+    MOBI_CUDA(cudaMemcpy(L->b1, b1.data(), b1.size() * 4, cudaMemcpyHostToDevice));
+    MOBI_CUDA(cudaMemcpy(L->w2, w2.data(), w2.size() * 4, cudaMemcpyHostToDevice));
+    MOBI_CUDA(cudaMemcpy(L->b2, b2.data(), b2.size() * 4, cudaMemcpyHostToDevice));
+    MOBI_CUDA(cudaDeviceSynchronize());
+    return MOBI_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_t* given_masks, void* y,
+              uint8_t* masks_out, cudaStream_t st) {
+    CHECK_ARG(T >= 0, "forward_elastic: negative token count " << T);
+    L->last_launches = 0;
+    if (T == 0) return MOBI_OK;
+    int rc;
+    if ((rc = ensure_ws(L, T))) return rc;
+    const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+    if (!given_masks && (rc = launch_router(L, xb, T, st))) return rc;
+    if ((rc = launch_bucket(L, T, delta, given_masks, nullptr, masks_out, nullptr, nullptr, nullptr, st))) return rc;
+    if ((rc = launch_gather(L, xb, T, st))) return rc;
+    __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
+    if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
+    return launch_gemm_tc(L, yb, T, st);
+}
+
+}  // namespace
+}  // namespace mobi
+
+using namespace mobi;
+
+extern "C" {
+
+const char* mobi_last_error(void) { return g_err.c_str(); }
+const char* mobi_version(void) { return "mobi_b200 0.1 (sm_100a)"; }
+
+int mobi_debug_set_impl(int impl) {
+    g_impl_override = impl;
+    return MOBI_OK;
+}
+
+int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out) {
+    CHECK_ARG(out != nullptr, "mobi_layer_create: null output handle");
+    *out = nullptr;
+    int ndev = 0;
+    MOBI_CUDA(cudaGetDeviceCount(&ndev));
+    CHECK_ARG(device >= 0 && device < ndev, "mobi_layer_create: device " << device << " out of [0," << ndev << ")");
+    DeviceGuard g(device);
+    mobi_layer* L = new mobi_layer;
+    L->device = device;
+    int rc = validate_and_fill(desc, L);
+    if (!rc) rc = upload_layer(desc, L);
+    if (rc) {
+        std::string keep = g_err;
+        mobi_layer_destroy(L);
+        g_err = keep;
+        return rc;
+    }
+    *out = L;
+    return MOBI_OK;
+}
+
+int mobi_layer_destroy(mobi_layer_t L) {
+    if (!L) return MOBI_OK;
+    DeviceGuard g(L->device);
+    cudaDeviceSynchronize();
+    free_ws(L);
+    dfree(L->codes8);
+    dfree(L->gscale);
+    dfree(L->gsz);
+    dfree(L->w1t);
+    dfree(L->b1);
+    dfree(L->w2);
+    dfree(L->b2);
+    if (L->x_dev) cudaFree(L->x_dev);
+    if (L->y_dev) cudaFree(L->y_dev);
+    if (L->h_x) cudaFreeHost(L->h_x);
+    if (L->h_y) cudaFreeHost(L->h_y);
+    delete L;
+    return MOBI_OK;
+}
+
+int mobi_layer_reserve(mobi_layer_t L, int64_t max_tokens) {
+    CHECK_ARG(L, "null layer");
+    CHECK_ARG(max_tokens >= 0, "mobi_layer_reserve: negative token count");
+    DeviceGuard g(L->device);
+    return ensure_ws(L, max_tokens);
+}
+
+int mobi_layer_info(mobi_layer_t L, int64_t* out, int64_t* in, int32_t* n_slices, int64_t* router_hidden,
+                    int64_t* device_bytes) {
+    CHECK_ARG(L, "null layer");
+    if (out) *out = L->out;
+    if (in) *in = L->in;
+    if (n_slices) *n_slices = L->E;
+    if (router_hidden) *router_hidden = L->h;
+    if (device_bytes) *device_bytes = L->device_bytes;
+    return MOBI_OK;
+}
+
+int mobi_layer_export_router(mobi_layer_t L, float* w1, float* b1, float* w2, float* b2) {
+    CHECK_ARG(L, "null layer");
+    DeviceGuard g(L->device);
+    std::vector<uint16_t> w1t((size_t)(L->h_pad * L->in_pad));
+    MOBI_CUDA(cudaMemcpy(w1t.data(), L->w1t, w1t.size() * 2, cudaMemcpyDeviceToHost));
+    if (w1)
+        for (int64_t k = 0; k < L->in; ++k)
+            for (int64_t j = 0; j < L->h; ++j) w1[k * L->h + j] = bf2f(w1t[(size_t)(j * L->in_pad + k)]);
+    if (b1) MOBI_CUDA(cudaMemcpy(b1, L->b1, L->h * 4, cudaMemcpyDeviceToHost));
+    if (w2) MOBI_CUDA(cudaMemcpy(w2, L->w2, L->h * L->nr * 4, cudaMemcpyDeviceToHost));
+    if (b2) MOBI_CUDA(cudaMemcpy(b2, L->b2, L->nr * 4, cudaMemcpyDeviceToHost));
+    return MOBI_OK;
+}
+
+int mobi_layer_unpack_codes(mobi_layer_t L, uint8_t* codes_host) {
+    CHECK_ARG(L && codes_host, "mobi_layer_unpack_codes: null argument");
+    DeviceGuard g(L->device);
+    uint8_t* tmp = nullptr;
+    const size_t n = (size_t)(L->E * L->out * L->in);
+    int rc;
+    if ((rc = dmalloc(&tmp, n, nullptr))) return rc;
+    rc = launch_unpack_codes(L, tmp, 0);
+    if (!rc) {
+        cudaError_t e = cudaMemcpy(codes_host, tmp, n, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) rc = set_error(MOBI_ERUNTIME, cudaGetErrorString(e));
+    }
+    dfree(tmp);
+    return rc;
+}
+
+int mobi_score(mobi_layer_t L, const void* x, int64_t T, float* scores, void* stream) {
+    CHECK_ARG(L, "null layer");
+    CHECK_ARG(T >= 0, "score: negative token count");
+    if (T == 0) return MOBI_OK;
+    DeviceGuard g(L->device);
+    int rc;
+    if ((rc = ensure_ws(L, T))) return rc;
+    L->last_launches = 0;
+    if ((rc = launch_router(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
+    return launch_bucket(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream));
+}
+
+int mobi_route(mobi_layer_t L, const void* x, int64_t T, float delta, float* scores, uint8_t* masks, int32_t* perm,
+               int32_t* inverse, int32_t* bucket_count, void* stream) {
+    CHECK_ARG(L, "null layer");
+    CHECK_ARG(T >= 0, "score: negative token count");
+    if (T == 0) return MOBI_OK;
+    DeviceGuard g(L->device);
+    int rc;
+    if ((rc = ensure_ws(L, T))) return rc;
+    L->last_launches = 0;
+    if ((rc = launch_router(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
+    return launch_bucket(L, T, delta, nullptr, scores, masks, perm, inverse, bucket_count, S(stream));
+}
+
+int mobi_forward(mobi_layer_t L, const void* x, int64_t T, float delta, void* y, uint8_t* masks, void* stream) {
+    CHECK_ARG(L, "null layer");
+    DeviceGuard g(L->device);
+    return run_layer(L, x, T, delta, nullptr, y, masks, S(stream));
+}
+
+int mobi_forward_masked(mobi_layer_t L, const void* x, int64_t T, const uint8_t* masks, void* y, void* stream) {
+    CHECK_ARG(L, "null layer");
+    CHECK_ARG(masks != nullptr || T == 0, "forward_elastic: null gate masks");
+    DeviceGuard g(L->device);
+    return run_layer(L, x, T, 0.f, masks, y, nullptr, S(stream));
+}
+
+int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta, void* y_host, uint8_t* masks_host,
+                      void* stream) {
+    CHECK_ARG(L && x_host && y_host, "mobi_forward_host: null argument");
+    CHECK_ARG(T >= 0, "forward_elastic: negative token count " << T);
+    if (T == 0) return MOBI_OK;
+    DeviceGuard g(L->device);
+    cudaStream_t st = S(stream);
+    const size_t xb = (size_t)(T * L->in * 2), yb = (size_t)(T * L->out * 2);
+    if (T > L->h_cap) {
+        if (L->x_dev) cudaFree(L->x_dev);
+        if (L->y_dev) cudaFree(L->y_dev);
+        if (L->h_x) cudaFreeHost(L->h_x);
+        if (L->h_y) cudaFreeHost(L->h_y);
+        L->x_dev = L->y_dev = L->h_x = L->h_y = nullptr;
+        MOBI_CUDA(cudaMalloc(&L->x_dev, xb + T));
+        MOBI_CUDA(cudaMalloc(&L->y_dev, yb));
+        MOBI_CUDA(cudaMallocHost(&L->h_x, xb));
+        MOBI_CUDA(cudaMallocHost(&L->h_y, yb + T));
+        L->h_cap = T;
+    }
+    auto pinned = [](const void* p) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    };
+    const bool xp = pinned(x_host), yp = pinned(y_host);
+    const void* xsrc = x_host;
+    if (!xp) {
+        std::memcpy(L->h_x, x_host, xb);
+        xsrc = L->h_x;
+    }
+    MOBI_CUDA(cudaMemcpyAsync(L->x_dev, xsrc, xb, cudaMemcpyHostToDevice, st));
+    uint8_t* mdev = masks_host ? reinterpret_cast<uint8_t*>(L->x_dev) + xb : nullptr;
+    int rc = run_layer(L, L->x_dev, T, delta, nullptr, L->y_dev, mdev, st);
+    if (rc) return rc;
+    void* ydst = yp ? y_host : L->h_y;
+    MOBI_CUDA(cudaMemcpyAsync(ydst, L->y_dev, yb, cudaMemcpyDeviceToHost, st));
+    if (masks_host) MOBI_CUDA(cudaMemcpyAsync(masks_host, mdev, (size_t)T, cudaMemcpyDeviceToHost, st));
+    MOBI_CUDA(cudaStreamSynchronize(st));
+    if (!yp) std::memcpy(y_host, L->h_y, yb);
+    return MOBI_OK;
+}
+
+int mobi_permute_by_slice(const uint8_t* masks, int64_t T, int32_t* perm, int32_t* inverse, uint8_t* group_mask,
+                          int64_t* group_len, int64_t* n_groups, void* stream) {
+    CHECK_ARG(T >= 0, "permute_by_slice: negative token count");
+    if (n_groups) *n_groups = 0;
+    if (T == 0) return MOBI_OK;
+    cudaStream_t st = S(stream);
+    uint8_t* keys = nullptr;
+    int32_t* hist = nullptr;
+    MOBI_CUDA(cudaMallocAsync(&keys, (size_t)T, st));
+    MOBI_CUDA(cudaMallocAsync(&hist, 256 * sizeof(int32_t), st));
+    int rc = launch_permute(masks, T, keys, perm, inverse, hist, st);
+    int32_t h[256];
+    if (!rc) {
+        cudaError_t e = cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = set_error(MOBI_ERUNTIME, cudaGetErrorString(e));
+    }
+    cudaFreeAsync(keys, st);
+    cudaFreeAsync(hist, st);
+    if (rc) return rc;
+    int64_t ng = 0;
+    for (int v = 0; v < 256; ++v)
+        if (h[v]) {
+            if (group_mask) group_mask[ng] = (uint8_t)v;
+            if (group_len) group_len[ng] = h[v];
+            ++ng;
+        }
+    if (n_groups) *n_groups = ng;
+    return MOBI_OK;
+}
+
+int mobi_calibrate_threshold(const float* scores, int64_t n, double rho, double* delta, void* stream) {
+    CHECK_ARG(n > 0, "calibrate_threshold: empty score sample");
+    CHECK_ARG(rho >= 0.0 && rho <= 1.0, "calibrate_threshold: rho " << rho << " outside [0,1]");
+    CHECK_ARG(delta, "calibrate_threshold: null output");
+    std::vector<float> h((size_t)n);
+    MOBI_CUDA(cudaMemcpyAsync(h.data(), scores, n * 4, cudaMemcpyDeviceToHost, S(stream)));
+    MOBI_CUDA(cudaStreamSynchronize(S(stream)));
+    std::vector<double> s(h.begin(), h.end());
+    // router.hpp:167-174: sort descending, delta = s[floor(rho*N + 1e-9)] (min-1 past the end)
+    const int64_t k = (int64_t)std::floor(rho * (double)n + 1e-9);
+    if (k >= n) {
+        *delta = *std::min_element(s.begin(), s.end()) - 1.0;
+    } else {
+        std::nth_element(s.begin(), s.begin() + k, s.end(), std::greater<double>());
+        *delta = s[(size_t)k];
+    }
+    return MOBI_OK;
+}
+
+int mobi_decompose(const double* w, int64_t out, int64_t in, int64_t group_size, const int32_t* slice_bits,
+                   int32_t n_slices, double gamma, uint8_t* codes, double* scale, double* zero, int64_t* clamp_counts,
+                   void* stream) {
+    CHECK_ARG(w && codes && scale && zero && slice_bits, "decompose: null argument");
+    return launch_decompose(w, out, in, group_size, slice_bits, n_slices, gamma, codes, scale, zero, clamp_counts,
+                            S(stream));
+}
+
+int mobi_layer_last_launches(mobi_layer_t L, int32_t* launches) {
+    CHECK_ARG(L && launches, "null argument");
+    *launches = L->last_launches;
+    return MOBI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// decompose.cu -- GPU slice decomposition: base params from clipping
+// (qcore.hpp:75-146, GroupStats + params_from_clip) and the recursive residual decomposition
+// (slicer.hpp:69-113), bit-exact with the reference.
+//
+// Exactness: every double operation is an explicit round-to-nearest intrinsic (no FMA
+// contraction; the file is also compiled with -fmad=false), the operation order is the
+// reference's, and the only transcendental (sigmoid of the clip gamma) is evaluated on the
+// host with the same libm the reference uses and passed in.
+#include <cmath>
+
+#include "mobi_internal.cuh"
+
+namespace mobi {
+namespace {
+
+// one thread per (row, group): stats -> params -> all slices of the group's elements
+__global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int64_t in, int64_t gs,
+                                 int64_t G, const int32_t* __restrict__ bits_dev, int E, double sq_lo,
+                                 double sq_hi, uint8_t* __restrict__ codes, double* __restrict__ scale,
+                                 double* __restrict__ zero, unsigned long long* __restrict__ clamp_counts) {
+    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= out * G) return;
+    const int64_t r = gi / G, g = gi % G;
+    const int64_t c0 = g * gs, c1 = min(in, c0 + gs);
+    const double* row = w + r * in;
+    double mn = row[c0], mx = row[c0];
+    for (int64_t c = c0 + 1; c < c1; ++c) {
+        const double v = row[c];
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+    }
+    // GroupStats::ref = min(max(0, min), max); clip_lo/hi; params_from_clip
+    const double lo0 = mn > 0.0 ? mn : 0.0;
+    const double ref = mx < lo0 ? mx : lo0;
+    const double lo = __dadd_rn(ref, __dmul_rn(sq_lo, __dsub_rn(mn, ref)));
+    const double hi = __dadd_rn(ref, __dmul_rn(sq_hi, __dsub_rn(mx, ref)));
+    const int b1 = bits_dev[0];
+    double s = __ddiv_rn(__dsub_rn(hi, lo), (double)((1 << b1) - 1));
+    if (!(s > 1e-8)) s = 1e-8;
+    const double z1 = __ddiv_rn(-lo, s);
+    scale[gi] = s;
+    zero[gi] = z1;
+    unsigned long long cl[MOBI_MAX_SLICES] = {0, 0, 0, 0};
+    for (int64_t c = c0; c < c1; ++c) {
+        double v = row[c];
+        int bb = 0;
+        for (int e = 0; e < E; ++e) {
+            const int be = bits_dev[e];
+            const double sc = e == 0 ? s : s * ldexp(1.0, -bb);  // exact power-of-two scaling
+            const double z = e == 0 ? z1 : ldexp(1.0, be - 1);
+            const double qmax = (double)((1 << be) - 1);
+            double u = floor(__dadd_rn(__ddiv_rn(v, sc), z));
+            if (u < 0.0 || u > qmax) {
+                ++cl[e];
+                u = fmin(fmax(u, 0.0), qmax);
+            }
+            codes[(int64_t)e * out * in + r * in + c] = (uint8_t)u;
+            v = __dsub_rn(v, __dmul_rn(sc, __dadd_rn(__dsub_rn(u, z), 0.5)));
+            bb += be;
+        }
+    }
+    for (int e = 0; e < E; ++e)
+        if (cl[e]) atomicAdd(&clamp_counts[e], cl[e]);
+}
+
+}  // namespace
+
+int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits, int32_t E,
+                     double gamma, uint8_t* codes, double* scale, double* zero, int64_t* clamp_counts_host,
+                     cudaStream_t st) {
+    if (E < 1 || E > MOBI_MAX_SLICES) return set_error(MOBI_EINVAL, "decompose: slice_bits is empty or too long");
+    int total = 0;
+    for (int e = 0; e < E; ++e) {
+        if (bits[e] < 1 || bits[e] > 8)
+            return set_error(MOBI_EINVAL, "decompose: slice bit width " + std::to_string(bits[e]) + " out of [1,8]");
+        total += bits[e];
+    }
+    if (total > 8)
+        return set_error(MOBI_EINVAL, "decompose: total bits " + std::to_string(total) + " exceed the 8-bit code budget");
+    if (out <= 0 || in <= 0 || gs <= 0) return set_error(MOBI_EINVAL, "decompose: empty weight");
+    // squash(gamma) = sigmoid(gamma) on the host (common.hpp:125-131), identical libm to the reference
+    const double sq = gamma >= 0.0 ? 1.0 / (1.0 + std::exp(-gamma)) : std::exp(gamma) / (1.0 + std::exp(gamma));
+    const int64_t G = cdiv(in, gs);
+    int32_t* bits_dev = nullptr;
+    unsigned long long* cc = nullptr;
+    MOBI_CUDA(cudaMallocAsync(&bits_dev, sizeof(int32_t) * E, st));
+    MOBI_CUDA(cudaMallocAsync(&cc, sizeof(unsigned long long) * MOBI_MAX_SLICES, st));
+    MOBI_CUDA(cudaMemcpyAsync(bits_dev, bits, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st));
+    MOBI_CUDA(cudaMemsetAsync(cc, 0, sizeof(unsigned long long) * MOBI_MAX_SLICES, st));
+    decompose_kernel<<<(unsigned)cdiv(out * G, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, sq, sq, codes,
+                                                                   scale, zero, cc);
+    MOBI_LAUNCH_CHECK();
+    unsigned long long h[MOBI_MAX_SLICES];
+    MOBI_CUDA(cudaMemcpyAsync(h, cc, sizeof(h), cudaMemcpyDeviceToHost, st));
+    MOBI_CUDA(cudaStreamSynchronize(st));
+    if (clamp_counts_host)
+        for (int e = 0; e < E; ++e) clamp_counts_host[e] = (int64_t)h[e];
+    cudaFreeAsync(bits_dev, st);
+    cudaFreeAsync(cc, st);
+    return MOBI_OK;
+}
+
+}  // namespace mobi

@@ -1,0 +1,111 @@
+// layer.cu -- device repacking of a layer's slice payload into the tiled merged-code layout
+// (mobi_internal.cuh) and the K6 read-back used for bit-exact verification.
+//
+// Reference layouts consumed:
+//   SliceStack::slices     [E][out][in] uint8 codes            (slicer.hpp:25-30)
+//   LayerRecord::planes    merged code INT = c1<<(E-1)b | ... | cE (slicer.hpp:150-161) as
+//                          `bits` planes of uint64 words, plane 0 = MSB, word r*wpr + c/64,
+//                          bit c%64 (bitplane.hpp:21-36, 48-73)
+#include "mobi_internal.cuh"
+
+namespace mobi {
+namespace {
+
+// one thread = one (row, 16-column chunk): merge E slice codes, store 16 bytes
+__global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, int64_t out, int64_t in,
+                                  int64_t out_pad, int64_t kblocks, int E, int b,
+                                  uint8_t* __restrict__ dst) {
+    const int64_t nchunks = kblocks * (kKBlock / 16);
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= out_pad * nchunks) return;
+    const int64_t R = idx / nchunks, ch = idx % nchunks;
+    const int64_t k0 = ch * 16;
+    uint8_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int64_t k = k0 + j;
+        unsigned m = 0;
+        if (R < out && k < in) {
+            for (int e = 0; e < E; ++e) m = (m << b) | codes[(int64_t)e * out * in + R * in + k];
+        }
+        v[j] = (uint8_t)m;
+    }
+    uint4 w;
+    memcpy(&w, v, 16);
+    *reinterpret_cast<uint4*>(dst + code_offset(R, k0, kblocks)) = w;
+}
+
+// one thread = one (row, 64-bit word): gather `bits` plane bits of 64 columns
+__global__ void pack_planes_kernel(const uint64_t* __restrict__ planes, int bits, int64_t wpr,
+                                   int64_t out, int64_t in, int64_t out_pad, int64_t kblocks,
+                                   uint8_t* __restrict__ dst) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= out_pad * kblocks) return;
+    const int64_t R = idx / kblocks, w = idx % kblocks;  // kKBlock == 64 == bits per word
+    uint64_t pw[8];
+    for (int p = 0; p < 8; ++p)
+        pw[p] = (p < bits && R < out && w < wpr) ? planes[(int64_t)p * out * wpr + R * wpr + w] : 0ull;
+    for (int c = 0; c < 4; ++c) {
+        uint8_t v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int col = c * 16 + j;
+            unsigned code = 0;
+            for (int bit = 0; bit < bits; ++bit)  // bit `bit` lives in plane bits-1-bit
+                code |= (unsigned)((pw[bits - 1 - bit] >> col) & 1ull) << bit;
+            if (w * 64 + col >= in) code = 0;
+            v[j] = (uint8_t)code;
+        }
+        uint4 q;
+        memcpy(&q, v, 16);
+        *reinterpret_cast<uint4*>(dst + code_offset(R, w * 64 + c * 16, kblocks)) = q;
+    }
+}
+
+// K6: tiled merged codes -> slice codes [E][out][in]  (LayerRecord::stack() split)
+__global__ void unpack_codes_kernel(const uint8_t* __restrict__ src, int64_t out, int64_t in,
+                                    int64_t kblocks, int E, int b, uint8_t* __restrict__ codes) {
+    const int64_t nchunks = kblocks * (kKBlock / 16);
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= out * nchunks) return;
+    const int64_t R = idx / nchunks, k0 = (idx % nchunks) * 16;
+    uint4 q = *reinterpret_cast<const uint4*>(src + code_offset(R, k0, kblocks));
+    uint8_t v[16];
+    memcpy(v, &q, 16);
+    const unsigned fm = (1u << b) - 1u;
+    for (int j = 0; j < 16; ++j) {
+        const int64_t k = k0 + j;
+        if (k >= in) break;
+        for (int e = 0; e < E; ++e)
+            codes[(int64_t)e * out * in + R * in + k] = (uint8_t)((v[j] >> ((E - 1 - e) * b)) & fm);
+    }
+}
+
+}  // namespace
+
+int launch_pack_codes(mobi_layer* L, const uint8_t* codes_dev, cudaStream_t st) {
+    const int64_t n = L->out_pad * L->kblocks * (kKBlock / 16);
+    pack_codes_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(codes_dev, L->out, L->in, L->out_pad,
+                                                             L->kblocks, L->E, L->b, L->codes8);
+    MOBI_LAUNCH_CHECK();
+    return MOBI_OK;
+}
+
+int launch_pack_planes(mobi_layer* L, const uint64_t* planes_dev, int bits, int64_t wpr,
+                       cudaStream_t st) {
+    const int64_t n = L->out_pad * L->kblocks;
+    pack_planes_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(planes_dev, bits, wpr, L->out, L->in,
+                                                              L->out_pad, L->kblocks, L->codes8);
+    MOBI_LAUNCH_CHECK();
+    return MOBI_OK;
+}
+
+int launch_unpack_codes(const mobi_layer* L, uint8_t* codes_dev, cudaStream_t st) {
+    const int64_t n = L->out * L->kblocks * (kKBlock / 16);
+    unpack_codes_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(L->codes8, L->out, L->in, L->kblocks,
+                                                               L->E, L->b, codes_dev);
+    MOBI_LAUNCH_CHECK();
+    return MOBI_OK;
+}
+
+}  // namespace mobi

@@ -1,0 +1,169 @@
+// mobi_internal.cuh -- device layout, workspace and launcher declarations shared by the
+// MoBi-linear kernels (sm_100a).  See DESIGN.md for the layouts and their rationale.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/mobi_b200.h"
+
+namespace mobi {
+
+// ---------------------------------------------------------------------------------------------
+// Geometry of the device weight layout ("tiled merged codes").
+//   kRowTile rows x kKBlock input columns form one 8 KiB block; inside a block the bytes are
+//   ordered [half h (2)][chunk c (2)][row r (128)][16 codes], so the 32 lanes of a warp that
+//   own 32 consecutive rows read 512 contiguous bytes per 16-byte load (coalesced), and each
+//   thread receives the 32 consecutive K-codes of its row that it dequantizes into one TMEM
+//   lane.  Rows are padded to kRowTile, K to kKBlock (padding codes are 0; padded X columns
+//   are 0, so padded weights never contribute).
+// ---------------------------------------------------------------------------------------------
+constexpr int kRowTile = 128;
+constexpr int kKBlock = 64;
+constexpr int kBlockBytes = kRowTile * kKBlock;  // 8192
+constexpr int kBucketAlign = 16;                 // bucket starts in the permuted token order
+constexpr int kTokTile = 256;                    // tokens per GEMM tile (MMA N <= 256)
+constexpr int kMaxBuckets = 1 << (MOBI_MAX_SLICES - 1);  // 8 masks (slice-1 bit always set)
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+
+// byte offset of code (row R, col k) in the tiled layout
+__host__ __device__ inline int64_t code_offset(int64_t R, int64_t k, int64_t kblocks) {
+    int64_t rt = R / kRowTile, r = R % kRowTile;
+    int64_t kb = k / kKBlock, kk = k % kKBlock;
+    int64_t h = kk / 32, c = (kk % 32) / 16, b = kk % 16;
+    return (rt * kblocks + kb) * kBlockBytes + ((h * 2 + c) * kRowTile + r) * 16 + b;
+}
+
+// One GEMM tile of the token dimension: a run of <= kTokTile permuted rows of one bucket.
+struct TokTile {
+    int32_t row0;   // first permuted row
+    int32_t n;      // valid rows (1..kTokTile)
+    int32_t mask;   // bucket slice mask (bit0 always set)
+    int32_t pad;
+};
+
+// Per-mask dequant constants (uniform b-bit slices): W = S*INT_m + C with
+//   INT_m = merged & maskbyte[m],  S = s / 2^P,  C = s*K[m]/2^(P+1) - s*z
+struct MaskTable {
+    uint32_t maskword[kMaxBuckets * 2];  // maskbyte replicated x4, indexed by mask value (<16)
+    float kc[kMaxBuckets * 2];           // K[m] / 2^(P+1)
+    float inv_2p;                        // 1 / 2^P
+};
+
+}  // namespace mobi
+
+struct mobi_layer {
+    int device = 0;
+    int64_t out = 0, in = 0, gs = 0, G = 0;  // G = groups per row
+    int32_t E = 0, b = 0;                    // slices, bits per slice
+    int32_t nr = 0;                          // routed slices = E-1
+    int64_t h = 0;                           // router hidden
+    int64_t out_pad = 0, in_pad = 0, kblocks = 0, h_pad = 0;
+    int64_t group_shift = -1;                // log2(gs) when gs is a power of two >= 32
+    bool single_group = false;               // gs >= in: one group per row
+
+    // device weights
+    uint8_t* codes8 = nullptr;        // tiled merged codes [out_pad/128][kblocks][8192]
+    float* gscale = nullptr;          // [out][G]  s
+    float* gsz = nullptr;             // [out][G]  s*z
+    __nv_bfloat16* w1t = nullptr;     // [h_pad][in_pad] bf16, K-major (router B operand)
+    float* b1 = nullptr;              // [h_pad]
+    float* w2 = nullptr;              // [h_pad][nr]
+    float* b2 = nullptr;              // [nr]
+    mobi::MaskTable mtab{};
+
+    // workspace (sized for ws_T tokens)
+    int64_t ws_T = -1;
+    int64_t tpad_max = 0, max_tiles = 0, htiles = 0;
+    float* s_part = nullptr;   // [htiles][T][nr]
+    float* scores = nullptr;   // [T][nr]
+    uint8_t* masks = nullptr;  // [T]
+    int32_t* perm = nullptr;   // [tpad_max] permuted row -> token (-1 pad)
+    int32_t* inverse = nullptr;// [T]
+    int32_t* cperm = nullptr;  // [T] compact (unpadded) permutation
+    float* escale = nullptr;   // [tpad_max] per-row power-of-two scale
+    __half* xperm = nullptr;   // [tpad_max][in_pad] fp16 permuted, scaled activations
+    mobi::TokTile* tiles = nullptr;  // [max_tiles]
+    int32_t* meta = nullptr;   // [0]=n_tiles [1]=total padded rows [2..2+16) bucket counts
+    void* x_dev = nullptr;     // staging for mobi_forward_host
+    void* y_dev = nullptr;
+    void* h_x = nullptr;       // pinned host staging
+    void* h_y = nullptr;
+    int64_t h_cap = 0;
+    CUtensorMap* tmap_x = nullptr;  // host copies, rebuilt when the workspace changes
+    int32_t last_launches = 0;
+    int64_t device_bytes = 0;
+};
+
+namespace mobi {
+
+// error plumbing (abi.cu)
+int set_error(int code, const std::string& msg);
+#define MOBI_CUDA(call)                                                                       \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return ::mobi::set_error(MOBI_ERUNTIME, std::string(#call) + ": " +              \
+                                                         cudaGetErrorString(e_));              \
+    } while (0)
+#define MOBI_LAUNCH_CHECK()                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                                  \
+        if (e_ != cudaSuccess)                                                                \
+            return ::mobi::set_error(MOBI_ERUNTIME, std::string("kernel launch: ") +         \
+                                                         cudaGetErrorString(e_));              \
+    } while (0)
+
+// ---- launchers (each returns MOBI_OK or an error code; each counts its launches) ----
+// layer.cu
+int launch_pack_codes(mobi_layer* L, const uint8_t* codes_dev, cudaStream_t st);
+int launch_pack_planes(mobi_layer* L, const uint64_t* planes_dev, int bits, int64_t wpr,
+                       cudaStream_t st);
+int launch_unpack_codes(const mobi_layer* L, uint8_t* codes_dev, cudaStream_t st);
+// router.cu
+int launch_router(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);
+// bucket.cu
+int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks,
+                  float* scores_out, uint8_t* masks_out, int32_t* cperm_out,
+                  int32_t* inverse_out, int32_t* counts_out, cudaStream_t st);
+int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);
+// gemm_tc.cu (tcgen05) / gemm_simt.cu (reference kernel, tests only)
+int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
+int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
+// decompose.cu
+int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,
+                     int32_t E, double gamma, uint8_t* codes, double* scale, double* zero,
+                     int64_t* clamp_counts_host, cudaStream_t st);
+
+// ---- small device helpers ----
+__device__ __forceinline__ float silu_f(float x) {
+    // common.hpp:125-133 sigmoid with the sign split; silu = x * sigmoid(x)
+    float s = x >= 0.f ? 1.f / (1.f + expf(-x)) : expf(x) / (1.f + expf(x));
+    return x * s;
+}
+
+// Dequantize 4 merged codes (one 32-bit word) of a bucket with mask word `mw` into two half2
+// words (elements 0,1 and 2,3):  W = S * (codes & mask) + C, exact INT->fp16 via the 0x6400
+// magic (1024 + n), exact subtraction of 1024, one HFMA2.
+__device__ __forceinline__ void dequant4(uint32_t codes4, uint32_t mw, __half2 S2, __half2 C2,
+                                         uint32_t& w01, uint32_t& w23) {
+    const uint32_t v = codes4 & mw;
+    uint32_t lo = __byte_perm(v, 0x64646464u, 0x4140);
+    uint32_t hi = __byte_perm(v, 0x64646464u, 0x4342);
+    const __half2 k1024 = __half2half2(__ushort_as_half((unsigned short)0x6400));
+    __half2 a = __hsub2(*reinterpret_cast<__half2*>(&lo), k1024);
+    __half2 c = __hsub2(*reinterpret_cast<__half2*>(&hi), k1024);
+    a = __hfma2(a, S2, C2);
+    c = __hfma2(c, S2, C2);
+    w01 = *reinterpret_cast<uint32_t*>(&a);
+    w23 = *reinterpret_cast<uint32_t*>(&c);
+}
+
+}  // namespace mobi
