@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""MoBi-linear benchmark (BASELINE.json metric: tokens/s at LLaMA3-8B shapes vs avg bits,
+% of tensor/HBM roofline).
+
+  python bench.py [--gpus N --steps K --warmup W] [--out 4096 --in 4096 --tokens 2048 --target-bits 3]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N     (token-sharded, weak scaling)
+  python bench.py --impl reference ...   (the reference's own CPU implementation, oracle/_ref)
+
+Default workload (configs[1]): LLaMA3-8B q_proj 4096x4096, T=2048 tokens per GPU per step,
+3.0 average bits (rho = 1/6 of the pooled routed scores above delta), router h = in/4, group 128,
+slices 2+2+2+2.  Synthetic data: W ~ N(0, 0.02^2) sliced by the GPU decompose (bit-exact with the
+reference), router per RouterState::init with w2 = 0.3 N(0,1), b2 = 0.1 N(0,1) (tools/mobi.cpp:211),
+X per gen_calibset (N(0,1), 5% channels x8).
+
+A step = one full layer forward (route -> bucket -> gather -> tcgen05 GEMM + un-permute) over one
+batch of T tokens.  L2 hygiene: the step cycles through a ring of R independent (layer, X, Y)
+triples whose combined footprint exceeds 2x the 126 MB L2, so no step finds its inputs in L2.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+L2_BYTES = 126 * 1024 * 1024
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="mobi", choices=["mobi", "reference"])
+    p.add_argument("--out", type=int, default=4096)
+    p.add_argument("--in", dest="inn", type=int, default=4096)
+    p.add_argument("--tokens", type=int, default=2048)
+    p.add_argument("--target-bits", type=float, default=3.0)
+    p.add_argument("--hidden", type=int, default=0, help="router hidden width (0 = in/4, the reference default)")
+    p.add_argument("--group-size", type=int, default=128)
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--cpu-threads", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--ring", type=int, default=0)
+    return p.parse_args()
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return d, "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# workload
+# ------------------------------------------------------------------------------------------
+def make_layer(args, dev, seed):
+    from paper_2602_20191_b200 import MobiLayer, decompose
+    g = torch.Generator(device=dev).manual_seed(seed)
+    out, inn, gs = args.out, args.inn, args.group_size
+    h = args.hidden if args.hidden else max(1, inn // 4)
+    w = torch.randn((out, inn), generator=g, device=dev, dtype=torch.float64) * 0.02
+    codes, scale, zero, _ = decompose(w, gs, [2, 2, 2, 2], 4.0)
+    del w
+    w1 = torch.randn((inn, h), generator=g, device=dev, dtype=torch.float64) / math.sqrt(inn)
+    w2 = torch.randn((h, 3), generator=g, device=dev, dtype=torch.float64) * 0.3
+    b2 = torch.randn(3, generator=g, device=dev, dtype=torch.float64) * 0.1
+    host = dict(codes=codes.cpu().numpy(), scale=scale.cpu().numpy(), zero=zero.cpu().numpy(),
+                w1=w1.cpu().numpy(), b1=np.zeros(h), w2=w2.cpu().numpy(), b2=b2.cpu().numpy())
+    layer = MobiLayer.from_stack(host["codes"], [2, 2, 2, 2], host["scale"], host["zero"], gs, host["w1"],
+                                 host["b1"], host["w2"], host["b2"], device=dev.index)
+    return layer, host
+
+
+def make_x(args, dev, seed):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    x = torch.randn((args.tokens, args.inn), generator=g, device=dev)
+    n_out = max(1, round(0.05 * args.inn))
+    ch = torch.randperm(args.inn, generator=g, device=dev)[:n_out]
+    x[:, ch] *= 8.0
+    return x.to(torch.bfloat16)
+
+
+def gemm_flops(args):
+    # the kernel folds a bucket's active slices into one effective weight (one MMA per k-step),
+    # so its algorithmic work is the dense contraction 2*T*in*out
+    return 2.0 * args.tokens * args.inn * args.out
+
+
+def router_flops(args):
+    h = args.hidden if args.hidden else max(1, args.inn // 4)
+    return 2.0 * args.tokens * (args.inn * h + 3 * h)
+
+
+# ------------------------------------------------------------------------------------------
+# CPU baseline: the reference itself (oracle/_ref), row-sharded across host threads
+# ------------------------------------------------------------------------------------------
+def ref_threads(args):
+    return args.cpu_threads or max(1, min(os.cpu_count() or 1, 64))
+
+
+def run_reference_steps(host, x_bf16_rows, delta, args, steps, threads):
+    """Each step: the reference's score -> gate_hard(delta) -> forward_elastic on the token sample."""
+    from oracle import oracle as O
+    ref = O.reference()
+    f = ref.lib.ref_layer_forward_rowsharded
+    P = lambda a: a.ctypes.data_as(C.c_void_p)
+    x = np.ascontiguousarray(x_bf16_rows, np.float64)
+    T = x.shape[0]
+    codes = np.ascontiguousarray(host["codes"])
+    sb = np.array([2, 2, 2, 2], np.int32)
+    arrs = {k: np.ascontiguousarray(host[k], np.float64) for k in ("scale", "zero", "w1", "b1", "w2", "b2")}
+    h = arrs["w1"].shape[1]
+    y = np.zeros((T, args.out))
+    g = np.zeros((T, 3))
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        rc = f(P(x), C.c_int64(T), C.c_int64(args.inn), P(codes), C.c_int32(4), P(sb), P(arrs["scale"]),
+               P(arrs["zero"]), C.c_int64(args.out), C.c_int64(args.group_size), C.c_int64(h), P(arrs["w1"]),
+               P(arrs["b1"]), P(arrs["w2"]), P(arrs["b2"]), C.c_double(delta), C.c_int(threads), P(g), P(y))
+        times.append(time.perf_counter() - t0)
+        if rc != 0:
+            raise RuntimeError(ref.lib.ref_last_error().decode())
+    return times, y, g
+
+
+def cpu_sample_tokens(args):
+    return min(args.tokens, 16)
+
+
+# ------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    config = {"workload": f"llama3-8b linear {args.out}x{args.inn} (q/o proj) MoBi 2+2+2+2 slices, "
+                          f"T={args.tokens} tokens/GPU/step, target {args.target_bits} avg bits, router h=in/4",
+              "out": args.out, "in": args.inn, "tokens_per_gpu": args.tokens, "target_bits": args.target_bits,
+              "group_size": args.group_size, "router_hidden": args.hidden or args.inn // 4,
+              "parallelism": f"token-sharded x{world}" if world > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        return main_reference(args, rank, world, dev, config)
+
+    from paper_2602_20191_b200 import calibrate_threshold, ratio_from_target_bits, avg_bits_from_masks
+    rho = ratio_from_target_bits(args.target_bits, [2, 2, 2, 2])
+    per_step_bytes = args.out * args.inn + 2 * args.tokens * args.inn * 2 + args.tokens * args.out * 2
+    R = args.ring or max(1, math.ceil(2 * L2_BYTES / per_step_bytes))
+    R = min(R, 16)
+    ring = []
+    for i in range(R):
+        layer, host = make_layer(args, dev, args.seed * 1000 + i)  # identical on every rank (replicas)
+        x = make_x(args, dev, args.seed * 7919 + 104729 * rank + i)
+        s = layer.score(x)
+        delta = calibrate_threshold(s, rho)
+        layer.reserve(args.tokens)
+        y = torch.empty((args.tokens, args.out), dtype=torch.bfloat16, device=dev)
+        ring.append(dict(layer=layer, host=host, x=x, y=y, delta=delta))
+    config["l2"] = f"ring of {R} independent layer/X/Y sets ({R * per_step_bytes / 2**20:.0f} MiB > 2x L2)"
+
+    def step(i, masks=False):
+        r = ring[i % R]
+        return r["layer"].forward(r["x"], r["delta"], y=r["y"], return_masks=masks)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    for r in ring:
+        r["layer"].profile(True)
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.05)
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(st)
+    for i in range(args.steps):
+        step(i)
+        launches += ring[i % R]["layer"].last_launches()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    # per-kernel device time inside the timed region
+    kern = {k: [0.0, 0] for k in ("router", "bucket", "gather", "gemm")}
+    for r in ring:
+        for k, (t_ms, n) in r["layer"].profile_read().items():
+            kern[k][0] += t_ms
+            kern[k][1] += n
+        r["layer"].profile(False)
+    tokens_total = args.tokens * args.steps * world
+    value = tokens_total / (ms / 1e3)
+    # realized bits on the last ring entry
+    _, m = step(0, masks=True)
+    realized = avg_bits_from_masks(m, [2, 2, 2, 2])
+    counts = torch.bincount(m.to(torch.int64), minlength=16).cpu().tolist()
+    config["realized_avg_bits"] = round(realized, 4)
+    config["buckets"] = {str(i): c for i, c in enumerate(counts) if c}
+
+    pk, pk_src = peaks()
+    gemm_ms = kern["gemm"][0] / max(1, kern["gemm"][1])
+    router_ms = kern["router"][0] / max(1, kern["router"][1])
+    peak_tf = pk.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+    achieved = gemm_flops(args) / (gemm_ms * 1e-3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "gemm_traffic.json"
+    if tf.exists():
+        d = json.loads(tf.read_text())
+        if d.get("out") == args.out and d.get("in") == args.inn and d.get("tokens") == args.tokens:
+            traffic = d.get("dram_bytes_per_launch")
+    roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": round(achieved / peak_tf, 4), "traffic": traffic,
+                "kernel": "mobi_gemm_tc_kernel", "flops_per_launch": gemm_flops(args),
+                "flops_basis": "dense 2*T*in*out (bucket slices folded into one effective weight per MMA)",
+                "peak_source": f"{pk_src} burst bf16 (MEASURED_PEAKS.json bf16_tflops)"}
+    hbm = pk.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    h_w = (args.hidden or args.inn // 4)
+    router_bytes = args.inn * h_w * 2 + args.tokens * args.inn * 2
+    kernels = {k: {"ms_per_launch": round(v[0] / max(1, v[1]), 5), "launches": v[1],
+                   "share": round(v[0] / max(1e-9, sum(x[0] for x in kern.values())), 4)} for k, v in kern.items()}
+    kernels["router"]["tflops"] = round(router_flops(args) / (router_ms * 1e-3) / 1e12, 2) if router_ms else None
+    kernels["router"]["frac_tensor"] = round(kernels["router"]["tflops"] / peak_tf, 4) if router_ms else None
+    kernels["gather"]["gbs"] = round(2 * args.tokens * args.inn * 2 / (kernels["gather"]["ms_per_launch"] * 1e-3) / 1e9, 1) if kern["gather"][1] else None
+
+    # ---------------- e2e through the public host-buffer API ----------------
+    e2e = None
+    if not args.no_e2e:
+        r = ring[0]
+        xh = r["x"].cpu().pin_memory()
+        yh = torch.empty((args.tokens, args.out), dtype=torch.bfloat16).pin_memory()
+        mh = torch.empty(args.tokens, dtype=torch.uint8).pin_memory()
+        for _ in range(3):
+            r["layer"].forward_host(xh, r["delta"], y_host=yh, masks_host=mh)
+        if dist:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        k2 = max(3, min(args.steps, 50))
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            r["layer"].forward_host(xh, r["delta"], y_host=yh, masks_host=mh)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([wall], device=dev, dtype=torch.float64)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            wall = float(t.item())
+        e2e = {"value": round(args.tokens * k2 * world / wall, 1), "unit": "tokens/s",
+               "h2d_bytes_per_step": args.tokens * args.inn * 2,
+               "d2h_bytes_per_step": args.tokens * args.out * 2 + args.tokens,
+               "steps": k2, "api": "mobi_forward_host (pinned host bf16 in/out, synchronous)"}
+
+    # ---------------- CPU baseline (rank 0, N=1): the reference itself ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            thr = ref_threads(args)
+            ts = cpu_sample_tokens(args)
+            r = ring[0]
+            xs = r["x"][:ts].double().cpu().numpy()
+            times, _, _ = run_reference_steps(r["host"], xs, r["delta"], args, 2, thr)
+            cpu = {"value": round(ts / min(times), 3), "unit": "tokens/s", "cores": thr, "kind": "reference",
+                   "sample": f"{ts} tokens of the same layer/X/delta, reference score->gate_hard->forward_elastic "
+                             f"(oracle/_ref, -O3), forward row-sharded over {thr} threads, best of 2 calls"}
+        except Exception as ex:  # the baseline is reported, never a reason to fail the bench
+            cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}
+
+    line = {"metric": "MoBi-linear tokens/s at LLaMA3-8B shapes vs avg bits; % of TC/HBM roofline",
+            "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp16 operands (exact bf16->fp16 rescale), fp32 accumulate, bf16 out",
+            "data": "synthetic (W~N(0,0.02^2) GPU-decomposed, random-init router, calibset-style X)",
+            "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks, "kernels": kernels,
+            "hbm_peak_gbs": hbm}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        tdist.destroy_process_group()
+
+
+def main_reference(args, rank, world, dev, config):
+    """--impl reference: the reference's own CPU implementation on the box's host cores."""
+    if rank != 0:
+        return
+    from paper_2602_20191_b200 import calibrate_threshold, ratio_from_target_bits
+    rho = ratio_from_target_bits(args.target_bits, [2, 2, 2, 2])
+    layer, host = make_layer(args, dev, args.seed * 1000)
+    x = make_x(args, dev, args.seed * 7919)
+    delta = calibrate_threshold(layer.score(x), rho)
+    thr = ref_threads(args)
+    ts = cpu_sample_tokens(args)
+    xs = x[:ts].double().cpu().numpy()
+    run_reference_steps(host, xs, delta, args, args.warmup, thr)
+    t0 = time.perf_counter()
+    times, _, _ = run_reference_steps(host, xs, delta, args, args.steps, thr)
+    wall = time.perf_counter() - t0
+    value = ts * args.steps / wall
+    sample = (f"{ts} tokens per step of the same layer ({args.out}x{args.inn}, delta for {args.target_bits} bits); "
+              f"reference score->gate_hard->forward_elastic, forward row-sharded over {thr} threads")
+    print(json.dumps({"impl": "reference", "metric": "MoBi-linear tokens/s at LLaMA3-8B shapes vs avg bits; % of TC/HBM roofline",
+                      "value": round(value, 3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 3),
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic (same generator as the GPU arm)", "config": config,
+                      "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": thr, "kind": "reference",
+                                       "sample": sample},
+                      "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}))
+
+
+if __name__ == "__main__":
+    main()

@@ -142,6 +142,15 @@ MOBI_API int mobi_decompose(const double* w, int64_t out, int64_t in, int64_t gr
                    const int32_t* slice_bits, int32_t n_slices, double gamma, uint8_t* codes,
                    double* scale, double* zero, int64_t* clamp_counts, void* stream);
 
+/* Per-kernel device timing (CUDA events recorded on the launch stream around every kernel the
+ * layer launches).  enable=1 starts a fresh accumulation; mobi_layer_profile_read synchronises
+ * and returns, per kernel id (0 router, 1 bucket, 2 gather, 3 gemm), the summed milliseconds and
+ * the number of launches since enabling. */
+#define MOBI_PROF_KERNELS 4
+MOBI_API int mobi_layer_profile(mobi_layer_t layer, int enable);
+MOBI_API int mobi_layer_profile_read(mobi_layer_t layer, double* ms /*[MOBI_PROF_KERNELS]*/,
+                                     int64_t* launches /*[MOBI_PROF_KERNELS]*/);
+
 /* Number of kernels the last forward on this layer launched (for launch accounting). */
 MOBI_API int mobi_layer_last_launches(mobi_layer_t layer, int32_t* launches);
 

@@ -322,4 +322,64 @@ int ref_layer_forward_threaded(const double* x, int64_t T, int64_t in, const uin
     });
 }
 
+// Same sequence, sharded for small token counts: score is token-sharded, forward_elastic is
+// ROW-sharded -- each thread runs the reference forward_elastic on the SliceStack of a block of
+// output rows (groups never span rows, qcore.hpp:30-34, so the split is exact and the output
+// columns are bit-identical to the unsharded call).  This amortises the reference's per-call
+// re-dequantization (router.hpp:115-120) across threads.
+int ref_layer_forward_rowsharded(const double* x, int64_t T, int64_t in, const uint8_t* codes,
+                                 int32_t n_slices, const int32_t* slice_bits, const double* scale,
+                                 const double* zero, int64_t out, int64_t gs, int64_t h,
+                                 const double* w1, const double* b1, const double* w2,
+                                 const double* b2, double delta, int threads, double* gates_out,
+                                 double* y) {
+    return guard([&] {
+        const int64_t nr = n_slices - 1;
+        const int64_t gpr = (in + gs - 1) / gs;
+        router::RouterState rs = router_of(in, h, nr, w1, b1, w2, b2);
+        Matrix xs = mat(x, T, in);
+        // score, token-sharded
+        Matrix g(static_cast<std::size_t>(T), static_cast<std::size_t>(nr));
+        {
+            int nt = std::max(1, std::min<int>(threads, static_cast<int>(T)));
+            std::vector<std::thread> pool;
+            for (int w = 0; w < nt; ++w)
+                pool.emplace_back([&, w] {
+                    int64_t t0 = T * w / nt, t1 = T * (w + 1) / nt;
+                    if (t1 <= t0) return;
+                    Matrix s = router::score(mat(x + t0 * in, t1 - t0, in), rs);
+                    Matrix gg = router::gate_hard(s, delta);
+                    std::memcpy(g.data() + t0 * nr, gg.data(), sizeof(double) * gg.size());
+                });
+            for (auto& t : pool) t.join();
+        }
+        if (gates_out) std::memcpy(gates_out, g.data(), sizeof(double) * g.size());
+        // forward_elastic, row-sharded over sub-stacks
+        int nt = std::max(1, std::min<int>(threads, static_cast<int>(out)));
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(static_cast<std::size_t>(nt));
+        for (int w = 0; w < nt; ++w)
+            pool.emplace_back([&, w] {
+                try {
+                    int64_t r0 = out * w / nt, r1 = out * (w + 1) / nt, nrow = r1 - r0;
+                    if (nrow <= 0) return;
+                    std::vector<uint8_t> sub(static_cast<std::size_t>(n_slices * nrow * in));
+                    for (int32_t e = 0; e < n_slices; ++e)
+                        std::memcpy(sub.data() + e * nrow * in, codes + e * out * in + r0 * in,
+                                    static_cast<std::size_t>(nrow * in));
+                    slicer::SliceStack st = stack_of(sub.data(), n_slices, slice_bits, nrow, in, gs,
+                                                     scale + r0 * gpr, zero + r0 * gpr);
+                    Matrix ys = router::forward_elastic(xs, st, g, router::GateMode::kHard);
+                    for (int64_t t = 0; t < T; ++t)
+                        std::memcpy(y + t * out + r0, ys.data() + t * nrow, sizeof(double) * nrow);
+                } catch (const std::exception& e) {
+                    errs[static_cast<std::size_t>(w)] = e.what();
+                }
+            });
+        for (auto& t : pool) t.join();
+        for (auto& e : errs)
+            if (!e.empty()) throw std::invalid_argument(e);
+    });
+}
+
 }  // extern "C"

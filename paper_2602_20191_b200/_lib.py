@@ -52,6 +52,8 @@ _SIGS = {
     "mobi_decompose": [_p, _i64, _i64, _i64, _p, _i32, _f64, _p, _p, _p, _p, _p],
     "mobi_layer_last_launches": [_p, C.POINTER(_i32)],
     "mobi_debug_set_impl": [C.c_int],
+    "mobi_layer_profile": [_p, C.c_int],
+    "mobi_layer_profile_read": [_p, _p, _p],
 }
 
 _lib = None

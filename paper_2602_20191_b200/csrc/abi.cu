@@ -247,6 +247,48 @@ struct DeviceGuard {
     }
 };
 
+// ---- profiling: event pairs around launches, resolved when the pool wraps or on read ----
+constexpr size_t kEvPool = 4096;
+
+void prof_resolve(mobi_layer* L) {
+    if (L->ev_marks.empty()) return;
+    cudaEventSynchronize(L->ev_pool[L->ev_marks.back().second.second]);
+    for (auto& m : L->ev_marks) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, L->ev_pool[m.second.first], L->ev_pool[m.second.second]) == cudaSuccess) {
+            L->prof_ms[m.first] += ms;
+            L->prof_n[m.first] += 1;
+        }
+    }
+    L->ev_marks.clear();
+    L->ev_next = 0;
+}
+
+int prof_event(mobi_layer* L) {
+    if (L->ev_next >= L->ev_pool.size()) prof_resolve(L);
+    return (int)L->ev_next++;
+}
+
+struct ProfScope {
+    mobi_layer* L;
+    int id, a = -1;
+    cudaStream_t st;
+    ProfScope(mobi_layer* L_, int id_, cudaStream_t st_) : L(L_), id(id_), st(st_) {
+        if (L->prof) {
+            a = prof_event(L);
+            cudaEventRecord(L->ev_pool[a], st);
+        }
+    }
+    ~ProfScope() {
+        if (L->prof && a >= 0) {
+            int b = prof_event(L);
+            if (b < a) return;  // pool wrapped between the pair: drop this sample
+            cudaEventRecord(L->ev_pool[b], st);
+            L->ev_marks.push_back({id, {a, b}});
+        }
+    }
+};
+
 int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_t* given_masks, void* y,
               uint8_t* masks_out, cudaStream_t st) {
     CHECK_ARG(T >= 0, "forward_elastic: negative token count " << T);
@@ -255,10 +297,21 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
-    if (!given_masks && (rc = launch_router(L, xb, T, st))) return rc;
-    if ((rc = launch_bucket(L, T, delta, given_masks, nullptr, masks_out, nullptr, nullptr, nullptr, st))) return rc;
-    if ((rc = launch_gather(L, xb, T, st))) return rc;
+    if (!given_masks) {
+        ProfScope p(L, 0, st);
+        if ((rc = launch_router(L, xb, T, st))) return rc;
+    }
+    {
+        ProfScope p(L, 1, st);
+        if ((rc = launch_bucket(L, T, delta, given_masks, nullptr, masks_out, nullptr, nullptr, nullptr, st)))
+            return rc;
+    }
+    {
+        ProfScope p(L, 2, st);
+        if ((rc = launch_gather(L, xb, T, st))) return rc;
+    }
     __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
+    ProfScope p(L, 3, st);
     if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
     return launch_gemm_tc(L, yb, T, st);
 }
@@ -315,6 +368,7 @@ int mobi_layer_destroy(mobi_layer_t L) {
     if (L->y_dev) cudaFree(L->y_dev);
     if (L->h_x) cudaFreeHost(L->h_x);
     if (L->h_y) cudaFreeHost(L->h_y);
+    for (auto& e : L->ev_pool) cudaEventDestroy(e);
     delete L;
     return MOBI_OK;
 }
@@ -507,6 +561,35 @@ int mobi_decompose(const double* w, int64_t out, int64_t in, int64_t group_size,
     CHECK_ARG(w && codes && scale && zero && slice_bits, "decompose: null argument");
     return launch_decompose(w, out, in, group_size, slice_bits, n_slices, gamma, codes, scale, zero, clamp_counts,
                             S(stream));
+}
+
+int mobi_layer_profile(mobi_layer_t L, int enable) {
+    CHECK_ARG(L, "null layer");
+    DeviceGuard g(L->device);
+    if (L->ev_pool.empty() && enable) {
+        L->ev_pool.resize(kEvPool);
+        for (auto& e : L->ev_pool) MOBI_CUDA(cudaEventCreate(&e));
+    }
+    if (L->prof) prof_resolve(L);
+    L->ev_marks.clear();
+    L->ev_next = 0;
+    for (int i = 0; i < MOBI_PROF_KERNELS; ++i) {
+        L->prof_ms[i] = 0.0;
+        L->prof_n[i] = 0;
+    }
+    L->prof = enable != 0;
+    return MOBI_OK;
+}
+
+int mobi_layer_profile_read(mobi_layer_t L, double* ms, int64_t* launches) {
+    CHECK_ARG(L, "null layer");
+    DeviceGuard g(L->device);
+    prof_resolve(L);
+    for (int i = 0; i < MOBI_PROF_KERNELS; ++i) {
+        if (ms) ms[i] = L->prof_ms[i];
+        if (launches) launches[i] = L->prof_n[i];
+    }
+    return MOBI_OK;
 }
 
 int mobi_layer_last_launches(mobi_layer_t L, int32_t* launches) {

@@ -9,6 +9,8 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/mobi_b200.h"
 
@@ -100,6 +102,13 @@ struct mobi_layer {
     CUtensorMap* tmap_x = nullptr;  // host copies, rebuilt when the workspace changes
     int32_t last_launches = 0;
     int64_t device_bytes = 0;
+    // profiling: event pairs around each launch, resolved lazily
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<int, std::pair<int, int>>> ev_marks;  // (kernel id, (start ev, stop ev))
+    size_t ev_next = 0;
+    double prof_ms[4] = {0, 0, 0, 0};
+    int64_t prof_n[4] = {0, 0, 0, 0};
 };
 
 namespace mobi {

@@ -120,6 +120,19 @@ class MobiLayer:
         check(lib().mobi_layer_last_launches(self._h, C.byref(n)))
         return n.value
 
+    KERNELS = ("router", "bucket", "gather", "gemm")
+
+    def profile(self, enable: bool = True):
+        """Start (or stop) per-kernel CUDA-event timing on the launch stream."""
+        check(lib().mobi_layer_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{kernel: (total_ms, launches)} accumulated since profile(True)."""
+        ms = np.zeros(4, np.float64)
+        n = np.zeros(4, np.int64)
+        check(lib().mobi_layer_profile_read(self._h, ms.ctypes.data, n.ctypes.data))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.KERNELS)}
+
     def export_router(self):
         w1 = np.zeros((self.inn, self.hidden), np.float32)
         b1 = np.zeros(self.hidden, np.float32)
