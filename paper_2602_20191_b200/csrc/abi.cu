@@ -234,6 +234,11 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L) {
     return MOBI_OK;
 }
 
+int route_scores(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st) {
+    if (g_impl_override != 1 && router_tc_supported(L, x)) return launch_router_tc(L, x, T, st);
+    return launch_router(L, x, T, st);
+}
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
@@ -299,7 +304,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
     if (!given_masks) {
         ProfScope p(L, 0, st);
-        if ((rc = launch_router(L, xb, T, st))) return rc;
+        if ((rc = route_scores(L, xb, T, st))) return rc;
     }
     {
         ProfScope p(L, 1, st);
@@ -364,6 +369,7 @@ int mobi_layer_destroy(mobi_layer_t L) {
     dfree(L->b1);
     dfree(L->w2);
     dfree(L->b2);
+    if (L->tmap_w1) delete L->tmap_w1;
     if (L->x_dev) cudaFree(L->x_dev);
     if (L->y_dev) cudaFree(L->y_dev);
     if (L->h_x) cudaFreeHost(L->h_x);
@@ -429,7 +435,7 @@ int mobi_score(mobi_layer_t L, const void* x, int64_t T, float* scores, void* st
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     L->last_launches = 0;
-    if ((rc = launch_router(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
+    if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
     return launch_bucket(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream));
 }
 
@@ -442,7 +448,7 @@ int mobi_route(mobi_layer_t L, const void* x, int64_t T, float delta, float* sco
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     L->last_launches = 0;
-    if ((rc = launch_router(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
+    if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
     return launch_bucket(L, T, delta, nullptr, scores, masks, perm, inverse, bucket_count, S(stream));
 }
 

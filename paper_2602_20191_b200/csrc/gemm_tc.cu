@@ -8,13 +8,13 @@
 // so slice e is read and contracted only for tiles whose bucket contains e, and one MMA per
 // k-step covers all of a bucket's active slices.
 //
-// Roles (one persistent CTA per SM, 448 threads):
+// Roles (one persistent CTA per SM, 704 threads):
 //   warp 0      TMA producer: X_perm tile [256 tokens x 64 k] fp16, 128-byte swizzle -> smem stage
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-9   dequantizers: each thread owns one weight row (= one TMEM lane) and 32 k of the
-//               64-k block; coalesced 16-byte code loads -> fp16 W_m -> tcgen05.st into the A
-//               stage in TMEM (A operand never touches shared memory)
-//   warps 10-13 epilogue: tcgen05.ld the fp32 accumulator, x 2^e row scale, bf16, scatter
+//   warps 2-17  dequantizers: each thread owns one weight row (= one TMEM lane) and 16 k of the
+//               64-k block; coalesced 16-byte code loads (3 k-blocks in flight) -> fp16 W_m ->
+//               tcgen05.st into the A stage in TMEM (A operand never touches shared memory)
+//   warps 18-21 epilogue: tcgen05.ld the fp32 accumulator, x 2^e row scale, bf16, scatter
 //               Y[perm[i], r] (the un-permute, bitplane.hpp:171-172, fused)
 // MMA: M=128 weight rows (TMEM lanes), N=tile tokens (<=256, multiple of 16), K=16 per
 // instruction, D fp32 in TMEM columns [0,256); A stages at columns 256 + 32*s.
@@ -27,7 +27,8 @@ namespace {
 using namespace sm100;
 
 constexpr int NSTAGE = 4;
-constexpr int kThreads = 448;
+constexpr int kDqWarps = 16;                       // 4 per TMEM lane quarter
+constexpr int kThreads = 32 * (2 + kDqWarps + 4);  // TMA, MMA, dequant, epilogue
 constexpr int kStageBytes = kTokTile * kKBlock * 2;  // 32 KiB
 constexpr int kAccCols = 256;
 constexpr int kACol0 = 256;
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1);
-            mbar_init(&full_a[s], 8);
+            mbar_init(&full_a[s], kDqWarps);
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
@@ -127,10 +128,11 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 __syncwarp();
             }
         }
-    } else if (warp < 10) {
+    } else if (warp < 2 + kDqWarps) {
         // ---------------- dequantizers ----------------
-        const int q = warp % 4;         // TMEM lane quarter this warp may access
-        const int hh = (warp - 2) / 4;  // which 32-k half of the 64-k block
+        // warp -> (TMEM lane quarter q, 16-code chunk j of the 64-k block); 4 warps per quarter
+        const int q = warp % 4;
+        const int j = (warp - 2) / 4;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
@@ -140,43 +142,59 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             const bool rv = R < p.out;
             const uint32_t mw = p.mt.maskword[tt.mask];
             const float kc = p.mt.kc[tt.mask];
-            const uint8_t* cbase = p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes +
-                                   ((hh * 2) * kRowTile + 32 * q + lane) * 16;
-            uint4 c0 = *reinterpret_cast<const uint4*>(cbase);
-            uint4 c1 = *reinterpret_cast<const uint4*>(cbase + kRowTile * 16);
+            const uint8_t* cbase = p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes + (j * kRowTile + 32 * q + lane) * 16;
+            const float* srow = p.gscale + (rv ? R : 0) * p.G;
+            const float* zrow = p.gsz + (rv ? R : 0) * p.G;
+            // codes ring, 3 k-blocks ahead
+            uint4 ca = *reinterpret_cast<const uint4*>(cbase);
+            uint4 cb = kb_n > 1 ? *reinterpret_cast<const uint4*>(cbase + kBlockBytes) : ca;
+            uint4 cc = kb_n > 2 ? *reinterpret_cast<const uint4*>(cbase + 2 * kBlockBytes) : ca;
+            // group tracking without division: k = kb*64 + 16j
+            int g = 0, kin = 16 * j;
+            if (!p.single_group)
+                while (kin >= p.gs) kin -= (int)p.gs, ++g;
+            __half2 S2, C2;
+            auto group_consts = [&](int gg) {
+                const float sc = rv ? __ldg(srow + gg) : 0.f;
+                const float sz = rv ? __ldg(zrow + gg) : 0.f;
+                S2 = __float2half2_rn(sc * p.mt.inv_2p);
+                C2 = __float2half2_rn(fmaf(sc, kc, -sz));
+            };
+            group_consts(g);
+            uint32_t v[8];
+            {
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(&ca);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) dequant4(w[u], mw, S2, C2, v[2 * u], v[2 * u + 1]);
+            }
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
-                // group constants for this row and k-half
-                const int64_t k0 = (int64_t)kb * kKBlock + hh * 32;
-                float sc = 0.f, sz = 0.f;
-                if (rv) {
-                    const int64_t g = p.single_group ? 0 : k0 / p.gs;
-                    sc = __ldg(p.gscale + R * p.G + g);
-                    sz = __ldg(p.gsz + R * p.G + g);
-                }
-                const __half2 S2 = __float2half2_rn(sc * p.mt.inv_2p);
-                const __half2 C2 = __float2half2_rn(fmaf(sc, kc, -sz));
-                uint32_t v[16];
-                const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&c0);
-                const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&c1);
-#pragma unroll
-                for (int w = 0; w < 4; ++w) dequant4(w0[w], mw, S2, C2, v[2 * w], v[2 * w + 1]);
-#pragma unroll
-                for (int w = 0; w < 4; ++w) dequant4(w1[w], mw, S2, C2, v[8 + 2 * w], v[8 + 2 * w + 1]);
-                // prefetch next k-block's codes while waiting for the stage
-                if (kb + 1 < kb_n) {
-                    const uint8_t* nb = cbase + (int64_t)(kb + 1) * kBlockBytes;
-                    c0 = *reinterpret_cast<const uint4*>(nb);
-                    c1 = *reinterpret_cast<const uint4*>(nb + kRowTile * 16);
-                }
                 mbar_wait(&empty[s], ph ^ 1);
                 tc_fence_after();
-                tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
+                tmem_st8(tmem + lane_base + kACol0 + s * 32 + j * 8, v);
+                // overlap the TMEM store with the next k-block's loads and dequantization
+                ca = cb;
+                cb = cc;
+                if (kb + 3 < kb_n) cc = *reinterpret_cast<const uint4*>(cbase + (int64_t)(kb + 3) * kBlockBytes);
+                uint32_t vn[8];
+                if (kb + 1 < kb_n) {
+                    if (!p.single_group) {
+                        kin += kKBlock;
+                        bool ch = false;
+                        while (kin >= p.gs) kin -= (int)p.gs, ++g, ch = true;
+                        if (ch) group_consts(g);
+                    }
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(&ca);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) dequant4(w[u], mw, S2, C2, vn[2 * u], vn[2 * u + 1]);
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full_a[s]);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = vn[u];
             }
         }
     } else {
@@ -196,12 +214,15 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 tmem_ld32(tmem + lane_base + c0, v);
                 tmem_ld_wait();
                 const int nn = min(32, tt.n - c0);
-                for (int j = 0; j < nn; ++j) {
-                    const int row = tt.row0 + c0 + j;
-                    const int32_t src = p.perm[row];
-                    const float es = p.escale[row];
-                    if (rv && src >= 0)
-                        p.y[(int64_t)src * p.out + R] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j < nn) {
+                        const int row = tt.row0 + c0 + j;
+                        const int32_t src = p.perm[row];
+                        const float es = p.escale[row];
+                        if (rv && src >= 0)
+                            p.y[(int64_t)src * p.out + R] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
+                    }
                 }
             }
             tc_fence_before();

@@ -100,6 +100,7 @@ struct mobi_layer {
     void* h_y = nullptr;
     int64_t h_cap = 0;
     CUtensorMap* tmap_x = nullptr;  // host copies, rebuilt when the workspace changes
+    CUtensorMap* tmap_w1 = nullptr; // router w1t (fixed for the layer's lifetime)
     int32_t last_launches = 0;
     int64_t device_bytes = 0;
     // profiling: event pairs around each launch, resolved lazily
@@ -137,7 +138,10 @@ int launch_pack_planes(mobi_layer* L, const uint64_t* planes_dev, int bits, int6
                        cudaStream_t st);
 int launch_unpack_codes(const mobi_layer* L, uint8_t* codes_dev, cudaStream_t st);
 // router.cu
-int launch_router(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);
+int launch_router(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);      // CUDA cores
+// router_tc.cu (tcgen05; needs in % 8 == 0 and a 16-byte aligned X for TMA)
+bool router_tc_supported(const mobi_layer* L, const void* x);
+int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);
 // bucket.cu
 int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks,
                   float* scores_out, uint8_t* masks_out, int32_t* cperm_out,

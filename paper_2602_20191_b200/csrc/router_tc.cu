@@ -1,0 +1,208 @@
+// router_tc.cu -- K1 on tcgen05: H = X[T,in] . w1[in,h] (bf16 operands, fp32 accumulate in TMEM),
+// with silu(H + b1) . w2 fused into the epilogue (router.hpp:63-76).
+//
+// Tile: M = 128 tokens (TMEM lanes) x N = 128 hidden units, K-blocks of 64.  Both operands are
+// TMA-loaded (128-byte swizzle) into a 6-stage shared-memory ring; one thread issues the MMAs;
+// the accumulator is double-buffered in TMEM (2 x 128 columns) so the epilogue of tile i overlaps
+// the MMAs of tile i+1.  Each epilogue thread owns one token and reduces its 128 hidden units to
+// E-1 partial scores, written to s_part[hidden tile][token][j] and summed in a fixed order by the
+// bucket kernel (deterministic, no atomics).
+#include <algorithm>
+
+#include "mobi_internal.cuh"
+#include "sm100.cuh"
+
+namespace mobi {
+int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int64_t rows, int64_t cols,
+                 int box_rows);
+namespace {
+
+using namespace sm100;
+
+constexpr int RS = 6;                       // smem stages
+constexpr int RM = 128, RN = 128;           // tokens x hidden per tile
+constexpr int kAB = RM * kKBlock * 2;       // 16 KiB per operand per stage
+constexpr int kRThreads = 192;              // TMA, MMA, 4 epilogue warps
+constexpr int kRSmem = RS * 2 * kAB + 1024 + 256;
+
+struct RParams {
+    int64_t T, h;
+    int kblocks, n_mt, n_nt, nr;
+    const float* b1;
+    const float* w2;
+    float* s_part;
+};
+
+__global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                                                                 const __grid_constant__ CUtensorMap tmap_b,
+                                                                 const RParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RS * 2 * kAB);
+    uint64_t* full = bars;              // [RS]
+    uint64_t* empty = bars + RS;        // [RS]
+    uint64_t* acc_full = bars + 2 * RS; // [2]
+    uint64_t* acc_empty = acc_full + 2; // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < RS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        fence_barrier_init();
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int total = p.n_mt * p.n_nt;
+
+    if (warp == 0) {
+        uint32_t it = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+            const int mt = tile % p.n_mt, nt = tile / p.n_mt;
+            for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+                const int s = it % RS;
+                mbar_wait(&empty[s], ((it / RS) & 1) ^ 1);
+                if (lane == 0) {
+                    uint8_t* a = smem + s * 2 * kAB;
+                    mbar_arrive_expect_tx(&full[s], 2 * kAB);
+                    tma_load_2d(a, &tmap_a, &full[s], kb * kKBlock, mt * RM);
+                    tma_load_2d(a + kAB, &tmap_b, &full[s], kb * kKBlock, nt * RN);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        uint32_t it = 0, tc = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+            const int nt = tile / p.n_mt;
+            const uint32_t n_mma = (uint32_t)std::min<int64_t>(RN, round_up(p.h - (int64_t)nt * RN, 16));
+            const uint32_t idesc = idesc_f16(RM, n_mma, 1);
+            const int buf = tc & 1;
+            mbar_wait(&acc_empty[buf], ((tc >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+                const int s = it % RS;
+                mbar_wait(&full[s], (it / RS) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a = smem_u32(smem + s * 2 * kAB);
+                    const uint64_t adesc = sdesc_sw128(a), bdesc = sdesc_sw128(a + kAB);
+#pragma unroll
+                    for (int j = 0; j < kKBlock / 16; ++j)
+                        mma_ss_f16(tmem + buf * RN, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc,
+                                   (kb | j) != 0);
+                    mma_commit(&empty[s]);
+                    if (kb == p.kblocks - 1) mma_commit(&acc_full[buf]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        const int q = warp % 4;
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        uint32_t tc = 0;
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+            const int mt = tile % p.n_mt, nt = tile / p.n_mt;
+            const int buf = tc & 1;
+            const int64_t t = (int64_t)mt * RM + 32 * q + lane;
+            const int64_t h0 = (int64_t)nt * RN;
+            const int nh = (int)std::min<int64_t>(RN, p.h - h0);
+            mbar_wait(&acc_full[buf], (tc >> 1) & 1);
+            tc_fence_after();
+            float part[MOBI_MAX_SLICES - 1] = {0.f, 0.f, 0.f};
+            for (int c0 = 0; c0 < nh; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + buf * RN + c0, v);
+                tmem_ld_wait();
+                const int nn = min(32, nh - c0);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    if (j < nn) {
+                        const int64_t hj = h0 + c0 + j;
+                        const float a = __uint_as_float(v[j]) + __ldg(p.b1 + hj);
+                        const float sv = a * __fdividef(1.f, 1.f + __expf(-a));
+#pragma unroll
+                        for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
+                            if (k < p.nr) part[k] = fmaf(sv, __ldg(p.w2 + hj * p.nr + k), part[k]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            if (t < p.T) {
+#pragma unroll
+                for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
+                    if (k < p.nr) p.s_part[((int64_t)nt * p.T + t) * p.nr + k] = part[k];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 256);
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+}  // namespace
+
+bool router_tc_supported(const mobi_layer* L, const void* x) {
+    return (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+}
+
+int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        MOBI_CUDA(cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem));
+        attr = true;
+    }
+    if (!L->tmap_w1) {
+        L->tmap_w1 = new CUtensorMap;
+        int rc = make_tmap_2d(L->tmap_w1, L->w1t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->h_pad, L->in_pad, RN);
+        if (rc) {
+            delete L->tmap_w1;
+            L->tmap_w1 = nullptr;
+            return rc;
+        }
+    }
+    CUtensorMap tmap_x;
+    int rc = make_tmap_2d(&tmap_x, x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, T, L->in, RM);
+    if (rc) return rc;
+    RParams p;
+    p.T = T;
+    p.h = L->h;
+    p.kblocks = (int)L->kblocks;
+    p.n_mt = (int)cdiv(T, RM);
+    p.n_nt = (int)cdiv(L->h, RN);
+    p.nr = L->nr;
+    p.b1 = L->b1;
+    p.w2 = L->w2;
+    p.s_part = L->s_part;
+    L->htiles = p.n_nt;
+    const int total = p.n_mt * p.n_nt;
+    const int grid = std::min(total, sm_count());
+    router_tc_kernel<<<grid, kRThreads, kRSmem, st>>>(tmap_x, *L->tmap_w1, p);
+    MOBI_LAUNCH_CHECK();
+    ++L->last_launches;
+    return MOBI_OK;
+}
+
+}  // namespace mobi

@@ -215,3 +215,19 @@ def test_llama_shapes(orc, out, inn, T):
     y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 128,
                                 gates_from_masks(m.cpu().numpy(), 3))
     assert_y_close(y, y_ref, f"{out}x{inn}")
+
+
+@pytest.mark.parametrize("inn,h,T", [(512, 128, 300), (4096, 1024, 130), (96, 16, 1)])
+def test_router_tcgen05_matches_cuda_core_router(orc, inn, h, T):
+    from paper_2602_20191_b200 import set_debug_impl
+    L, layer = make_layer(64, inn, gs=32 if inn < 128 else 128, hidden=h, seed=inn)
+    xb, x64 = make_x(T, inn, seed=T)
+    s_tc = layer.score(xb).cpu().numpy()
+    set_debug_impl(1)
+    try:
+        s_cc = layer.score(xb).cpu().numpy()
+    finally:
+        set_debug_impl(0)
+    s_ref = oracle_scores(orc, layer, x64)
+    for s in (s_tc, s_cc):
+        assert np.all(np.abs(s - s_ref) <= SCORE_ATOL + SCORE_RTOL * np.abs(s_ref))
