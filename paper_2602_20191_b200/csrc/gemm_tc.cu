@@ -210,19 +210,24 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             mbar_wait(acc_full, tc & 1);
             tc_fence_after();
             for (int c0 = 0; c0 < tt.n; c0 += 32) {
+                // lane j fetches the destination row and scale of token c0+j; issued before the
+                // TMEM load so their latency overlaps it, then broadcast with shuffles
+                const int nn = min(32, tt.n - c0);
+                int32_t my_src = -1;
+                float my_es = 0.f;
+                if (lane < nn) {
+                    my_src = __ldg(p.perm + tt.row0 + c0 + lane);
+                    my_es = __ldg(p.escale + tt.row0 + c0 + lane);
+                }
                 uint32_t v[32];
                 tmem_ld32(tmem + lane_base + c0, v);
                 tmem_ld_wait();
-                const int nn = min(32, tt.n - c0);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    if (j < nn) {
-                        const int row = tt.row0 + c0 + j;
-                        const int32_t src = p.perm[row];
-                        const float es = p.escale[row];
-                        if (rv && src >= 0)
-                            p.y[(int64_t)src * p.out + R] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
-                    }
+                    const int32_t src = __shfl_sync(0xffffffffu, my_src, j);
+                    const float es = __shfl_sync(0xffffffffu, my_es, j);
+                    if (rv && src >= 0)
+                        p.y[(int64_t)src * p.out + R] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
                 }
             }
             tc_fence_before();
