@@ -13,7 +13,8 @@
 namespace mobi {
 
 static thread_local std::string g_err;
-static int g_impl_override = 0;  // test hook: 1 = CUDA-core reference GEMM
+static int g_impl_override = 0;  // test hook: 1 = CUDA-core reference GEMM, 2 = traced tcgen05
+static unsigned long long* g_trace_buf = nullptr;
 
 int set_error(int code, const std::string& msg) {
     g_err = msg;
@@ -318,6 +319,13 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
     ProfScope p(L, 3, st);
     if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
+    if (g_impl_override == 2) {  // traced tcgen05 kernel (development hook)
+        static unsigned long long* tbuf = nullptr;
+        if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, 16 * 1024 * sizeof(unsigned long long)));
+        MOBI_CUDA(cudaMemsetAsync(tbuf, 0, 16 * 1024 * sizeof(unsigned long long), st));
+        g_trace_buf = tbuf;
+        return launch_gemm_tc(L, yb, T, st, tbuf);
+    }
     return launch_gemm_tc(L, yb, T, st);
 }
 
@@ -333,6 +341,14 @@ const char* mobi_version(void) { return "mobi_b200 0.1 (sm_100a)"; }
 
 int mobi_debug_set_impl(int impl) {
     g_impl_override = impl;
+    return MOBI_OK;
+}
+
+/* development hook: copy the last traced GEMM's per-CTA counters (16 x u64 per CTA) to host */
+MOBI_API int mobi_debug_read_trace(unsigned long long* host, int n_cta) {
+    if (!g_trace_buf) return set_error(MOBI_EINVAL, "no trace recorded");
+    MOBI_CUDA(cudaDeviceSynchronize());
+    MOBI_CUDA(cudaMemcpy(host, g_trace_buf, (size_t)n_cta * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     return MOBI_OK;
 }
 

@@ -47,10 +47,28 @@ struct Params {
     const TokTile* tiles;
     const int32_t* meta;
     __nv_bfloat16* y;
+    unsigned long long* trace;
 };
 
+// TRACE=true: clock64 accounting of each role's barrier waits (debug hook impl 2), written to
+// p.trace[cta][0..15]: 0 tma wait empty | 1 mma wait acc_empty | 2 mma wait full_b | 3 mma wait
+// full_a | 4 mma loop | 5 dequant(w2) wait empty | 6 dequant(w2) loop | 7 epi(w18) wait acc_full |
+// 8 epi(w18) loop | 9 tiles
+template <bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                                                    const Params p) {
+    long long tr[4] = {0, 0, 0, 0};
+#define TW(i, stmt)                                   \
+    do {                                              \
+        if (TRACE) {                                  \
+            long long t0_ = clock64();                \
+            stmt;                                     \
+            tr[i] += clock64() - t0_;                 \
+        } else {                                      \
+            stmt;                                     \
+        }                                             \
+    } while (0)
+    long long tstart = TRACE ? clock64() : 0;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stage_b = smem;
@@ -92,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
+                TW(0, mbar_wait(&empty[s], ph ^ 1));
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full_b[s], kStageBytes);
                     tma_load_2d(stage_b + s * kStageBytes, &tmap_x, &full_b[s], kb * kKBlock, tt.row0);
@@ -107,13 +125,13 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             const uint32_t n_mma = (uint32_t)round_up(tt.n, 16);
             const uint32_t idesc = idesc_f16(128, n_mma, 0);
-            mbar_wait(acc_empty, (tc & 1) ^ 1);
+            TW(0, mbar_wait(acc_empty, (tc & 1) ^ 1));
             tc_fence_after();
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
-                mbar_wait(&full_b[s], ph);
-                mbar_wait(&full_a[s], ph);
+                TW(1, mbar_wait(&full_b[s], ph));
+                TW(2, mbar_wait(&full_a[s], ph));
                 tc_fence_after();
                 if (lane == 0) {
                     const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
@@ -170,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
+                TW(0, mbar_wait(&empty[s], ph ^ 1));
                 tc_fence_after();
                 tmem_st8(tmem + lane_base + kACol0 + s * 32 + j * 8, v);
                 // overlap the TMEM store with the next k-block's loads and dequantization
@@ -207,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             const int rt = tile % p.n_row_tiles;
             const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
             const bool rv = R < p.out;
-            mbar_wait(acc_full, tc & 1);
+            TW(0, mbar_wait(acc_full, tc & 1));
             tc_fence_after();
             for (int c0 = 0; c0 < tt.n; c0 += 32) {
                 // lane j fetches the destination row and scale of token c0+j; issued before the
@@ -235,6 +253,16 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             if (lane == 0) mbar_arrive(acc_empty);
         }
     }
+    if (TRACE && lane == 0) {
+        unsigned long long* o = p.trace + blockIdx.x * 16;
+        const long long tot = clock64() - tstart;
+        if (warp == 0) o[0] = tr[0];
+        if (warp == 1) { o[1] = tr[0]; o[2] = tr[1]; o[3] = tr[2]; o[4] = tot; }
+        if (warp == 2) { o[5] = tr[0]; o[6] = tot; }
+        if (warp == 2 + kDqWarps) { o[7] = tr[0]; o[8] = tot; }
+        if (warp == 0) o[9] = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    }
+#undef TW
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, 512);
@@ -285,10 +313,13 @@ int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int
     return MOBI_OK;
 }
 
-int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st) {
+int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace) {
     static bool attr = false;
     if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBytes));
+        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBytes));
         attr = true;
     }
     if (!L->tmap_x) {
@@ -318,7 +349,11 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st) 
     p.y = y;
     const int64_t max_total = (int64_t)p.n_row_tiles * L->max_tiles;
     const int grid = (int)std::min<int64_t>(sm_count(), max_total);
-    mobi_gemm_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
+    p.trace = trace;
+    if (trace)
+        mobi_gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
+    else
+        mobi_gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

@@ -148,7 +148,8 @@ int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_ma
                   int32_t* inverse_out, int32_t* counts_out, cudaStream_t st);
 int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);
 // gemm_tc.cu (tcgen05) / gemm_simt.cu (reference kernel, tests only)
-int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
+int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
+                   unsigned long long* trace = nullptr);
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
 // decompose.cu
 int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,

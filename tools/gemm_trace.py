@@ -1,0 +1,42 @@
+"""Development tool: run the traced tcgen05 GEMM (debug impl 2) on the bench workload and print
+where each warp role spends its cycles (barrier waits vs. work)."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import bench  # noqa: E402
+from paper_2602_20191_b200 import _lib, calibrate_threshold, set_debug_impl  # noqa: E402
+
+
+def main():
+    a = bench.parse.__wrapped__() if hasattr(bench.parse, "__wrapped__") else None
+    sys.argv = [sys.argv[0]] + sys.argv[1:]
+    args = bench.parse()
+    dev = torch.device("cuda", 0)
+    layer, _ = bench.make_layer(args, dev, 1)
+    x = bench.make_x(args, dev, 2)
+    delta = calibrate_threshold(layer.score(x), (args.target_bits - 2) / 6)
+    for _ in range(3):
+        layer.forward(x, delta)
+    set_debug_impl(2)
+    layer.forward(x, delta)
+    torch.cuda.synchronize()
+    set_debug_impl(0)
+    n = torch.cuda.get_device_properties(0).multi_processor_count
+    buf = np.zeros((n, 16), np.uint64)
+    lib = _lib.lib()
+    lib.mobi_debug_read_trace.argtypes = [C.c_void_p, C.c_int]
+    _lib.check(lib.mobi_debug_read_trace(buf.ctypes.data, n))
+    names = ["tma wait empty", "mma wait acc_empty", "mma wait full_b", "mma wait full_a", "mma loop total",
+             "dq wait empty", "dq loop total", "epi wait acc_full", "epi loop total", "tiles"]
+    for i, nm in enumerate(names):
+        col = buf[:, i].astype(np.float64)
+        print(f"{nm:22s} mean {col.mean():12.0f}  min {col.min():12.0f}  max {col.max():12.0f}")
+
+
+if __name__ == "__main__":
+    main()
