@@ -11,11 +11,13 @@
 // Roles (one persistent CTA per SM, 704 threads):
 //   warp 0      TMA producer: X_perm tile [256 tokens x 64 k] fp16, 128-byte swizzle -> smem stage
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-17  dequantizers: each thread owns one weight row (= one TMEM lane) and 16 k of the
-//               64-k block; coalesced 16-byte code loads (3 k-blocks in flight) -> fp16 W_m ->
-//               tcgen05.st into the A stage in TMEM (A operand never touches shared memory)
-//   warps 18-21 epilogue: tcgen05.ld the fp32 accumulator, x 2^e row scale, bf16, scatter
-//               Y[perm[i], r] (the un-permute, bitplane.hpp:171-172, fused)
+//   warps 2-17  dequantizers: each thread owns one weight row (= one TMEM lane) and 32 k of every
+//               other 64-k block (two k-blocks in flight); coalesced 16-byte code loads, three
+//               k-blocks ahead -> fp16 W_m -> tcgen05.st into the A stage in TMEM (the A operand
+//               never touches shared memory)
+//   warps 18-21 epilogue: tcgen05.ld the fp32 accumulator, x 2^e row scale, bf16 into a smem
+//               staging tile, release TMEM, then scatter 256-byte token rows to Y[perm[i]]
+//               (the un-permute, bitplane.hpp:171-172, fused)
 // MMA: M=128 weight rows (TMEM lanes), N=tile tokens (<=256, multiple of 16), K=16 per
 // instruction, D fp32 in TMEM columns [0,256); A stages at columns 256 + 32*s.
 #include "mobi_internal.cuh"
@@ -32,7 +34,8 @@ constexpr int kThreads = 32 * (2 + kDqWarps + 4);  // TMA, MMA, dequant, epilogu
 constexpr int kStageBytes = kTokTile * kKBlock * 2;  // 32 KiB
 constexpr int kAccCols = 256;
 constexpr int kACol0 = 256;
-constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kYStageBytes = kTokTile * kRowTile * 2;  // 64 KiB bf16 output staging
+constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kYStageBytes + kTokTile * 4;
 
 struct Params {
     const uint8_t* codes8;
@@ -47,6 +50,7 @@ struct Params {
     const TokTile* tiles;
     const int32_t* meta;
     __nv_bfloat16* y;
+    int vec_y;
     unsigned long long* trace;
 };
 
@@ -79,12 +83,15 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     uint64_t* acc_full = bars + 3 * NSTAGE;   // accumulator ready for the epilogue
     uint64_t* acc_empty = acc_full + 1;       // epilogue drained the accumulator (4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 256);
+    int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 256 + kYStageBytes);
+    auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1);
-            mbar_init(&full_a[s], kDqWarps);
+            mbar_init(&full_a[s], kDqWarps / 2);
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
@@ -148,27 +155,36 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         }
     } else if (warp < 2 + kDqWarps) {
         // ---------------- dequantizers ----------------
-        // warp -> (TMEM lane quarter q, 16-code chunk j of the 64-k block); 4 warps per quarter
+        // 16 warps = 4 TMEM lane quarters x 2 k-halves x 2 k-block parities: a warp dequantizes
+        // 32 codes of its row for every other k-block, so two k-blocks are in flight at once.
+        const int idx = warp - 2;
         const int q = warp % 4;
-        const int j = (warp - 2) / 4;
+        const int par = (idx / 4) & 1;
+        const int hh = idx / 8;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        uint32_t it = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
+        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, base += kb_n) {
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             const int rt = tile % p.n_row_tiles;
             const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
             const bool rv = R < p.out;
             const uint32_t mw = p.mt.maskword[tt.mask];
             const float kc = p.mt.kc[tt.mask];
-            const uint8_t* cbase = p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes + (j * kRowTile + 32 * q + lane) * 16;
+            const uint8_t* cbase =
+                p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes + ((hh * 2) * kRowTile + 32 * q + lane) * 16;
             const float* srow = p.gscale + (rv ? R : 0) * p.G;
             const float* zrow = p.gsz + (rv ? R : 0) * p.G;
-            // codes ring, 3 k-blocks ahead
-            uint4 ca = *reinterpret_cast<const uint4*>(cbase);
-            uint4 cb = kb_n > 1 ? *reinterpret_cast<const uint4*>(cbase + kBlockBytes) : ca;
-            uint4 cc = kb_n > 2 ? *reinterpret_cast<const uint4*>(cbase + 2 * kBlockBytes) : ca;
-            // group tracking without division: k = kb*64 + 16j
-            int g = 0, kin = 16 * j;
+            auto ld = [&](int kb, uint4& c0, uint4& c1) {
+                const uint8_t* b0 = cbase + (int64_t)kb * kBlockBytes;
+                c0 = *reinterpret_cast<const uint4*>(b0);
+                c1 = *reinterpret_cast<const uint4*>(b0 + kRowTile * 16);
+            };
+            // codes ring: this warp's next three k-blocks
+            uint4 a0, a1, b0, b1, d0, d1;
+            if (par < kb_n) ld(par, a0, a1);
+            if (par + 2 < kb_n) ld(par + 2, b0, b1);
+            if (par + 4 < kb_n) ld(par + 4, d0, d1);
+            int g = 0, kin = par * kKBlock + hh * 32;
             if (!p.single_group)
                 while (kin >= p.gs) kin -= (int)p.gs, ++g;
             __half2 S2, C2;
@@ -179,57 +195,62 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 C2 = __float2half2_rn(fmaf(sc, kc, -sz));
             };
             group_consts(g);
-            uint32_t v[8];
-            {
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(&ca);
+            auto dq = [&](const uint4& c0, const uint4& c1, uint32_t (&v)[16]) {
+                const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&c0);
+                const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&c1);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) dequant4(w[u], mw, S2, C2, v[2 * u], v[2 * u + 1]);
-            }
-            for (int kb = 0; kb < kb_n; ++kb, ++it) {
-                const int s = it % NSTAGE;
-                const uint32_t ph = (it / NSTAGE) & 1;
+                for (int u = 0; u < 4; ++u) dequant4(w0[u], mw, S2, C2, v[2 * u], v[2 * u + 1]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) dequant4(w1[u], mw, S2, C2, v[8 + 2 * u], v[8 + 2 * u + 1]);
+            };
+            uint32_t v[16];
+            if (par < kb_n) dq(a0, a1, v);
+            for (int kb = par; kb < kb_n; kb += 2) {
+                const uint32_t itk = base + kb;
+                const int s = itk % NSTAGE;
+                const uint32_t ph = (itk / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
                 tc_fence_after();
-                tmem_st8(tmem + lane_base + kACol0 + s * 32 + j * 8, v);
-                // overlap the TMEM store with the next k-block's loads and dequantization
-                ca = cb;
-                cb = cc;
-                if (kb + 3 < kb_n) cc = *reinterpret_cast<const uint4*>(cbase + (int64_t)(kb + 3) * kBlockBytes);
-                uint32_t vn[8];
-                if (kb + 1 < kb_n) {
+                tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
+                // overlap the TMEM store with the next loads and dequantization
+                a0 = b0;
+                a1 = b1;
+                b0 = d0;
+                b1 = d1;
+                if (kb + 6 < kb_n) ld(kb + 6, d0, d1);
+                uint32_t vn[16];
+                if (kb + 2 < kb_n) {
                     if (!p.single_group) {
-                        kin += kKBlock;
+                        kin += 2 * kKBlock;
                         bool ch = false;
                         while (kin >= p.gs) kin -= (int)p.gs, ++g, ch = true;
                         if (ch) group_consts(g);
                     }
-                    const uint32_t* w = reinterpret_cast<const uint32_t*>(&ca);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) dequant4(w[u], mw, S2, C2, vn[2 * u], vn[2 * u + 1]);
+                    dq(a0, a1, vn);
                 }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full_a[s]);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = vn[u];
+                for (int u = 0; u < 16; ++u) v[u] = vn[u];
             }
         }
     } else {
         // ---------------- epilogue ----------------
+        // drain TMEM -> (x 2^e) -> bf16 -> smem tile [token][128 rows], release the accumulator,
+        // then scatter whole 256-byte token rows into Y[perm[i]] with 16-byte stores
         const int q = warp % 4;
+        const int et = threadIdx.x - 32 * (2 + kDqWarps);  // 0..127
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t tc = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             const int rt = tile % p.n_row_tiles;
-            const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
-            const bool rv = R < p.out;
             TW(0, mbar_wait(acc_full, tc & 1));
             tc_fence_after();
+            epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
             for (int c0 = 0; c0 < tt.n; c0 += 32) {
-                // lane j fetches the destination row and scale of token c0+j; issued before the
-                // TMEM load so their latency overlaps it, then broadcast with shuffles
                 const int nn = min(32, tt.n - c0);
                 int32_t my_src = -1;
                 float my_es = 0.f;
@@ -237,20 +258,32 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                     my_src = __ldg(p.perm + tt.row0 + c0 + lane);
                     my_es = __ldg(p.escale + tt.row0 + c0 + lane);
                 }
+                if (q == 0) tok_src[c0 + lane] = lane < nn ? my_src : -1;
                 uint32_t v[32];
                 tmem_ld32(tmem + lane_base + c0, v);
                 tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const int32_t src = __shfl_sync(0xffffffffu, my_src, j);
                     const float es = __shfl_sync(0xffffffffu, my_es, j);
-                    if (rv && src >= 0)
-                        p.y[(int64_t)src * p.out + R] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
+                    stage_y[(c0 + j) * kRowTile + 32 * q + lane] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty);
+            epi_bar_sync();  // staging tile complete
+            const int64_t r0 = (int64_t)rt * kRowTile + 8 * (et % 16);
+            for (int t = et / 16; t < tt.n; t += 8) {
+                const int32_t src = tok_src[t];
+                if (src < 0 || r0 >= p.out) continue;
+                const __nv_bfloat16* sp = stage_y + t * kRowTile + 8 * (et % 16);
+                __nv_bfloat16* dp = p.y + (int64_t)src * p.out + r0;
+                if (p.vec_y && r0 + 8 <= p.out) {
+                    *reinterpret_cast<uint4*>(dp) = *reinterpret_cast<const uint4*>(sp);
+                } else {
+                    for (int u = 0; u < 8 && r0 + u < p.out; ++u) dp[u] = sp[u];
+                }
+            }
         }
     }
     if (TRACE && lane == 0) {
@@ -347,6 +380,7 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     p.tiles = L->tiles;
     p.meta = L->meta;
     p.y = y;
+    p.vec_y = (L->out % 8 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
     const int64_t max_total = (int64_t)p.n_row_tiles * L->max_tiles;
     const int grid = (int)std::min<int64_t>(sm_count(), max_total);
     p.trace = trace;
