@@ -204,15 +204,16 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L) {
         dfree(tmp);
         if (rc) return rc;
     }
-    std::vector<float> s(ng), sz(ng);
-    for (int64_t g = 0; g < ng; ++g) {
-        s[g] = (float)d->scale[g];
-        sz[g] = (float)(d->scale[g] * d->zero[g]);
-    }
-    if ((rc = dmalloc(&L->gscale, (size_t)ng, L))) return rc;
-    if ((rc = dmalloc(&L->gsz, (size_t)ng, L))) return rc;
-    MOBI_CUDA(cudaMemcpy(L->gscale, s.data(), ng * 4, cudaMemcpyHostToDevice));
-    MOBI_CUDA(cudaMemcpy(L->gsz, sz.data(), ng * 4, cudaMemcpyHostToDevice));
+    // group constants transposed to [G][out_pad] (s, s*z): a warp's 32 rows read 256 contiguous bytes
+    std::vector<float2> gc((size_t)(L->G * L->out_pad), make_float2(0.f, 0.f));
+    for (int64_t r = 0; r < L->out; ++r)
+        for (int64_t g = 0; g < L->G; ++g) {
+            const double sc = d->scale[r * L->G + g];
+            gc[(size_t)(g * L->out_pad + r)] = make_float2((float)sc, (float)(sc * d->zero[r * L->G + g]));
+        }
+    (void)ng;
+    if ((rc = dmalloc(&L->gconst, gc.size(), L))) return rc;
+    MOBI_CUDA(cudaMemcpy(L->gconst, gc.data(), gc.size() * sizeof(float2), cudaMemcpyHostToDevice));
     // router: w1 transposed to [h_pad][in_pad] bf16 (K-major B operand), zero padded
     std::vector<uint16_t> w1t((size_t)(L->h_pad * L->in_pad), 0);
     for (int64_t k = 0; k < L->in; ++k)
@@ -379,8 +380,7 @@ int mobi_layer_destroy(mobi_layer_t L) {
     cudaDeviceSynchronize();
     free_ws(L);
     dfree(L->codes8);
-    dfree(L->gscale);
-    dfree(L->gsz);
+    dfree(L->gconst);
     dfree(L->w1t);
     dfree(L->b1);
     dfree(L->w2);

@@ -20,18 +20,20 @@ namespace mobi {
 namespace {
 
 constexpr int BK_THREADS = 1024;
-constexpr int NKEY = 256;  // uint8 keys (GEMM masks are < 2^MOBI_MAX_SLICES)
+constexpr int NKEY_ALL = 256;              // generic uint8 keys (permute_by_slice API)
+constexpr int NKEY_MASK = 2 * kMaxBuckets;  // slice masks on the GEMM path (< 2^MOBI_MAX_SLICES)
 
 // Stable counting sort on one CTA.  Keys are processed in chunks of 1024 tokens in token
 // order; inside a chunk, __match_any_sync ranks equal keys within a warp and a per-key scan
 // over the 32 warps orders the warps, so every token's position equals std::stable_sort's.
+template <int NKEY>
 __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
     const float* __restrict__ s_part, int htiles, int64_t T, int nr, const float* __restrict__ b2,
     float delta, const uint8_t* __restrict__ given_masks, int sanitize, float* __restrict__ scores_out,
     uint8_t* __restrict__ keys, uint8_t* __restrict__ masks_out, int32_t* __restrict__ perm,
     int64_t tpad_max, int32_t* __restrict__ cperm_out, int32_t* __restrict__ inverse_out,
     int32_t* __restrict__ counts_out, TokTile* __restrict__ tiles, int32_t* __restrict__ meta) {
-    __shared__ int hist[NKEY], cstart[NKEY], run[NKEY], pstart[2 * kMaxBuckets];
+    __shared__ int hist[NKEY], cstart[NKEY], run[NKEY], pstart[NKEY_MASK];
     __shared__ int warp_hist[BK_THREADS / 32][NKEY];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int vmask = (1 << (nr + 1)) - 1;
@@ -69,11 +71,11 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
         for (int v = 0; v < NKEY; ++v) {
             cstart[v] = c;
             c += hist[v];
-            if (counts_out && (v < 2 * kMaxBuckets || !perm)) counts_out[v] = hist[v];
+            if (counts_out) counts_out[v] = hist[v];
         }
         if (perm) {
             int a = 0, n = 0;
-            for (int v = 0; v < 2 * kMaxBuckets; ++v) {
+            for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) {
                 pstart[v] = a;
                 for (int j = 0; j < hist[v]; j += kTokTile) {
                     TokTile tt;
@@ -87,7 +89,7 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
             }
             meta[0] = n;
             meta[1] = a;
-            for (int v = 0; v < 2 * kMaxBuckets; ++v) meta[2 + v] = hist[v];
+            for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) meta[2 + v] = hist[v];
         }
     }
     __syncthreads();
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
         if (valid) {
             const int off = warp_hist[wid][key] + rank;
             const int cpos = cstart[key] + off;
-            if (perm) perm[pstart[key] + off] = (int32_t)t;
+            if (perm && key < NKEY_MASK) perm[pstart[key] + off] = (int32_t)t;
             if (cperm_out) cperm_out[cpos] = (int32_t)t;
             if (inverse_out) inverse_out[t] = cpos;
         }
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
 int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks,
                   float* scores_out, uint8_t* masks_out, int32_t* cperm_out, int32_t* inverse_out,
                   int32_t* counts_out, cudaStream_t st) {
-    bucket_kernel<<<1, BK_THREADS, 0, st>>>(L->s_part, (int)L->htiles, T, L->nr, L->b2, delta,
+    bucket_kernel<NKEY_MASK><<<1, BK_THREADS, 0, st>>>(L->s_part, (int)L->htiles, T, L->nr, L->b2, delta,
                                              given_masks, 1, scores_out, L->masks, masks_out, L->perm,
                                              L->tpad_max, cperm_out, inverse_out, counts_out, L->tiles,
                                              L->meta);
@@ -198,7 +200,7 @@ int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_ma
 
 int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* cperm, int32_t* inverse,
                    int32_t* hist256, cudaStream_t st) {
-    bucket_kernel<<<1, BK_THREADS, 0, st>>>(nullptr, 0, T, 0, nullptr, 0.f, masks, 0, nullptr, keys_tmp,
+    bucket_kernel<NKEY_ALL><<<1, BK_THREADS, 0, st>>>(nullptr, 0, T, 0, nullptr, 0.f, masks, 0, nullptr, keys_tmp,
                                              nullptr, nullptr, 0, cperm, inverse, hist256, nullptr, nullptr);
     MOBI_LAUNCH_CHECK();
     return MOBI_OK;

@@ -10,8 +10,8 @@ namespace {
 constexpr int SM_ROWS = 64, SM_TOK = 64;
 
 __global__ void __launch_bounds__(256) gemm_simt_kernel(
-    const uint8_t* __restrict__ codes8, const float* __restrict__ gscale,
-    const float* __restrict__ gsz, MaskTable mt, int64_t out, int64_t G, int64_t gs,
+    const uint8_t* __restrict__ codes8, const float2* __restrict__ gconst, int64_t out_pad,
+    MaskTable mt, int64_t out, int64_t G, int64_t gs,
     bool single_group, int64_t kblocks, int64_t in_pad, const __half* __restrict__ xperm,
     const float* __restrict__ escale, const int32_t* __restrict__ perm,
     const TokTile* __restrict__ tiles, const int32_t* __restrict__ meta,
@@ -37,8 +37,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(
             float s = 0.f, sz = 0.f;
             if (R < out) {
                 const int64_t g = single_group ? 0 : k0 / gs;
-                s = gscale[R * G + g];
-                sz = gsz[R * G + g];
+                const float2 c = gconst[g * out_pad + R];
+                s = c.x;
+                sz = c.y;
             }
             const __half2 S2 = __float2half2_rn(s * mt.inv_2p);
             const __half2 C2 = __float2half2_rn(fmaf(s, kc, -sz));
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(
 
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st) {
     dim3 grid((unsigned)(L->out_pad / SM_ROWS), (unsigned)L->max_tiles, kTokTile / SM_TOK);
-    gemm_simt_kernel<<<grid, 256, 0, st>>>(L->codes8, L->gscale, L->gsz, L->mtab, L->out, L->G, L->gs,
+    gemm_simt_kernel<<<grid, 256, 0, st>>>(L->codes8, L->gconst, L->out_pad, L->mtab, L->out, L->G, L->gs,
                                            L->single_group, L->kblocks, L->in_pad, L->xperm, L->escale,
                                            L->perm, L->tiles, L->meta, y);
     MOBI_LAUNCH_CHECK();

@@ -12,8 +12,8 @@
 //   warp 0      TMA producer: X_perm tile [256 tokens x 64 k] fp16, 128-byte swizzle -> smem stage
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2-17  dequantizers: each thread owns one weight row (= one TMEM lane) and 32 k of every
-//               other 64-k block (two k-blocks in flight); coalesced 16-byte code loads, three
-//               k-blocks ahead -> fp16 W_m -> tcgen05.st into the A stage in TMEM (the A operand
+//               other 64-k block (two k-blocks in flight); coalesced 16-byte code loads, two of
+//               its k-blocks ahead -> fp16 W_m -> tcgen05.st into the A stage in TMEM (the A operand
 //               never touches shared memory)
 //   warps 18-21 epilogue: tcgen05.ld the fp32 accumulator, x 2^e row scale, bf16 into a smem
 //               staging tile, release TMEM, then scatter 256-byte token rows to Y[perm[i]]
@@ -39,8 +39,8 @@ constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 /*align*/ + 256 /*barrier
 
 struct Params {
     const uint8_t* codes8;
-    const float* gscale;
-    const float* gsz;
+    const float2* gconst;  // [G][out_pad]
+    int64_t out_pad;
     MaskTable mt;
     int64_t out, G, gs, kblocks;
     int single_group;
@@ -172,30 +172,34 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             const float kc = p.mt.kc[tt.mask];
             const uint8_t* cbase =
                 p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes + ((hh * 2) * kRowTile + 32 * q + lane) * 16;
-            const float* srow = p.gscale + (rv ? R : 0) * p.G;
-            const float* zrow = p.gsz + (rv ? R : 0) * p.G;
+            const float2* gcol = p.gconst + (rv ? R : 0);
+            auto ldc = [&](int gg) { return rv ? __ldg(gcol + (int64_t)gg * p.out_pad) : make_float2(0.f, 0.f); };
             auto ld = [&](int kb, uint4& c0, uint4& c1) {
                 const uint8_t* b0 = cbase + (int64_t)kb * kBlockBytes;
                 c0 = *reinterpret_cast<const uint4*>(b0);
                 c1 = *reinterpret_cast<const uint4*>(b0 + kRowTile * 16);
             };
-            // codes ring: this warp's next three k-blocks
-            uint4 a0, a1, b0, b1, d0, d1;
-            if (par < kb_n) ld(par, a0, a1);
-            if (par + 2 < kb_n) ld(par + 2, b0, b1);
-            if (par + 4 < kb_n) ld(par + 4, d0, d1);
-            int g = 0, kin = par * kKBlock + hh * 32;
-            if (!p.single_group)
-                while (kin >= p.gs) kin -= (int)p.gs, ++g;
-            __half2 S2, C2;
-            auto group_consts = [&](int gg) {
-                const float sc = rv ? __ldg(srow + gg) : 0.f;
-                const float sz = rv ? __ldg(zrow + gg) : 0.f;
-                S2 = __float2half2_rn(sc * p.mt.inv_2p);
-                C2 = __float2half2_rn(fmaf(sc, kc, -sz));
+            // group of k = kb*64 + 32*hh, tracked incrementally (k advances by 128 per step)
+            auto group_of = [&](int kb) {
+                if (p.single_group) return 0;
+                int gg = 0, kin = kb * kKBlock + hh * 32;
+                while (kin >= p.gs) kin -= (int)p.gs, ++gg;
+                return gg;
             };
-            group_consts(g);
-            auto dq = [&](const uint4& c0, const uint4& c1, uint32_t (&v)[16]) {
+            // rings: codes and group constants of this warp's next two k-blocks (4 k-blocks of
+            // MMA time ahead, > L2 latency)
+            uint4 a0, a1, b0, b1;
+            float2 ga = make_float2(0.f, 0.f), gb = ga;
+            if (par < kb_n) { ld(par, a0, a1); ga = ldc(group_of(par)); }
+            int gp = group_of(par + 2), kinp = 0;  // prefetch cursor at k-block par+2
+            if (!p.single_group) {
+                kinp = (par + 2) * kKBlock + hh * 32;
+                while (kinp >= p.gs) kinp -= (int)p.gs;
+            }
+            if (par + 2 < kb_n) { ld(par + 2, b0, b1); gb = ldc(gp); }
+            auto dq = [&](const uint4& c0, const uint4& c1, float2 gcst, uint32_t (&v)[16]) {
+                const __half2 S2 = __float2half2_rn(gcst.x * p.mt.inv_2p);
+                const __half2 C2 = __float2half2_rn(fmaf(gcst.x, kc, -gcst.y));
                 const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&c0);
                 const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&c1);
 #pragma unroll
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 for (int u = 0; u < 4; ++u) dequant4(w1[u], mw, S2, C2, v[8 + 2 * u], v[8 + 2 * u + 1]);
             };
             uint32_t v[16];
-            if (par < kb_n) dq(a0, a1, v);
+            if (par < kb_n) dq(a0, a1, ga, v);
             for (int kb = par; kb < kb_n; kb += 2) {
                 const uint32_t itk = base + kb;
                 const int s = itk % NSTAGE;
@@ -215,19 +219,17 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 // overlap the TMEM store with the next loads and dequantization
                 a0 = b0;
                 a1 = b1;
-                b0 = d0;
-                b1 = d1;
-                if (kb + 6 < kb_n) ld(kb + 6, d0, d1);
-                uint32_t vn[16];
-                if (kb + 2 < kb_n) {
+                ga = gb;
+                if (kb + 4 < kb_n) {
                     if (!p.single_group) {
-                        kin += 2 * kKBlock;
-                        bool ch = false;
-                        while (kin >= p.gs) kin -= (int)p.gs, ++g, ch = true;
-                        if (ch) group_consts(g);
+                        kinp += 2 * kKBlock;
+                        while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
                     }
-                    dq(a0, a1, vn);
+                    ld(kb + 4, b0, b1);
+                    gb = ldc(gp);
                 }
+                uint32_t vn[16];
+                if (kb + 2 < kb_n) dq(a0, a1, ga, vn);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
@@ -366,8 +368,8 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     }
     Params p;
     p.codes8 = L->codes8;
-    p.gscale = L->gscale;
-    p.gsz = L->gsz;
+    p.gconst = L->gconst;
+    p.out_pad = L->out_pad;
     p.mt = L->mtab;
     p.out = L->out;
     p.G = L->G;

@@ -73,8 +73,7 @@ struct mobi_layer {
 
     // device weights
     uint8_t* codes8 = nullptr;        // tiled merged codes [out_pad/128][kblocks][8192]
-    float* gscale = nullptr;          // [out][G]  s
-    float* gsz = nullptr;             // [out][G]  s*z
+    float2* gconst = nullptr;         // [G][out_pad] (s, s*z) per group: coalesced across rows
     __nv_bfloat16* w1t = nullptr;     // [h_pad][in_pad] bf16, K-major (router B operand)
     float* b1 = nullptr;              // [h_pad]
     float* w2 = nullptr;              // [h_pad][nr]
