@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
             if (counts_out) counts_out[v] = hist[v];
         }
         if (perm) {
+            // token tiles, largest first (the GEMM claims them dynamically in this order)
             int a = 0, n = 0;
             for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) {
                 pstart[v] = a;
@@ -83,13 +84,19 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
                     tt.n = min(kTokTile, hist[v] - j);
                     tt.mask = v;
                     tt.pad = 0;
-                    tiles[n++] = tt;
+                    int i = n++;
+                    while (i > 0 && tiles[i - 1].n < tt.n) {
+                        tiles[i] = tiles[i - 1];
+                        --i;
+                    }
+                    tiles[i] = tt;
                 }
                 a += (int)round_up(hist[v], kBucketAlign);
             }
             meta[0] = n;
             meta[1] = a;
             for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) meta[2 + v] = hist[v];
+            meta[32] = 0;  // GEMM dynamic tile counter
         }
     }
     __syncthreads();

@@ -29,6 +29,7 @@ namespace {
 using namespace sm100;
 
 constexpr int NSTAGE = 4;
+constexpr int kSched = 4;  // tile-id ring depth
 constexpr int kDqWarps = 16;                       // 4 per TMEM lane quarter
 constexpr int kThreads = 32 * (2 + kDqWarps + 4);  // TMA, MMA, dequant, epilogue
 constexpr int kStageBytes = kTokTile * kKBlock * 2;  // 32 KiB
@@ -51,6 +52,7 @@ struct Params {
     const int32_t* meta;
     __nv_bfloat16* y;
     int vec_y;
+    int* tile_counter;  // zeroed by the bucket kernel before every launch
     unsigned long long* trace;
 };
 
@@ -82,7 +84,10 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     uint64_t* empty = bars + 2 * NSTAGE;      // [NSTAGE] MMAs reading the stage completed
     uint64_t* acc_full = bars + 3 * NSTAGE;   // accumulator ready for the epilogue
     uint64_t* acc_empty = acc_full + 1;       // epilogue drained the accumulator (4 warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    uint64_t* sched_full = acc_empty + 1;       // [kSched] tile id published
+    uint64_t* sched_empty = sched_full + kSched; // [kSched] all consumer warps read it
+    int32_t* sched = reinterpret_cast<int32_t*>(sched_empty + kSched);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched + kSched);
     __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 256);
     int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 256 + kYStageBytes);
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
@@ -96,6 +101,10 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
+        for (int i = 0; i < kSched; ++i) {
+            mbar_init(&sched_full[i], 1);
+            mbar_init(&sched_empty[i], 1 + kDqWarps + 4);
+        }
         fence_barrier_init();
         prefetch_tmap(&tmap_x);
     }
@@ -108,11 +117,39 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     const int n_tok_tiles = p.meta[0];
     const int total = n_tok_tiles * p.n_row_tiles;
     const int kb_n = (int)p.kblocks;
+    // Dynamic tile scheduler: the TMA warp claims tile ids from a global counter (token tiles are
+    // listed largest first, so the costliest tiles are claimed first) and publishes them through
+    // an smem ring; every other role reads the same sequence.
+    auto next_tile = [&](uint32_t ti) -> int {
+        const int slot = ti % kSched;
+        const uint32_t ph = (ti / kSched) & 1;
+        int tile;
+        if (warp == 0) {
+            mbar_wait(&sched_empty[slot], ph ^ 1);
+            if (lane == 0) {
+                const int t = atomicAdd(p.tile_counter, 1);
+                sched[slot] = t < total ? t : -1;
+                mbar_arrive(&sched_full[slot]);
+            }
+            __syncwarp();
+            mbar_wait(&sched_full[slot], ph);
+            tile = sched[slot];
+        } else {
+            mbar_wait(&sched_full[slot], ph);
+            tile = sched[slot];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sched_empty[slot]);
+        }
+        return tile;
+    };
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         uint32_t it = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        for (uint32_t ti = 0;; ++ti) {
+            const int tile = next_tile(ti);
+            if (tile < 0) break;
+            if (TRACE && lane == 0) ++tr[3];
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
@@ -128,7 +165,9 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         uint32_t it = 0, tc = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+        for (uint32_t ti = 0;; ++ti, ++tc) {
+            const int tile = next_tile(ti);
+            if (tile < 0) break;
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             const uint32_t n_mma = (uint32_t)round_up(tt.n, 16);
             const uint32_t idesc = idesc_f16(128, n_mma, 0);
@@ -163,7 +202,9 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         const int hh = idx / 8;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, base += kb_n) {
+        for (uint32_t ti = 0;; ++ti, base += kb_n) {
+            const int tile = next_tile(ti);
+            if (tile < 0) break;
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             const int rt = tile % p.n_row_tiles;
             const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
@@ -246,7 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         const int et = threadIdx.x - 32 * (2 + kDqWarps);  // 0..127
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t tc = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+        for (uint32_t ti = 0;; ++ti, ++tc) {
+            const int tile = next_tile(ti);
+            if (tile < 0) break;
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             const int rt = tile % p.n_row_tiles;
             TW(0, mbar_wait(acc_full, tc & 1));
@@ -295,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         if (warp == 1) { o[1] = tr[0]; o[2] = tr[1]; o[3] = tr[2]; o[4] = tot; }
         if (warp == 2) { o[5] = tr[0]; o[6] = tot; }
         if (warp == 2 + kDqWarps) { o[7] = tr[0]; o[8] = tot; }
-        if (warp == 0) o[9] = (total - blockIdx.x + gridDim.x - 1) / gridDim.x;
+        if (warp == 0) o[9] = tr[3];
     }
 #undef TW
     tc_fence_before();
@@ -386,6 +429,7 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     const int64_t max_total = (int64_t)p.n_row_tiles * L->max_tiles;
     const int grid = (int)std::min<int64_t>(sm_count(), max_total);
     p.trace = trace;
+    p.tile_counter = L->meta + 32;
     if (trace)
         mobi_gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
     else
