@@ -221,23 +221,6 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 c1 = *reinterpret_cast<const uint4*>(b0 + kRowTile * 16);
             };
             // group of k = kb*64 + 32*hh, tracked incrementally (k advances by 128 per step)
-            auto group_of = [&](int kb) {
-                if (p.single_group) return 0;
-                int gg = 0, kin = kb * kKBlock + hh * 32;
-                while (kin >= p.gs) kin -= (int)p.gs, ++gg;
-                return gg;
-            };
-            // rings: codes and group constants of this warp's next two k-blocks (4 k-blocks of
-            // MMA time ahead, > L2 latency)
-            uint4 a0, a1, b0, b1;
-            float2 ga = make_float2(0.f, 0.f), gb = ga;
-            if (par < kb_n) { ld(par, a0, a1); ga = ldc(group_of(par)); }
-            int gp = group_of(par + 2), kinp = 0;  // prefetch cursor at k-block par+2
-            if (!p.single_group) {
-                kinp = (par + 2) * kKBlock + hh * 32;
-                while (kinp >= p.gs) kinp -= (int)p.gs;
-            }
-            if (par + 2 < kb_n) { ld(par + 2, b0, b1); gb = ldc(gp); }
             auto dq = [&](const uint4& c0, const uint4& c1, float2 gcst, uint32_t (&v)[16]) {
                 const __half2 S2 = __float2half2_rn(gcst.x * p.mt.inv_2p);
                 const __half2 C2 = __float2half2_rn(fmaf(gcst.x, kc, -gcst.y));
@@ -248,35 +231,52 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
 #pragma unroll
                 for (int u = 0; u < 4; ++u) dequant4(w1[u], mw, S2, C2, v[8 + 2 * u], v[8 + 2 * u + 1]);
             };
+            // Ring of three static slots (codes + group constants), unrolled so a slot is refilled
+            // right after it was consumed and each load has two iterations of lead time; no
+            // register moves touch a pending load.
+            uint4 c00, c01, c10, c11, c20, c21;
+            float2 g0 = make_float2(0.f, 0.f), g1 = g0, g2 = g0;
+            int gp = 0, kinp = 0;  // group cursor at the next k-block to prefetch
+            if (!p.single_group) {
+                kinp = par * kKBlock + hh * 32;
+                while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
+            }
+            auto fetch = [&](int kb, uint4& c0, uint4& c1, float2& gc) {
+                if (kb < kb_n) {
+                    ld(kb, c0, c1);
+                    gc = ldc(gp);
+                }
+                if (!p.single_group) {
+                    kinp += 2 * kKBlock;
+                    while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
+                }
+            };
+            fetch(par, c00, c01, g0);
+            fetch(par + 2, c10, c11, g1);
+            fetch(par + 4, c20, c21, g2);
             uint32_t v[16];
-            if (par < kb_n) dq(a0, a1, ga, v);
-            for (int kb = par; kb < kb_n; kb += 2) {
+            auto step = [&](int kb, uint4& ca, uint4& cb, float2& ga, uint4& na, uint4& nb, float2& gn) -> bool {
+                // v holds k-block kb (dequantized from the slot (ca, cb)); (na, nb) holds kb+2
+                if (kb >= kb_n) return false;
                 const uint32_t itk = base + kb;
                 const int s = itk % NSTAGE;
                 const uint32_t ph = (itk / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
                 tc_fence_after();
                 tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
-                // overlap the TMEM store with the next loads and dequantization
-                a0 = b0;
-                a1 = b1;
-                ga = gb;
-                if (kb + 4 < kb_n) {
-                    if (!p.single_group) {
-                        kinp += 2 * kKBlock;
-                        while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
-                    }
-                    ld(kb + 4, b0, b1);
-                    gb = ldc(gp);
-                }
-                uint32_t vn[16];
-                if (kb + 2 < kb_n) dq(a0, a1, ga, vn);
-                tmem_st_wait();
+                fetch(kb + 6, ca, cb, ga);  // refill the consumed slot three of this warp's k-blocks ahead
+                if (kb + 2 < kb_n) TW(1, dq(na, nb, gn, v));
+                TW(2, tmem_st_wait());
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&full_a[s]);
-#pragma unroll
-                for (int u = 0; u < 16; ++u) v[u] = vn[u];
+                return true;
+            };
+            if (par < kb_n) dq(c00, c01, g0, v);
+            for (int kb = par; kb < kb_n; kb += 6) {
+                if (!step(kb, c00, c01, g0, c10, c11, g1)) break;
+                if (!step(kb + 2, c10, c11, g1, c20, c21, g2)) break;
+                if (!step(kb + 4, c20, c21, g2, c00, c01, g0)) break;
             }
         }
     } else {
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         const long long tot = clock64() - tstart;
         if (warp == 0) o[0] = tr[0];
         if (warp == 1) { o[1] = tr[0]; o[2] = tr[1]; o[3] = tr[2]; o[4] = tot; }
-        if (warp == 2) { o[5] = tr[0]; o[6] = tot; }
+        if (warp == 2) { o[5] = tr[0]; o[6] = tot; o[10] = tr[1]; o[11] = tr[2]; }
         if (warp == 2 + kDqWarps) { o[7] = tr[0]; o[8] = tot; }
         if (warp == 0) o[9] = tr[3];
     }

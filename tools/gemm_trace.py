@@ -32,7 +32,8 @@ def main():
     lib.mobi_debug_read_trace.argtypes = [C.c_void_p, C.c_int]
     _lib.check(lib.mobi_debug_read_trace(buf.ctypes.data, n))
     names = ["tma wait empty", "mma wait acc_empty", "mma wait full_b", "mma wait full_a", "mma loop total",
-             "dq wait empty", "dq loop total", "epi wait acc_full", "epi loop total", "tiles"]
+             "dq wait empty", "dq loop total", "epi wait acc_full", "epi loop total", "tiles", "dq compute next",
+             "dq wait::st"]
     for i, nm in enumerate(names):
         col = buf[:, i].astype(np.float64)
         print(f"{nm:22s} mean {col.mean():12.0f}  min {col.min():12.0f}  max {col.max():12.0f}")
