@@ -10,7 +10,7 @@ import subprocess
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libmobi_b200.so"
+LIB_PATH = Path(os.environ.get("MOBI_LIB_PATH", PKG / "libmobi_b200.so"))  # override: dev experiments
 
 MOBI_OK, MOBI_EINVAL, MOBI_ERUNTIME = 0, 1, 2
 

@@ -322,8 +322,8 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
     if (g_impl_override == 2) {  // traced tcgen05 kernel (development hook)
         static unsigned long long* tbuf = nullptr;
-        if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, 16 * 1024 * sizeof(unsigned long long)));
-        MOBI_CUDA(cudaMemsetAsync(tbuf, 0, 16 * 1024 * sizeof(unsigned long long), st));
+        if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
+        MOBI_CUDA(cudaMemsetAsync(tbuf, 0, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long), st));
         g_trace_buf = tbuf;
         return launch_gemm_tc(L, yb, T, st, tbuf);
     }
@@ -349,7 +349,9 @@ int mobi_debug_set_impl(int impl) {
 MOBI_API int mobi_debug_read_trace(unsigned long long* host, int n_cta) {
     if (!g_trace_buf) return set_error(MOBI_EINVAL, "no trace recorded");
     MOBI_CUDA(cudaDeviceSynchronize());
-    MOBI_CUDA(cudaMemcpy(host, g_trace_buf, (size_t)n_cta * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    MOBI_CUDA(cudaMemcpy(host, g_trace_buf, (size_t)(16 * 1024 + 16 * 1024) * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+    (void)n_cta;
     return MOBI_OK;
 }
 

@@ -28,7 +28,10 @@ namespace {
 
 using namespace sm100;
 
-constexpr int NSTAGE = 4;
+#ifndef MOBI_NSTAGE
+#define MOBI_NSTAGE 4
+#endif
+constexpr int NSTAGE = MOBI_NSTAGE;
 constexpr int kSched = 4;  // tile-id ring depth
 constexpr int kDqWarps = 16;                       // 4 per TMEM lane quarter
 constexpr int kThreads = 32 * (2 + kDqWarps + 4);  // TMA, MMA, dequant, epilogue
@@ -63,7 +66,7 @@ struct Params {
 template <bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                                                    const Params p) {
-    long long tr[4] = {0, 0, 0, 0};
+    long long tr[6] = {0, 0, 0, 0, 0, 0};
 #define TW(i, stmt)                                   \
     do {                                              \
         if (TRACE) {                                  \
@@ -173,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             const uint32_t idesc = idesc_f16(128, n_mma, 0);
             TW(0, mbar_wait(acc_empty, (tc & 1) ^ 1));
             tc_fence_after();
+            long long t_tile0 = TRACE ? clock64() : 0;
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
@@ -191,6 +195,10 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 }
                 __syncwarp();
             }
+            if (TRACE && lane == 0 && tc < 8) {  // per-tile: N and cycles from first wait to last issue
+                p.trace[16 * 1024 + (blockIdx.x * 8 + tc) * 2] = (unsigned long long)n_mma;
+                p.trace[16 * 1024 + (blockIdx.x * 8 + tc) * 2 + 1] = (unsigned long long)(clock64() - t_tile0);
+            }
         }
     } else if (warp < 2 + kDqWarps) {
         // ---------------- dequantizers ----------------
@@ -203,7 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
         for (uint32_t ti = 0;; ++ti, base += kb_n) {
-            const int tile = next_tile(ti);
+            int tile;
+            TW(5, tile = next_tile(ti));
             if (tile < 0) break;
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
             const int rt = tile % p.n_row_tiles;
@@ -263,8 +272,8 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 const uint32_t ph = (itk / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
                 tc_fence_after();
-                tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
-                fetch(kb + 6, ca, cb, ga);  // refill the consumed slot three of this warp's k-blocks ahead
+                TW(3, tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v));
+                TW(4, fetch(kb + 6, ca, cb, ga));  // refill the consumed slot three of this warp's k-blocks ahead
                 if (kb + 2 < kb_n) TW(1, dq(na, nb, gn, v));
                 TW(2, tmem_st_wait());
                 tc_fence_before();
@@ -336,7 +345,9 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         const long long tot = clock64() - tstart;
         if (warp == 0) o[0] = tr[0];
         if (warp == 1) { o[1] = tr[0]; o[2] = tr[1]; o[3] = tr[2]; o[4] = tot; }
-        if (warp == 2) { o[5] = tr[0]; o[6] = tot; o[10] = tr[1]; o[11] = tr[2]; }
+        if (warp == 2) {
+            o[5] = tr[0]; o[6] = tot; o[10] = tr[1]; o[11] = tr[2]; o[12] = tr[3]; o[13] = tr[4]; o[14] = tr[5];
+        }
         if (warp == 2 + kDqWarps) { o[7] = tr[0]; o[8] = tot; }
         if (warp == 0) o[9] = tr[3];
     }

@@ -27,16 +27,23 @@ def main():
     torch.cuda.synchronize()
     set_debug_impl(0)
     n = torch.cuda.get_device_properties(0).multi_processor_count
-    buf = np.zeros((n, 16), np.uint64)
+    full = np.zeros(32 * 1024, np.uint64)
+    buf = full[: 16 * 1024].reshape(1024, 16)[:n]
     lib = _lib.lib()
     lib.mobi_debug_read_trace.argtypes = [C.c_void_p, C.c_int]
-    _lib.check(lib.mobi_debug_read_trace(buf.ctypes.data, n))
+    _lib.check(lib.mobi_debug_read_trace(full.ctypes.data, n))
     names = ["tma wait empty", "mma wait acc_empty", "mma wait full_b", "mma wait full_a", "mma loop total",
              "dq wait empty", "dq loop total", "epi wait acc_full", "epi loop total", "tiles", "dq compute next",
-             "dq wait::st"]
+             "dq wait::st", "dq st16 issue", "dq fetch issue", "dq next_tile"]
     for i, nm in enumerate(names):
         col = buf[:, i].astype(np.float64)
         print(f"{nm:22s} mean {col.mean():12.0f}  min {col.min():12.0f}  max {col.max():12.0f}")
+    per = full[16 * 1024:].reshape(1024, 8, 2)[:n].reshape(-1, 2)
+    per = per[per[:, 0] > 0]
+    for N in sorted(set(per[:, 0].tolist())):
+        c = per[per[:, 0] == N][:, 1].astype(np.float64)
+        print(f"tile N={N:4d}: {len(c):4d} tiles  cycles mean {c.mean():9.0f} min {c.min():9.0f} max {c.max():9.0f}"
+              f"   ideal MMA {64 * 4 * 137.5 * N / 256:9.0f}")
 
 
 if __name__ == "__main__":
