@@ -59,6 +59,17 @@ struct Params {
     unsigned long long* trace;
 };
 
+// One 64-k block: four K=16 MMAs, D at TMEM column 0, A (fp16 weights) at TMEM column acol,
+// B (fp16 tokens) from the 128B-swizzled smem stage; N is a compile-time constant so the
+// instruction descriptor is an immediate.
+template <uint32_t N>
+__device__ __forceinline__ void issue_kblock_ts(uint32_t acol, uint64_t bdesc, bool first) {
+    constexpr uint32_t idesc = idesc_f16(128, N, 0);
+#pragma unroll
+    for (int j = 0; j < kKBlock / 16; ++j)
+        mma_ts_f16(0u, acol + j * 8, bdesc + (uint64_t)(j * 2), idesc, (!first || j != 0) ? 1u : 0u);
+}
+
 // TRACE=true: clock64 accounting of each role's barrier waits (debug hook impl 2), written to
 // p.trace[cta][0..15]: 0 tma wait empty | 1 mma wait acc_empty | 2 mma wait full_b | 3 mma wait
 // full_a | 4 mma loop | 5 dequant(w2) wait empty | 6 dequant(w2) loop | 7 epi(w18) wait acc_full |
@@ -95,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 256 + kYStageBytes);
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
 
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1);
@@ -115,7 +126,10 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    // the CTA owns all 512 TMEM columns, so the allocation base is column 0 / lane 0; using the
+    // constant keeps every tcgen05 operand in uniform registers (no per-instruction R2UR waterfall)
+    if (*tmem_slot != 0) __trap();
+    constexpr uint32_t tmem = 0;
 
     const int n_tok_tiles = p.meta[0];
     const int total = n_tok_tiles * p.n_row_tiles;
@@ -172,8 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
             const int tile = next_tile(ti);
             if (tile < 0) break;
             const TokTile tt = p.tiles[tile / p.n_row_tiles];
-            const uint32_t n_mma = (uint32_t)round_up(tt.n, 16);
-            const uint32_t idesc = idesc_f16(128, n_mma, 0);
+            // N class: 16, or a multiple of 32 (constant instruction descriptors per class)
+            const uint32_t n_mma = tt.n <= 16 ? 16u : (uint32_t)round_up(tt.n, 32);
             TW(0, mbar_wait(acc_empty, (tc & 1) ^ 1));
             tc_fence_after();
             long long t_tile0 = TRACE ? clock64() : 0;
@@ -183,12 +197,20 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                 TW(1, mbar_wait(&full_b[s], ph));
                 TW(2, mbar_wait(&full_a[s], ph));
                 tc_fence_after();
-                if (lane == 0) {
+                if (elect_one_sync()) {
                     const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
-#pragma unroll
-                    for (int j = 0; j < kKBlock / 16; ++j) {
-                        mma_ts_f16(tmem, tmem + kACol0 + s * 32 + j * 8, bdesc + (uint64_t)(j * 2), idesc,
-                                   (kb | j) != 0);
+                    const uint32_t acol = tmem + kACol0 + s * 32;
+                    const bool first = kb == 0;
+                    switch (n_mma) {
+                        case 16: issue_kblock_ts<16>(acol, bdesc, first); break;
+                        case 32: issue_kblock_ts<32>(acol, bdesc, first); break;
+                        case 64: issue_kblock_ts<64>(acol, bdesc, first); break;
+                        case 96: issue_kblock_ts<96>(acol, bdesc, first); break;
+                        case 128: issue_kblock_ts<128>(acol, bdesc, first); break;
+                        case 160: issue_kblock_ts<160>(acol, bdesc, first); break;
+                        case 192: issue_kblock_ts<192>(acol, bdesc, first); break;
+                        case 224: issue_kblock_ts<224>(acol, bdesc, first); break;
+                        default: issue_kblock_ts<256>(acol, bdesc, first); break;
                     }
                     mma_commit(&empty[s]);
                     if (kb == kb_n - 1) mma_commit(acc_full);

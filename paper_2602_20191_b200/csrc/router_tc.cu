@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     uint64_t* acc_full = bars + 2 * RS; // [2]
     uint64_t* acc_empty = acc_full + 2; // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         for (int s = 0; s < RS; ++s) {
             mbar_init(&full[s], 1);
@@ -58,11 +58,12 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 256);
+    if (warp == 1) tmem_alloc(tmem_slot, 512);  // all columns: base is the constant 0
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    if (*tmem_slot != 0) __trap();
+    constexpr uint32_t tmem = 0;
     const int total = p.n_mt * p.n_nt;
 
     if (warp == 0) {
@@ -86,7 +87,6 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
             const int nt = tile / p.n_mt;
             const uint32_t n_mma = (uint32_t)std::min<int64_t>(RN, round_up(p.h - (int64_t)nt * RN, 16));
-            const uint32_t idesc = idesc_f16(RM, n_mma, 1);
             const int buf = tc & 1;
             mbar_wait(&acc_empty[buf], ((tc >> 1) & 1) ^ 1);
             tc_fence_after();
@@ -94,13 +94,21 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
                 const int s = it % RS;
                 mbar_wait(&full[s], (it / RS) & 1);
                 tc_fence_after();
-                if (lane == 0) {
+                if (elect_one_sync()) {
                     const uint32_t a = smem_u32(smem + s * 2 * kAB);
                     const uint64_t adesc = sdesc_sw128(a), bdesc = sdesc_sw128(a + kAB);
+                    const uint32_t d = tmem + buf * RN;
+                    if (n_mma == RN) {
+                        constexpr uint32_t idesc = idesc_f16(RM, RN, 1);
 #pragma unroll
-                    for (int j = 0; j < kKBlock / 16; ++j)
-                        mma_ss_f16(tmem + buf * RN, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc,
-                                   (kb | j) != 0);
+                        for (int j = 0; j < kKBlock / 16; ++j)
+                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb | j) != 0);
+                    } else {  // partial hidden tile (h % 128 != 0): runtime descriptor
+                        const uint32_t idesc = idesc_f16(RM, n_mma, 1);
+#pragma unroll
+                        for (int j = 0; j < kKBlock / 16; ++j)
+                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb | j) != 0);
+                    }
                     mma_commit(&empty[s]);
                     if (kb == p.kblocks - 1) mma_commit(&acc_full[buf]);
                 }
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 256);
+    if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 int sm_count() {

@@ -17,13 +17,16 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int N, int iters, int 
                                                unsigned long long* out, const CUtensorMap* tmap, int use_tma) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 160 * 1024);
-    uint64_t* tbar = bar + 1;
+    uint64_t* tbar = bar + 1;  // [0] TMA, [1] pre-completed, [2] commit sink
     __shared__ uint32_t slot;
     __shared__ int done;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         mbar_init(tbar, 1);
+        mbar_init(tbar + 1, 1);
+        mbar_arrive(tbar + 1);   // complete phase 0
+        mbar_init(tbar + 2, 1);
         fence_barrier_init();
         done = 0;
     }
@@ -41,12 +44,16 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int N, int iters, int 
             const uint64_t bdesc = sdesc_sw128(smem_u32(smem + 32768));
             long long t0 = clock64();
             for (int i = 0; i < iters; ++i) {
+                if (mode >= 3) tc_fence_after();                 // per-k-block fence (GEMM pattern)
+                if (mode >= 4) mbar_wait(tbar + 1, 0);            // already-complete barrier probe
                 for (int j = 0; j < 4; ++j) {
                     if (mode == 0)
                         mma_ss_f16(tmem, adesc + j * 2, bdesc + j * 2, idesc, 1);
                     else
-                        mma_ts_f16(tmem, tmem + 256 + j * 8, bdesc + j * 2, idesc, 1);
+                        mma_ts_f16(tmem, tmem + 256 + (mode >= 5 ? (i & 3) * 32 : 0) + j * 8, bdesc + j * 2, idesc,
+                                   (mode >= 6) ? ((i & 63) | j) != 0 : 1);
                 }
+                if (mode >= 2) mma_commit(tbar + 2);              // per-k-block commit
             }
             mma_commit(bar);
             mbar_wait(bar, 0);
