@@ -158,7 +158,7 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L) {
     CHECK_ARG(d->router_hidden >= 1, "RouterState: hidden width must be >= 1");
     CHECK_ARG(d->w1 && d->b1 && d->w2 && d->b2, "RouterState: missing router weights");
     L->h = d->router_hidden;
-    L->out_pad = round_up(L->out, kRowTile);
+    L->out_pad = round_up(L->out, 2 * kRowTile);  // row tiles come in pairs (GEMM CTA clusters)
     L->in_pad = round_up(L->in, kKBlock);
     L->kblocks = L->in_pad / kKBlock;
     L->h_pad = round_up(L->h, 128);

@@ -32,7 +32,8 @@ using namespace sm100;
 #define MOBI_NSTAGE 4
 #endif
 constexpr int NSTAGE = MOBI_NSTAGE;
-constexpr int kSched = 4;  // tile-id ring depth
+constexpr int kBoxRows = 32;                      // TMA box: 32 token rows x 64 k (4 KiB)
+constexpr int kBoxBytes = kBoxRows * kKBlock * 2;
 constexpr int kDqWarps = 16;                       // 4 per TMEM lane quarter
 constexpr int kThreads = 32 * (2 + kDqWarps + 4);  // TMA, MMA, dequant, epilogue
 constexpr int kStageBytes = kTokTile * kKBlock * 2;  // 32 KiB
@@ -75,8 +76,8 @@ __device__ __forceinline__ void issue_kblock_ts(uint32_t acol, uint64_t bdesc, b
 // full_a | 4 mma loop | 5 dequant(w2) wait empty | 6 dequant(w2) loop | 7 epi(w18) wait acc_full |
 // 8 epi(w18) loop | 9 tiles
 template <bool TRACE>
-__global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
-                                                                   const Params p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    mobi_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
     long long tr[6] = {0, 0, 0, 0, 0, 0};
 #define TW(i, stmt)                                   \
     do {                                              \
@@ -98,10 +99,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     uint64_t* empty = bars + 2 * NSTAGE;      // [NSTAGE] MMAs reading the stage completed
     uint64_t* acc_full = bars + 3 * NSTAGE;   // accumulator ready for the epilogue
     uint64_t* acc_empty = acc_full + 1;       // epilogue drained the accumulator (4 warps)
-    uint64_t* sched_full = acc_empty + 1;       // [kSched] tile id published
-    uint64_t* sched_empty = sched_full + kSched; // [kSched] all consumer warps read it
-    int32_t* sched = reinterpret_cast<int32_t*>(sched_empty + kSched);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched + kSched);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
     __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 256);
     int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 256 + kYStageBytes);
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
@@ -111,70 +109,55 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1);
             mbar_init(&full_a[s], kDqWarps / 2);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], 2);  // MMA completion of BOTH CTAs of the pair (shared B stages)
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
-        for (int i = 0; i < kSched; ++i) {
-            mbar_init(&sched_full[i], 1);
-            mbar_init(&sched_empty[i], 1 + kDqWarps + 4);
-        }
         fence_barrier_init();
         prefetch_tmap(&tmap_x);
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // peer barriers initialised before any multicast lands
     tc_fence_after();
     // the CTA owns all 512 TMEM columns, so the allocation base is column 0 / lane 0; using the
     // constant keeps every tcgen05 operand in uniform registers (no per-instruction R2UR waterfall)
     if (*tmem_slot != 0) __trap();
     constexpr uint32_t tmem = 0;
 
+    // Static schedule over CTA pairs (clusters of 2): a pair works on one token tile and two
+    // adjacent 128-row weight tiles; each CTA TMA-loads half of the token tile's 32-row boxes and
+    // multicasts them to both, so every CTA receives the full B tile for half the L2 traffic.
+    const uint32_t rank = cluster_ctarank();
     const int n_tok_tiles = p.meta[0];
-    const int total = n_tok_tiles * p.n_row_tiles;
+    const int n_pairs_row = p.n_row_tiles / 2;
+    const int total = n_tok_tiles * n_pairs_row;
     const int kb_n = (int)p.kblocks;
-    // Dynamic tile scheduler: the TMA warp claims tile ids from a global counter (token tiles are
-    // listed largest first, so the costliest tiles are claimed first) and publishes them through
-    // an smem ring; every other role reads the same sequence.
-    auto next_tile = [&](uint32_t ti) -> int {
-        const int slot = ti % kSched;
-        const uint32_t ph = (ti / kSched) & 1;
-        int tile;
-        if (warp == 0) {
-            mbar_wait(&sched_empty[slot], ph ^ 1);
-            if (lane == 0) {
-                const int t = atomicAdd(p.tile_counter, 1);
-                sched[slot] = t < total ? t : -1;
-                mbar_arrive(&sched_full[slot]);
-            }
-            __syncwarp();
-            mbar_wait(&sched_full[slot], ph);
-            tile = sched[slot];
-        } else {
-            mbar_wait(&sched_full[slot], ph);
-            tile = sched[slot];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sched_empty[slot]);
-        }
-        return tile;
+    const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+    auto tile_of = [&](int pair, TokTile& tt, int& rt) {
+        tt = p.tiles[pair / n_pairs_row];
+        rt = (pair % n_pairs_row) * 2 + (int)rank;
     };
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         uint32_t it = 0;
-        for (uint32_t ti = 0;; ++ti) {
-            const int tile = next_tile(ti);
-            if (tile < 0) break;
+        for (int pair = cid; pair < total; pair += ncl) {
+            TokTile tt;
+            int rt;
+            tile_of(pair, tt, rt);
             if (TRACE && lane == 0) ++tr[3];
-            const TokTile tt = p.tiles[tile / p.n_row_tiles];
+            const int nbox = (tt.n + kBoxRows - 1) / kBoxRows;
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&full_b[s], kStageBytes);
-                    tma_load_2d(stage_b + s * kStageBytes, &tmap_x, &full_b[s], kb * kKBlock, tt.row0);
+                    mbar_arrive_expect_tx(&full_b[s], nbox * kBoxBytes);
+                    for (int j = (int)rank; j < nbox; j += 2)
+                        tma_load_2d_mc(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, &full_b[s], kb * kKBlock,
+                                       tt.row0 + j * kBoxRows, (uint16_t)0x3);
                 }
                 __syncwarp();
             }
@@ -182,10 +165,10 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         uint32_t it = 0, tc = 0;
-        for (uint32_t ti = 0;; ++ti, ++tc) {
-            const int tile = next_tile(ti);
-            if (tile < 0) break;
-            const TokTile tt = p.tiles[tile / p.n_row_tiles];
+        for (int pair = cid; pair < total; pair += ncl, ++tc) {
+            TokTile tt;
+            int rt;
+            tile_of(pair, tt, rt);
             // N class: 16, or a multiple of 32 (constant instruction descriptors per class)
             const uint32_t n_mma = tt.n <= 16 ? 16u : (uint32_t)round_up(tt.n, 32);
             TW(0, mbar_wait(acc_empty, (tc & 1) ^ 1));
@@ -212,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
                         case 224: issue_kblock_ts<224>(acol, bdesc, first); break;
                         default: issue_kblock_ts<256>(acol, bdesc, first); break;
                     }
-                    mma_commit(&empty[s]);
+                    mma_commit_mc(&empty[s], (uint16_t)0x3);  // frees the shared B stage in both CTAs
                     if (kb == kb_n - 1) mma_commit(acc_full);
                 }
                 __syncwarp();
@@ -232,12 +215,10 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         const int hh = idx / 8;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
-        for (uint32_t ti = 0;; ++ti, base += kb_n) {
-            int tile;
-            TW(5, tile = next_tile(ti));
-            if (tile < 0) break;
-            const TokTile tt = p.tiles[tile / p.n_row_tiles];
-            const int rt = tile % p.n_row_tiles;
+        for (int pair = cid; pair < total; pair += ncl, base += kb_n) {
+            TokTile tt;
+            int rt;
+            tile_of(pair, tt, rt);
             const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
             const bool rv = R < p.out;
             const uint32_t mw = p.mt.maskword[tt.mask];
@@ -318,11 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
         const int et = threadIdx.x - 32 * (2 + kDqWarps);  // 0..127
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t tc = 0;
-        for (uint32_t ti = 0;; ++ti, ++tc) {
-            const int tile = next_tile(ti);
-            if (tile < 0) break;
-            const TokTile tt = p.tiles[tile / p.n_row_tiles];
-            const int rt = tile % p.n_row_tiles;
+        for (int pair = cid; pair < total; pair += ncl, ++tc) {
+            TokTile tt;
+            int rt;
+            tile_of(pair, tt, rt);
             TW(0, mbar_wait(acc_full, tc & 1));
             tc_fence_after();
             epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
@@ -376,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) mobi_gemm_tc_kernel(const __grid_
 #undef TW
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // no CTA leaves while its peer may still multicast into it
     if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -435,7 +416,7 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     }
     if (!L->tmap_x) {
         L->tmap_x = new CUtensorMap;
-        int rc = make_tmap_2d(L->tmap_x, L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad, kTokTile);
+        int rc = make_tmap_2d(L->tmap_x, L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad, kBoxRows);
         if (rc) {
             delete L->tmap_x;
             L->tmap_x = nullptr;
@@ -459,8 +440,8 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     p.meta = L->meta;
     p.y = y;
     p.vec_y = (L->out % 8 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
-    const int64_t max_total = (int64_t)p.n_row_tiles * L->max_tiles;
-    const int grid = (int)std::min<int64_t>(sm_count(), max_total);
+    const int64_t max_pairs = (int64_t)(p.n_row_tiles / 2) * L->max_tiles;
+    const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
     p.trace = trace;
     p.tile_counter = L->meta + 32;
     if (trace)

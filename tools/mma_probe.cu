@@ -13,48 +13,49 @@
 
 using namespace mobi::sm100;
 
-__global__ void __launch_bounds__(256, 1) probe(int mode, int N, int iters, int store_warps,
-                                               unsigned long long* out, const CUtensorMap* tmap, int use_tma) {
+template <int MODE, int N>
+__device__ __forceinline__ void issue_loop(int iters, uint64_t adesc, uint64_t bdesc, uint64_t* sink, uint64_t* done_bar) {
+    constexpr uint32_t idesc = idesc_f16(128, N, 0);
+    for (int i = 0; i < iters; ++i) {
+        if (MODE >= 3) tc_fence_after();
+        if (MODE >= 4) mbar_wait(done_bar, 0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (MODE == 0)
+                mma_ss_f16(0u, adesc + j * 2, bdesc + j * 2, idesc, 1u);
+            else
+                mma_ts_f16(0u, 256u + j * 8, bdesc + j * 2, idesc, 1u);
+        }
+        if (MODE >= 2) mma_commit(sink);
+    }
+}
+
+template <int MODE, int N>
+__global__ void __launch_bounds__(256, 1) probe(int iters, int store_warps, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 160 * 1024);
-    uint64_t* tbar = bar + 1;  // [0] TMA, [1] pre-completed, [2] commit sink
     __shared__ uint32_t slot;
     __shared__ int done;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
-        mbar_init(tbar, 1);
-        mbar_init(tbar + 1, 1);
-        mbar_arrive(tbar + 1);   // complete phase 0
-        mbar_init(tbar + 2, 1);
+        mbar_init(bar + 1, 1);
+        mbar_arrive(bar + 1);  // phase 0 complete
+        mbar_init(bar + 2, 1);
         fence_barrier_init();
         done = 0;
     }
-    // zero the operands
     for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tmem_alloc(&slot, 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = slot;
     if (warp == 0) {
-        if (lane == 0) {
-            const uint32_t idesc = idesc_f16(128, N, 0);
+        if (elect_one_sync()) {
             const uint64_t adesc = sdesc_sw128(smem_u32(smem));
             const uint64_t bdesc = sdesc_sw128(smem_u32(smem + 32768));
             long long t0 = clock64();
-            for (int i = 0; i < iters; ++i) {
-                if (mode >= 3) tc_fence_after();                 // per-k-block fence (GEMM pattern)
-                if (mode >= 4) mbar_wait(tbar + 1, 0);            // already-complete barrier probe
-                for (int j = 0; j < 4; ++j) {
-                    if (mode == 0)
-                        mma_ss_f16(tmem, adesc + j * 2, bdesc + j * 2, idesc, 1);
-                    else
-                        mma_ts_f16(tmem, tmem + 256 + (mode >= 5 ? (i & 3) * 32 : 0) + j * 8, bdesc + j * 2, idesc,
-                                   (mode >= 6) ? ((i & 63) | j) != 0 : 1);
-                }
-                if (mode >= 2) mma_commit(tbar + 2);              // per-k-block commit
-            }
+            issue_loop<MODE, N>(iters, adesc, bdesc, bar + 2, bar + 1);
             mma_commit(bar);
             mbar_wait(bar, 0);
             long long t1 = clock64();
@@ -62,29 +63,17 @@ __global__ void __launch_bounds__(256, 1) probe(int mode, int N, int iters, int 
             done = 1;
         }
         __syncwarp();
-    } else if (warp == 1 && use_tma) {
-        if (lane == 0) {
-            uint32_t ph = 0;
-            for (int i = 0; i < iters; ++i) {
-                mbar_arrive_expect_tx(tbar, 32768);
-                tma_load_2d(smem + 65536 + (i & 1) * 32768 * 0, tmap, tbar, 0, (blockIdx.x * 256) % 8192);
-                mbar_wait(tbar, ph);
-                ph ^= 1;
-                if (*(volatile int*)&done) break;
-            }
-        }
-        __syncwarp();
     } else if (warp >= 2 && warp < 2 + store_warps) {
         uint32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const uint32_t lb = (uint32_t)(32 * (warp % 4)) << 16;
         for (int i = 0; i < iters * 4 && !*(volatile int*)&done; ++i) {
-            tmem_st8(tmem + lb + 256 + 128 + (i & 7) * 8, v);
+            tmem_st8(lb + 256 + 128 + (i & 7) * 8, v);
             tmem_st_wait();
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, 512);
+    if (warp == 0) tmem_dealloc(0, 512);
 }
 
 // L2 -> SM streaming bandwidth with TMA: each CTA keeps `depth` 32 KiB loads in flight over a
@@ -141,35 +130,31 @@ int main() {
     CUtensorMap* dmap;
     cudaMalloc(&dmap, sizeof(hmap));
     cudaMemcpy(dmap, &hmap, sizeof(hmap), cudaMemcpyHostToDevice);
-    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024 + 64);
     const int iters = 2000;
-    struct Cfg { int mode, N, store, tma, grid; const char* name; } cfgs[] = {
-        {0, 256, 0, 0, 1, "SS N=256 1 SM"},        {0, 256, 0, 0, nsm, "SS N=256 all SMs"},
-        {0, 128, 0, 0, nsm, "SS N=128 all SMs"},   {1, 256, 0, 0, 1, "TS N=256 1 SM"},
-        {1, 256, 0, 0, nsm, "TS N=256 all SMs"},   {1, 128, 0, 0, nsm, "TS N=128 all SMs"},
-        {1, 256, 4, 0, nsm, "TS N=256 + 4 st warps"}, {1, 256, 0, 1, nsm, "TS N=256 + TMA 32KB stream"},
-        {0, 256, 0, 1, nsm, "SS N=256 + TMA stream"}, {1, 256, 4, 1, nsm, "TS N=256 + st + TMA"},
-    };
-    for (auto& c : cfgs) {
-        cudaMemset(d_out, 0, sizeof(unsigned long long) * nsm);
-        probe<<<c.grid, 256, 161 * 1024 + 64>>>(c.mode, c.N, iters, c.store, d_out, dmap, c.tma);
+    auto runp = [&](auto kern, int N, int store, const char* name) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024 + 64);
+        kern<<<nsm, 256, 161 * 1024 + 64>>>(iters, store, d_out);
         cudaError_t e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) {
-            printf("%s: error %s\n", c.name, cudaGetErrorString(e));
-            return 1;
-        }
+        if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); exit(1); }
         unsigned long long h[256];
-        cudaMemcpy(h, d_out, sizeof(unsigned long long) * c.grid, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h, d_out, sizeof(unsigned long long) * nsm, cudaMemcpyDeviceToHost);
         double avg = 0;
-        for (int i = 0; i < c.grid; ++i) avg += h[i];
-        avg /= c.grid;
+        for (int i = 0; i < nsm; ++i) avg += h[i];
+        avg /= nsm;
         double per = avg / (iters * 4.0);
-        double flops = 2.0 * 128 * c.N * 16;
-        printf("%-32s cycles/MMA %8.1f (ideal %5.1f)  chip TFLOP/s at %d MHz: %7.1f\n", c.name, per, 128.0 * c.N / 256,
-               clk / 1000, flops / per * (clk * 1e3) * nsm / 1e12);
-    }
+        printf("%-30s N=%3d cycles/MMA %7.1f (ideal %5.1f)  chip TFLOP/s @%d MHz: %7.1f\n", name, N, per, 128.0 * N / 256,
+               clk / 1000, 2.0 * 128 * N * 16 / per * (clk * 1e3) * nsm / 1e12);
+    };
+    runp(probe<0, 16>, 16, 0, "SS");  runp(probe<0, 64>, 64, 0, "SS");  runp(probe<0, 128>, 128, 0, "SS");
+    runp(probe<0, 256>, 256, 0, "SS");
+    runp(probe<1, 16>, 16, 0, "TS");  runp(probe<1, 64>, 64, 0, "TS");  runp(probe<1, 128>, 128, 0, "TS");
+    runp(probe<1, 256>, 256, 0, "TS");
+    runp(probe<1, 256>, 256, 8, "TS + 8 st warps");
+    runp(probe<2, 16>, 16, 0, "TS +commit/kblk"); runp(probe<2, 256>, 256, 0, "TS +commit/kblk");
+    runp(probe<3, 16>, 16, 0, "TS +commit+fence"); runp(probe<3, 256>, 256, 0, "TS +commit+fence");
+    runp(probe<4, 16>, 16, 0, "TS +c+f+trywait"); runp(probe<4, 256>, 256, 0, "TS +c+f+trywait");
     // L2 bandwidth: 64 MiB buffer (L2 resident) and 1 GiB (HBM)
-    for (long long rows : {8192LL * 64, 8192LL * 1024}) {
+    for (long long rows : {8192LL * 64}) {
         void* big;
         cudaMalloc(&big, rows * 128);
         cudaMemset(big, 1, rows * 128);
