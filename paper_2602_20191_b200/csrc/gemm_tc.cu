@@ -28,6 +28,9 @@ namespace {
 
 using namespace sm100;
 
+#ifndef MOBI_ABLATE
+#define MOBI_ABLATE 0  // development ablations: 1 = no code loads, 2 = no dequantization
+#endif
 #ifndef MOBI_NSTAGE
 #define MOBI_NSTAGE 4
 #endif
@@ -254,6 +257,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
             }
             auto fetch = [&](int kb, uint4& c0, uint4& c1, float2& gc) {
+#if MOBI_ABLATE >= 1
+                c0 = make_uint4(kb, kb, kb, kb); c1 = c0; gc = make_float2(1.f, 0.f);
+                return;
+#endif
                 if (kb < kb_n) {
                     ld(kb, c0, c1);
                     gc = ldc(gp);
@@ -277,7 +284,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 TW(3, tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v));
                 TW(4, fetch(kb + 6, ca, cb, ga));  // refill the consumed slot three of this warp's k-blocks ahead
+#if MOBI_ABLATE >= 2
+                (void)na; (void)nb; (void)gn;
+#else
                 if (kb + 2 < kb_n) TW(1, dq(na, nb, gn, v));
+#endif
                 TW(2, tmem_st_wait());
                 tc_fence_before();
                 __syncwarp();
