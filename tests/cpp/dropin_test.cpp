@@ -1,0 +1,105 @@
+// dropin_test.cpp -- the reference's own hot-path calls next to the drop-in (include/mobi_b200.hpp):
+// builds a layer with the reference's decompose/RouterState, runs router::score + gate_hard +
+// forward_elastic from the reference and the same calls through the B200 shim, and compares
+// (scores within 2e-3+1e-4|S|, masks equal outside a 1e-2 margin, outputs rel-L2 per token <= 1e-2).
+// Built by tests/cpp/Makefile against /root/reference (test infrastructure), run by
+// tests/test_cpp_dropin.py on a GPU box.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "mobi/bench/calibset.hpp"
+#include "mobi/router.hpp"
+#include "mobi/slicer.hpp"
+#include "mobi_b200.hpp"
+
+using namespace mobi;
+
+static int fails = 0;
+#define EXPECT(c, ...)                 \
+    do {                               \
+        if (!(c)) {                    \
+            std::printf("FAIL: " __VA_ARGS__); \
+            std::printf("\n");         \
+            ++fails;                   \
+        }                              \
+    } while (0)
+
+int run_case(size_t out, size_t in, size_t gs, size_t T, unsigned seed) {
+    Rng rng(seed);
+    Matrix w(out, in);
+    for (size_t i = 0; i < w.size(); ++i) w[i] = 0.02 * rng.normal();
+    qcore::GroupStats gst = qcore::GroupStats::from_weights(w, gs);
+    qcore::ClipParams cp = qcore::ClipParams::identity_init(gst.min.size(), 4.0);
+    qcore::QuantParams base = qcore::params_from_clip(w, gst, cp, 2, gs);
+    slicer::SliceStack st = slicer::decompose(w, base, {2, 2, 2, 2});
+    router::RouterState rs = router::RouterState::init(in, 3, 1000, rng);
+    for (auto& v : rs.w2.vec()) v = 0.3 * rng.normal();
+    for (auto& v : rs.b2) v = 0.1 * rng.normal();
+    bench::CalibSet cs = bench::gen_calibset(1, T, in, 0.05, 8.0, seed + 1);
+    Matrix x = cs.batches[0];
+    // feed both sides the same bf16-representable inputs and device-rounded router weights
+    for (size_t i = 0; i < x.size(); ++i) x[i] = mobi_b200::from_bf16(mobi_b200::to_bf16(x[i]));
+    for (size_t i = 0; i < rs.w1.size(); ++i) rs.w1[i] = mobi_b200::from_bf16(mobi_b200::to_bf16(rs.w1[i]));
+    for (auto& v : rs.w2.vec()) v = static_cast<float>(v);
+    for (auto& v : rs.b2) v = static_cast<float>(v);
+
+    mobi_b200::Layer layer(st, rs);
+    Matrix s_ref = router::score(x, rs);
+    Matrix s_gpu = layer.score(x);
+    double max_ds = 0;
+    for (size_t i = 0; i < s_ref.size(); ++i) {
+        double d = std::fabs(s_ref[i] - s_gpu[i]);
+        max_ds = std::max(max_ds, d);
+        EXPECT(d <= 2e-3 + 1e-4 * std::fabs(s_ref[i]), "score %zu: %g vs %g", i, s_ref[i], s_gpu[i]);
+    }
+    double delta = router::calibrate_threshold(s_ref.vec(), 1.0 / 6.0);
+    Matrix g_ref = router::gate_hard(s_ref, delta);
+    Matrix g_gpu;
+    Matrix y_full = layer.forward(x, delta, &g_gpu);
+    size_t flips = 0;
+    for (size_t t = 0; t < T; ++t) {
+        bool near = false;
+        for (size_t j = 0; j < 3; ++j) near |= std::fabs(s_ref(t, j) - delta) <= 1e-2;
+        for (size_t j = 0; j < 3; ++j)
+            if (g_ref(t, j) != g_gpu(t, j)) {
+                ++flips;
+                EXPECT(near, "gate flip outside margin at token %zu", t);
+            }
+    }
+    // forward_elastic with the GPU's own gates: reference vs drop-in
+    Matrix y_ref = router::forward_elastic(x, st, g_gpu, router::GateMode::kHard);
+    Matrix y_gpu = layer.forward_elastic(x, g_gpu);
+    double worst = 0;
+    for (size_t t = 0; t < T; ++t) {
+        double num = 0, den = 0, num2 = 0;
+        for (size_t r = 0; r < out; ++r) {
+            double d = y_gpu(t, r) - y_ref(t, r), d2 = y_full(t, r) - y_ref(t, r);
+            num += d * d;
+            num2 += d2 * d2;
+            den += y_ref(t, r) * y_ref(t, r);
+        }
+        double rel = std::sqrt(num / den), rel2 = std::sqrt(num2 / den);
+        worst = std::max(worst, std::max(rel, rel2));
+        EXPECT(rel <= 1e-2 && rel2 <= 1e-2, "token %zu rel-L2 %g / %g", t, rel, rel2);
+    }
+    // error behaviour mirrors MOBI_CHECK
+    bool threw = false;
+    try {
+        layer.forward_elastic(x, Matrix(T, 2, 1.0));
+    } catch (const std::invalid_argument&) {
+        threw = true;
+    }
+    EXPECT(threw, "gate shape mismatch must throw std::invalid_argument");
+    std::printf("case %zux%zu gs=%zu T=%zu: max|dS| %.2e, gate flips %zu, worst rel-L2 %.2e\n", out, in, gs, T, max_ds,
+                flips, worst);
+    return 0;
+}
+
+int main() {
+    run_case(256, 512, 128, 64, 3);
+    run_case(130, 96, 32, 37, 5);
+    run_case(32, 32, 128, 128, 1);
+    std::printf(fails ? "DROPIN FAIL (%d)\n" : "DROPIN OK\n", fails);
+    return fails ? 1 : 0;
+}

@@ -26,8 +26,46 @@ __device__ __forceinline__ void issue_loop(int iters, uint64_t adesc, uint64_t b
             else
                 mma_ts_f16(0u, 256u + j * 8, bdesc + j * 2, idesc, 1u);
         }
-        if (MODE >= 2) mma_commit(sink);
+        if (MODE == 7) mma_commit_mc(sink, (uint16_t)0x3);
+        else if (MODE >= 2) mma_commit(sink);
     }
+}
+
+// cluster-of-2 variant for the multicast commit
+template <int MODE, int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1) probe_cl(int iters, int store_warps,
+                                                                             unsigned long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 160 * 1024);
+    __shared__ uint32_t slot;
+    const int warp = warp_idx_uniform();
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        mbar_arrive(bar + 1);
+        mbar_init(bar + 2, 2 * 1000000);
+        fence_barrier_init();
+    }
+    for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    if (warp == 0) tmem_alloc(&slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 0 && elect_one_sync()) {
+        const uint64_t adesc = sdesc_sw128(smem_u32(smem));
+        const uint64_t bdesc = sdesc_sw128(smem_u32(smem + 32768));
+        long long t0 = clock64();
+        issue_loop<MODE, N>(iters, adesc, bdesc, bar + 2, bar + 1);
+        mma_commit(bar);
+        mbar_wait(bar, 0);
+        out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0) tmem_dealloc(0, 512);
 }
 
 template <int MODE, int N>
@@ -153,8 +191,11 @@ int main() {
     runp(probe<2, 16>, 16, 0, "TS +commit/kblk"); runp(probe<2, 256>, 256, 0, "TS +commit/kblk");
     runp(probe<3, 16>, 16, 0, "TS +commit+fence"); runp(probe<3, 256>, 256, 0, "TS +commit+fence");
     runp(probe<4, 16>, 16, 0, "TS +c+f+trywait"); runp(probe<4, 256>, 256, 0, "TS +c+f+trywait");
+    runp(probe_cl<2, 16>, 16, 0, "TS cluster2 +commit");
+    runp(probe_cl<7, 16>, 16, 0, "TS cluster2 +commit multicast");
+    runp(probe_cl<7, 256>, 256, 0, "TS cluster2 +commit multicast");
     // L2 bandwidth: 64 MiB buffer (L2 resident) and 1 GiB (HBM)
-    for (long long rows : {8192LL * 64}) {
+    for (long long rows : std::initializer_list<long long>{}) {
         void* big;
         cudaMalloc(&big, rows * 128);
         cudaMemset(big, 1, rows * 128);
