@@ -79,6 +79,8 @@ void free_ws(mobi_layer* L) {
     dfree(L->meta);
     if (L->tmap_x) delete L->tmap_x;
     L->tmap_x = nullptr;
+    if (L->tmap_x2) delete L->tmap_x2;
+    L->tmap_x2 = nullptr;
     L->ws_T = -1;
 }
 
@@ -327,7 +329,8 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
         g_trace_buf = tbuf;
         return launch_gemm_tc(L, yb, T, st, tbuf);
     }
-    return launch_gemm_tc(L, yb, T, st);
+    if (g_impl_override == 3) return launch_gemm_tc(L, yb, T, st);  // 1-CTA kernel (comparison)
+    return launch_gemm_tc2(L, yb, T, st);
 }
 
 }  // namespace

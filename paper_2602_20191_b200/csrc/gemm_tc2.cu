@@ -1,0 +1,367 @@
+// gemm_tc2.cu -- K3/K5 on CTA PAIRS: the nested residual MoBi GEMM with tcgen05.mma.cta_group::2
+// (M = 256 weight rows per pair instruction), un-permute scatter fused in the epilogue.
+//
+// Same math and per-thread roles as gemm_tc.cu (see its header); what changes with cta_group::2:
+//   * A (dequantized fp16 weights, 128 rows) is written by each CTA's dequantizers into its OWN
+//     TMEM; the leader CTA's single MMA thread issues M=256 MMAs that read both CTAs' A;
+//   * B (the bucket's token tile, N tokens) is split: each CTA TMA-loads N/2 token rows into its
+//     own smem and the pair instruction reads both halves -> half the L2->SM bytes and half the
+//     smem operand traffic per SM compared with the 1-CTA kernel (which was B-bandwidth bound);
+//   * D: each CTA's TMEM holds its 128 rows x all N tokens;
+//   * barriers: the peer's TMA completes on the leader's full_b, the peer's dequantizers and
+//     epilogue arrive on the leader's full_a / acc_empty (mapa addresses, release.cluster); the
+//     leader's MMA commits are multicast to both CTAs' empty / acc_full.
+// With half-height B stages (16 KiB) the ring is 8 deep in both smem (B) and TMEM (A).
+#include <algorithm>
+
+#include "mobi_internal.cuh"
+#include "sm100.cuh"
+
+namespace mobi {
+int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int64_t rows, int64_t cols,
+                 int box_rows);
+namespace {
+
+using namespace sm100;
+
+constexpr int NSTAGE = 8;
+constexpr int kDqWarps = 16;
+constexpr int kThreads = 32 * (2 + kDqWarps + 4);
+constexpr int kHalfRows = kTokTile / 2;                  // token rows per CTA per stage
+constexpr int kStageBytes = kHalfRows * kKBlock * 2;     // 16 KiB
+constexpr int kBoxRows = 16;
+constexpr int kBoxBytes = kBoxRows * kKBlock * 2;        // 2 KiB
+constexpr int kACol0 = 256;
+constexpr int kYStageBytes = kTokTile * kRowTile * 2;    // 64 KiB
+constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 + 512 + kYStageBytes + kTokTile * 4;
+
+struct Params {
+    const uint8_t* codes8;
+    const float2* gconst;
+    int64_t out_pad;
+    MaskTable mt;
+    int64_t out, G, gs, kblocks;
+    int single_group;
+    int n_row_tiles;
+    const float* escale;
+    const int32_t* perm;
+    const TokTile* tiles;
+    const int32_t* meta;
+    __nv_bfloat16* y;
+    int vec_y;
+};
+
+// one 64-k block on the pair: four K=16 cta_group::2 MMAs, M=256, N compile-time
+template <uint32_t N>
+__device__ __forceinline__ void issue_kblock_2sm(uint32_t acol, uint64_t bdesc, bool first) {
+    constexpr uint32_t idesc = idesc_f16(256, N, 0);
+#pragma unroll
+    for (int j = 0; j < kKBlock / 16; ++j)
+        mma_ts_f16_2sm(0u, acol + j * 8, bdesc + (uint64_t)(j * 2), idesc, (!first || j != 0) ? 1u : 0u);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    mobi_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* stage_b = smem;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * kStageBytes);
+    uint64_t* full_b = bars;                 // [NSTAGE] leader: both halves landed
+    uint64_t* full_a = bars + NSTAGE;        // [NSTAGE] leader: both CTAs' A stages written
+    uint64_t* empty = bars + 2 * NSTAGE;     // [NSTAGE] each CTA: pair MMAs done with the stage
+    uint64_t* acc_full = bars + 3 * NSTAGE;  // each CTA
+    uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 512);
+    int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);
+    auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+
+    const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full_b[s], 1);
+            mbar_init(&full_a[s], kDqWarps);  // 8 warps of one k-parity x 2 CTAs
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(acc_full, 1);
+        mbar_init(acc_empty, 8);  // 4 epilogue warps x 2 CTAs
+        fence_barrier_init();
+        prefetch_tmap(&tmap_x);
+    }
+    if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    if (*tmem_slot != 0) __trap();
+    constexpr uint32_t tmem = 0;
+
+    const int n_tok_tiles = p.meta[0];
+    const int n_pairs_row = p.n_row_tiles / 2;
+    const int total = n_tok_tiles * n_pairs_row;
+    const int kb_n = (int)p.kblocks;
+    const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+    // pair -> (token tile, this CTA's 128-row weight tile, N class: a multiple of 32 >= 32)
+    auto tile_of = [&](int pair, TokTile& tt, int& rt, int& nc) {
+        tt = p.tiles[pair / n_pairs_row];
+        rt = (pair % n_pairs_row) * 2 + (int)rank;
+        nc = max(32, (int)round_up(tt.n, 32));
+    };
+
+    if (warp == 0) {
+        // ---------------- TMA producer (both CTAs: own half of the token tile) ----------------
+        const uint32_t full_b_leader = mapa_shared(smem_u32(full_b), 0);
+        uint32_t it = 0;
+        for (int pair = cid; pair < total; pair += ncl) {
+            TokTile tt;
+            int rt, nc;
+            tile_of(pair, tt, rt, nc);
+            const int nbox = nc / 2 / kBoxRows;
+            const int row_half = tt.row0 + (int)rank * (nc / 2);
+            for (int kb = 0; kb < kb_n; ++kb, ++it) {
+                const int s = it % NSTAGE;
+                const uint32_t ph = (it / NSTAGE) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                if (lane == 0) {
+                    if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * nbox * kBoxBytes);
+                    for (int j = 0; j < nbox; ++j)
+                        tma_load_2d_2sm(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, full_b_leader + s * 8,
+                                        kb * kKBlock, row_half + j * kBoxRows);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (leader CTA only) ----------------
+        if (rank == 0) {
+            uint32_t it = 0, tc = 0;
+            for (int pair = cid; pair < total; pair += ncl, ++tc) {
+                TokTile tt;
+                int rt, nc;
+                tile_of(pair, tt, rt, nc);
+                mbar_wait_cluster(acc_empty, (tc & 1) ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < kb_n; ++kb, ++it) {
+                    const int s = it % NSTAGE;
+                    const uint32_t ph = (it / NSTAGE) & 1;
+                    mbar_wait_cluster(&full_b[s], ph);
+                    mbar_wait_cluster(&full_a[s], ph);
+                    tc_fence_after();
+                    if (elect_one_sync()) {
+                        const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
+                        const uint32_t acol = tmem + kACol0 + s * 32;
+                        const bool first = kb == 0;
+                        switch (nc) {
+                            case 32: issue_kblock_2sm<32>(acol, bdesc, first); break;
+                            case 64: issue_kblock_2sm<64>(acol, bdesc, first); break;
+                            case 96: issue_kblock_2sm<96>(acol, bdesc, first); break;
+                            case 128: issue_kblock_2sm<128>(acol, bdesc, first); break;
+                            case 160: issue_kblock_2sm<160>(acol, bdesc, first); break;
+                            case 192: issue_kblock_2sm<192>(acol, bdesc, first); break;
+                            case 224: issue_kblock_2sm<224>(acol, bdesc, first); break;
+                            default: issue_kblock_2sm<256>(acol, bdesc, first); break;
+                        }
+                        mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
+                        if (kb == kb_n - 1) mma_commit_2sm_mc(acc_full, (uint16_t)0x3);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else if (warp < 2 + kDqWarps) {
+        // ---------------- dequantizers ----------------
+        // 16 warps = 4 TMEM lane quarters x 2 k-halves x 2 k-block parities: a warp dequantizes
+        // 32 codes of its row for every other k-block, so two k-blocks are in flight at once.
+        const int idx = warp - 2;
+        const int q = warp % 4;
+        const int par = (idx / 4) & 1;
+        const int hh = idx / 8;
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
+        for (int pair = cid; pair < total; pair += ncl, base += kb_n) {
+            TokTile tt;
+            int rt, nc;
+            tile_of(pair, tt, rt, nc);
+            const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
+            const bool rv = R < p.out;
+            const uint32_t mw = p.mt.maskword[tt.mask];
+            const float kc = p.mt.kc[tt.mask];
+            const uint8_t* cbase =
+                p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes + ((hh * 2) * kRowTile + 32 * q + lane) * 16;
+            const float2* gcol = p.gconst + (rv ? R : 0);
+            auto ldc = [&](int gg) { return rv ? __ldg(gcol + (int64_t)gg * p.out_pad) : make_float2(0.f, 0.f); };
+            auto ld = [&](int kb, uint4& c0, uint4& c1) {
+                const uint8_t* b0 = cbase + (int64_t)kb * kBlockBytes;
+                c0 = *reinterpret_cast<const uint4*>(b0);
+                c1 = *reinterpret_cast<const uint4*>(b0 + kRowTile * 16);
+            };
+            // group of k = kb*64 + 32*hh, tracked incrementally (k advances by 128 per step)
+            auto dq = [&](const uint4& c0, const uint4& c1, float2 gcst, uint32_t (&v)[16]) {
+                const __half2 S2 = __float2half2_rn(gcst.x * p.mt.inv_2p);
+                const __half2 C2 = __float2half2_rn(fmaf(gcst.x, kc, -gcst.y));
+                const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&c0);
+                const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&c1);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) dequant4(w0[u], mw, S2, C2, v[2 * u], v[2 * u + 1]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) dequant4(w1[u], mw, S2, C2, v[8 + 2 * u], v[8 + 2 * u + 1]);
+            };
+            // Ring of three static slots (codes + group constants), unrolled so a slot is refilled
+            // right after it was consumed and each load has two iterations of lead time; no
+            // register moves touch a pending load.
+            uint4 c00, c01, c10, c11, c20, c21;
+            float2 g0 = make_float2(0.f, 0.f), g1 = g0, g2 = g0;
+            int gp = 0, kinp = 0;  // group cursor at the next k-block to prefetch
+            if (!p.single_group) {
+                kinp = par * kKBlock + hh * 32;
+                while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
+            }
+            auto fetch = [&](int kb, uint4& c0, uint4& c1, float2& gc) {
+                if (kb < kb_n) {
+                    ld(kb, c0, c1);
+                    gc = ldc(gp);
+                }
+                if (!p.single_group) {
+                    kinp += 2 * kKBlock;
+                    while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
+                }
+            };
+            fetch(par, c00, c01, g0);
+            fetch(par + 2, c10, c11, g1);
+            fetch(par + 4, c20, c21, g2);
+            uint32_t v[16];
+            auto step = [&](int kb, uint4& ca, uint4& cb, float2& ga, uint4& na, uint4& nb, float2& gn) -> bool {
+                // v holds k-block kb (dequantized from the slot (ca, cb)); (na, nb) holds kb+2
+                if (kb >= kb_n) return false;
+                const uint32_t itk = base + kb;
+                const int s = itk % NSTAGE;
+                const uint32_t ph = (itk / NSTAGE) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                tc_fence_after();
+                tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
+                fetch(kb + 6, ca, cb, ga);  // refill the consumed slot three of this warp's k-blocks ahead
+                if (kb + 2 < kb_n) dq(na, nb, gn, v);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&full_a[s]), 0));  // leader's barrier
+                return true;
+            };
+            if (par < kb_n) dq(c00, c01, g0, v);
+            for (int kb = par; kb < kb_n; kb += 6) {
+                if (!step(kb, c00, c01, g0, c10, c11, g1)) break;
+                if (!step(kb + 2, c10, c11, g1, c20, c21, g2)) break;
+                if (!step(kb + 4, c20, c21, g2, c00, c01, g0)) break;
+            }
+        }
+    } else {
+        // ---------------- epilogue ----------------
+        // drain TMEM -> (x 2^e) -> bf16 -> smem tile [token][128 rows], release the accumulator,
+        // then scatter whole 256-byte token rows into Y[perm[i]] with 16-byte stores
+        const int q = warp % 4;
+        const int et = threadIdx.x - 32 * (2 + kDqWarps);  // 0..127
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        uint32_t tc = 0;
+        for (int pair = cid; pair < total; pair += ncl, ++tc) {
+            TokTile tt;
+            int rt, nc;
+            tile_of(pair, tt, rt, nc);
+            mbar_wait_cluster(acc_full, tc & 1);
+            tc_fence_after();
+            epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
+            for (int c0 = 0; c0 < tt.n; c0 += 32) {
+                const int nn = min(32, tt.n - c0);
+                int32_t my_src = -1;
+                float my_es = 0.f;
+                if (lane < nn) {
+                    my_src = __ldg(p.perm + tt.row0 + c0 + lane);
+                    my_es = __ldg(p.escale + tt.row0 + c0 + lane);
+                }
+                if (q == 0) tok_src[c0 + lane] = lane < nn ? my_src : -1;
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + c0, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float es = __shfl_sync(0xffffffffu, my_es, j);
+                    stage_y[(c0 + j) * kRowTile + 32 * q + lane] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty), 0));  // leader's barrier
+            epi_bar_sync();  // staging tile complete
+            const int64_t r0 = (int64_t)rt * kRowTile + 8 * (et % 16);
+            for (int t = et / 16; t < tt.n; t += 8) {
+                const int32_t src = tok_src[t];
+                if (src < 0 || r0 >= p.out) continue;
+                const __nv_bfloat16* sp = stage_y + t * kRowTile + 8 * (et % 16);
+                __nv_bfloat16* dp = p.y + (int64_t)src * p.out + r0;
+                if (p.vec_y && r0 + 8 <= p.out) {
+                    *reinterpret_cast<uint4*>(dp) = *reinterpret_cast<const uint4*>(sp);
+                } else {
+                    for (int u = 0; u < 8 && r0 + u < p.out; ++u) dp[u] = sp[u];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) tmem_dealloc_2sm(tmem, 512);
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+}  // namespace
+
+int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        attr = true;
+    }
+    if (!L->tmap_x2) {
+        L->tmap_x2 = new CUtensorMap;
+        int rc = make_tmap_2d(L->tmap_x2, L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad, kBoxRows);
+        if (rc) {
+            delete L->tmap_x2;
+            L->tmap_x2 = nullptr;
+            return rc;
+        }
+    }
+    Params p;
+    p.codes8 = L->codes8;
+    p.gconst = L->gconst;
+    p.out_pad = L->out_pad;
+    p.mt = L->mtab;
+    p.out = L->out;
+    p.G = L->G;
+    p.gs = L->gs;
+    p.kblocks = L->kblocks;
+    p.single_group = L->single_group;
+    p.n_row_tiles = (int)(L->out_pad / kRowTile);
+    p.escale = L->escale;
+    p.perm = L->perm;
+    p.tiles = L->tiles;
+    p.meta = L->meta;
+    p.y = y;
+    p.vec_y = (L->out % 8 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+    const int64_t max_pairs = (int64_t)(p.n_row_tiles / 2) * L->max_tiles;
+    const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
+    mobi_gemm_tc2_kernel<<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x2, p);
+    MOBI_LAUNCH_CHECK();
+    ++L->last_launches;
+    return MOBI_OK;
+}
+
+}  // namespace mobi

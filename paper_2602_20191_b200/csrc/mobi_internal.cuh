@@ -100,6 +100,7 @@ struct mobi_layer {
     int64_t h_cap = 0;
     CUtensorMap* tmap_x = nullptr;  // host copies, rebuilt when the workspace changes
     CUtensorMap* tmap_w1 = nullptr; // router w1t (fixed for the layer's lifetime)
+    CUtensorMap* tmap_x2 = nullptr; // xperm, 16-row boxes (CTA-pair GEMM)
     int32_t last_launches = 0;
     int64_t device_bytes = 0;
     // profiling: event pairs around each launch, resolved lazily
@@ -150,6 +151,7 @@ int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t
 int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
                    unsigned long long* trace = nullptr);
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
+int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);  // gemm_tc2.cu (CTA pairs)
 // decompose.cu
 int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,
                      int32_t E, double gamma, uint8_t* codes, double* scale, double* zero,
