@@ -329,8 +329,8 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
         g_trace_buf = tbuf;
         return launch_gemm_tc(L, yb, T, st, tbuf);
     }
-    if (g_impl_override == 3) return launch_gemm_tc(L, yb, T, st);  // 1-CTA kernel (comparison)
-    return launch_gemm_tc2(L, yb, T, st);
+    if (g_impl_override == 3) return launch_gemm_tc2(L, yb, T, st);  // CTA-pair kernel (comparison)
+    return launch_gemm_tc(L, yb, T, st);
 }
 
 }  // namespace

@@ -82,6 +82,11 @@ template <bool TRACE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mobi_gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
     long long tr[6] = {0, 0, 0, 0, 0, 0};
+    // per-k-block event timeline (CTA 0, first tile): trace[20480 + ev*64 + kb]
+    auto EV = [&](int ev, int kb, uint32_t tile_idx) {
+        if (TRACE && blockIdx.x == 0 && tile_idx == 0 && kb < 64 && (threadIdx.x % 32) == 0)
+            p.trace[20480 + ev * 64 + kb] = (unsigned long long)clock64();
+    };
 #define TW(i, stmt)                                   \
     do {                                              \
         if (TRACE) {                                  \
@@ -156,6 +161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
+                EV(0, kb, (uint32_t)(pair != cid));
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full_b[s], nbox * kBoxBytes);
                     for (int j = (int)rank; j < nbox; j += 2)
@@ -181,7 +187,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 TW(1, mbar_wait(&full_b[s], ph));
+                EV(1, kb, tc);
                 TW(2, mbar_wait(&full_a[s], ph));
+                EV(2, kb, tc);
                 tc_fence_after();
                 if (elect_one_sync()) {
                     const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
@@ -202,6 +210,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     if (kb == kb_n - 1) mma_commit(acc_full);
                 }
                 __syncwarp();
+                EV(3, kb, tc);
             }
             if (TRACE && lane == 0 && tc < 8) {  // per-tile: N and cycles from first wait to last issue
                 p.trace[16 * 1024 + (blockIdx.x * 8 + tc) * 2] = (unsigned long long)n_mma;
@@ -281,6 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = itk % NSTAGE;
                 const uint32_t ph = (itk / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
+                if (warp == 2 || warp == 6) EV(4, kb, base);
                 tc_fence_after();
                 TW(3, tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v));
                 TW(4, fetch(kb + 6, ca, cb, ga));  // refill the consumed slot three of this warp's k-blocks ahead
@@ -289,9 +299,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #else
                 if (kb + 2 < kb_n) TW(1, dq(na, nb, gn, v));
 #endif
+                if (warp == 2 || warp == 6) EV(5, kb, base);
                 TW(2, tmem_st_wait());
                 tc_fence_before();
                 __syncwarp();
+                if (warp == 2 || warp == 6) EV(6, kb, base);
                 if (lane == 0) mbar_arrive(&full_a[s]);
                 return true;
             };

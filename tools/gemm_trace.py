@@ -38,12 +38,22 @@ def main():
     for i, nm in enumerate(names):
         col = buf[:, i].astype(np.float64)
         print(f"{nm:22s} mean {col.mean():12.0f}  min {col.min():12.0f}  max {col.max():12.0f}")
-    per = full[16 * 1024:].reshape(1024, 8, 2)[:n].reshape(-1, 2)
+    timeline(full)
+    per = full[16 * 1024:20480].reshape(-1, 2)
     per = per[per[:, 0] > 0]
     for N in sorted(set(per[:, 0].tolist())):
         c = per[per[:, 0] == N][:, 1].astype(np.float64)
         print(f"tile N={N:4d}: {len(c):4d} tiles  cycles mean {c.mean():9.0f} min {c.min():9.0f} max {c.max():9.0f}"
               f"   ideal MMA {64 * 4 * 137.5 * N / 256:9.0f}")
+
+
+def timeline(full):
+    ev = full[20480:20480 + 8 * 64].reshape(8, 64).astype(np.int64)
+    t0 = ev[0][ev[0] > 0].min() if (ev[0] > 0).any() else 0
+    names = ["tma:empty ok", "mma:full_b ok", "mma:full_a ok", "mma:issued", "dq:empty ok", "dq:dq done", "dq:arrive"]
+    print("kb  " + " ".join(f"{n:>14s}" for n in names))
+    for kb in range(0, 24):
+        print(f"{kb:2d}  " + " ".join(f"{(ev[e][kb] - t0) if ev[e][kb] else -1:14d}" for e in range(7)))
 
 
 if __name__ == "__main__":
