@@ -31,6 +31,9 @@ using namespace sm100;
 #ifndef MOBI_ABLATE
 #define MOBI_ABLATE 0  // development ablations: 1 = no code loads, 2 = no dequantization
 #endif
+#ifndef MOBI_EV_MAX
+#define MOBI_EV_MAX 4
+#endif
 #ifndef MOBI_NSTAGE
 #define MOBI_NSTAGE 4
 #endif
@@ -84,7 +87,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     long long tr[6] = {0, 0, 0, 0, 0, 0};
     // per-k-block event timeline (CTA 0, first tile): trace[20480 + ev*64 + kb]
     auto EV = [&](int ev, int kb, uint32_t tile_idx) {
-        if (TRACE && blockIdx.x == 0 && tile_idx == 0 && kb < 64 && (threadIdx.x % 32) == 0)
+        if (TRACE && ev < MOBI_EV_MAX && blockIdx.x == 0 && tile_idx == 0 && kb < 64 && (threadIdx.x % 32) == 0)
             p.trace[20480 + ev * 64 + kb] = (unsigned long long)clock64();
     };
 #define TW(i, stmt)                                   \
@@ -144,7 +147,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int kb_n = (int)p.kblocks;
     const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
     auto tile_of = [&](int pair, TokTile& tt, int& rt) {
-        tt = p.tiles[pair / n_pairs_row];
+        tt = uniform_tile(p.tiles[pair / n_pairs_row]);
         rt = (pair % n_pairs_row) * 2 + (int)rank;
     };
 
@@ -162,7 +165,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const uint32_t ph = (it / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
                 EV(0, kb, (uint32_t)(pair != cid));
-                if (lane == 0) {
+                if (elect_one_sync()) {
                     mbar_arrive_expect_tx(&full_b[s], nbox * kBoxBytes);
                     for (int j = (int)rank; j < nbox; j += 2)
                         tma_load_2d_mc(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, &full_b[s], kb * kKBlock,

@@ -104,7 +104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
     // pair -> (token tile, this CTA's 128-row weight tile, N class: a multiple of 32 >= 32)
     auto tile_of = [&](int pair, TokTile& tt, int& rt, int& nc) {
-        tt = p.tiles[pair / n_pairs_row];
+        tt = uniform_tile(p.tiles[pair / n_pairs_row]);
         rt = (pair % n_pairs_row) * 2 + (int)rank;
         nc = max(32, (int)round_up(tt.n, 32));
     };
@@ -123,7 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
-                if (lane == 0) {
+                if (elect_one_sync()) {
                     if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * nbox * kBoxBytes);
                     for (int j = 0; j < nbox; ++j)
                         tma_load_2d_2sm(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, full_b_leader + s * 8,

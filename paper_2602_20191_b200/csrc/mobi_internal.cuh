@@ -51,6 +51,17 @@ struct TokTile {
     int32_t pad;
 };
 
+// Tile record read from global memory, broadcast from lane 0 so the compiler can prove the
+// fields warp-uniform (keeps TMA / tcgen05 operands derived from them in uniform registers).
+__device__ __forceinline__ TokTile uniform_tile(const TokTile& t) {
+    TokTile u;
+    u.row0 = __shfl_sync(0xffffffffu, t.row0, 0);
+    u.n = __shfl_sync(0xffffffffu, t.n, 0);
+    u.mask = __shfl_sync(0xffffffffu, t.mask, 0);
+    u.pad = 0;
+    return u;
+}
+
 // Per-mask dequant constants (uniform b-bit slices): W = S*INT_m + C with
 //   INT_m = merged & maskbyte[m],  S = s / 2^P,  C = s*K[m]/2^(P+1) - s*z
 struct MaskTable {
