@@ -35,9 +35,10 @@ using namespace sm100;
 #define MOBI_EV_MAX 4
 #endif
 #ifndef MOBI_NSTAGE
-#define MOBI_NSTAGE 4
+#define MOBI_NSTAGE 5
 #endif
-constexpr int NSTAGE = MOBI_NSTAGE;
+constexpr int NSTAGE = MOBI_NSTAGE;  // B stages (smem, 32 KiB each)
+constexpr int NSA = 8;               // A stages (TMEM, 32 columns each)
 constexpr int kBoxRows = 32;                      // TMA box: 32 token rows x 64 k (4 KiB)
 constexpr int kBoxBytes = kBoxRows * kKBlock * 2;
 constexpr int kDqWarps = 16;                       // 4 per TMEM lane quarter
@@ -106,9 +107,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* stage_b = smem;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * kStageBytes);
     uint64_t* full_b = bars;                  // [NSTAGE] TMA landed
-    uint64_t* full_a = bars + NSTAGE;         // [NSTAGE] A stage written to TMEM (8 warps)
-    uint64_t* empty = bars + 2 * NSTAGE;      // [NSTAGE] MMAs reading the stage completed
-    uint64_t* acc_full = bars + 3 * NSTAGE;   // accumulator ready for the epilogue
+    uint64_t* empty = bars + NSTAGE;          // [NSTAGE] MMAs of BOTH CTAs done with the B stage
+    uint64_t* full_a = bars + 2 * NSTAGE;     // [NSA] A stage written to TMEM (8 warps)
+    uint64_t* empty_a = full_a + NSA;         // [NSA] local MMAs done with the A stage
+    uint64_t* acc_full = empty_a + NSA;       // accumulator ready for the epilogue
     uint64_t* acc_empty = acc_full + 1;       // epilogue drained the accumulator (4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
     __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 256);
@@ -119,8 +121,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1);
-            mbar_init(&full_a[s], kDqWarps / 2);
             mbar_init(&empty[s], 2);  // MMA completion of BOTH CTAs of the pair (shared B stages)
+        }
+        for (int s = 0; s < NSA; ++s) {
+            mbar_init(&full_a[s], kDqWarps / 2);
+            mbar_init(&empty_a[s], 1);
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 4);
@@ -189,14 +194,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
+                const int sa = it % NSA;
+                const uint32_t pha = (it / NSA) & 1;
                 TW(1, mbar_wait(&full_b[s], ph));
                 EV(1, kb, tc);
-                TW(2, mbar_wait(&full_a[s], ph));
+                TW(2, mbar_wait(&full_a[sa], pha));
                 EV(2, kb, tc);
                 tc_fence_after();
                 if (elect_one_sync()) {
                     const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
-                    const uint32_t acol = tmem + kACol0 + s * 32;
+                    const uint32_t acol = tmem + kACol0 + sa * 32;
                     const bool first = kb == 0;
                     switch (n_mma) {
                         case 16: issue_kblock_ts<16>(acol, bdesc, first); break;
@@ -210,6 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         default: issue_kblock_ts<256>(acol, bdesc, first); break;
                     }
                     mma_commit_mc(&empty[s], (uint16_t)0x3);  // frees the shared B stage in both CTAs
+                    mma_commit(&empty_a[sa]);                 // frees the local A stage
                     if (kb == kb_n - 1) mma_commit(acc_full);
                 }
                 __syncwarp();
@@ -290,9 +298,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // v holds k-block kb (dequantized from the slot (ca, cb)); (na, nb) holds kb+2
                 if (kb >= kb_n) return false;
                 const uint32_t itk = base + kb;
-                const int s = itk % NSTAGE;
-                const uint32_t ph = (itk / NSTAGE) & 1;
-                TW(0, mbar_wait(&empty[s], ph ^ 1));
+                const int s = itk % NSA;
+                const uint32_t ph = (itk / NSA) & 1;
+                TW(0, mbar_wait(&empty_a[s], ph ^ 1));
                 if (warp == 2 || warp == 6) EV(4, kb, base);
                 tc_fence_after();
                 TW(3, tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v));
