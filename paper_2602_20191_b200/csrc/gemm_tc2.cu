@@ -27,6 +27,7 @@ using namespace sm100;
 constexpr int NSTAGE = 8;
 constexpr int kDqWarps = 16;
 constexpr int kThreads = 32 * (2 + kDqWarps + 4);
+constexpr int kWarpDq0 = 0, kWarpEpi0 = kDqWarps, kWarpTma = kDqWarps + 4, kWarpMma = kDqWarps + 5;
 constexpr int kHalfRows = kTokTile / 2;                  // token rows per CTA per stage
 constexpr int kStageBytes = kHalfRows * kKBlock * 2;     // 16 KiB
 constexpr int kBoxRows = 16;
@@ -89,7 +90,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_barrier_init();
         prefetch_tmap(&tmap_x);
     }
-    if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
+    if (warp == kWarpMma) tmem_alloc_2sm(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     cluster_sync();
@@ -109,7 +110,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         nc = max(32, (int)round_up(tt.n, 32));
     };
 
-    if (warp == 0) {
+    if (warp == kWarpTma) {
         // ---------------- TMA producer (both CTAs: own half of the token tile) ----------------
         const uint32_t full_b_leader = mapa_shared(smem_u32(full_b), 0);
         uint32_t it = 0;
@@ -132,7 +133,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 __syncwarp();
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kWarpMma) {
         // ---------------- MMA issuer (leader CTA only) ----------------
         if (rank == 0) {
             uint32_t it = 0, tc = 0;
@@ -169,11 +170,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp < 2 + kDqWarps) {
+    } else if (warp < kWarpEpi0) {
         // ---------------- dequantizers ----------------
         // 16 warps = 4 TMEM lane quarters x 2 k-halves x 2 k-block parities: a warp dequantizes
         // 32 codes of its row for every other k-block, so two k-blocks are in flight at once.
-        const int idx = warp - 2;
+        const int idx = warp - kWarpDq0;
         const int q = warp % 4;
         const int par = (idx / 4) & 1;
         const int hh = idx / 8;
@@ -260,7 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // drain TMEM -> (x 2^e) -> bf16 -> smem tile [token][128 rows], release the accumulator,
         // then scatter whole 256-byte token rows into Y[perm[i]] with 16-byte stores
         const int q = warp % 4;
-        const int et = threadIdx.x - 32 * (2 + kDqWarps);  // 0..127
+        const int et = threadIdx.x - 32 * kWarpEpi0;  // 0..127
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t tc = 0;
         for (int pair = cid; pair < total; pair += ncl, ++tc) {
@@ -309,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     cluster_sync();
-    if (warp == 1) tmem_dealloc_2sm(tmem, 512);
+    if (warp == kWarpMma) tmem_dealloc_2sm(tmem, 512);
 }
 
 int sm_count() {

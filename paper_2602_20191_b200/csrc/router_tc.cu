@@ -22,7 +22,8 @@ using namespace sm100;
 constexpr int RS = 6;                       // smem stages
 constexpr int RM = 128, RN = 128;           // tokens x hidden per tile
 constexpr int kAB = RM * kKBlock * 2;       // 16 KiB per operand per stage
-constexpr int kRThreads = 192;              // TMA, MMA, 4 epilogue warps
+constexpr int kRThreads = 192;              // 4 epilogue warps, TMA, MMA (highest ids = priority)
+constexpr int kRWarpTma = 4, kRWarpMma = 5;
 constexpr int kRSmem = RS * 2 * kAB + 1024 + 256;
 
 struct RParams {
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);  // all columns: base is the constant 0
+    if (warp == kRWarpMma) tmem_alloc(tmem_slot, 512);  // all columns: base is the constant 0
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -66,14 +67,14 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     constexpr uint32_t tmem = 0;
     const int total = p.n_mt * p.n_nt;
 
-    if (warp == 0) {
+    if (warp == kRWarpTma) {
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
             const int mt = tile % p.n_mt, nt = tile / p.n_mt;
             for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
                 const int s = it % RS;
                 mbar_wait(&empty[s], ((it / RS) & 1) ^ 1);
-                if (lane == 0) {
+                if (elect_one_sync()) {
                     uint8_t* a = smem + s * 2 * kAB;
                     mbar_arrive_expect_tx(&full[s], 2 * kAB);
                     tma_load_2d(a, &tmap_a, &full[s], kb * kKBlock, mt * RM);
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
                 __syncwarp();
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kRWarpMma) {
         uint32_t it = 0, tc = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
             const int nt = tile / p.n_mt;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 512);
+    if (warp == kRWarpMma) tmem_dealloc(tmem, 512);
 }
 
 int sm_count() {
