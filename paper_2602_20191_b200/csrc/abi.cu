@@ -322,11 +322,12 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
     ProfScope p(L, 3, st);
     if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
-    if (g_impl_override == 2) {  // traced tcgen05 kernel (development hook)
+    if (g_impl_override == 2 || g_impl_override == 4) {  // traced tcgen05 kernels (development hook)
         static unsigned long long* tbuf = nullptr;
         if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
         MOBI_CUDA(cudaMemsetAsync(tbuf, 0, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long), st));
         g_trace_buf = tbuf;
+        if (g_impl_override == 4) return launch_gemm_tc2(L, yb, T, st, tbuf);
         return launch_gemm_tc(L, yb, T, st, tbuf);
     }
     if (g_impl_override == 3) return launch_gemm_tc2(L, yb, T, st);  // CTA-pair kernel (comparison)

@@ -50,6 +50,7 @@ struct Params {
     const int32_t* meta;
     __nv_bfloat16* y;
     int vec_y;
+    unsigned long long* trace;
 };
 
 // one 64-k block on the pair: four K=16 cta_group::2 MMAs, M=256, N compile-time
@@ -61,8 +62,14 @@ __device__ __forceinline__ void issue_kblock_2sm(uint32_t acol, uint64_t bdesc, 
         mma_ts_f16_2sm(0u, acol + j * 8, bdesc + (uint64_t)(j * 2), idesc, (!first || j != 0) ? 1u : 0u);
 }
 
+template <bool TRACE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mobi_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
+    // per-k-block event timeline (cluster 0, first tile): trace[20480 + (rank*8+ev)*64 + kb]
+    auto EV = [&](int ev, int kb, uint32_t tile_idx) {
+        if (TRACE && blockIdx.x < 2 && tile_idx == 0 && kb < 64 && (threadIdx.x % 32) == 0)
+            p.trace[20480 + (cluster_ctarank() * 8 + ev) * 64 + kb] = (unsigned long long)clock64();
+    };
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stage_b = smem;
@@ -124,6 +131,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
+                EV(0, kb, (uint32_t)(pair != cid));
                 if (elect_one_sync()) {
                     if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * nbox * kBoxBytes);
                     for (int j = 0; j < nbox; ++j)
@@ -147,7 +155,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int s = it % NSTAGE;
                     const uint32_t ph = (it / NSTAGE) & 1;
                     mbar_wait_cluster(&full_b[s], ph);
+                    EV(1, kb, tc);
                     mbar_wait_cluster(&full_a[s], ph);
+                    EV(2, kb, tc);
                     tc_fence_after();
                     if (elect_one_sync()) {
                         const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
@@ -167,6 +177,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         if (kb == kb_n - 1) mma_commit_2sm_mc(acc_full, (uint16_t)0x3);
                     }
                     __syncwarp();
+                    EV(3, kb, tc);
                 }
             }
         }
@@ -239,6 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = itk % NSTAGE;
                 const uint32_t ph = (itk / NSTAGE) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
+                if (warp == 0 || warp == 4) EV(4, kb, base);
                 tc_fence_after();
                 tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
                 fetch(kb + 6, ca, cb, ga);  // refill the consumed slot three of this warp's k-blocks ahead
@@ -246,6 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
+                if (warp == 0 || warp == 4) EV(5, kb, base);
                 if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&full_a[s]), 0));  // leader's barrier
                 return true;
             };
@@ -325,10 +338,13 @@ int sm_count() {
 
 }  // namespace
 
-int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st) {
+int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace) {
     static bool attr = false;
     if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBytes));
+        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kSmemBytes));
         attr = true;
     }
     if (!L->tmap_x2) {
@@ -359,7 +375,11 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st)
     p.vec_y = (L->out % 8 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
     const int64_t max_pairs = (int64_t)(p.n_row_tiles / 2) * L->max_tiles;
     const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
-    mobi_gemm_tc2_kernel<<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x2, p);
+    p.trace = trace;
+    if (trace)
+        mobi_gemm_tc2_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x2, p);
+    else
+        mobi_gemm_tc2_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x2, p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

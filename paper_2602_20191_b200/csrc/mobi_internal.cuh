@@ -162,7 +162,8 @@ int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t
 int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
                    unsigned long long* trace = nullptr);
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
-int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);  // gemm_tc2.cu (CTA pairs)
+int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
+                    unsigned long long* trace = nullptr);  // gemm_tc2.cu (CTA pairs)
 // decompose.cu
 int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,
                      int32_t E, double gamma, uint8_t* codes, double* scale, double* zero,

@@ -22,7 +22,9 @@ def main():
     delta = calibrate_threshold(layer.score(x), (args.target_bits - 2) / 6)
     for _ in range(3):
         layer.forward(x, delta)
-    set_debug_impl(2)
+    import os
+    impl = int(os.environ.get("MOBI_TRACE_IMPL", "2"))
+    set_debug_impl(impl)
     layer.forward(x, delta)
     torch.cuda.synchronize()
     set_debug_impl(0)
@@ -39,6 +41,9 @@ def main():
         col = buf[:, i].astype(np.float64)
         print(f"{nm:22s} mean {col.mean():12.0f}  min {col.min():12.0f}  max {col.max():12.0f}")
     timeline(full)
+    if impl == 4:
+        print("-- peer CTA")
+        timeline(full, 20480 + 512)
     per = full[16 * 1024:20480].reshape(-1, 2)
     per = per[per[:, 0] > 0]
     for N in sorted(set(per[:, 0].tolist())):
@@ -47,8 +52,8 @@ def main():
               f"   ideal MMA {64 * 4 * 137.5 * N / 256:9.0f}")
 
 
-def timeline(full):
-    ev = full[20480:20480 + 8 * 64].reshape(8, 64).astype(np.int64)
+def timeline(full, base=20480):
+    ev = full[base:base + 8 * 64].reshape(8, 64).astype(np.int64)
     t0 = ev[0][ev[0] > 0].min() if (ev[0] > 0).any() else 0
     names = ["tma:empty ok", "mma:full_b ok", "mma:full_a ok", "mma:issued", "dq:empty ok", "dq:dq done", "dq:arrive"]
     print("kb  " + " ".join(f"{n:>14s}" for n in names))
