@@ -79,7 +79,7 @@ void free_ws(mobi_layer* L) {
     dfree(L->meta);
     if (L->tmap_x) delete L->tmap_x;
     L->tmap_x = nullptr;
-    if (L->tmap_x2) delete L->tmap_x2;
+    if (L->tmap_x2) delete[] L->tmap_x2;
     L->tmap_x2 = nullptr;
     L->ws_T = -1;
 }

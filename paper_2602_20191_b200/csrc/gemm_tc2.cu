@@ -35,6 +35,7 @@ constexpr int kBoxBytes = kBoxRows * kKBlock * 2;        // 2 KiB
 constexpr int kACol0 = 256;
 constexpr int kYStageBytes = kTokTile * kRowTile * 2;    // 64 KiB
 constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 + 512 + kYStageBytes + kTokTile * 4;
+constexpr int kBigBoxRows = kHalfRows;  // one TMA box per full half-tile
 
 struct Params {
     const uint8_t* codes8;
@@ -64,7 +65,8 @@ __device__ __forceinline__ void issue_kblock_2sm(uint32_t acol, uint64_t bdesc, 
 
 template <bool TRACE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    mobi_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const Params p) {
+    mobi_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_big,
+                         const Params p) {
     // per-k-block event timeline (cluster 0, first tile): trace[20480 + (rank*8+ev)*64 + kb]
     auto EV = [&](int ev, int kb, uint32_t tile_idx) {
         if (TRACE && blockIdx.x < 2 && tile_idx == 0 && kb < 64 && (threadIdx.x % 32) == 0)
@@ -79,7 +81,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* empty = bars + 2 * NSTAGE;     // [NSTAGE] each CTA: pair MMAs done with the stage
     uint64_t* acc_full = bars + 3 * NSTAGE;  // each CTA
     uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+    uint64_t* full_a_loc = acc_empty + 1;    // [NSTAGE] peer: its own 8 dequant warps (forwarded)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full_a_loc + NSTAGE);
     __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 512);
     int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
@@ -89,13 +92,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1);
-            mbar_init(&full_a[s], kDqWarps);  // 8 warps of one k-parity x 2 CTAs
+            mbar_init(&full_a[s], kDqWarps / 2 + 1);  // leader's 8 warps of one k-parity + 1 peer forward
+            mbar_init(&full_a_loc[s], kDqWarps / 2);
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 8);  // 4 epilogue warps x 2 CTAs
         fence_barrier_init();
         prefetch_tmap(&tmap_x);
+        prefetch_tmap(&tmap_big);
     }
     if (warp == kWarpMma) tmem_alloc_2sm(tmem_slot, 512);
     tc_fence_before();
@@ -125,7 +130,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
-            const int nbox = nc / 2 / kBoxRows;
+            const bool big = nc == kTokTile;  // full tile: one 128-row box per CTA
+            const int nbox = big ? 1 : nc / 2 / kBoxRows;
             const int row_half = tt.row0 + (int)rank * (nc / 2);
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
@@ -133,16 +139,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 mbar_wait(&empty[s], ph ^ 1);
                 EV(0, kb, (uint32_t)(pair != cid));
                 if (elect_one_sync()) {
-                    if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * nbox * kBoxBytes);
-                    for (int j = 0; j < nbox; ++j)
-                        tma_load_2d_2sm(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, full_b_leader + s * 8,
-                                        kb * kKBlock, row_half + j * kBoxRows);
+                    if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * (big ? kStageBytes : nbox * kBoxBytes));
+                    if (big)
+                        tma_load_2d_2sm(stage_b + s * kStageBytes, &tmap_big, full_b_leader + s * 8, kb * kKBlock,
+                                        row_half);
+                    else
+                        for (int j = 0; j < nbox; ++j)
+                            tma_load_2d_2sm(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, full_b_leader + s * 8,
+                                            kb * kKBlock, row_half + j * kBoxRows);
                 }
                 __syncwarp();
             }
         }
     } else if (warp == kWarpMma) {
-        // ---------------- MMA issuer (leader CTA only) ----------------
+        // ---------------- MMA issuer (leader) / A-stage forwarder (peer) ----------------
+        if (rank != 0) {
+            // one cluster-scope arrive per k-block instead of one per dequant warp
+            const uint32_t full_a_leader = mapa_shared(smem_u32(full_a), 0);
+            uint32_t it = 0;
+            for (int pair = cid; pair < total; pair += ncl)
+                for (int kb = 0; kb < kb_n; ++kb, ++it) {
+                    const int s = it % NSTAGE;
+                    mbar_wait(&full_a_loc[s], (it / NSTAGE) & 1);
+                    tc_fence_after();
+                    tc_fence_before();
+                    if (elect_one_sync()) mbar_arrive_cluster(full_a_leader + s * 8);
+                    __syncwarp();
+                }
+        }
         if (rank == 0) {
             uint32_t it = 0, tc = 0;
             for (int pair = cid; pair < total; pair += ncl, ++tc) {
@@ -259,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (warp == 0 || warp == 4) EV(5, kb, base);
-                if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&full_a[s]), 0));  // leader's barrier
+                if (lane == 0) mbar_arrive(rank == 0 ? &full_a[s] : &full_a_loc[s]);  // peer: forwarded below
                 return true;
             };
             if (par < kb_n) dq(c00, c01, g0, v);
@@ -348,10 +372,13 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
         attr = true;
     }
     if (!L->tmap_x2) {
-        L->tmap_x2 = new CUtensorMap;
-        int rc = make_tmap_2d(L->tmap_x2, L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad, kBoxRows);
+        L->tmap_x2 = new CUtensorMap[2];
+        int rc = make_tmap_2d(&L->tmap_x2[0], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad, kBoxRows);
+        if (!rc)
+            rc = make_tmap_2d(&L->tmap_x2[1], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad,
+                              kBigBoxRows);
         if (rc) {
-            delete L->tmap_x2;
+            delete[] L->tmap_x2;
             L->tmap_x2 = nullptr;
             return rc;
         }
@@ -377,9 +404,9 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
     p.trace = trace;
     if (trace)
-        mobi_gemm_tc2_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x2, p);
+        mobi_gemm_tc2_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(L->tmap_x2[0], L->tmap_x2[1], p);
     else
-        mobi_gemm_tc2_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x2, p);
+        mobi_gemm_tc2_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(L->tmap_x2[0], L->tmap_x2[1], p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;
