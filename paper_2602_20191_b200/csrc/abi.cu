@@ -71,6 +71,7 @@ void free_ws(mobi_layer* L) {
     dfree(L->scores);
     dfree(L->masks);
     dfree(L->perm);
+    dfree(L->pinv);
     dfree(L->inverse);
     dfree(L->cperm);
     dfree(L->escale);
@@ -97,12 +98,15 @@ int ensure_ws(mobi_layer* L, int64_t T) {
     if ((rc = dmalloc(&L->scores, (size_t)(Tc * L->nr), nullptr))) return rc;
     if ((rc = dmalloc(&L->masks, (size_t)Tc, nullptr))) return rc;
     if ((rc = dmalloc(&L->perm, (size_t)L->tpad_max, nullptr))) return rc;
+    if ((rc = dmalloc(&L->pinv, (size_t)Tc, nullptr))) return rc;
     if ((rc = dmalloc(&L->inverse, (size_t)Tc, nullptr))) return rc;
     if ((rc = dmalloc(&L->cperm, (size_t)Tc, nullptr))) return rc;
     if ((rc = dmalloc(&L->escale, (size_t)L->tpad_max, nullptr))) return rc;
     if ((rc = dmalloc(&L->xperm, (size_t)(L->tpad_max * L->in_pad), nullptr))) return rc;
     if ((rc = dmalloc(&L->tiles, (size_t)L->max_tiles, nullptr))) return rc;
     if ((rc = dmalloc(&L->meta, 64, nullptr))) return rc;
+    if (!L->gpart && (rc = dmalloc(&L->gpart, (size_t)(8 * 64 * L->out_pad), nullptr))) return rc;
+    if (!L->hpart && (rc = dmalloc(&L->hpart, (size_t)(16 * 64 * L->h_pad), nullptr))) return rc;
     L->ws_T = Tc;
     return MOBI_OK;
 }
@@ -387,6 +391,8 @@ int mobi_layer_destroy(mobi_layer_t L) {
     free_ws(L);
     dfree(L->codes8);
     dfree(L->gconst);
+    dfree(L->gpart);
+    dfree(L->hpart);
     dfree(L->w1t);
     dfree(L->b1);
     dfree(L->w2);

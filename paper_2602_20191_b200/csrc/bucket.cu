@@ -11,7 +11,7 @@
 // tile never mixes masks.  It also emits the GEMM's token-tile list (bucket mask, first row,
 // valid rows), so no host round trip is needed between routing and the GEMM.
 //
-// gather_kernel: one CTA per permuted row copies X[perm[i]] (bf16) into xperm[i] (fp16) scaled
+// gather_kernel: one CTA per token copies X[t] (bf16) into xperm[pinv[t]] (fp16) scaled
 // by a per-row power of two 2^-e (max|x| lands in [2^14, 2^15)); the GEMM epilogue multiplies
 // by 2^e.  The scaling is exact, so fp16 operands lose nothing against the bf16 input.
 #include "mobi_internal.cuh"
@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
     float delta, const uint8_t* __restrict__ given_masks, int sanitize, float* __restrict__ scores_out,
     uint8_t* __restrict__ keys, uint8_t* __restrict__ masks_out, int32_t* __restrict__ perm,
     int64_t tpad_max, int32_t* __restrict__ cperm_out, int32_t* __restrict__ inverse_out,
-    int32_t* __restrict__ counts_out, TokTile* __restrict__ tiles, int32_t* __restrict__ meta) {
+    int32_t* __restrict__ counts_out, TokTile* __restrict__ tiles, int32_t* __restrict__ meta,
+    int32_t* __restrict__ pinv) {
     __shared__ int hist[NKEY], cstart[NKEY], run[NKEY], pstart[NKEY_MASK];
     __shared__ int warp_hist[BK_THREADS / 32][NKEY];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
             meta[1] = a;
             for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) meta[2 + v] = hist[v];
             meta[32] = 0;  // GEMM dynamic tile counter
+            meta[33] = 1;  // GEMM split count (the GEMM overwrites it when it splits K)
         }
     }
     __syncthreads();
@@ -124,7 +126,10 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
         if (valid) {
             const int off = warp_hist[wid][key] + rank;
             const int cpos = cstart[key] + off;
-            if (perm && key < NKEY_MASK) perm[pstart[key] + off] = (int32_t)t;
+            if (perm && key < NKEY_MASK) {
+                perm[pstart[key] + off] = (int32_t)t;
+                pinv[t] = pstart[key] + off;
+            }
             if (cperm_out) cperm_out[cpos] = (int32_t)t;
             if (inverse_out) inverse_out[t] = cpos;
         }
@@ -132,20 +137,16 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
     }
 }
 
+// One CTA per token t: write its permuted row pinv[t].  Padding rows between buckets are never
+// written: the GEMM only ever reads them as B columns whose outputs it discards.
 __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __restrict__ x, int64_t in,
-                                                     int64_t in_pad, const int32_t* __restrict__ perm,
+                                                     int64_t in_pad, const int32_t* __restrict__ pinv,
                                                      __half* __restrict__ xperm, float* __restrict__ escale,
                                                      bool vec) {
     __shared__ float red[4];
-    const int64_t i = blockIdx.x;
-    const int32_t src = perm[i];
+    const int64_t src = blockIdx.x;
+    const int64_t i = pinv[src];
     __half* dst = xperm + i * in_pad;
-    if (src < 0) {
-        for (int64_t k = threadIdx.x * 8; k < in_pad; k += 128 * 8)
-            *reinterpret_cast<uint4*>(dst + k) = make_uint4(0, 0, 0, 0);
-        if (threadIdx.x == 0) escale[i] = 1.f;
-        return;
-    }
     const __nv_bfloat16* row = x + (int64_t)src * in;
     float m = 0.f;
     if (vec) {
@@ -199,7 +200,7 @@ int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_ma
     bucket_kernel<NKEY_MASK><<<1, BK_THREADS, 0, st>>>(L->s_part, (int)L->htiles, T, L->nr, L->b2, delta,
                                              given_masks, 1, scores_out, L->masks, masks_out, L->perm,
                                              L->tpad_max, cperm_out, inverse_out, counts_out, L->tiles,
-                                             L->meta);
+                                             L->meta, L->pinv);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;
@@ -208,15 +209,14 @@ int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_ma
 int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* cperm, int32_t* inverse,
                    int32_t* hist256, cudaStream_t st) {
     bucket_kernel<NKEY_ALL><<<1, BK_THREADS, 0, st>>>(nullptr, 0, T, 0, nullptr, 0.f, masks, 0, nullptr, keys_tmp,
-                                             nullptr, nullptr, 0, cperm, inverse, hist256, nullptr, nullptr);
+                                             nullptr, nullptr, 0, cperm, inverse, hist256, nullptr, nullptr, nullptr);
     MOBI_LAUNCH_CHECK();
     return MOBI_OK;
 }
 
 int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st) {
     const bool vec = (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    gather_kernel<<<(unsigned)L->tpad_max, 128, 0, st>>>(x, L->in, L->in_pad, L->perm, L->xperm,
-                                                          L->escale, vec);
+    gather_kernel<<<(unsigned)T, 128, 0, st>>>(x, L->in, L->in_pad, L->pinv, L->xperm, L->escale, vec);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

@@ -41,6 +41,8 @@ using namespace sm100;
 #endif
 constexpr int NSTAGE = MOBI_NSTAGE;  // B stages (smem, 32 KiB each)
 constexpr int NSA = 8;               // A stages (TMEM, 32 columns each)
+constexpr int kSplitMaxT = 64;   // split-K only for decode-size batches
+constexpr int kMaxSplit = 8;
 constexpr int kBoxRows = 32;                      // TMA box: 32 token rows x 64 k (4 KiB)
 constexpr int kBoxBytes = kBoxRows * kKBlock * 2;
 constexpr int kDqWarps = 16;                       // 4 per TMEM lane quarter
@@ -72,6 +74,9 @@ struct Params {
     __nv_bfloat16* y;
     int vec_y;
     int* tile_counter;  // zeroed by the bucket kernel before every launch
+    int max_split;      // split-K allowed (small T only): partials go to gpart, reduced by splitk_reduce
+    int T;
+    float* gpart;       // [split][T][out] fp32 (x 2^e applied)
     unsigned long long* trace;
 };
 
@@ -156,12 +161,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rank = cluster_ctarank();
     const int n_tok_tiles = p.meta[0];
     const int n_pairs_row = p.n_row_tiles / 2;
-    const int total = n_tok_tiles * n_pairs_row;
     const int kb_n = (int)p.kblocks;
     const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
-    auto tile_of = [&](int pair, TokTile& tt, int& rt) {
-        tt = uniform_tile(p.tiles[pair / n_pairs_row]);
-        rt = (pair % n_pairs_row) * 2 + (int)rank;
+    // split-K when the (token tile x row pair) grid cannot fill the clusters (decode-size T):
+    // every CTA derives the same split count from the device-side tile count
+    int nsplit = 1;
+    if (p.max_split > 1) nsplit = max(1, min(p.max_split, ncl / max(1, n_tok_tiles * n_pairs_row)));
+    const int kb_per = (kb_n + nsplit - 1) / nsplit;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && p.max_split > 1) p.tile_counter[1] = nsplit;  // for the reduce
+    const int total = n_tok_tiles * n_pairs_row * nsplit;
+    // pair -> (token tile, this CTA's 128-row tile, k-block range [kb0, kb1))
+    auto tile_of = [&](int pair, TokTile& tt, int& rt, int& ks, int& kb0, int& kb1) {
+        ks = pair % nsplit;
+        const int q = pair / nsplit;
+        tt = uniform_tile(p.tiles[q / n_pairs_row]);
+        rt = (q % n_pairs_row) * 2 + (int)rank;
+        kb0 = ks * kb_per;
+        kb1 = min(kb_n, kb0 + kb_per);
     };
 
     if (warp == kWarpTma) {
@@ -169,11 +185,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t it = 0;
         for (int pair = cid; pair < total; pair += ncl) {
             TokTile tt;
-            int rt;
-            tile_of(pair, tt, rt);
+            int rt, ks, kb0, kb1;
+            tile_of(pair, tt, rt, ks, kb0, kb1);
             if (TRACE && lane == 0) ++tr[3];
             const int nbox = (tt.n + kBoxRows - 1) / kBoxRows;
-            for (int kb = 0; kb < kb_n; ++kb, ++it) {
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
@@ -192,14 +208,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t it = 0, tc = 0;
         for (int pair = cid; pair < total; pair += ncl, ++tc) {
             TokTile tt;
-            int rt;
-            tile_of(pair, tt, rt);
+            int rt, ks, kb0, kb1;
+            tile_of(pair, tt, rt, ks, kb0, kb1);
             // N class: 16, or a multiple of 32 (constant instruction descriptors per class)
             const uint32_t n_mma = tt.n <= 16 ? 16u : (uint32_t)round_up(tt.n, 32);
             TW(0, mbar_wait(acc_empty, (tc & 1) ^ 1));
             tc_fence_after();
             long long t_tile0 = TRACE ? clock64() : 0;
-            for (int kb = 0; kb < kb_n; ++kb, ++it) {
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 const int sa = it % NSA;
@@ -212,7 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (elect_one_sync()) {
                     const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
                     const uint32_t acol = tmem + kACol0 + sa * 32;
-                    const bool first = kb == 0;
+                    const bool first = kb == kb0;
                     switch (n_mma) {
                         case 16: issue_kblock_ts<16>(acol, bdesc, first); break;
                         case 32: issue_kblock_ts<32>(acol, bdesc, first); break;
@@ -226,7 +242,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     }
                     mma_commit_mc(&empty[s], (uint16_t)0x3);  // frees the shared B stage in both CTAs
                     mma_commit(&empty_a[sa]);                 // frees the local A stage
-                    if (kb == kb_n - 1) mma_commit(acc_full);
+                    if (kb == kb1 - 1) mma_commit(acc_full);
                 }
                 __syncwarp();
                 EV(3, kb, tc);
@@ -246,10 +262,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int hh = idx / 8;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
-        for (int pair = cid; pair < total; pair += ncl, base += kb_n) {
+        for (int pair = cid; pair < total; pair += ncl) {
             TokTile tt;
-            int rt;
-            tile_of(pair, tt, rt);
+            int rt, ks, kb0, kb1;
+            tile_of(pair, tt, rt, ks, kb0, kb1);
+            const int kb_lim = kb1;  // this tile's k-blocks are [kb0, kb1); stage index = base + kb - kb0
             const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
             const bool rv = R < p.out;
             const uint32_t mw = p.mt.maskword[tt.mask];
@@ -281,15 +298,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             float2 g0 = make_float2(0.f, 0.f), g1 = g0, g2 = g0;
             int gp = 0, kinp = 0;  // group cursor at the next k-block to prefetch
             if (!p.single_group) {
-                kinp = par * kKBlock + hh * 32;
-                while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
+                const int k0 = (kb0 + par) * kKBlock + hh * 32;
+                gp = k0 / (int)p.gs;
+                kinp = k0 - gp * (int)p.gs;
             }
             auto fetch = [&](int kb, uint4& c0, uint4& c1, float2& gc) {
 #if MOBI_ABLATE >= 1
                 c0 = make_uint4(kb, kb, kb, kb); c1 = c0; gc = make_float2(1.f, 0.f);
                 return;
 #endif
-                if (kb < kb_n) {
+                if (kb < kb_lim) {
                     ld(kb, c0, c1);
                     gc = ldc(gp);
                 }
@@ -298,14 +316,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
                 }
             };
-            fetch(par, c00, c01, g0);
-            fetch(par + 2, c10, c11, g1);
-            fetch(par + 4, c20, c21, g2);
+            fetch(kb0 + par, c00, c01, g0);
+            fetch(kb0 + par + 2, c10, c11, g1);
+            fetch(kb0 + par + 4, c20, c21, g2);
             uint32_t v[16];
             auto step = [&](int kb, uint4& ca, uint4& cb, float2& ga, uint4& na, uint4& nb, float2& gn) -> bool {
                 // v holds k-block kb (dequantized from the slot (ca, cb)); (na, nb) holds kb+2
-                if (kb >= kb_n) return false;
-                const uint32_t itk = base + kb;
+                if (kb >= kb_lim) return false;
+                const uint32_t itk = base + (kb - kb0);
                 const int s = itk % NSA;
                 const uint32_t ph = (itk / NSA) & 1;
                 TW(0, mbar_wait(&empty_a[s], ph ^ 1));
@@ -316,7 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #if MOBI_ABLATE >= 2
                 (void)na; (void)nb; (void)gn;
 #else
-                if (kb + 2 < kb_n) TW(1, dq(na, nb, gn, v));
+                if (kb + 2 < kb_lim) TW(1, dq(na, nb, gn, v));
 #endif
                 if (warp == 0 || warp == 4) EV(5, kb, base);
                 TW(2, tmem_st_wait());
@@ -326,12 +344,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(&full_a[s]);
                 return true;
             };
-            if (par < kb_n) dq(c00, c01, g0, v);
-            for (int kb = par; kb < kb_n; kb += 6) {
+            if (kb0 + par < kb_lim) dq(c00, c01, g0, v);
+            for (int kb = kb0 + par; kb < kb_lim; kb += 6) {
                 if (!step(kb, c00, c01, g0, c10, c11, g1)) break;
                 if (!step(kb + 2, c10, c11, g1, c20, c21, g2)) break;
                 if (!step(kb + 4, c20, c21, g2, c00, c01, g0)) break;
             }
+            base += kb1 - kb0;
         }
     } else {
         // ---------------- epilogue ----------------
@@ -343,10 +362,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t tc = 0;
         for (int pair = cid; pair < total; pair += ncl, ++tc) {
             TokTile tt;
-            int rt;
-            tile_of(pair, tt, rt);
+            int rt, ks, kb0, kb1;
+            tile_of(pair, tt, rt, ks, kb0, kb1);
             TW(0, mbar_wait(acc_full, tc & 1));
             tc_fence_after();
+            if (nsplit > 1) {
+                // split-K partial: fp32 x 2^e straight to gpart[ks][token][row] (coalesced over rows)
+                const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
+                for (int c0 = 0; c0 < tt.n; c0 += 32) {
+                    const int nn = min(32, tt.n - c0);
+                    int32_t my_src = -1;
+                    float my_es = 0.f;
+                    if (lane < nn) {
+                        my_src = __ldg(p.perm + tt.row0 + c0 + lane);
+                        my_es = __ldg(p.escale + tt.row0 + c0 + lane);
+                    }
+                    uint32_t v[32];
+                    tmem_ld32(tmem + lane_base + c0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int32_t src = __shfl_sync(0xffffffffu, my_src, j);
+                        const float es = __shfl_sync(0xffffffffu, my_es, j);
+                        if (src >= 0 && R < p.out)
+                            p.gpart[((int64_t)ks * p.T + src) * p.out + R] = __uint_as_float(v[j]) * es;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(acc_empty);
+                continue;
+            }
             epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
             for (int c0 = 0; c0 < tt.n; c0 += 32) {
                 const int nn = min(32, tt.n - c0);
@@ -400,6 +446,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncthreads();
     cluster_sync();  // no CTA leaves while its peer may still multicast into it
     if (warp == kWarpMma) tmem_dealloc(tmem, 512);
+}
+
+// y[t][r] = bf16( sum_{ks < nsplit} gpart[ks][t][r] ) in a fixed order (deterministic)
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ gpart, const int* __restrict__ meta,
+                                                            int T, int64_t out, __nv_bfloat16* __restrict__ y) {
+    const int nsplit = meta[33];
+    if (nsplit <= 1) return;  // the GEMM epilogue already wrote bf16
+    const int t = blockIdx.x;
+    for (int64_t r = threadIdx.x; r < out; r += blockDim.x) {
+        float acc = 0.f;
+        for (int ks = 0; ks < nsplit; ++ks) acc += gpart[((int64_t)ks * T + t) * out + r];
+        y[(int64_t)t * out + r] = __float2bfloat16_rn(acc);
+    }
 }
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -486,12 +545,20 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
     p.trace = trace;
     p.tile_counter = L->meta + 32;
+    p.T = (int)T;
+    p.max_split = (T <= kSplitMaxT && L->gpart) ? kMaxSplit : 1;
+    p.gpart = L->gpart;
     if (trace)
         mobi_gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
     else
         mobi_gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
+    if (p.max_split > 1) {
+        splitk_reduce_kernel<<<(unsigned)T, 256, 0, st>>>(L->gpart, L->meta, (int)T, L->out, y);
+        MOBI_LAUNCH_CHECK();
+        ++L->last_launches;
+    }
     return MOBI_OK;
 }
 

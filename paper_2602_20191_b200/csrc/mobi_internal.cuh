@@ -98,11 +98,14 @@ struct mobi_layer {
     float* scores = nullptr;   // [T][nr]
     uint8_t* masks = nullptr;  // [T]
     int32_t* perm = nullptr;   // [tpad_max] permuted row -> token (-1 pad)
+    int32_t* pinv = nullptr;   // [T] token -> permuted row
     int32_t* inverse = nullptr;// [T]
     int32_t* cperm = nullptr;  // [T] compact (unpadded) permutation
     float* escale = nullptr;   // [tpad_max] per-row power-of-two scale
     __half* xperm = nullptr;   // [tpad_max][in_pad] fp16 permuted, scaled activations
     mobi::TokTile* tiles = nullptr;  // [max_tiles]
+    float* gpart = nullptr;    // [8][64][out] split-K partials (decode-size T)
+    float* hpart = nullptr;    // [16][64][h_pad] router split-K partials
     int32_t* meta = nullptr;   // [0]=n_tiles [1]=total padded rows [2..2+16) bucket counts
     void* x_dev = nullptr;     // staging for mobi_forward_host
     void* y_dev = nullptr;

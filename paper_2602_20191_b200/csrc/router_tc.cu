@@ -27,11 +27,13 @@ constexpr int kRWarpTma = 4, kRWarpMma = 5;
 constexpr int kRSmem = RS * 2 * kAB + 1024 + 256;
 
 struct RParams {
-    int64_t T, h;
+    int64_t T, h, h_pad;
     int kblocks, n_mt, n_nt, nr;
+    int nsplit, kb_per;  // split-K (decode-size T): raw hidden partials to hpart, reduced below
     const float* b1;
     const float* w2;
     float* s_part;
+    float* hpart;        // [nsplit][T][h_pad]
 };
 
 __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -65,13 +67,23 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     tc_fence_after();
     if (*tmem_slot != 0) __trap();
     constexpr uint32_t tmem = 0;
-    const int total = p.n_mt * p.n_nt;
+    const int total = p.n_mt * p.n_nt * p.nsplit;
+    // tile -> (token tile mt, hidden tile nt, k-split ks)
+    auto tile_of = [&](int tile, int& mt, int& nt, int& ks, int& kb0, int& kb1) {
+        ks = tile % p.nsplit;
+        const int q = tile / p.nsplit;
+        mt = q % p.n_mt;
+        nt = q / p.n_mt;
+        kb0 = ks * p.kb_per;
+        kb1 = min(p.kblocks, kb0 + p.kb_per);
+    };
 
     if (warp == kRWarpTma) {
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-            const int mt = tile % p.n_mt, nt = tile / p.n_mt;
-            for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+            int mt, nt, ks, kb0, kb1;
+            tile_of(tile, mt, nt, ks, kb0, kb1);
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % RS;
                 mbar_wait(&empty[s], ((it / RS) & 1) ^ 1);
                 if (elect_one_sync()) {
@@ -86,12 +98,13 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     } else if (warp == kRWarpMma) {
         uint32_t it = 0, tc = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
-            const int nt = tile / p.n_mt;
+            int mt, nt, ks, kb0, kb1;
+            tile_of(tile, mt, nt, ks, kb0, kb1);
             const uint32_t n_mma = (uint32_t)std::min<int64_t>(RN, round_up(p.h - (int64_t)nt * RN, 16));
             const int buf = tc & 1;
             mbar_wait(&acc_empty[buf], ((tc >> 1) & 1) ^ 1);
             tc_fence_after();
-            for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+            for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % RS;
                 mbar_wait(&full[s], (it / RS) & 1);
                 tc_fence_after();
@@ -103,15 +116,15 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
                         constexpr uint32_t idesc = idesc_f16(RM, RN, 1);
 #pragma unroll
                         for (int j = 0; j < kKBlock / 16; ++j)
-                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb | j) != 0);
+                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb != kb0) || (j != 0));
                     } else {  // partial hidden tile (h % 128 != 0): runtime descriptor
                         const uint32_t idesc = idesc_f16(RM, n_mma, 1);
 #pragma unroll
                         for (int j = 0; j < kKBlock / 16; ++j)
-                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb | j) != 0);
+                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb != kb0) || (j != 0));
                     }
                     mma_commit(&empty[s]);
-                    if (kb == p.kblocks - 1) mma_commit(&acc_full[buf]);
+                    if (kb == kb1 - 1) mma_commit(&acc_full[buf]);
                 }
                 __syncwarp();
             }
@@ -121,13 +134,31 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         uint32_t tc = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
-            const int mt = tile % p.n_mt, nt = tile / p.n_mt;
+            int mt, nt, ks, kb0, kb1;
+            tile_of(tile, mt, nt, ks, kb0, kb1);
             const int buf = tc & 1;
             const int64_t t = (int64_t)mt * RM + 32 * q + lane;
             const int64_t h0 = (int64_t)nt * RN;
             const int nh = (int)std::min<int64_t>(RN, p.h - h0);
             mbar_wait(&acc_full[buf], (tc >> 1) & 1);
             tc_fence_after();
+            if (p.nsplit > 1) {  // raw hidden partial H[t, h0..h0+nh) for this k-split
+                for (int c0 = 0; c0 < nh; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + lane_base + buf * RN + c0, v);
+                    tmem_ld_wait();
+                    if (t < p.T) {
+                        float* dst = p.hpart + ((int64_t)ks * p.T + t) * p.h_pad + h0 + c0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (c0 + j < nh) dst[j] = __uint_as_float(v[j]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[buf]);
+                continue;
+            }
             float part[MOBI_MAX_SLICES - 1] = {0.f, 0.f, 0.f};
             for (int c0 = 0; c0 < nh; c0 += 32) {
                 uint32_t v[32];
@@ -159,6 +190,33 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     tc_fence_before();
     __syncthreads();
     if (warp == kRWarpMma) tmem_dealloc(tmem, 512);
+}
+
+// split-K finish: H = sum_ks hpart (fixed order) -> silu(H + b1) . w2 -> s_part[nt][t][k]
+__global__ void __launch_bounds__(RN) router_reduce_kernel(const float* __restrict__ hpart, int nsplit, int64_t T,
+                                                           int64_t h, int64_t h_pad, const float* __restrict__ b1,
+                                                           const float* __restrict__ w2, int nr,
+                                                           float* __restrict__ s_part) {
+    __shared__ float red[MOBI_MAX_SLICES - 1][RN];
+    const int64_t t = blockIdx.x;
+    const int nt = blockIdx.y;
+    const int64_t j = (int64_t)nt * RN + threadIdx.x;
+    float sv = 0.f;
+    if (j < h) {
+        float H = 0.f;
+        for (int ks = 0; ks < nsplit; ++ks) H += hpart[((int64_t)ks * T + t) * h_pad + j];
+        const float a = H + b1[j];
+        sv = a * __fdividef(1.f, 1.f + __expf(-a));
+    }
+    for (int k = 0; k < nr; ++k) red[k][threadIdx.x] = j < h ? sv * w2[j * nr + k] : 0.f;
+    __syncthreads();
+    for (int w = RN / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w)
+            for (int k = 0; k < nr; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int k = 0; k < nr; ++k) s_part[((int64_t)nt * T + t) * nr + k] = red[k][0];
 }
 
 int sm_count() {
@@ -198,6 +256,8 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStrea
     RParams p;
     p.T = T;
     p.h = L->h;
+    p.h_pad = L->h_pad;
+    p.hpart = L->hpart;
     p.kblocks = (int)L->kblocks;
     p.n_mt = (int)cdiv(T, RM);
     p.n_nt = (int)cdiv(L->h, RN);
@@ -206,11 +266,26 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStrea
     p.w2 = L->w2;
     p.s_part = L->s_part;
     L->htiles = p.n_nt;
-    const int total = p.n_mt * p.n_nt;
+    const int total = p.n_mt * p.n_nt * p.nsplit;
+    // tile -> (token tile mt, hidden tile nt, k-split ks)
+    auto tile_of = [&](int tile, int& mt, int& nt, int& ks, int& kb0, int& kb1) {
+        ks = tile % p.nsplit;
+        const int q = tile / p.nsplit;
+        mt = q % p.n_mt;
+        nt = q / p.n_mt;
+        kb0 = ks * p.kb_per;
+        kb1 = min(p.kblocks, kb0 + p.kb_per);
+    };
     const int grid = std::min(total, sm_count());
     router_tc_kernel<<<grid, kRThreads, kRSmem, st>>>(tmap_x, *L->tmap_w1, p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
+    if (p.nsplit > 1) {
+        router_reduce_kernel<<<dim3((unsigned)T, (unsigned)p.n_nt), RN, 0, st>>>(L->hpart, p.nsplit, T, L->h, L->h_pad,
+                                                                                L->b1, L->w2, L->nr, L->s_part);
+        MOBI_LAUNCH_CHECK();
+        ++L->last_launches;
+    }
     return MOBI_OK;
 }
 
