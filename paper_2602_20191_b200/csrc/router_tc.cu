@@ -266,16 +266,12 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStrea
     p.w2 = L->w2;
     p.s_part = L->s_part;
     L->htiles = p.n_nt;
+    // split K when the tile grid cannot fill the SMs (decode-size T)
+    p.nsplit = 1;
+    if (T <= 64 && L->hpart) p.nsplit = std::max(1, std::min(16, sm_count() / (p.n_mt * p.n_nt)));
+    p.kb_per = (p.kblocks + p.nsplit - 1) / p.nsplit;
+    p.nsplit = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty splits
     const int total = p.n_mt * p.n_nt * p.nsplit;
-    // tile -> (token tile mt, hidden tile nt, k-split ks)
-    auto tile_of = [&](int tile, int& mt, int& nt, int& ks, int& kb0, int& kb1) {
-        ks = tile % p.nsplit;
-        const int q = tile / p.nsplit;
-        mt = q % p.n_mt;
-        nt = q / p.n_mt;
-        kb0 = ks * p.kb_per;
-        kb1 = min(p.kblocks, kb0 + p.kb_per);
-    };
     const int grid = std::min(total, sm_count());
     router_tc_kernel<<<grid, kRThreads, kRSmem, st>>>(tmap_x, *L->tmap_w1, p);
     MOBI_LAUNCH_CHECK();
