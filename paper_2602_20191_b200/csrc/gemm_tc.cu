@@ -166,8 +166,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // split-K when the (token tile x row pair) grid cannot fill the clusters (decode-size T):
     // every CTA derives the same split count from the device-side tile count
     int nsplit = 1;
-    if (p.max_split > 1) nsplit = max(1, min(p.max_split, ncl / max(1, n_tok_tiles * n_pairs_row)));
+    if (p.max_split > 1) nsplit = max(1, min(min(p.max_split, kb_n), ncl / max(1, n_tok_tiles * n_pairs_row)));
     const int kb_per = (kb_n + nsplit - 1) / nsplit;
+    nsplit = (kb_n + kb_per - 1) / kb_per;  // every split owns at least one k-block (no empty ranges)
     if (blockIdx.x == 0 && threadIdx.x == 0 && p.max_split > 1) p.tile_counter[1] = nsplit;  // for the reduce
     const int total = n_tok_tiles * n_pairs_row * nsplit;
     // pair -> (token tile, this CTA's 128-row tile, k-block range [kb0, kb1))
