@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--ring", type=int, default=0)
+    p.add_argument("--graph", action="store_true",
+                   help="replay each ring slot's forward from a captured CUDA graph (decode-size T: removes "
+                        "host launch overhead); per-kernel times then come from an eager profiled pass")
     return p.parse_args()
 
 
@@ -235,8 +238,25 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    for r in ring:
-        r["layer"].profile(True)
+    graphs = None
+    if args.graph:
+        graphs = []
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            for r in ring:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cs):
+                    r["layer"].forward(r["x"], r["delta"], y=r["y"])
+                graphs.append(g)
+        torch.cuda.current_stream().wait_stream(cs)
+        for i in range(args.warmup):
+            graphs[i % R].replay()
+        torch.cuda.synchronize()
+        config["launch"] = "CUDA graph per ring slot (captured forward), replayed each step"
+    else:
+        for r in ring:
+            r["layer"].profile(True)
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.05)
@@ -246,10 +266,15 @@ def main():
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
+    per_step_launches = [r["layer"].last_launches() for r in ring]
     e0.record(st)
     for i in range(args.steps):
-        step(i)
-        launches += ring[i % R]["layer"].last_launches()
+        if graphs is not None:
+            graphs[i % R].replay()
+            launches += per_step_launches[i % R]
+        else:
+            step(i)
+            launches += ring[i % R]["layer"].last_launches()
     e1.record(st)
     torch.cuda.synchronize()
     if dist:
@@ -260,7 +285,14 @@ def main():
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms = float(t.item())
-    # per-kernel device time inside the timed region
+    # per-kernel device time inside the timed region (graph mode: an eager profiled pass after it)
+    if graphs is not None:
+        for r in ring:
+            r["layer"].profile(True)
+        for i in range(min(args.steps, 50)):
+            step(i)
+        torch.cuda.synchronize()
+        config["kernel_times"] = "eager profiled pass after the graph-timed region (no PDL overlap)"
     kern = {k: [0.0, 0] for k in ("router", "bucket", "gather", "gemm")}
     for r in ring:
         for k, (t_ms, n) in r["layer"].profile_read().items():

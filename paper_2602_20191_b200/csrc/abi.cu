@@ -13,7 +13,8 @@
 namespace mobi {
 
 static thread_local std::string g_err;
-static int g_impl_override = 0;  // test hook: 1 = CUDA-core reference GEMM, 2 = traced tcgen05
+static int g_impl_override = 0;  // test hook: 1 = CUDA-core reference GEMM, 2 = traced tcgen05,
+                                 // 5 = bucketed tcgen05 path at every T (no decode path), 6 = decode path without PDL
 static unsigned long long* g_trace_buf = nullptr;
 
 int set_error(int code, const std::string& msg) {
@@ -107,6 +108,16 @@ int ensure_ws(mobi_layer* L, int64_t T) {
     if ((rc = dmalloc(&L->meta, 64, nullptr))) return rc;
     if (!L->gpart && (rc = dmalloc(&L->gpart, (size_t)(8 * 64 * L->out_pad), nullptr))) return rc;
     if (!L->hpart && (rc = dmalloc(&L->hpart, (size_t)(16 * 64 * L->h_pad), nullptr))) return rc;
+    if (!L->dec_cnt) {
+        int nsm = 0, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t n_rt = cdiv(L->out, kRowTile), n_mt = L->h_pad / 16;
+        if ((rc = dmalloc(&L->dec_part, (size_t)((std::max(nsm, 1) + n_rt) * kDecMaxT * kRowTile), nullptr))) return rc;
+        if ((rc = dmalloc(&L->dec_spart, (size_t)(n_mt * kDecMaxT * L->nr), nullptr))) return rc;
+        if ((rc = dmalloc(&L->dec_cnt, (size_t)(n_rt + n_mt + 1), nullptr))) return rc;
+        MOBI_CUDA(cudaMemset(L->dec_cnt, 0, (size_t)(n_rt + n_mt + 1) * sizeof(int32_t)));
+    }
     L->ws_T = Tc;
     return MOBI_OK;
 }
@@ -310,6 +321,16 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+    if ((g_impl_override == 0 || g_impl_override == 6) && decode_supported(L, x, T)) {
+        // decode-size batch: router GEMV -> (PDL) stream-K decode GEMM, no bucketing
+        if (!given_masks) {
+            ProfScope p(L, 0, st);
+            if ((rc = launch_router_dec(L, xb, T, delta, masks_out, nullptr, st))) return rc;
+        }
+        ProfScope p(L, 3, st);
+        return launch_decode_gemm(L, xb, T, given_masks, reinterpret_cast<__nv_bfloat16*>(y),
+                                  !given_masks && g_impl_override != 6 && !L->prof, st);
+    }
     if (!given_masks) {
         ProfScope p(L, 0, st);
         if ((rc = route_scores(L, xb, T, st))) return rc;
@@ -393,6 +414,9 @@ int mobi_layer_destroy(mobi_layer_t L) {
     dfree(L->gconst);
     dfree(L->gpart);
     dfree(L->hpart);
+    dfree(L->dec_part);
+    dfree(L->dec_spart);
+    dfree(L->dec_cnt);
     dfree(L->w1t);
     dfree(L->b1);
     dfree(L->w2);

@@ -31,6 +31,7 @@ constexpr int kBlockBytes = kRowTile * kKBlock;  // 8192
 constexpr int kBucketAlign = 16;                 // bucket starts in the permuted token order
 constexpr int kTokTile = 256;                    // tokens per GEMM tile (MMA N <= 256)
 constexpr int kMaxBuckets = 1 << (MOBI_MAX_SLICES - 1);  // 8 masks (slice-1 bit always set)
+constexpr int kDecMaxT = 32;                     // decode path (decode.cu): up to 32 tokens per call
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return cdiv(a, b) * b; }
@@ -106,6 +107,9 @@ struct mobi_layer {
     mobi::TokTile* tiles = nullptr;  // [max_tiles]
     float* gpart = nullptr;    // [8][64][out] split-K partials (decode-size T)
     float* hpart = nullptr;    // [16][64][h_pad] router split-K partials
+    float* dec_part = nullptr; // decode path: [(sm + n_rt)][kDecMaxT][128] row-tile partials
+    float* dec_spart = nullptr;// decode router: [h_pad/16][kDecMaxT][nr] score partials
+    int32_t* dec_cnt = nullptr;// decode arrival counters [n_rt + h_pad/16 + 1], zero between launches
     int32_t* meta = nullptr;   // [0]=n_tiles [1]=total padded rows [2..2+16) bucket counts
     void* x_dev = nullptr;     // staging for mobi_forward_host
     void* y_dev = nullptr;
@@ -167,6 +171,12 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
 int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
                     unsigned long long* trace = nullptr);  // gemm_tc2.cu (CTA pairs)
+// decode.cu (T <= kDecMaxT: router GEMV + stream-K decode GEMM, PDL-chained)
+bool decode_supported(const mobi_layer* L, const void* x, int64_t T);
+int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, uint8_t* masks_out,
+                      float* scores_out, cudaStream_t st);
+int launch_decode_gemm(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks,
+                       __nv_bfloat16* y, bool pdl, cudaStream_t st);
 // decompose.cu
 int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,
                      int32_t E, double gamma, uint8_t* codes, double* scale, double* zero,
