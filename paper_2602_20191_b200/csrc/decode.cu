@@ -30,7 +30,9 @@ namespace {
 using namespace sm100;
 
 constexpr int kDecWarps = 8;                     // MMA warps, 16 weight rows each
-constexpr int kDecThreads = 32 * (kDecWarps + 1);  // + 1 producer warp
+constexpr int kDecThreads = 32 * kDecWarps;      // thread 0 doubles as the TMA producer (a 9th warp
+                                                 // would put 3 warps on one SM sub-partition and cap
+                                                 // registers at 168)
 constexpr int kDecStages = 8;                    // 8 KiB code blocks in flight per CTA
 constexpr int kRdWarps = 4;                      // router: warps per CTA (split K inside the CTA)
 constexpr int kRdRows = 16;                      // router: hidden units per CTA (one m16 tile)
@@ -241,7 +243,7 @@ __host__ __device__ inline DecSmem dec_smem(int T, int len_max, int xs_stride) {
 __device__ __forceinline__ int cta_of(int64_t u, int64_t U, int n) { return (int)(((u + 1) * n + U - 1) / U) - 1; }
 
 template <int MAXT>
-__global__ void __maxnreg__(224) decode_gemm_kernel(const __grid_constant__ DParams p) {
+__global__ void __launch_bounds__(kDecThreads, 1) decode_gemm_kernel(const __grid_constant__ DParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ float s_escale[kDecMaxT + 1], s_scl[kDecMaxT + 1];
     __shared__ int s_max[kDecMaxT + 1];
@@ -268,18 +270,16 @@ __global__ void __maxnreg__(224) decode_gemm_kernel(const __grid_constant__ DPar
     }
     __syncthreads();
 
-    if (warp == kDecWarps) {
-        // ---------------- producer: stream this CTA's code blocks (independent of the router) ----------------
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            for (int64_t it = 0; it < u1 - u0; ++it) {
-                const int s = (int)(it % kDecStages);
-                if (it >= kDecStages) mbar_wait(&empty[s], (uint32_t)((it / kDecStages - 1) & 1));
-                mbar_arrive_expect_tx(&full[s], kBlockBytes);
-                bulk_load(ring + (size_t)s * kBlockBytes, p.codes8 + (u0 + it) * kBlockBytes, kBlockBytes, &full[s], pol);
-            }
+    // thread 0 streams this CTA's code blocks (independent of the router: starts before the
+    // grid dependency resolves); the first kDecStages now, the rest as stages are released
+    const int64_t nblk = u1 - u0;
+    uint64_t pol = 0;
+    if (threadIdx.x == 0) {
+        pol = policy_evict_first();
+        for (int64_t it = 0; it < nblk && it < kDecStages; ++it) {
+            mbar_arrive_expect_tx(&full[it], kBlockBytes);
+            bulk_load(ring + (size_t)it * kBlockBytes, p.codes8 + (u0 + it) * kBlockBytes, kBlockBytes, &full[it], pol);
         }
-        return;
     }
 
     // ---------------- MMA warps ----------------
@@ -462,6 +462,15 @@ __global__ void __maxnreg__(224) decode_gemm_kernel(const __grid_constant__ DPar
             cur_rt = rt;
 #pragma unroll
             for (int i = 0; i < MAXT; ++i) yp[i][0] = yp[i][1] = yp[i][2] = yp[i][3] = 0.f;
+        }
+        if (threadIdx.x == 0 && it >= 1 && it - 1 + kDecStages < nblk) {
+            // refill the stage every warp released in the previous iteration
+            const int64_t j = it - 1;
+            const int sj = (int)(j % kDecStages);
+            mbar_wait(&empty[sj], (uint32_t)((j / kDecStages) & 1));
+            mbar_arrive_expect_tx(&full[sj], kBlockBytes);
+            bulk_load(ring + (size_t)sj * kBlockBytes, p.codes8 + (u0 + j + kDecStages) * kBlockBytes, kBlockBytes,
+                      &full[sj], pol);
         }
         const float2 g0 = gn0, g1 = gn1;
         if (u + 1 < u1) gc_load(u + 1, gn0, gn1);
