@@ -140,13 +140,15 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
 // One CTA per token t: write its permuted row pinv[t].  Padding rows between buckets are never
 // written: the GEMM only ever reads them as B columns whose outputs it discards.
 __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __restrict__ x, int64_t in,
-                                                     int64_t in_pad, const int32_t* __restrict__ pinv,
+                                                     int64_t in_pad, int64_t tpad, const int32_t* __restrict__ pinv,
                                                      __half* __restrict__ xperm, float* __restrict__ escale,
                                                      bool vec) {
     __shared__ float red[4];
     const int64_t src = blockIdx.x;
     const int64_t i = pinv[src];
-    __half* dst = xperm + i * in_pad;
+    // k-block slab layout [in_pad/64][tpad][64]: element k of permuted row i at (k/64*tpad + i)*64 + k%64
+    __half* dst = xperm + i * kKBlock;
+    auto at = [&](int64_t k) { return dst + (k / kKBlock) * tpad * kKBlock + (k % kKBlock); };
     const __nv_bfloat16* row = x + (int64_t)src * in;
     float m = 0.f;
     if (vec) {
@@ -184,11 +186,11 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
                     h[j] = __floats2half2_rn(f.x * sc, f.y * sc);
                 }
             }
-            *reinterpret_cast<uint4*>(dst + k) = o;
+            *reinterpret_cast<uint4*>(at(k)) = o;
         }
     } else {
         for (int64_t k = threadIdx.x; k < in_pad; k += 128)
-            dst[k] = __float2half_rn(k < in ? __bfloat162float(row[k]) * sc : 0.f);
+            *at(k) = __float2half_rn(k < in ? __bfloat162float(row[k]) * sc : 0.f);
     }
 }
 
@@ -216,7 +218,7 @@ int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* 
 
 int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st) {
     const bool vec = (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    gather_kernel<<<(unsigned)T, 128, 0, st>>>(x, L->in, L->in_pad, L->pinv, L->xperm, L->escale, vec);
+    gather_kernel<<<(unsigned)T, 128, 0, st>>>(x, L->in, L->in_pad, L->tpad_max, L->pinv, L->xperm, L->escale, vec);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

@@ -12,7 +12,7 @@ constexpr int SM_ROWS = 64, SM_TOK = 64;
 __global__ void __launch_bounds__(256) gemm_simt_kernel(
     const uint8_t* __restrict__ codes8, const float2* __restrict__ gconst, int64_t out_pad,
     MaskTable mt, int64_t out, int64_t G, int64_t gs,
-    bool single_group, int64_t kblocks, int64_t in_pad, const __half* __restrict__ xperm,
+    bool single_group, int64_t kblocks, int64_t tpad, const __half* __restrict__ xperm,
     const float* __restrict__ escale, const int32_t* __restrict__ perm,
     const TokTile* __restrict__ tiles, const int32_t* __restrict__ meta,
     __nv_bfloat16* __restrict__ y) {
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(
         for (int i = tid; i < SM_TOK * kKBlock; i += 256) {  // activations
             const int tt = i / kKBlock, kk = i % kKBlock;
             const int64_t row = tile.row0 + sub0 + tt;
-            xs[kk][tt] = (sub0 + tt < tile.n) ? __half2float(xperm[row * in_pad + kb * kKBlock + kk]) : 0.f;
+            xs[kk][tt] = (sub0 + tt < tile.n) ? __half2float(xperm[(kb * tpad + row) * kKBlock + kk]) : 0.f;
         }
         __syncthreads();
 #pragma unroll 8
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st) {
     dim3 grid((unsigned)(L->out_pad / SM_ROWS), (unsigned)L->max_tiles, kTokTile / SM_TOK);
     gemm_simt_kernel<<<grid, 256, 0, st>>>(L->codes8, L->gconst, L->out_pad, L->mtab, L->out, L->G, L->gs,
-                                           L->single_group, L->kblocks, L->in_pad, L->xperm, L->escale,
+                                           L->single_group, L->kblocks, L->tpad_max, L->xperm, L->escale,
                                            L->perm, L->tiles, L->meta, y);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;

@@ -43,16 +43,26 @@ constexpr int NSTAGE = MOBI_NSTAGE;  // B stages (smem, 32 KiB each)
 constexpr int NSA = 8;               // A stages (TMEM, 32 columns each)
 constexpr int kSplitMaxT = 64;   // split-K only for decode-size batches
 constexpr int kMaxSplit = 8;
-constexpr int kBoxRows = 32;                      // TMA box: 32 token rows x 64 k (4 KiB)
+#ifndef MOBI_BOXR
+#define MOBI_BOXR 128
+#endif
+constexpr int kBoxRows = MOBI_BOXR;               // TMA box: token rows x 64 k (contiguous in xperm)
 constexpr int kBoxBytes = kBoxRows * kKBlock * 2;
+#ifndef MOBI_MC
+#define MOBI_MC 1  // 1: the CTA pair multicasts the shared token tile; 0: every CTA loads its own copy
+#endif
+#ifndef MOBI_NPROD
+#define MOBI_NPROD 1
+#endif
+constexpr int kNProd = MOBI_NPROD;                 // TMA producer warps (alternating k-blocks)
 constexpr int kDqWarps = 16;                       // 4 per TMEM lane quarter
-constexpr int kThreads = 32 * (2 + kDqWarps + 4);  // dequant, epilogue, TMA, MMA
+constexpr int kThreads = 32 * (1 + kNProd + kDqWarps + 4);  // dequant, epilogue, TMA, MMA
 // Warp roles, ordered by scheduling priority (the SM's warp arbiter favours higher warp ids):
 // the single-thread TMA and MMA issuers get the top ids so ALU-heavy dequant warps never starve them.
 constexpr int kWarpDq0 = 0;                  // 16 dequantizer warps
 constexpr int kWarpEpi0 = kDqWarps;          // 4 epilogue warps
-constexpr int kWarpTma = kDqWarps + 4;       // TMA producer
-constexpr int kWarpMma = kDqWarps + 5;       // TMEM allocator + MMA issuer
+constexpr int kWarpTma = kDqWarps + 4;       // TMA producer(s)
+constexpr int kWarpMma = kDqWarps + 4 + kNProd;  // TMEM allocator + MMA issuer
 constexpr int kStageBytes = kTokTile * kKBlock * 2;  // 32 KiB
 constexpr int kAccCols = 256;
 constexpr int kACol0 = 256;
@@ -65,6 +75,7 @@ struct Params {
     int64_t out_pad;
     MaskTable mt;
     int64_t out, G, gs, kblocks;
+    int64_t tpad;       // rows per k-block slab of xperm
     int single_group;
     int n_row_tiles;
     const float* escale;
@@ -134,7 +145,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1);
-            mbar_init(&empty[s], 2);  // MMA completion of BOTH CTAs of the pair (shared B stages)
+            mbar_init(&empty[s], MOBI_MC ? 2 : 1);  // MMA completion of BOTH CTAs of the pair (shared B stages)
         }
         for (int s = 0; s < NSA; ++s) {
             mbar_init(&full_a[s], kDqWarps / 2);
@@ -181,8 +192,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         kb1 = min(kb_n, kb0 + kb_per);
     };
 
-    if (warp == kWarpTma) {
-        // ---------------- TMA producer ----------------
+    if (warp >= kWarpTma && warp < kWarpTma + kNProd) {
+        // ---------------- TMA producer(s): producer w owns the k-block iterations it % kNProd == w ----------------
+        const uint32_t pw = (uint32_t)(warp - kWarpTma);
         uint32_t it = 0;
         for (int pair = cid; pair < total; pair += ncl) {
             TokTile tt;
@@ -191,15 +203,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (TRACE && lane == 0) ++tr[3];
             const int nbox = (tt.n + kBoxRows - 1) / kBoxRows;
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                if (kNProd > 1 && it % kNProd != pw) continue;
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 TW(0, mbar_wait(&empty[s], ph ^ 1));
                 EV(0, kb, (uint32_t)(pair != cid));
                 if (elect_one_sync()) {
                     mbar_arrive_expect_tx(&full_b[s], nbox * kBoxBytes);
-                    for (int j = (int)rank; j < nbox; j += 2)
-                        tma_load_2d_mc(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, &full_b[s], kb * kKBlock,
-                                       tt.row0 + j * kBoxRows, (uint16_t)0x3);
+                    if (MOBI_MC) {
+                        for (int j = (int)rank; j < nbox; j += 2)
+                            tma_load_2d_mc(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, &full_b[s], 0,
+                                           (int)(kb * p.tpad) + tt.row0 + j * kBoxRows, (uint16_t)0x3);
+                    } else {
+                        for (int j = 0; j < nbox; ++j)
+                            tma_load_2d(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, &full_b[s], 0,
+                                        (int)(kb * p.tpad) + tt.row0 + j * kBoxRows);
+                    }
                 }
                 __syncwarp();
             }
@@ -241,7 +260,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         case 224: issue_kblock_ts<224>(acol, bdesc, first); break;
                         default: issue_kblock_ts<256>(acol, bdesc, first); break;
                     }
-                    mma_commit_mc(&empty[s], (uint16_t)0x3);  // frees the shared B stage in both CTAs
+                    if (MOBI_MC)
+                        mma_commit_mc(&empty[s], (uint16_t)0x3);  // frees the shared B stage in both CTAs
+                    else
+                        mma_commit(&empty[s]);
                     mma_commit(&empty_a[sa]);                 // frees the local A stage
                     if (kb == kb1 - 1) mma_commit(acc_full);
                 }
@@ -518,7 +540,8 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     }
     if (!L->tmap_x) {
         L->tmap_x = new CUtensorMap;
-        int rc = make_tmap_2d(L->tmap_x, L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad, kBoxRows);
+        int rc = make_tmap_2d(L->tmap_x, L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->kblocks * L->tpad_max, kKBlock,
+                              kBoxRows);
         if (rc) {
             delete L->tmap_x;
             L->tmap_x = nullptr;
@@ -534,6 +557,7 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     p.G = L->G;
     p.gs = L->gs;
     p.kblocks = L->kblocks;
+    p.tpad = L->tpad_max;
     p.single_group = L->single_group;
     p.n_row_tiles = (int)(L->out_pad / kRowTile);
     p.escale = L->escale;

@@ -43,6 +43,7 @@ struct Params {
     int64_t out_pad;
     MaskTable mt;
     int64_t out, G, gs, kblocks;
+    int64_t tpad;
     int single_group;
     int n_row_tiles;
     const float* escale;
@@ -141,12 +142,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (elect_one_sync()) {
                     if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * (big ? kStageBytes : nbox * kBoxBytes));
                     if (big)
-                        tma_load_2d_2sm(stage_b + s * kStageBytes, &tmap_big, full_b_leader + s * 8, kb * kKBlock,
-                                        row_half);
+                        tma_load_2d_2sm(stage_b + s * kStageBytes, &tmap_big, full_b_leader + s * 8, 0,
+                                        (int)(kb * p.tpad) + row_half);
                     else
                         for (int j = 0; j < nbox; ++j)
                             tma_load_2d_2sm(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, full_b_leader + s * 8,
-                                            kb * kKBlock, row_half + j * kBoxRows);
+                                            0, (int)(kb * p.tpad) + row_half + j * kBoxRows);
                 }
                 __syncwarp();
             }
@@ -373,10 +374,9 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     }
     if (!L->tmap_x2) {
         L->tmap_x2 = new CUtensorMap[2];
-        int rc = make_tmap_2d(&L->tmap_x2[0], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad, kBoxRows);
-        if (!rc)
-            rc = make_tmap_2d(&L->tmap_x2[1], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, L->tpad_max, L->in_pad,
-                              kBigBoxRows);
+        const int64_t rows = L->kblocks * L->tpad_max;
+        int rc = make_tmap_2d(&L->tmap_x2[0], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, kKBlock, kBoxRows);
+        if (!rc) rc = make_tmap_2d(&L->tmap_x2[1], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, kKBlock, kBigBoxRows);
         if (rc) {
             delete[] L->tmap_x2;
             L->tmap_x2 = nullptr;
@@ -392,6 +392,7 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     p.G = L->G;
     p.gs = L->gs;
     p.kblocks = L->kblocks;
+    p.tpad = L->tpad_max;
     p.single_group = L->single_group;
     p.n_row_tiles = (int)(L->out_pad / kRowTile);
     p.escale = L->escale;

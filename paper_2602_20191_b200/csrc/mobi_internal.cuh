@@ -103,7 +103,8 @@ struct mobi_layer {
     int32_t* inverse = nullptr;// [T]
     int32_t* cperm = nullptr;  // [T] compact (unpadded) permutation
     float* escale = nullptr;   // [tpad_max] per-row power-of-two scale
-    __half* xperm = nullptr;   // [tpad_max][in_pad] fp16 permuted, scaled activations
+    __half* xperm = nullptr;   // [kblocks][tpad_max][64] fp16 permuted, scaled activations: k-block slabs,
+                               // so a TMA box of consecutive permuted rows is one contiguous span
     mobi::TokTile* tiles = nullptr;  // [max_tiles]
     float* gpart = nullptr;    // [8][64][out] split-K partials (decode-size T)
     float* hpart = nullptr;    // [16][64][h_pad] router split-K partials

@@ -28,7 +28,9 @@ def main():
     set_debug_impl(int(os.environ.get("MOBI_IMPL", "0")))
     dev = torch.device("cuda", 0)
     layer, _ = bench.make_layer(args, dev, 1)
-    for T in (256, 2048, 8192):
+    import os
+    quick = os.environ.get('GB_QUICK')
+    for T in ((2048, 8192) if quick else (256, 2048, 8192)):
         args.tokens = T
         x = bench.make_x(args, dev, 2)
         flops = 2.0 * T * args.inn * args.out
@@ -41,6 +43,8 @@ def main():
                                               p=np.array([1181, 234, 151, 36, 334, 72, 31, 9]) / 2048),
         }
         for name, m in dists.items():
+            if quick and name not in ('all mask 1', 'realistic 3-bit mix'):
+                continue
             masks = torch.from_numpy(m.astype(np.uint8)).to(dev)
             g, ga, bk = run(layer, x, masks)
             print(f"T={T:5d} {name:28s} gemm {g * 1e3:8.1f} us  {flops / (g * 1e-3) / 1e12:7.1f} TFLOP/s   "

@@ -7,8 +7,8 @@
 #include "../paper_2602_20191_b200/csrc/sm100.cuh"
 using namespace mobi::sm100;
 
-template <int NS, int NW, int ST, int WST, int PAR, int N, int TMA = 0>
-__global__ void __launch_bounds__(32 * (2 + NW), 1) pipe(int kblocks, unsigned long long* out,
+template <int NS, int NW, int ST, int WST, int PAR, int N, int TMA = 0, int BOXR = 32, int NPROD = 1, int CONTIG = 0>
+__global__ void __launch_bounds__(32 * (1 + NPROD + NW), 1) pipe(int kblocks, unsigned long long* out,
                                                          const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(1024) uint8_t dsm[];
     uint8_t* bsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
@@ -49,17 +49,21 @@ __global__ void __launch_bounds__(32 * (2 + NW), 1) pipe(int kblocks, unsigned l
         }
         mbar_wait(&done, 0);
         if (lane == 0) out[blockIdx.x] = (unsigned long long)(clock64() - t0);
-    } else if (warp == 1 + NW) {
+    } else if (warp >= 1 + NW) {
         if (TMA) {
-            for (int kb = 0; kb < kblocks; ++kb) {
+            for (int kb = warp - 1 - NW; kb < kblocks; kb += NPROD) {
                 const int s = kb % NS;
                 mbar_wait(&empty[s], ((kb / NS) & 1) ^ 1);
                 if (lane == 0) {
-                    constexpr int nbox = (N + 31) / 32;
-                    mbar_arrive_expect_tx(&fullb[s], nbox * 4096);
+                    constexpr int nbox = (N + BOXR - 1) / BOXR;
+                    mbar_arrive_expect_tx(&fullb[s], nbox * BOXR * 128);
                     for (int j = 0; j < nbox; ++j)
-                        tma_load_2d(bsm + s * 32768 + j * 4096, &tmap, &fullb[s], (kb % 64) * 64,
-                                    ((blockIdx.x * 13 + kb) % 64) * 256 + j * 32);
+                        if (CONTIG)
+                            tma_load_2d(bsm + s * 32768 + j * BOXR * 128, &tmap, &fullb[s], 0,
+                                        ((blockIdx.x * 13 + kb) % 1024) * 256 + j * BOXR);
+                        else
+                        tma_load_2d(bsm + s * 32768 + j * BOXR * 128, &tmap, &fullb[s], (kb % 64) * 64,
+                                    ((blockIdx.x * 13 + kb) % 64) * 256 + j * BOXR);
                 }
                 __syncwarp();
             }
@@ -110,16 +114,25 @@ int main() {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
-    CUtensorMap tm;
+    CUtensorMap tm, tm256, tmc;
     cuuint64_t dims[2] = {4096, (cuuint64_t)rows};
     cuuint64_t strides[1] = {4096 * 2};
     cuuint32_t box[2] = {64, 32};
     cuuint32_t es[2] = {1, 1};
     ((PFN_encodeTiled)f)(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    auto run = [&](auto k, int nthreads, const char* name) {
+    cuuint32_t box256[2] = {64, 256};
+    {
+        cuuint64_t dc[2] = {64, (cuuint64_t)rows * 64};
+        cuuint64_t sc[1] = {128};
+        ((PFN_encodeTiled)f)(&tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, buf, dc, sc, box256, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    ((PFN_encodeTiled)f)(&tm256, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, buf, dims, strides, box256, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    auto run = [&](auto k, int nthreads, const char* name, int big = 0) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * 32768 + 1024);
-        k<<<nsm, nthreads + 32, 6 * 32768 + 1024>>>(kb, d, tm);
+        k<<<nsm, nthreads + 32, 6 * 32768 + 1024>>>(kb, d, big == 2 ? tmc : big ? tm256 : tm);
         cudaError_t e = cudaGetLastError(); if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); exit(1); }
         unsigned long long h[256];
@@ -128,19 +141,9 @@ int main() {
         for (int i = 0; i < nsm; ++i) a += h[i];
         printf("%-44s cycles/k-block %7.1f\n", name, a / nsm / kb);
     };
-    run(pipe<4, 16, 1, 1, 1, 16>, 32 * 17, "NS4 16w parity st+wait N16 (GEMM-like)");
-    run(pipe<4, 16, 1, 0, 1, 16>, 32 * 17, "NS4 16w parity st, no wait::st N16");
-    run(pipe<4, 16, 0, 0, 1, 16>, 32 * 17, "NS4 16w parity no st N16");
-    run(pipe<4, 8, 1, 1, 0, 16>, 32 * 9, "NS4 8w st+wait N16");
-    run(pipe<4, 4, 1, 1, 0, 16>, 32 * 5, "NS4 4w st+wait N16");
-    //run(pipe<8, 16, 1, 1, 1, 16>, 32 * 17, "NS8 16w parity st+wait N16");
-    run(pipe<4, 16, 1, 1, 1, 256>, 32 * 17, "NS4 16w parity st+wait N256");
-    //run(pipe<8, 16, 1, 1, 1, 256>, 32 * 17, "NS8 16w parity st+wait N256");
-    run(pipe<4, 4, 1, 1, 0, 256>, 32 * 5, "NS4 4w st+wait N256");
-    run(pipe<4, 16, 1, 1, 1, 16, 1>, 32 * 17, "TMA NS4 16w parity N16 (1 box)");
-    run(pipe<2, 16, 1, 1, 1, 16, 1>, 32 * 17, "TMA NS2 16w parity N16");
-    run(pipe<6, 16, 1, 1, 1, 16, 1>, 32 * 17, "TMA NS6 16w parity N16");
-    run(pipe<4, 16, 1, 1, 1, 256, 1>, 32 * 17, "TMA NS4 16w parity N256 (8 boxes)");
-    run(pipe<6, 16, 1, 1, 1, 256, 1>, 32 * 17, "TMA NS6 16w parity N256");
+    run(pipe<6, 16, 1, 1, 1, 256, 1, 256, 1>, 32 * 17, "TMA NS6 N256 1 box x256 strided", 1);
+    run(pipe<6, 16, 1, 1, 1, 256, 1, 256, 1, 1>, 32 * 17, "TMA NS6 N256 1 box x256 contiguous", 2);
+    run(pipe<6, 16, 1, 1, 1, 256, 1, 256, 2, 1>, 32 * 18, "TMA NS6 N256 1 box x256 contiguous 2 prod", 2);
+    run(pipe<6, 16, 1, 1, 1, 128, 1, 256, 1, 1>, 32 * 17, "TMA NS6 N128 1 box x256 contiguous", 2);
     return 0;
 }
