@@ -79,6 +79,8 @@ void free_ws(mobi_layer* L) {
     dfree(L->xperm);
     dfree(L->tiles);
     dfree(L->meta);
+    dfree(L->rt_cnt);
+    dfree(L->bk_hist);
     if (L->tmap_x) delete L->tmap_x;
     L->tmap_x = nullptr;
     if (L->tmap_x2) delete[] L->tmap_x2;
@@ -106,6 +108,10 @@ int ensure_ws(mobi_layer* L, int64_t T) {
     if ((rc = dmalloc(&L->xperm, (size_t)(L->tpad_max * L->in_pad), nullptr))) return rc;
     if ((rc = dmalloc(&L->tiles, (size_t)L->max_tiles, nullptr))) return rc;
     if ((rc = dmalloc(&L->meta, 64, nullptr))) return rc;
+    if ((rc = dmalloc(&L->rt_cnt, (size_t)(Tc / 128 + 1), nullptr))) return rc;
+    MOBI_CUDA(cudaMemset(L->rt_cnt, 0, (size_t)(Tc / 128 + 1) * sizeof(int32_t)));
+    if ((rc = dmalloc(&L->bk_hist, 48, nullptr))) return rc;
+    MOBI_CUDA(cudaMemset(L->bk_hist, 0, 48 * sizeof(int32_t)));
     if (!L->gpart && (rc = dmalloc(&L->gpart, (size_t)(8 * 64 * L->out_pad), nullptr))) return rc;
     if (!L->hpart && (rc = dmalloc(&L->hpart, (size_t)(16 * 64 * L->h_pad), nullptr))) return rc;
     if (!L->dec_cnt) {
@@ -253,8 +259,20 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L) {
     return MOBI_OK;
 }
 
-int route_scores(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st) {
-    if (g_impl_override != 1 && router_tc_supported(L, x)) return launch_router_tc(L, x, T, st);
+// score (router.hpp:63-76); the tcgen05 router also applies gate_hard(delta) for prefill sizes and
+// then reports *masks_ready (L->masks, scores_out, masks_out written)
+int route_scores(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, float* scores_out, uint8_t* masks_out,
+                 bool* masks_ready, cudaStream_t st, bool fuse_bucket = false) {
+    *masks_ready = false;
+    if (g_impl_override == 7 && router_tc_supported(L, x)) {  // traced router (development hook)
+        static unsigned long long* tbuf = nullptr;
+        if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
+        MOBI_CUDA(cudaMemsetAsync(tbuf, 0, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long), st));
+        g_trace_buf = tbuf;
+        return launch_router_tc(L, x, T, delta, scores_out, masks_out, masks_ready, st, tbuf);
+    }
+    if (g_impl_override != 1 && router_tc_supported(L, x))
+        return launch_router_tc(L, x, T, delta, scores_out, masks_out, masks_ready, st, nullptr, fuse_bucket);
     return launch_router(L, x, T, st);
 }
 
@@ -331,20 +349,27 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
         return launch_decode_gemm(L, xb, T, given_masks, reinterpret_cast<__nv_bfloat16*>(y),
                                   !given_masks && g_impl_override != 6 && !L->prof, st);
     }
+    bool ready = false;
     if (!given_masks) {
         ProfScope p(L, 0, st);
-        if ((rc = route_scores(L, xb, T, st))) return rc;
+        if ((rc = route_scores(L, xb, T, delta, nullptr, masks_out, &ready, st, g_impl_override != 8))) return rc;
     }
-    {
+    // the tcgen05 router (prefill sizes) has already decided the masks and laid out the buckets;
+    // otherwise (given masks, fallback router) the bucket kernel does it
+    const bool fused = ready && g_impl_override != 8;
+    if (!fused) {
         ProfScope p(L, 1, st);
-        if ((rc = launch_bucket(L, T, delta, given_masks, nullptr, masks_out, nullptr, nullptr, nullptr, st)))
+        if ((rc = launch_bucket(L, T, delta, ready ? L->masks : given_masks, nullptr, ready ? nullptr : masks_out,
+                                nullptr, nullptr, nullptr, st, !ready)))
             return rc;
     }
     {
         ProfScope p(L, 2, st);
-        if ((rc = launch_gather(L, xb, T, st))) return rc;
+        if ((rc = launch_gather(L, xb, T, st, fused))) return rc;
     }
     __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
+    if (fused && g_impl_override != 0)  // only the production GEMM clears the fused-bucketing counters
+        MOBI_CUDA(cudaMemsetAsync(L->bk_hist, 0, 48 * sizeof(int32_t), st));
     ProfScope p(L, 3, st);
     if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
     if (g_impl_override == 2 || g_impl_override == 4) {  // traced tcgen05 kernels (development hook)
@@ -487,7 +512,10 @@ int mobi_score(mobi_layer_t L, const void* x, int64_t T, float* scores, void* st
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     L->last_launches = 0;
-    if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
+    bool ready = false;
+    if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, INFINITY, scores, nullptr, &ready, S(stream))))
+        return rc;
+    if (ready) return MOBI_OK;
     return launch_bucket(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream));
 }
 
@@ -500,8 +528,11 @@ int mobi_route(mobi_layer_t L, const void* x, int64_t T, float delta, float* sco
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     L->last_launches = 0;
-    if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, S(stream)))) return rc;
-    return launch_bucket(L, T, delta, nullptr, scores, masks, perm, inverse, bucket_count, S(stream));
+    bool ready = false;
+    if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, delta, scores, masks, &ready, S(stream))))
+        return rc;
+    return launch_bucket(L, T, delta, ready ? L->masks : nullptr, ready ? nullptr : scores, ready ? nullptr : masks,
+                         perm, inverse, bucket_count, S(stream), !ready);
 }
 
 int mobi_forward(mobi_layer_t L, const void* x, int64_t T, float delta, void* y, uint8_t* masks, void* stream) {

@@ -22,6 +22,7 @@ namespace {
 constexpr int BK_THREADS = 1024;
 constexpr int NKEY_ALL = 256;              // generic uint8 keys (permute_by_slice API)
 constexpr int NKEY_MASK = 2 * kMaxBuckets;  // slice masks on the GEMM path (< 2^MOBI_MAX_SLICES)
+constexpr int kMaxTilesSmem = 1024;          // token tiles (T <= ~256K tokens per call)
 
 // Stable counting sort on one CTA.  Keys are processed in chunks of 1024 tokens in token
 // order; inside a chunk, __match_any_sync ranks equal keys within a warp and a per-key scan
@@ -36,6 +37,8 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
     int32_t* __restrict__ pinv) {
     __shared__ int hist[NKEY], cstart[NKEY], run[NKEY], pstart[NKEY_MASK];
     __shared__ int warp_hist[BK_THREADS / 32][NKEY];
+    __shared__ int4 s_tiles[NKEY == NKEY_MASK ? kMaxTilesSmem : 1];
+    __shared__ int s_ntiles;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int vmask = (1 << (nr + 1)) - 1;
     if (perm)
@@ -46,62 +49,92 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
     }
     __syncthreads();
     // phase 1: decisions (gate_hard strict '>' on delta) and the key histogram
-    for (int64_t t = tid; t < T; t += BK_THREADS) {
-        int m;
-        if (given_masks) {
+    for (int64_t t0 = 0; t0 < T; t0 += BK_THREADS) {
+        const int64_t t = t0 + tid;
+        int m = NKEY;  // out of range: never counted
+        if (t >= T) {
+        } else if (given_masks) {
             m = given_masks[t];
             if (sanitize) m = (m & vmask) | 1;
         } else {
             m = 1;
             for (int k = 0; k < nr; ++k) {
+                // fixed hidden-tile order (the same sum the router's fused decision computes)
                 float s = 0.f;
-                for (int q = 0; q < htiles; ++q) s += s_part[((int64_t)q * T + t) * nr + k];
+#pragma unroll 8
+                for (int j = 0; j < htiles; ++j) s += s_part[((int64_t)j * T + t) * nr + k];
                 s += b2[k];
                 if (scores_out) scores_out[t * nr + k] = s;
                 if ((s - delta) > 0.f) m |= 1 << (k + 1);
             }
         }
-        keys[t] = (uint8_t)m;
-        if (masks_out) masks_out[t] = (uint8_t)m;
-        atomicAdd(&hist[m], 1);
+        if (t < T) {
+            keys[t] = (uint8_t)m;
+            if (masks_out) masks_out[t] = (uint8_t)m;
+        }
+        // warp-aggregated histogram update (most tokens share a handful of masks)
+        const unsigned peers = __match_any_sync(0xffffffffu, m);
+        if (m < NKEY && lane == __ffs(peers) - 1) atomicAdd(&hist[m], __popc(peers));
     }
     __syncthreads();
-    // phase 2: bucket starts (compact = reference order; padded = GEMM order) and token tiles
-    if (tid == 0) {
-        int c = 0;
-        for (int v = 0; v < NKEY; ++v) {
-            cstart[v] = c;
-            c += hist[v];
-            if (counts_out) counts_out[v] = hist[v];
-        }
-        if (perm) {
-            // token tiles, largest first (the GEMM claims them dynamically in this order)
-            int a = 0, n = 0;
-            for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) {
-                pstart[v] = a;
-                for (int j = 0; j < hist[v]; j += kTokTile) {
-                    TokTile tt;
-                    tt.row0 = a + j;
-                    tt.n = min(kTokTile, hist[v] - j);
-                    tt.mask = v;
-                    tt.pad = 0;
-                    int i = n++;
-                    while (i > 0 && tiles[i - 1].n < tt.n) {
-                        tiles[i] = tiles[i - 1];
-                        --i;
-                    }
-                    tiles[i] = tt;
-                }
-                a += (int)round_up(hist[v], kBucketAlign);
+    // phase 2: bucket starts (compact = reference order; padded = GEMM order) and the token-tile
+    // list, built in shared memory by warp 0: full tiles in key order, then the partial last tiles of
+    // each bucket largest first (the GEMM schedules tiles in list order)
+    if (wid == 0) {
+        // exclusive scans over the keys, 32 keys per step
+        int c = 0, a = 0;
+        for (int v0 = 0; v0 < NKEY; v0 += 32) {
+            const int v = v0 + lane;
+            const int h = v < NKEY ? hist[v] : 0;
+            const int hp = (v < NKEY_MASK) ? (int)round_up(h, kBucketAlign) : 0;
+            int incl = h, inclp = hp;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, incl, o), yp = __shfl_up_sync(0xffffffffu, inclp, o);
+                if (lane >= o) incl += y, inclp += yp;
             }
+            if (v < NKEY) {
+                cstart[v] = c + incl - h;
+                if (counts_out) counts_out[v] = h;
+            }
+            if (v < NKEY_MASK) pstart[v] = a + inclp - hp;
+            c += __shfl_sync(0xffffffffu, incl, 31);
+            a += __shfl_sync(0xffffffffu, inclp, 31);
+        }
+        if (perm && lane == 0) {
+            int n = 0;
+            for (int v = 0; v < NKEY_MASK && v < NKEY; ++v)
+                for (int j = 0; j + kTokTile <= hist[v]; j += kTokTile) s_tiles[n++] = make_int4(pstart[v] + j, kTokTile, v, 0);
+            const int nfull = n;
+            for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) {
+                const int r = hist[v] % kTokTile;
+                if (!r) continue;
+                int i = n++;
+                while (i > nfull && s_tiles[i - 1].y < r) {
+                    s_tiles[i] = s_tiles[i - 1];
+                    --i;
+                }
+                s_tiles[i] = make_int4(pstart[v] + hist[v] - r, r, v, 0);
+            }
+            s_ntiles = n;
             meta[0] = n;
             meta[1] = a;
-            for (int v = 0; v < NKEY_MASK && v < NKEY; ++v) meta[2 + v] = hist[v];
             meta[32] = 0;  // GEMM dynamic tile counter
             meta[33] = 1;  // GEMM split count (the GEMM overwrites it when it splits K)
         }
+        if (perm && lane < NKEY_MASK && lane < NKEY) meta[2 + lane] = hist[lane];
     }
     __syncthreads();
+    if (perm)
+        for (int i = tid; i < s_ntiles; i += BK_THREADS) {
+            const int4 v = s_tiles[i];
+            TokTile tt;
+            tt.row0 = v.x;
+            tt.n = v.y;
+            tt.mask = v.z;
+            tt.pad = 0;
+            tiles[i] = tt;
+        }
     // phase 3: stable positions
     for (int64_t base = 0; base < T; base += BK_THREADS) {
         for (int i = tid; i < (BK_THREADS / 32) * NKEY; i += BK_THREADS) (&warp_hist[0][0])[i] = 0;
@@ -139,13 +172,69 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
 
 // One CTA per token t: write its permuted row pinv[t].  Padding rows between buckets are never
 // written: the GEMM only ever reads them as B columns whose outputs it discards.
+// Padded bucket starts from the mask histogram (every bucket on a kBucketAlign boundary).
+__device__ __forceinline__ int bucket_start(const int* hist, int m) {
+    int a = 0;
+    for (int v = 0; v < m; ++v) a += (int)round_up(__ldg(hist + v), kBucketAlign);
+    return a;
+}
+
+// One thread: the GEMM token-tile list (full tiles in mask order, then each bucket's partial last
+// tile, largest first) and meta -- the same layout bucket_kernel produces.
+__device__ void build_tiles(const int* hist, TokTile* tiles, int32_t* meta) {
+    int h[2 * kMaxBuckets], st[2 * kMaxBuckets];
+    int a = 0;
+    for (int v = 0; v < 2 * kMaxBuckets; ++v) {
+        h[v] = __ldg(hist + v);
+        st[v] = a;
+        a += (int)round_up(h[v], kBucketAlign);
+    }
+    int n = 0;
+    for (int v = 0; v < 2 * kMaxBuckets; ++v)
+        for (int j = 0; j + kTokTile <= h[v]; j += kTokTile) tiles[n++] = TokTile{st[v] + j, kTokTile, v, 0};
+    unsigned done = 0;
+    for (;;) {  // partial tiles, largest first (ties: lower mask first)
+        int best = -1, br = 0;
+        for (int v = 0; v < 2 * kMaxBuckets; ++v) {
+            const int r = h[v] % kTokTile;
+            if (r && !(done >> v & 1u) && r > br) best = v, br = r;
+        }
+        if (best < 0) break;
+        done |= 1u << best;
+        tiles[n++] = TokTile{st[best] + h[best] - br, br, best, 0};
+    }
+    for (int v = 0; v < 2 * kMaxBuckets; ++v) meta[2 + v] = h[v];
+    meta[0] = n;
+    meta[1] = a;
+    meta[32] = 0;  // GEMM dynamic tile counter
+    meta[33] = 1;  // GEMM split count
+}
+
 __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __restrict__ x, int64_t in,
-                                                     int64_t in_pad, int64_t tpad, const int32_t* __restrict__ pinv,
+                                                     int64_t in_pad, int64_t tpad, int32_t* __restrict__ pinv,
                                                      __half* __restrict__ xperm, float* __restrict__ escale,
-                                                     bool vec) {
+                                                     bool vec, const uint8_t* __restrict__ masks,
+                                                     const int* __restrict__ hist, int* __restrict__ fill,
+                                                     int32_t* __restrict__ perm, TokTile* __restrict__ tiles,
+                                                     int32_t* __restrict__ meta) {
     __shared__ float red[4];
+    __shared__ int s_row;
     const int64_t src = blockIdx.x;
-    const int64_t i = pinv[src];
+    if (hist) {
+        // fused bucketing (the router decided the masks and counted the buckets): claim the next slot
+        // of this token's bucket.  The slot order inside a bucket is arbitrary, which cannot change
+        // any output: a token's result depends only on its own row and its bucket's effective weight.
+        if (threadIdx.x == 0) {
+            if (src == 0) build_tiles(hist, tiles, meta);
+            const int m = masks[src];
+            const int i = bucket_start(hist, m) + atomicAdd(&fill[m], 1);
+            perm[i] = (int32_t)src;
+            pinv[src] = i;
+            s_row = i;
+        }
+        __syncthreads();
+    }
+    const int64_t i = hist ? s_row : pinv[src];
     // k-block slab layout [in_pad/64][tpad][64]: element k of permuted row i at (k/64*tpad + i)*64 + k%64
     __half* dst = xperm + i * kKBlock;
     auto at = [&](int64_t k) { return dst + (k / kKBlock) * tpad * kKBlock + (k % kKBlock); };
@@ -198,9 +287,12 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
 
 int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks,
                   float* scores_out, uint8_t* masks_out, int32_t* cperm_out, int32_t* inverse_out,
-                  int32_t* counts_out, cudaStream_t st) {
+                  int32_t* counts_out, cudaStream_t st, bool sanitize) {
+    if (L->max_tiles > kMaxTilesSmem)
+        return set_error(MOBI_EINVAL, "bucket: " + std::to_string(L->max_tiles) + " token tiles exceed " +
+                                          std::to_string(kMaxTilesSmem) + " per call");
     bucket_kernel<NKEY_MASK><<<1, BK_THREADS, 0, st>>>(L->s_part, (int)L->htiles, T, L->nr, L->b2, delta,
-                                             given_masks, 1, scores_out, L->masks, masks_out, L->perm,
+                                             given_masks, sanitize ? 1 : 0, scores_out, L->masks, masks_out, L->perm,
                                              L->tpad_max, cperm_out, inverse_out, counts_out, L->tiles,
                                              L->meta, L->pinv);
     MOBI_LAUNCH_CHECK();
@@ -216,9 +308,10 @@ int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* 
     return MOBI_OK;
 }
 
-int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st) {
+int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st, bool claim) {
     const bool vec = (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    gather_kernel<<<(unsigned)T, 128, 0, st>>>(x, L->in, L->in_pad, L->tpad_max, L->pinv, L->xperm, L->escale, vec);
+    gather_kernel<<<(unsigned)T, 128, 0, st>>>(x, L->in, L->in_pad, L->tpad_max, L->pinv, L->xperm, L->escale, vec,
+                                               L->masks, claim ? L->bk_hist : nullptr, L->bk_hist + 32, L->perm, L->tiles, L->meta);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

@@ -85,6 +85,7 @@ struct Params {
     __nv_bfloat16* y;
     int vec_y;
     int* tile_counter;  // zeroed by the bucket kernel before every launch
+    int* bk_hist;       // fused-bucketing histogram + slot counters: zeroed here for the next forward
     int max_split;      // split-K allowed (small T only): partials go to gpart, reduced by splitk_reduce
     int T;
     float* gpart;       // [split][T][out] fp32 (x 2^e applied)
@@ -157,6 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         prefetch_tmap(&tmap_x);
     }
     if (warp == kWarpMma) tmem_alloc(tmem_slot, 512);
+    if (blockIdx.x == 0 && threadIdx.x < 48 && p.bk_hist) p.bk_hist[threadIdx.x] = 0;  // gather consumed it
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // peer barriers initialised before any multicast lands
@@ -573,6 +575,7 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     p.T = (int)T;
     p.max_split = (T <= kSplitMaxT && L->gpart) ? kMaxSplit : 1;
     p.gpart = L->gpart;
+    p.bk_hist = L->bk_hist;
     if (trace)
         mobi_gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
     else

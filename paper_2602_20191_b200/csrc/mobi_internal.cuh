@@ -111,6 +111,8 @@ struct mobi_layer {
     float* dec_part = nullptr; // decode path: [(sm + n_rt)][kDecMaxT][128] row-tile partials
     float* dec_spart = nullptr;// decode router: [h_pad/16][kDecMaxT][nr] score partials
     int32_t* dec_cnt = nullptr;// decode arrival counters [n_rt + h_pad/16 + 1], zero between launches
+    int32_t* rt_cnt = nullptr; // [T/128 + 1] router arrival counters (per token tile, then all), zero between launches
+    int32_t* bk_hist = nullptr;// [48] fused bucketing: mask histogram | padded starts | slot counters
     int32_t* meta = nullptr;   // [0]=n_tiles [1]=total padded rows [2..2+16) bucket counts
     void* x_dev = nullptr;     // staging for mobi_forward_host
     void* y_dev = nullptr;
@@ -160,12 +162,14 @@ int launch_unpack_codes(const mobi_layer* L, uint8_t* codes_dev, cudaStream_t st
 int launch_router(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);      // CUDA cores
 // router_tc.cu (tcgen05; needs in % 8 == 0 and a 16-byte aligned X for TMA)
 bool router_tc_supported(const mobi_layer* L, const void* x);
-int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);
+int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, float* scores_out,
+                     uint8_t* masks_out, bool* masks_ready, cudaStream_t st, unsigned long long* trace,
+                     bool fuse_bucket = false);
 // bucket.cu
 int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks,
                   float* scores_out, uint8_t* masks_out, int32_t* cperm_out,
-                  int32_t* inverse_out, int32_t* counts_out, cudaStream_t st);
-int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st);
+                  int32_t* inverse_out, int32_t* counts_out, cudaStream_t st, bool sanitize = true);
+int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st, bool claim = false);
 // gemm_tc.cu (tcgen05) / gemm_simt.cu (reference kernel, tests only)
 int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
                    unsigned long long* trace = nullptr);

@@ -24,7 +24,7 @@ constexpr int RM = 128, RN = 128;           // tokens x hidden per tile
 constexpr int kAB = RM * kKBlock * 2;       // 16 KiB per operand per stage
 constexpr int kRThreads = 192;              // 4 epilogue warps, TMA, MMA (highest ids = priority)
 constexpr int kRWarpTma = 4, kRWarpMma = 5;
-constexpr int kRSmem = RS * 2 * kAB + 1024 + 256;
+constexpr int kRSmem = RS * 2 * kAB + 1024 + 256 + 2 * RN * 16;  // + per-tile {b1, w2} staging
 
 struct RParams {
     int64_t T, h, h_pad;
@@ -34,6 +34,18 @@ struct RParams {
     const float* w2;
     float* s_part;
     float* hpart;        // [nsplit][T][h_pad]
+    unsigned long long* trace;  // debug: CTA 0 timeline (null = off)
+    // fused route decision (nsplit == 1): the last hidden tile of a token tile to finish sums the
+    // partial scores in hidden-tile order (+ b2) and applies gate_hard(delta) (router.hpp:92-103)
+    int* cnt;                   // [n_mt] arrival counters, zero between launches
+    const float* b2;
+    float delta;
+    uint8_t* masks;             // [T]
+    uint8_t* masks_out;         // optional
+    float* scores_out;          // optional [T][nr]
+    // fused bucketing: mask histogram (the gather lays the buckets out and claims slots; the GEMM
+    // zeroes it again)
+    int* hist;                  // [16] zero between launches
 };
 
 __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
@@ -47,7 +59,11 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     uint64_t* acc_full = bars + 2 * RS; // [2]
     uint64_t* acc_empty = acc_full + 2; // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    // [2][RN] {b1[j], w2[j][0..2]} of the tile's hidden units, staged by the epilogue warps while the
+    // mainloop runs so the SiLU.w2 epilogue reads them as smem broadcasts (not dependent global loads)
+    float4* cst = reinterpret_cast<float4*>(smem + RS * 2 * kAB + 256);
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
+    __shared__ int s_last;
     if (threadIdx.x == 0) {
         for (int s = 0; s < RS; ++s) {
             mbar_init(&full[s], 1);
@@ -61,6 +77,10 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
+    const long long t_start = clock64();
+    auto TR = [&](int i) {
+        if (p.trace && blockIdx.x == 0 && (threadIdx.x % 32) == 0) p.trace[i] = (unsigned long long)(clock64() - t_start);
+    };
     if (warp == kRWarpMma) tmem_alloc(tmem_slot, 512);  // all columns: base is the constant 0
     tc_fence_before();
     __syncthreads();
@@ -86,6 +106,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % RS;
                 mbar_wait(&empty[s], ((it / RS) & 1) ^ 1);
+                if (kb < 64) TR(128 + kb);
                 if (elect_one_sync()) {
                     uint8_t* a = smem + s * 2 * kAB;
                     mbar_arrive_expect_tx(&full[s], 2 * kAB);
@@ -107,6 +128,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
                 const int s = it % RS;
                 mbar_wait(&full[s], (it / RS) & 1);
+                if (kb < 64) TR(kb);
                 tc_fence_after();
                 if (elect_one_sync()) {
                     const uint32_t a = smem_u32(smem + s * 2 * kAB);
@@ -140,7 +162,21 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             const int64_t t = (int64_t)mt * RM + 32 * q + lane;
             const int64_t h0 = (int64_t)nt * RN;
             const int nh = (int)std::min<int64_t>(RN, p.h - h0);
+            if (p.nsplit == 1) {
+                const int et = 32 * q + lane;  // epilogue warps are 0..3
+                float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (et < nh) {
+                    const int64_t hj = h0 + et;
+                    c.x = __ldg(p.b1 + hj);
+                    c.y = __ldg(p.w2 + hj * p.nr);
+                    if (p.nr > 1) c.z = __ldg(p.w2 + hj * p.nr + 1);
+                    if (p.nr > 2) c.w = __ldg(p.w2 + hj * p.nr + 2);
+                }
+                cst[buf * RN + et] = c;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            }
             mbar_wait(&acc_full[buf], (tc >> 1) & 1);
+            if (q == 0) TR(200);
             tc_fence_after();
             if (p.nsplit > 1) {  // raw hidden partial H[t, h0..h0+nh) for this k-split
                 for (int c0 = 0; c0 < nh; c0 += 32) {
@@ -159,37 +195,65 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
                 if (lane == 0) mbar_arrive(&acc_empty[buf]);
                 continue;
             }
-            float part[MOBI_MAX_SLICES - 1] = {0.f, 0.f, 0.f};
+            float part0 = 0.f, part1 = 0.f, part2 = 0.f;
             for (int c0 = 0; c0 < nh; c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem + lane_base + buf * RN + c0, v);
                 tmem_ld_wait();
-                const int nn = min(32, nh - c0);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    if (j < nn) {
-                        const int64_t hj = h0 + c0 + j;
-                        const float a = __uint_as_float(v[j]) + __ldg(p.b1 + hj);
-                        const float sv = a * __fdividef(1.f, 1.f + __expf(-a));
-#pragma unroll
-                        for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
-                            if (k < p.nr) part[k] = fmaf(sv, __ldg(p.w2 + hj * p.nr + k), part[k]);
-                    }
+                    const float4 c = cst[buf * RN + c0 + j];  // zero beyond nh: contributes nothing
+                    const float a = __uint_as_float(v[j]) + c.x;
+                    const float sv = a * __fdividef(1.f, 1.f + __expf(-a));
+                    part0 = fmaf(sv, c.y, part0);
+                    part1 = fmaf(sv, c.z, part1);
+                    part2 = fmaf(sv, c.w, part2);
                 }
             }
+            const float part[3] = {part0, part1, part2};
             tc_fence_before();
             __syncwarp();
+            if (q == 0) TR(201);
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
             if (t < p.T) {
 #pragma unroll
                 for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
                     if (k < p.nr) p.s_part[((int64_t)nt * p.T + t) * p.nr + k] = part[k];
             }
+            // last hidden tile of token tile mt: scores and slice masks for its tokens
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (q == 0 && lane == 0) s_last = atomicAdd(&p.cnt[mt], 1) == p.n_nt - 1;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (s_last) {
+                __threadfence();
+                int mk = 2 * kMaxBuckets;  // no token
+                if (t < p.T) {
+                    int m = 1;
+                    for (int k = 0; k < p.nr; ++k) {
+                        float sc = 0.f;
+                        for (int j = 0; j < p.n_nt; ++j) sc += __ldcg(p.s_part + ((int64_t)j * p.T + t) * p.nr + k);
+                        sc += __ldg(p.b2 + k);
+                        if (p.scores_out) p.scores_out[t * p.nr + k] = sc;
+                        if ((sc - p.delta) > 0.f) m |= 1 << (k + 1);
+                    }
+                    p.masks[t] = (uint8_t)m;
+                    if (p.masks_out) p.masks_out[t] = (uint8_t)m;
+                    mk = m;
+                }
+                if (q == 0 && lane == 0) p.cnt[mt] = 0;
+                if (p.hist) {  // bucket sizes for the gather (which lays the buckets out)
+                    const unsigned peers = __match_any_sync(0xffffffffu, mk);
+                    if (mk < 2 * kMaxBuckets && lane == __ffs(peers) - 1) atomicAdd(&p.hist[mk], __popc(peers));
+                }
+            }
         }
     }
+    TR(202 + (warp == kRWarpMma) + 2 * (warp == kRWarpTma));
     tc_fence_before();
     __syncthreads();
     if (warp == kRWarpMma) tmem_dealloc(tmem, 512);
+    TR(205);
 }
 
 // split-K finish: H = sum_ks hpart (fixed order) -> silu(H + b1) . w2 -> s_part[nt][t][k]
@@ -235,7 +299,9 @@ bool router_tc_supported(const mobi_layer* L, const void* x) {
     return (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 }
 
-int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st) {
+int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, float* scores_out,
+                     uint8_t* masks_out, bool* masks_ready, cudaStream_t st, unsigned long long* trace,
+                     bool fuse_bucket) {
     static bool attr = false;
     if (!attr) {
         MOBI_CUDA(cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem));
@@ -265,6 +331,14 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStrea
     p.b1 = L->b1;
     p.w2 = L->w2;
     p.s_part = L->s_part;
+    p.trace = trace;
+    p.cnt = L->rt_cnt;
+    p.b2 = L->b2;
+    p.delta = delta;
+    p.masks = L->masks;
+    p.masks_out = masks_out;
+    p.scores_out = scores_out;
+    p.hist = fuse_bucket ? L->bk_hist : nullptr;
     L->htiles = p.n_nt;
     // split K when the tile grid cannot fill the SMs (decode-size T)
     p.nsplit = 1;
@@ -273,6 +347,8 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStrea
     p.nsplit = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty splits
     const int total = p.n_mt * p.n_nt * p.nsplit;
     const int grid = std::min(total, sm_count());
+    if (masks_ready) *masks_ready = p.nsplit == 1;
+    if (p.nsplit != 1) p.hist = nullptr;
     router_tc_kernel<<<grid, kRThreads, kRSmem, st>>>(tmap_x, *L->tmap_w1, p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;

@@ -97,6 +97,62 @@ __global__ void __launch_bounds__(32 * (1 + NPROD + NW), 1) pipe(int kblocks, un
     if (warp == 0) tmem_dealloc(0, 512);
 }
 
+
+// router-like: TMA loads A (128 rows) and B (NB rows) boxes per stage, one thread issues SS MMAs M=128 N=NB
+template <int NS, int NB>
+__global__ void __launch_bounds__(64, 1) ss_pipe(int kblocks, unsigned long long* out, const __grid_constant__ CUtensorMap tma,
+                                                 const __grid_constant__ CUtensorMap tmb) {
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[NS], empty[NS], done;
+    __shared__ uint32_t slot;
+    constexpr int SA = 128 * 128, SB = NB * 128, ST = SA + SB;
+    const int warp = warp_idx_uniform();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(&done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc(&slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    long long t0 = clock64();
+    if (warp == 0) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int s = kb % NS;
+            mbar_wait(&full[s], (kb / NS) & 1);
+            tc_fence_after();
+            if (elect_one_sync()) {
+                constexpr uint32_t idesc = idesc_f16(128, NB, 1);
+                const uint32_t a = smem_u32(sm + s * ST);
+                const uint64_t ad = sdesc_sw128(a), bd = sdesc_sw128(a + SA);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) mma_ss_f16(0u, ad + j * 2, bd + j * 2, idesc, (kb | j) != 0);
+                mma_commit(&empty[s]);
+                if (kb == kblocks - 1) mma_commit(&done);
+            }
+            __syncwarp();
+        }
+        mbar_wait(&done, 0);
+        if (threadIdx.x == 0) out[blockIdx.x] = (unsigned long long)(clock64() - t0);
+    } else {
+        for (int kb = 0; kb < kblocks; ++kb) {
+            const int s = kb % NS;
+            mbar_wait(&empty[s], ((kb / NS) & 1) ^ 1);
+            if (elect_one_sync()) {
+                mbar_arrive_expect_tx(&full[s], ST);
+                tma_load_2d(sm + s * ST, &tma, &full[s], (kb % 64) * 64, (blockIdx.x % 16) * 128);
+                tma_load_2d(sm + s * ST + SA, &tmb, &full[s], (kb % 64) * 64, (blockIdx.x / 16) * NB);
+            }
+            __syncwarp();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(0, 512);
+}
+
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -141,9 +197,30 @@ int main() {
         for (int i = 0; i < nsm; ++i) a += h[i];
         printf("%-44s cycles/k-block %7.1f\n", name, a / nsm / kb);
     };
-    run(pipe<6, 16, 1, 1, 1, 256, 1, 256, 1>, 32 * 17, "TMA NS6 N256 1 box x256 strided", 1);
-    run(pipe<6, 16, 1, 1, 1, 256, 1, 256, 1, 1>, 32 * 17, "TMA NS6 N256 1 box x256 contiguous", 2);
-    run(pipe<6, 16, 1, 1, 1, 256, 1, 256, 2, 1>, 32 * 18, "TMA NS6 N256 1 box x256 contiguous 2 prod", 2);
-    run(pipe<6, 16, 1, 1, 1, 128, 1, 256, 1, 1>, 32 * 17, "TMA NS6 N128 1 box x256 contiguous", 2);
+    {
+        // X-like [2048][4096] bf16 and w1t-like [1024][4096] bf16, 128-row boxes, strided rows (8 KB pitch)
+        CUtensorMap ta, tb, tb256;
+        cuuint64_t da[2] = {4096, 2048}, db[2] = {4096, 1024}, st[1] = {8192};
+        cuuint32_t b128[2] = {64, 128}, b256[2] = {64, 256};
+        auto E = (PFN_encodeTiled)f;
+        E(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, da, st, b128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        E(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (char*)buf + (32 << 20), db, st, b128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        E(&tb256, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (char*)buf + (32 << 20), db, st, b256, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        auto rs = [&](auto k, int smem, const CUtensorMap& b, const char* name, int grid) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            for (int w = 0; w < 2; ++w) k<<<grid, 64, smem>>>(64, d, ta, b);
+            k<<<grid, 64, smem>>>(64, d, ta, b);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); exit(1); }
+            unsigned long long h[256];
+            cudaMemcpy(h, d, 8 * grid, cudaMemcpyDeviceToHost);
+            double a = 0;
+            for (int i = 0; i < grid; ++i) a += h[i];
+            printf("%-44s cycles/k-block %7.1f\n", name, a / grid / 64);
+        };
+        rs(ss_pipe<6, 128>, 6 * 32768 + 1024, tb, "SS router-like NS6 N128 grid128", 128);
+        rs(ss_pipe<4, 256>, 4 * 49152 + 1024, tb256, "SS router-like NS4 N256 grid64", 64);
+        rs(ss_pipe<6, 128>, 6 * 32768 + 1024, tb, "SS router-like NS6 N128 grid16", 16);
+    }
     return 0;
 }
