@@ -339,15 +339,22 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
-    if ((g_impl_override == 0 || g_impl_override == 6) && decode_supported(L, x, T)) {
+    if ((g_impl_override == 0 || g_impl_override == 6 || g_impl_override == 9) && decode_supported(L, x, T)) {
         // decode-size batch: router GEMV -> (PDL) stream-K decode GEMM, no bucketing
-        if (!given_masks) {
+        unsigned long long* tbuf = nullptr;
+        if (g_impl_override == 9) {  // traced (development hook): per-CTA globaltimer marks
+            static unsigned long long* buf = nullptr;
+            if (!buf) MOBI_CUDA(cudaMalloc(&buf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
+            MOBI_CUDA(cudaMemsetAsync(buf, 0, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long), st));
+            g_trace_buf = tbuf = buf;
+        }
+        if (!given_masks) {  // partial scores per hidden tile; the GEMM sums them and applies gate_hard
             ProfScope p(L, 0, st);
-            if ((rc = launch_router_dec(L, xb, T, delta, masks_out, nullptr, st))) return rc;
+            if ((rc = launch_router_dec(L, xb, T, delta, masks_out, nullptr, st, tbuf))) return rc;
         }
         ProfScope p(L, 3, st);
-        return launch_decode_gemm(L, xb, T, given_masks, reinterpret_cast<__nv_bfloat16*>(y),
-                                  !given_masks && g_impl_override != 6 && !L->prof, st);
+        return launch_decode_gemm(L, xb, T, given_masks, delta, masks_out, nullptr, reinterpret_cast<__nv_bfloat16*>(y),
+                                  !given_masks && g_impl_override != 6 && !L->prof, st, tbuf);
     }
     bool ready = false;
     if (!given_masks) {

@@ -179,9 +179,10 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
 // decode.cu (T <= kDecMaxT: router GEMV + stream-K decode GEMM, PDL-chained)
 bool decode_supported(const mobi_layer* L, const void* x, int64_t T);
 int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, uint8_t* masks_out,
-                      float* scores_out, cudaStream_t st);
-int launch_decode_gemm(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks,
-                       __nv_bfloat16* y, bool pdl, cudaStream_t st);
+                      float* scores_out, cudaStream_t st, unsigned long long* trace = nullptr);
+int launch_decode_gemm(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
+                       uint8_t* masks_out, float* scores_out, __nv_bfloat16* y, bool pdl, cudaStream_t st,
+                       unsigned long long* trace = nullptr);
 // decompose.cu
 int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,
                      int32_t E, double gamma, uint8_t* codes, double* scale, double* zero,
