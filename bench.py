@@ -37,6 +37,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 L2_BYTES = 126 * 1024 * 1024
+DECODE_MAX_T = 32  # the C-ABI's decode path (kDecMaxT)
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -239,7 +240,7 @@ def main():
         step(i)
     torch.cuda.synchronize()
     graphs = None
-    if args.graph:
+    if args.graph or args.tokens <= 64:  # decode sizes: host launch overhead would dominate
         # one graph per ring slot plus one graph of the whole ring (R consecutive steps), so the
         # host issues one launch per R steps and the device never waits for the host
         graphs = []
@@ -262,9 +263,6 @@ def main():
         torch.cuda.synchronize()
         config["launch"] = (f"CUDA graphs: the ring's {R} forwards captured as one graph (replayed steps//{R} "
                             f"times) + per-slot graphs for the remainder")
-    else:
-        for r in ring:
-            r["layer"].profile(True)
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.05)
@@ -296,16 +294,16 @@ def main():
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms = float(t.item())
-    # per-kernel device time inside the timed region (graph mode: an eager profiled pass after it)
-    if graphs is not None:
-        for r in ring:
-            r["layer"].profile(True)
-        torch.cuda._sleep(int(2e7))  # queue the profiled launches behind a ~10 ms spin: device time only
-        for i in range(min(args.steps, 50)):
-            step(i)
-        torch.cuda.synchronize()
-        config["kernel_times"] = ("eager profiled pass after the graph-timed region, launches queued behind a "
-                                  "device spin (no host gaps, no PDL overlap)")
+    # per-kernel device times: a separate eager pass after the timed region with CUDA events around
+    # every launch, queued behind a device spin (device time only; PDL overlap disabled in this pass)
+    for r in ring:
+        r["layer"].profile(True)
+    torch.cuda._sleep(int(2e7))
+    for i in range(min(args.steps, 50)):
+        step(i)
+    torch.cuda.synchronize()
+    config["kernel_times"] = ("eager profiled pass after the timed region, launches queued behind a device spin "
+                              "(no host gaps, no PDL overlap)")
     kern = {k: [0.0, 0] for k in ("router", "bucket", "gather", "gemm")}
     for r in ring:
         for k, (t_ms, n) in r["layer"].profile_read().items():
@@ -338,12 +336,31 @@ def main():
                 "flops_basis": "dense 2*T*in*out (bucket slices folded into one effective weight per MMA)",
                 "peak_source": f"{pk_src} burst bf16 (MEASURED_PEAKS.json bf16_tflops)"}
     hbm = pk.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+    if args.tokens <= DECODE_MAX_T:
+        # decode sizes are HBM-bound: algorithmic bytes = the union of the batch's active
+        # slices (2 bits each per weight) + group constants (s, s*z) + activations in/out
+        union = 0
+        for v in (int(k) for k in config["buckets"]):
+            union |= v
+        n_sl = bin(union).count("1")
+        G = math.ceil(args.inn / args.group_size)
+        alg = args.out * args.inn * 2 * n_sl / 8 + args.out * G * 8 + args.tokens * (args.inn + args.out) * 2
+        read = args.out * args.inn + args.out * G * 8 + args.tokens * (args.inn + args.out) * 2
+        gb = alg / (gemm_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(gb, 1), "peak": hbm, "unit": "GB/s", "frac": round(gb / hbm, 4),
+                    "traffic": None, "kernel": "decode GEMM (decode_fma_kernel T<=4 / decode_gemm_kernel)",
+                    "bytes_per_launch": alg, "bytes_basis": f"union of active slices ({n_sl} of 4) x 2 bit/weight + "
+                    "group constants 8 B/group + bf16 X and Y; the kernel streams the merged 8-bit codes "
+                    f"({read:.0f} B/launch)", "peak_source": f"{pk_src} HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"}
     h_w = (args.hidden or args.inn // 4)
     router_bytes = args.inn * h_w * 2 + args.tokens * args.inn * 2
     kernels = {k: {"ms_per_launch": round(v[0] / max(1, v[1]), 5), "launches": v[1],
                    "share": round(v[0] / max(1e-9, sum(x[0] for x in kern.values())), 4)} for k, v in kern.items()}
     kernels["router"]["tflops"] = round(router_flops(args) / (router_ms * 1e-3) / 1e12, 2) if router_ms else None
     kernels["router"]["frac_tensor"] = round(kernels["router"]["tflops"] / peak_tf, 4) if router_ms else None
+    if router_ms:
+        kernels["router"]["gbs"] = round(router_bytes / (router_ms * 1e-3) / 1e9, 1)
+        kernels["router"]["frac_hbm"] = round(kernels["router"]["gbs"] / hbm, 4)
     kernels["gather"]["gbs"] = round(2 * args.tokens * args.inn * 2 / (kernels["gather"]["ms_per_launch"] * 1e-3) / 1e9, 1) if kern["gather"][1] else None
 
     # ---------------- e2e through the public host-buffer API ----------------
