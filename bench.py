@@ -58,6 +58,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--ring", type=int, default=0)
+    p.add_argument("--parallel", default="token", choices=["token", "column"],
+                   help="N>1: token-sharded prefill (weak scaling, no collective) or column-parallel rows with an "
+                        "NCCL all-gather of the outputs (strong scaling of one layer)")
     p.add_argument("--graph", action="store_true",
                    help="replay each ring slot's forward from a captured CUDA graph (decode-size T: removes "
                         "host launch overhead); per-kernel times then come from an eager profiled pass")
@@ -211,7 +214,10 @@ def main():
                           f"T={args.tokens} tokens/GPU/step, target {args.target_bits} avg bits, router h=in/4",
               "out": args.out, "in": args.inn, "tokens_per_gpu": args.tokens, "target_bits": args.target_bits,
               "group_size": args.group_size, "router_hidden": args.hidden or args.inn // 4,
-              "parallelism": f"token-sharded x{world}" if world > 1 else "single GPU"}
+              "parallelism": (f"column-parallel x{world} (rows split, router replicated, NCCL all-gather of Y)"
+                              if args.parallel == "column" and world > 1 else
+                              f"token-sharded x{world}" if world > 1 else "single GPU")}
+    column = args.parallel == "column" and world > 1
 
     if args.impl == "reference":
         return main_reference(args, rank, world, dev, config)
@@ -224,8 +230,17 @@ def main():
     ring = []
     for i in range(R):
         layer, host = make_layer(args, dev, args.seed * 1000 + i)  # identical on every rank (replicas)
-        x = make_x(args, dev, args.seed * 7919 + 104729 * rank + i)
-        s = layer.score(x)
+        # column-parallel: every rank sees the same tokens; token-sharded: every rank its own
+        x = make_x(args, dev, args.seed * 7919 + (0 if column else 104729 * rank) + i)
+        if column:
+            from paper_2602_20191_b200.sharding import ColumnParallelMobiLayer
+            full = layer
+            h = host
+            layer = ColumnParallelMobiLayer(h["codes"], [2, 2, 2, 2], h["scale"], h["zero"], args.group_size,
+                                            h["w1"], h["b1"], h["w2"], h["b2"], device=local, rank=rank, world=world)
+            s0 = full.score(x)
+            del full
+        s = s0 if column else layer.score(x)
         delta = calibrate_threshold(s, rho)
         layer.reserve(args.tokens)
         y = torch.empty((args.tokens, args.out), dtype=torch.bfloat16, device=dev)
@@ -310,7 +325,7 @@ def main():
             kern[k][0] += t_ms
             kern[k][1] += n
         r["layer"].profile(False)
-    tokens_total = args.tokens * args.steps * world
+    tokens_total = args.tokens * args.steps * (1 if column else world)
     value = tokens_total / (ms / 1e3)
     # realized bits on the last ring entry
     _, m = step(0, masks=True)
@@ -408,7 +423,8 @@ def main():
     line = {"metric": "MoBi-linear tokens/s at LLaMA3-8B shapes vs avg bits; % of TC/HBM roofline",
             "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "fp16 operands (exact bf16->fp16 rescale), fp32 accumulate, bf16 out",
+            "scaling": "strong" if column else "weak", "vs_baseline": None,
+            "dtype": "fp16 operands (exact bf16->fp16 rescale), fp32 accumulate, bf16 out",
             "data": "synthetic (W~N(0,0.02^2) GPU-decomposed, random-init router, calibset-style X)",
             "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clocks, "kernels": kernels,
