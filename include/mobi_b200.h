@@ -85,6 +85,11 @@ typedef struct {
 
 /* Upload, validate and repack a layer onto `device`.  The handle owns its device weights. */
 MOBI_API int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out);
+/* Same as mobi_layer_create, but desc->codes ([n_slices][out][in] uint8 slice codes) already resides in
+ * device memory on `device` (e.g. the output of mobi_decompose): validated and repacked on the GPU,
+ * no host staging.  Every other descriptor array stays on the host.  No reference counterpart: it is
+ * the device-resident ingest for model-scale stacks (hundreds of matrices). */
+MOBI_API int mobi_layer_create_device(const mobi_layer_desc* desc, int device, mobi_layer_t* out);
 MOBI_API int mobi_layer_destroy(mobi_layer_t layer);
 /* Pre-size the internal workspace for up to max_tokens tokens (avoids allocation inside
  * forward, required before stream capture into a CUDA graph). */

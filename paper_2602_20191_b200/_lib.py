@@ -37,6 +37,7 @@ class LayerDesc(C.Structure):
 
 _SIGS = {
     "mobi_layer_create": [C.POINTER(LayerDesc), C.c_int, C.POINTER(_p)],
+    "mobi_layer_create_device": [C.POINTER(LayerDesc), C.c_int, C.POINTER(_p)],
     "mobi_layer_destroy": [_p],
     "mobi_layer_reserve": [_p, _i64],
     "mobi_layer_info": [_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i64)],

@@ -128,7 +128,7 @@ int ensure_ws(mobi_layer* L, int64_t T) {
     return MOBI_OK;
 }
 
-int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L) {
+int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_device = false) {
     CHECK_ARG(d != nullptr, "mobi_layer_create: null descriptor");
     CHECK_ARG(d->out > 0 && d->in > 0, "mobi_layer_create: empty weight " << d->out << "x" << d->in);
     CHECK_ARG(d->group_size >= 1, "QuantParams: group_size must be >= 1");
@@ -163,7 +163,7 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L) {
     }
     CHECK_ARG((d->codes != nullptr) != (d->planes != nullptr),
               "mobi_layer_create: give exactly one of codes (SliceStack) or planes (LayerRecord)");
-    if (d->codes) {
+    if (d->codes && !codes_on_device) {
         const int qmax = (1 << L->b) - 1;
         const int64_t n = L->out * L->in;
         for (int e = 0; e < L->E; ++e)
@@ -173,7 +173,7 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L) {
                                                       " out of [0," + std::to_string(qmax) + "] at (" +
                                                       std::to_string(i / L->in) + "," + std::to_string(i % L->in) +
                                                       ")");
-    } else {
+    } else if (!d->codes) {
         CHECK_ARG(d->plane_bits == total, "bitplane: planes carry " << d->plane_bits << " bits, slices need " << total);
         CHECK_ARG(d->words_per_row == cdiv(d->in, 64),
                   "bitplane: words_per_row " << d->words_per_row << " != ceil(in/64) = " << cdiv(d->in, 64));
@@ -203,12 +203,24 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L) {
     return MOBI_OK;
 }
 
-int upload_layer(const mobi_layer_desc* d, mobi_layer* L) {
+int upload_layer(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_device = false) {
     int rc;
     const int64_t ng = L->out * L->G;
     // weights: tiled merged codes (repacked on the device)
     if ((rc = dmalloc(&L->codes8, (size_t)(L->out_pad * L->in_pad), L))) return rc;
-    if (d->codes) {
+    if (d->codes && codes_on_device) {
+        int64_t bad = -1;
+        if ((rc = check_codes_device(d->codes, (int64_t)L->E * L->out * L->in, (1 << L->b) - 1, &bad))) return rc;
+        if (bad >= 0) {
+            const int64_t i = bad % (L->out * L->in);
+            return set_error(MOBI_EINVAL, "dequantize_centered: code out of [0," + std::to_string((1 << L->b) - 1) +
+                                              "] at (" + std::to_string(i / L->in) + "," + std::to_string(i % L->in) +
+                                              ")");
+        }
+        rc = launch_pack_codes(L, d->codes, 0);
+        cudaDeviceSynchronize();
+        if (rc) return rc;
+    } else if (d->codes) {
         uint8_t* tmp = nullptr;
         const size_t n = (size_t)(L->E * L->out * L->in);
         if ((rc = dmalloc(&tmp, n, nullptr))) return rc;
@@ -416,7 +428,7 @@ MOBI_API int mobi_debug_read_trace(unsigned long long* host, int n_cta) {
     return MOBI_OK;
 }
 
-int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out) {
+static int create_impl(const mobi_layer_desc* desc, int device, mobi_layer_t* out, bool codes_on_device) {
     CHECK_ARG(out != nullptr, "mobi_layer_create: null output handle");
     *out = nullptr;
     int ndev = 0;
@@ -425,8 +437,17 @@ int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out
     DeviceGuard g(device);
     mobi_layer* L = new mobi_layer;
     L->device = device;
-    int rc = validate_and_fill(desc, L);
-    if (!rc) rc = upload_layer(desc, L);
+    int rc = validate_and_fill(desc, L, codes_on_device);
+    if (!rc && codes_on_device) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, desc->codes) != cudaSuccess || pa.type != cudaMemoryTypeDevice ||
+            pa.device != device) {
+            cudaGetLastError();
+            rc = set_error(MOBI_EINVAL, "mobi_layer_create_device: codes must be device memory on device " +
+                                            std::to_string(device));
+        }
+    }
+    if (!rc) rc = upload_layer(desc, L, codes_on_device);
     if (rc) {
         std::string keep = g_err;
         mobi_layer_destroy(L);
@@ -435,6 +456,15 @@ int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out
     }
     *out = L;
     return MOBI_OK;
+}
+
+int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out) {
+    return create_impl(desc, device, out, false);
+}
+
+int mobi_layer_create_device(const mobi_layer_desc* desc, int device, mobi_layer_t* out) {
+    CHECK_ARG(desc && desc->codes && !desc->planes, "mobi_layer_create_device: give device slice codes");
+    return create_impl(desc, device, out, true);
 }
 
 int mobi_layer_destroy(mobi_layer_t L) {

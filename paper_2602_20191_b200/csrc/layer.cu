@@ -81,7 +81,27 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ src, int64_t out
     }
 }
 
+__global__ void check_codes_kernel(const uint8_t* __restrict__ codes, int64_t n, int qmax,
+                                   unsigned long long* __restrict__ first_bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (codes[i] > qmax) atomicMin(first_bad, (unsigned long long)i);
+}
+
 }  // namespace
+
+// index of the first slice code above qmax, or -1 (device-resident SliceStack ingest)
+int check_codes_device(const uint8_t* codes_dev, int64_t n, int qmax, int64_t* bad) {
+    unsigned long long* d = nullptr;
+    MOBI_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+    unsigned long long init = ~0ull, h = 0;
+    MOBI_CUDA(cudaMemcpy(d, &init, sizeof(init), cudaMemcpyHostToDevice));
+    check_codes_kernel<<<592, 256>>>(codes_dev, n, qmax, d);
+    cudaError_t e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return set_error(MOBI_ERUNTIME, std::string("check_codes: ") + cudaGetErrorString(e));
+    *bad = h == ~0ull ? -1 : (int64_t)h;
+    return MOBI_OK;
+}
 
 int launch_pack_codes(mobi_layer* L, const uint8_t* codes_dev, cudaStream_t st) {
     const int64_t n = L->out_pad * L->kblocks * (kKBlock / 16);

@@ -154,6 +154,7 @@ int set_error(int code, const std::string& msg);
 
 // ---- launchers (each returns MOBI_OK or an error code; each counts its launches) ----
 // layer.cu
+int check_codes_device(const uint8_t* codes_dev, int64_t n, int qmax, int64_t* bad);
 int launch_pack_codes(mobi_layer* L, const uint8_t* codes_dev, cudaStream_t st);
 int launch_pack_planes(mobi_layer* L, const uint64_t* planes_dev, int bits, int64_t wpr,
                        cudaStream_t st);

@@ -71,6 +71,17 @@ class MobiLayer:
         return cls._create(out, inn, group_size, slice_bits, scale, zero, codes, None, 0, 0, w1, b1, w2, b2, device)
 
     @classmethod
+    def from_device_stack(cls, codes: torch.Tensor, slice_bits, scale, zero, group_size, w1, b1, w2, b2):
+        """From a SliceStack whose codes [E,out,in] uint8 already live on the GPU (e.g. decompose()'s
+        output): validated and repacked on the device (mobi_layer_create_device)."""
+        if not (codes.is_cuda and codes.dtype == torch.uint8 and codes.dim() == 3):
+            raise ValueError("from_device_stack expects CUDA uint8 codes [E, out, in]")
+        codes = codes.contiguous()
+        E, out, inn = codes.shape
+        return cls._create(out, inn, group_size, slice_bits, scale, zero, codes, None, 0, 0, w1, b1, w2, b2,
+                           codes.device.index)
+
+    @classmethod
     def from_record(cls, rec, device: int = 0):
         """From a checkpoint LayerRecord (merged-code bit-planes, checkpoint.hpp:30-74)."""
         planes = _arr(rec.planes, np.uint64)
@@ -80,6 +91,7 @@ class MobiLayer:
     @classmethod
     def _create(cls, out, inn, gs, slice_bits, scale, zero, codes, planes, plane_bits, wpr, w1, b1, w2, b2, device):
         sb = _arr(slice_bits, np.int32)
+        dev_codes = isinstance(codes, torch.Tensor)
         scale, zero = _arr(scale, np.float64), _arr(zero, np.float64)
         w1, b1, w2, b2 = (_arr(a, np.float64) for a in (w1, b1, w2, b2))
         if w1.ndim != 2 or w1.shape[0] != inn:
@@ -87,12 +99,15 @@ class MobiLayer:
         if w2.ndim != 2 or w2.shape[1] != sb.size - 1:
             raise ValueError(f"forward_elastic: router emits {w2.shape[-1]} scores for {sb.size - 1} routed slices")
         d = LayerDesc(out=out, in_=inn, group_size=gs, n_slices=sb.size, slice_bits=_ptr(sb, _i32),
-                      scale=_ptr(scale, _f64), zero=_ptr(zero, _f64), codes=_ptr(codes, C.c_uint8),
+                      scale=_ptr(scale, _f64), zero=_ptr(zero, _f64),
+                      codes=(C.cast(C.c_void_p(codes.data_ptr()), C.POINTER(C.c_uint8)) if dev_codes
+                             else _ptr(codes, C.c_uint8)),
                       planes=_ptr(planes, C.c_uint64), plane_bits=plane_bits, words_per_row=wpr,
                       router_hidden=w1.shape[1], w1=_ptr(w1, _f64), b1=_ptr(b1, _f64), w2=_ptr(w2, _f64),
                       b2=_ptr(b2, _f64))
         h = C.c_void_p()
-        check(lib().mobi_layer_create(C.byref(d), device, C.byref(h)))
+        create = lib().mobi_layer_create_device if dev_codes else lib().mobi_layer_create
+        check(create(C.byref(d), device, C.byref(h)))
         return cls(h.value, sb.tolist(), out, inn, w1.shape[1], device)
 
     def close(self):

@@ -1,0 +1,87 @@
+"""BASELINE config 5: the full LLaMA3-8B layer stack (32 blocks x 7 MoBi linears, random-init slices),
+token-adaptive routing sweep of average bits.  For every target budget the per-layer thresholds are
+calibrated on the batch (pipeline.hpp:146-160), the realized bits are measured (acceptance criterion 6:
+within +-0.15 of the target, acceptance.cpp:334-353), and the whole-stack forward is timed as one CUDA
+graph replay.
+
+  python tools/stack_sweep.py [--blocks 32 --tokens 2048 --steps 10]
+  python -m torch.distributed.run --nproc-per-node N tools/stack_sweep.py ...   (replicas, token-sharded)
+
+Prints one JSON line per target budget (rank 0; tokens/s is the whole job, time = max over ranks).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--blocks", type=int, default=32)
+    ap.add_argument("--tokens", type=int, default=2048, help="tokens per GPU per forward")
+    ap.add_argument("--targets", type=float, nargs="+", default=[2.0, 2.5, 3.0, 3.5, 4.0])
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--seed", type=int, default=1)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    from paper_2602_20191_b200.stack import MobiStack
+    t0 = time.time()
+    stack = MobiStack(blocks=args.blocks, device=local, seed=args.seed, max_tokens=args.tokens)
+    build_s = time.time() - t0
+    g = torch.Generator(device="cuda").manual_seed(args.seed * 7919 + rank)
+    x = torch.randn((args.tokens, stack.d), generator=g, device="cuda")
+    ch = torch.randperm(stack.d, generator=g, device="cuda")[: round(0.05 * stack.d)]
+    x[:, ch] *= 8.0
+    x = x.to(torch.bfloat16)
+    for target in args.targets:
+        res = stack.sweep_point(x, target)
+        deltas = {id(layer): d for layer, d in zip(stack.layers, res.per_layer_delta)}
+        graph, _ = stack.capture(x, deltas)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        del graph
+        if rank == 0:
+            print(json.dumps({
+                "config": "llama3-8b MoBi stack", "blocks": args.blocks, "linears": 7 * args.blocks,
+                "tokens_per_gpu": args.tokens, "n_gpus": world, "parallelism": f"replicas, token-sharded x{world}",
+                "target_bits": target, "realized_avg_bits": round(res.realized_bits, 4),
+                "criterion6_within_0.15": abs(res.realized_bits - target) <= 0.15,
+                "per_layer_bits_min": round(min(res.per_layer_bits), 4),
+                "per_layer_bits_max": round(max(res.per_layer_bits), 4),
+                "ms_per_forward": round(ms, 3), "tokens_per_s": round(args.tokens * world / (ms / 1e3), 1),
+                "device_gib": round(stack.device_bytes() / 2**30, 2), "build_s": round(build_s, 1),
+                "data": "random-init slices (uniform 2-bit codes, unit-gain group scales), calibset-style X"}),
+                flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
