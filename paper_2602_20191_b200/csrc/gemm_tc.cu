@@ -40,7 +40,10 @@ using namespace sm100;
 #define MOBI_NSTAGE 5
 #endif
 constexpr int NSTAGE = MOBI_NSTAGE;  // B stages (smem, 32 KiB each)
-constexpr int NSA = 8;               // A stages (TMEM, 32 columns each)
+#ifndef MOBI_UNIFIED
+#define MOBI_UNIFIED 1  // 1: one full/empty barrier pair per stage for both A (TMEM) and B (smem)
+#endif
+constexpr int NSA = MOBI_UNIFIED ? NSTAGE : 8;  // A stages (TMEM, 32 columns each)
 constexpr int kSplitMaxT = 64;   // split-K only for decode-size batches
 constexpr int kMaxSplit = 8;
 #ifndef MOBI_BOXR
@@ -136,6 +139,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* full_a = bars + 2 * NSTAGE;     // [NSA] A stage written to TMEM (8 warps)
     uint64_t* empty_a = full_a + NSA;         // [NSA] local MMAs done with the A stage
     uint64_t* acc_full = empty_a + NSA;       // accumulator ready for the epilogue
+    // unified stages: the dequantizers arrive on the TMA's full barrier and wait on the MMA's empty one
+    uint64_t* a_full = MOBI_UNIFIED ? full_b : full_a;
+    uint64_t* a_empty = MOBI_UNIFIED ? empty : empty_a;
     uint64_t* acc_empty = acc_full + 1;       // epilogue drained the accumulator (4 warps)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
     __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 256);
@@ -145,7 +151,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full_b[s], 1);
+            mbar_init(&full_b[s], MOBI_UNIFIED ? 1 + kDqWarps / 2 : 1);
             mbar_init(&empty[s], MOBI_MC ? 2 : 1);  // MMA completion of BOTH CTAs of the pair (shared B stages)
         }
         for (int s = 0; s < NSA; ++s) {
@@ -244,7 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const uint32_t pha = (it / NSA) & 1;
                 TW(1, mbar_wait(&full_b[s], ph));
                 EV(1, kb, tc);
-                TW(2, mbar_wait(&full_a[sa], pha));
+                if (!MOBI_UNIFIED) TW(2, mbar_wait(&full_a[sa], pha));
                 EV(2, kb, tc);
                 tc_fence_after();
                 if (elect_one_sync()) {
@@ -266,7 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         mma_commit_mc(&empty[s], (uint16_t)0x3);  // frees the shared B stage in both CTAs
                     else
                         mma_commit(&empty[s]);
-                    mma_commit(&empty_a[sa]);                 // frees the local A stage
+                    if (!MOBI_UNIFIED) mma_commit(&empty_a[sa]);  // frees the local A stage
                     if (kb == kb1 - 1) mma_commit(acc_full);
                 }
                 __syncwarp();
@@ -351,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const uint32_t itk = base + (kb - kb0);
                 const int s = itk % NSA;
                 const uint32_t ph = (itk / NSA) & 1;
-                TW(0, mbar_wait(&empty_a[s], ph ^ 1));
+                TW(0, mbar_wait(&a_empty[s], ph ^ 1));
                 if (warp == 0 || warp == 4) EV(4, kb, base);
                 tc_fence_after();
                 TW(3, tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v));
@@ -366,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (warp == 0 || warp == 4) EV(6, kb, base);
-                if (lane == 0) mbar_arrive(&full_a[s]);
+                if (lane == 0) mbar_arrive(&a_full[s]);
                 return true;
             };
             if (kb0 + par < kb_lim) dq(c00, c01, g0, v);
@@ -389,6 +395,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             TokTile tt;
             int rt, ks, kb0, kb1;
             tile_of(pair, tt, rt, ks, kb0, kb1);
+            // the tile's token sources and row scales, fetched while the MMAs run (not per drained chunk)
+            int32_t src_r[kTokTile / 32];
+            float es_r[kTokTile / 32];
+#pragma unroll
+            for (int c = 0; c < kTokTile / 32; ++c) {
+                const bool ok = 32 * c + lane < tt.n;
+                src_r[c] = ok ? __ldg(p.perm + tt.row0 + 32 * c + lane) : -1;
+                es_r[c] = ok ? __ldg(p.escale + tt.row0 + 32 * c + lane) : 0.f;
+            }
             TW(0, mbar_wait(acc_full, tc & 1));
             tc_fence_after();
             if (nsplit > 1) {
@@ -419,22 +434,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 continue;
             }
             epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
-            for (int c0 = 0; c0 < tt.n; c0 += 32) {
-                const int nn = min(32, tt.n - c0);
-                int32_t my_src = -1;
-                float my_es = 0.f;
-                if (lane < nn) {
-                    my_src = __ldg(p.perm + tt.row0 + c0 + lane);
-                    my_es = __ldg(p.escale + tt.row0 + c0 + lane);
-                }
-                if (q == 0) tok_src[c0 + lane] = lane < nn ? my_src : -1;
-                uint32_t v[32];
-                tmem_ld32(tmem + lane_base + c0, v);
-                tmem_ld_wait();
+            // 16-column TMEM loads, the next one in flight while the current one is converted
+            uint32_t va[16], vb[16];
+            tmem_ld16(tmem + lane_base, va);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float es = __shfl_sync(0xffffffffu, my_es, j);
-                    stage_y[(c0 + j) * kRowTile + 32 * q + lane] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
+            for (int c = 0; c < kTokTile / 16; ++c) {
+                const int c0 = 16 * c;
+                if (c0 >= tt.n) break;
+                tmem_ld_wait();
+                uint32_t(&cur)[16] = (c & 1) ? vb : va;
+                uint32_t(&nxt)[16] = (c & 1) ? va : vb;
+                if (c0 + 16 < tt.n) tmem_ld16(tmem + lane_base + c0 + 16, nxt);
+                const float my_es = es_r[c / 2];
+                if (q == 0 && (c & 1) == 0) tok_src[c0 + lane] = src_r[c / 2];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const float es = __shfl_sync(0xffffffffu, my_es, (c & 1) * 16 + j);
+                    stage_y[(c0 + j) * kRowTile + 32 * q + lane] = __float2bfloat16_rn(__uint_as_float(cur[j]) * es);
                 }
             }
             tc_fence_before();
