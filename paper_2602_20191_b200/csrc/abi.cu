@@ -387,7 +387,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
         if ((rc = launch_gather(L, xb, T, st, fused))) return rc;
     }
     __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
-    if (fused && g_impl_override != 0)  // only the production GEMM clears the fused-bucketing counters
+    if (fused && g_impl_override != 0 && g_impl_override != 3 && g_impl_override != 5)  // the tcgen05 GEMMs clear them
         MOBI_CUDA(cudaMemsetAsync(L->bk_hist, 0, 48 * sizeof(int32_t), st));
     ProfScope p(L, 3, st);
     if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
@@ -399,8 +399,12 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
         if (g_impl_override == 4) return launch_gemm_tc2(L, yb, T, st, tbuf);
         return launch_gemm_tc(L, yb, T, st, tbuf);
     }
-    if (g_impl_override == 3) return launch_gemm_tc2(L, yb, T, st);  // CTA-pair kernel (comparison)
-    return launch_gemm_tc(L, yb, T, st);
+    if (g_impl_override == 3) return launch_gemm_tc2(L, yb, T, st);  // CTA-pair kernel
+    if (g_impl_override == 5) return launch_gemm_tc(L, yb, T, st);   // 1-CTA kernel (comparison)
+    // production: the CTA-pair kernel (B split across the pair: half the smem operand traffic per SM);
+    // the 1-CTA kernel for batches small enough to need split-K
+    if (T <= 64) return launch_gemm_tc(L, yb, T, st);
+    return launch_gemm_tc2(L, yb, T, st);
 }
 
 }  // namespace

@@ -25,6 +25,9 @@
 #include "mobi_internal.cuh"
 #include "sm100.cuh"
 
+#ifndef MOBI_RELAXED
+#define MOBI_RELAXED 1
+#endif
 namespace mobi {
 namespace {
 
@@ -372,7 +375,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (warp == 0 || warp == 4) EV(6, kb, base);
-                if (lane == 0) mbar_arrive(&a_full[s]);
+                if (lane == 0) {
+#if MOBI_RELAXED
+                    mbar_arrive_relaxed(&a_full[s]);
+#else
+                    mbar_arrive(&a_full[s]);
+#endif
+                }
                 return true;
             };
             if (kb0 + par < kb_lim) dq(c00, c01, g0, v);

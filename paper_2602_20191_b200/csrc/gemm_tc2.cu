@@ -17,6 +17,9 @@
 #include "mobi_internal.cuh"
 #include "sm100.cuh"
 
+#ifndef MOBI_RELAXED
+#define MOBI_RELAXED 1
+#endif
 namespace mobi {
 int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int64_t rows, int64_t cols,
                  int box_rows);
@@ -52,6 +55,7 @@ struct Params {
     const int32_t* meta;
     __nv_bfloat16* y;
     int vec_y;
+    int* bk_hist;  // fused-bucketing histogram + slot counters: zeroed here for the next forward
     unsigned long long* trace;
 };
 
@@ -77,13 +81,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stage_b = smem;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * kStageBytes);
-    uint64_t* full_b = bars;                 // [NSTAGE] leader: both halves landed
-    uint64_t* full_a = bars + NSTAGE;        // [NSTAGE] leader: both CTAs' A stages written
+    // one full barrier per stage, in the leader: both halves' TMA bytes (one expect_tx arrival) and the
+    // 8 + 8 dequant warps of the pair (the peer's arrive remotely)
+    uint64_t* full_b = bars;                 // [NSTAGE] leader: stage complete (A in both TMEMs, B in both smems)
     uint64_t* empty = bars + 2 * NSTAGE;     // [NSTAGE] each CTA: pair MMAs done with the stage
     uint64_t* acc_full = bars + 3 * NSTAGE;  // each CTA
     uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
-    uint64_t* full_a_loc = acc_empty + 1;    // [NSTAGE] peer: its own 8 dequant warps (forwarded)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full_a_loc + NSTAGE);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1 + NSTAGE);
     __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 512);
     int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
@@ -92,9 +96,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t rank = cluster_ctarank();
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full_b[s], 1);
-            mbar_init(&full_a[s], kDqWarps / 2 + 1);  // leader's 8 warps of one k-parity + 1 peer forward
-            mbar_init(&full_a_loc[s], kDqWarps / 2);
+            mbar_init(&full_b[s], 1 + kDqWarps);  // TMA expect_tx + 8 dequant warps per CTA x 2
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
@@ -104,6 +106,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         prefetch_tmap(&tmap_big);
     }
     if (warp == kWarpMma) tmem_alloc_2sm(tmem_slot, 512);
+    if (blockIdx.x == 0 && threadIdx.x < 48 && p.bk_hist) p.bk_hist[threadIdx.x] = 0;  // gather consumed it
     tc_fence_before();
     __syncthreads();
     cluster_sync();
@@ -153,21 +156,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == kWarpMma) {
-        // ---------------- MMA issuer (leader) / A-stage forwarder (peer) ----------------
-        if (rank != 0) {
-            // one cluster-scope arrive per k-block instead of one per dequant warp
-            const uint32_t full_a_leader = mapa_shared(smem_u32(full_a), 0);
-            uint32_t it = 0;
-            for (int pair = cid; pair < total; pair += ncl)
-                for (int kb = 0; kb < kb_n; ++kb, ++it) {
-                    const int s = it % NSTAGE;
-                    mbar_wait(&full_a_loc[s], (it / NSTAGE) & 1);
-                    tc_fence_after();
-                    tc_fence_before();
-                    if (elect_one_sync()) mbar_arrive_cluster(full_a_leader + s * 8);
-                    __syncwarp();
-                }
-        }
+        // ---------------- MMA issuer (leader) ----------------
         if (rank == 0) {
             uint32_t it = 0, tc = 0;
             for (int pair = cid; pair < total; pair += ncl, ++tc) {
@@ -181,8 +170,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint32_t ph = (it / NSTAGE) & 1;
                     mbar_wait_cluster(&full_b[s], ph);
                     EV(1, kb, tc);
-                    mbar_wait_cluster(&full_a[s], ph);
-                    EV(2, kb, tc);
                     tc_fence_after();
                     if (elect_one_sync()) {
                         const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
@@ -215,6 +202,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int par = (idx / 4) & 1;
         const int hh = idx / 8;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        const uint32_t full_leader = mapa_shared(smem_u32(full_b), 0);
         uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
         for (int pair = cid; pair < total; pair += ncl, base += kb_n) {
             TokTile tt;
@@ -284,7 +272,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (warp == 0 || warp == 4) EV(5, kb, base);
-                if (lane == 0) mbar_arrive(rank == 0 ? &full_a[s] : &full_a_loc[s]);  // peer: forwarded below
+                if (lane == 0) {
+#if MOBI_RELAXED
+                    if (rank == 0)
+                        mbar_arrive_relaxed(&full_b[s]);
+                    else
+                        mbar_arrive_relaxed_cluster(full_leader + s * 8);
+#else
+                    if (rank == 0)
+                        mbar_arrive(&full_b[s]);
+                    else
+                        mbar_arrive_cluster(full_leader + s * 8);
+#endif
+                }
                 return true;
             };
             if (par < kb_n) dq(c00, c01, g0, v);
@@ -306,25 +306,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
+            int32_t src_r[kTokTile / 32];
+            float es_r[kTokTile / 32];
+#pragma unroll
+            for (int c = 0; c < kTokTile / 32; ++c) {
+                const bool ok = 32 * c + lane < tt.n;
+                src_r[c] = ok ? __ldg(p.perm + tt.row0 + 32 * c + lane) : -1;
+                es_r[c] = ok ? __ldg(p.escale + tt.row0 + 32 * c + lane) : 0.f;
+            }
             mbar_wait_cluster(acc_full, tc & 1);
             tc_fence_after();
             epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
-            for (int c0 = 0; c0 < tt.n; c0 += 32) {
-                const int nn = min(32, tt.n - c0);
-                int32_t my_src = -1;
-                float my_es = 0.f;
-                if (lane < nn) {
-                    my_src = __ldg(p.perm + tt.row0 + c0 + lane);
-                    my_es = __ldg(p.escale + tt.row0 + c0 + lane);
-                }
-                if (q == 0) tok_src[c0 + lane] = lane < nn ? my_src : -1;
-                uint32_t v[32];
-                tmem_ld32(tmem + lane_base + c0, v);
-                tmem_ld_wait();
+            uint32_t va[16], vb[16];
+            tmem_ld16(tmem + lane_base, va);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float es = __shfl_sync(0xffffffffu, my_es, j);
-                    stage_y[(c0 + j) * kRowTile + 32 * q + lane] = __float2bfloat16_rn(__uint_as_float(v[j]) * es);
+            for (int c = 0; c < kTokTile / 16; ++c) {
+                const int c0 = 16 * c;
+                if (c0 >= tt.n) break;
+                tmem_ld_wait();
+                uint32_t(&cur)[16] = (c & 1) ? vb : va;
+                uint32_t(&nxt)[16] = (c & 1) ? va : vb;
+                if (c0 + 16 < tt.n) tmem_ld16(tmem + lane_base + c0 + 16, nxt);
+                const float my_es = es_r[c / 2];
+                if (q == 0 && (c & 1) == 0) tok_src[c0 + lane] = src_r[c / 2];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const float es = __shfl_sync(0xffffffffu, my_es, (c & 1) * 16 + j);
+                    stage_y[(c0 + j) * kRowTile + 32 * q + lane] = __float2bfloat16_rn(__uint_as_float(cur[j]) * es);
                 }
             }
             tc_fence_before();
@@ -404,6 +412,7 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     const int64_t max_pairs = (int64_t)(p.n_row_tiles / 2) * L->max_tiles;
     const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
     p.trace = trace;
+    p.bk_hist = L->bk_hist;
     if (trace)
         mobi_gemm_tc2_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(L->tmap_x2[0], L->tmap_x2[1], p);
     else
