@@ -17,6 +17,9 @@
 #include "mobi_internal.cuh"
 #include "sm100.cuh"
 
+#ifndef MOBI_MMA_WAIT
+#define MOBI_MMA_WAIT 0
+#endif
 #ifndef MOBI_RELAXED
 #define MOBI_RELAXED 1
 #endif
@@ -168,7 +171,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < kb_n; ++kb, ++it) {
                     const int s = it % NSTAGE;
                     const uint32_t ph = (it / NSTAGE) & 1;
+#if MOBI_MMA_WAIT == 0
                     mbar_wait_cluster(&full_b[s], ph);
+#elif MOBI_MMA_WAIT == 1
+                    mbar_wait(&full_b[s], ph);
+#else
+                    mbar_wait_relaxed(&full_b[s], ph);
+#endif
                     EV(1, kb, tc);
                     tc_fence_after();
                     if (elect_one_sync()) {

@@ -115,6 +115,17 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_wait_relaxed(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAITR_%=:\n\t"
+        "mbarrier.try_wait.parity.relaxed.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONER_%=;\n\t"
+        "bra WAITR_%=;\n\t"
+        "DONER_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 // 2-SM TMA: data lands in the issuing CTA's smem, complete_tx goes to the barrier at cluster
 // address `bar_cluster` (the leader CTA's)
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
