@@ -347,7 +347,8 @@ def main():
             traffic = d.get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": round(achieved, 2), "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": round(achieved / peak_tf, 4), "traffic": traffic,
-                "kernel": "mobi_gemm_tc_kernel", "flops_per_launch": gemm_flops(args),
+                "kernel": "mobi_gemm_tc2_kernel" if args.tokens > 64 else "mobi_gemm_tc_kernel (split-K)",
+                "flops_per_launch": gemm_flops(args),
                 "flops_basis": "dense 2*T*in*out (bucket slices folded into one effective weight per MMA)",
                 "peak_source": f"{pk_src} burst bf16 (MEASURED_PEAKS.json bf16_tflops)"}
     hbm = pk.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
