@@ -239,6 +239,12 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_device =
         dfree(tmp);
         if (rc) return rc;
     }
+    // decode slice planes (2-bit slices only): the decode GEMV streams just the slices a batch uses
+    if (L->b == 2) {
+        if ((rc = dmalloc(&L->dplanes, (size_t)(L->E * (L->out_pad / 32) * L->kblocks * 512), L))) return rc;
+        if ((rc = launch_pack_dplanes(L, 0))) return rc;
+        MOBI_CUDA(cudaDeviceSynchronize());
+    }
     // group constants transposed to [G][out_pad] (s, s*z): a warp's 32 rows read 256 contiguous bytes
     std::vector<float2> gc((size_t)(L->G * L->out_pad), make_float2(0.f, 0.f));
     for (int64_t r = 0; r < L->out; ++r)
@@ -365,8 +371,12 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
             if ((rc = launch_router_dec(L, xb, T, delta, masks_out, nullptr, st, tbuf))) return rc;
         }
         ProfScope p(L, 3, st);
+        const bool pdl = !given_masks && g_impl_override != 6 && !L->prof;
+        if (decode_planes_supported(L, x, T))  // slice planes: stream only the slices the batch uses
+            return launch_decode_planes(L, xb, T, given_masks, delta, masks_out, nullptr,
+                                        reinterpret_cast<__nv_bfloat16*>(y), pdl, st, tbuf);
         return launch_decode_gemm(L, xb, T, given_masks, delta, masks_out, nullptr, reinterpret_cast<__nv_bfloat16*>(y),
-                                  !given_masks && g_impl_override != 6 && !L->prof, st, tbuf);
+                                  pdl, st, tbuf);
     }
     bool ready = false;
     if (!given_masks) {
@@ -477,6 +487,7 @@ int mobi_layer_destroy(mobi_layer_t L) {
     cudaDeviceSynchronize();
     free_ws(L);
     dfree(L->codes8);
+    dfree(L->dplanes);
     dfree(L->gconst);
     dfree(L->gpart);
     dfree(L->hpart);

@@ -1,0 +1,426 @@
+// decode2.cu -- decode GEMV on slice planes (T <= kD2MaxT tokens): stream only the slices a batch uses.
+//
+// At one to four tokens the layer is bound by the bytes it streams.  The merged 8-bit codes hold all
+// four 2-bit slices, so a token that only needs slice 1 would still pay 1 B/weight.  Here every slice
+// has its own plane (layer.cu: pack_dplanes_kernel), already arranged as mma.sync A fragments, and the
+// kernel reads slice 1 (always on) while the router is still running, then -- once the masks are
+// known (griddepcontrol.wait) -- only the planes of the union of the batch's slices.
+//
+// The contraction is split per slice (router.hpp:105-132 is exactly this sum):
+//     y_t = sum_{e in m_t} sum_g (s_g / 64) 4^(4-e) (x_t . c_e)_g  +  kc[m_t] A_t - B_t
+//     A_t = sum_g s_g sum_{k in g} x_t,   B_t = sum_g s_g z_g sum_{k in g} x_t
+// which is the folded weight W_m = S (INT & maskbyte(m)) + C_m of the prefill GEMM
+// (mobi_internal.cuh) regrouped per slice.  (x_t . c_e)_g runs on mma.sync m16n8k16 with the
+// fragment-ordered 2-bit codes expanded to exact fp16 (1024 + c, the offset cancelled with the
+// group's activation sum) and x scaled per token by 2^-e into fp16 (exact).
+//
+// One CTA owns a 32-row tile over the whole K (no cross-CTA reduction); its eight warps split K and
+// are summed in warp order at the end (deterministic).
+#include "mobi_internal.cuh"
+#include "sm100.cuh"
+
+namespace mobi {
+namespace {
+
+using namespace sm100;
+
+constexpr int kD2Warps = 8, kD2Threads = 32 * kD2Warps;
+constexpr int kD2MaxT = 4;
+constexpr int kD2Acc = 3 * 2 * 4;  // per lane: y over the token's slices, A, B  ([2][4] each)
+
+struct D2Params {
+    const uint4* dplanes;     // [E][n_rt32][kblocks][32] 16 B
+    const float2* gconst;     // [G][out_pad] (s, s*z)
+    const __nv_bfloat16* x;   // [T][in]
+    const uint8_t* masks;     // given masks (forward_masked) or null
+    const float* spart;       // [n_mt][T][nr] router tile partial scores
+    const float* b2;
+    uint8_t* masks_dev;
+    uint8_t* masks_out;
+    float* scores_out;
+    __nv_bfloat16* y;
+    MaskTable mt;
+    int64_t out, out_pad, in, in_pad, kblocks, gs;
+    float delta;
+    int single_group, T, E, nr, n_mt, vmask, n_rt32, xs_stride;
+    int gpw;          // groups per warp (bound) for the staged constants
+    int64_t gcs_off;  // byte offset of the staged constants in dynamic smem
+    int64_t ring_off; // byte offset of the per-lane cp.async rings
+    unsigned long long* trace;  // debug: per-CTA globaltimer marks [2048 + cta][8]
+};
+__device__ __forceinline__ unsigned long long gtimer2() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void mma_f16_acc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                            uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void grid_dep_wait2() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// 2-bit fields i and i+8 of a fragment word -> half2 (1024 + lo, 1024 + hi)
+__device__ __forceinline__ uint32_t frag(uint32_t w, int i) { return ((w >> (2 * i)) & 0x00030003u) | 0x64006400u; }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kD2Ring = 8;  // k-blocks in flight per lane (16 B each)
+
+// One slice over the warp's k-blocks [kw0, kw1), folded per group into ys.  Each lane streams its own
+// 16-byte fragment words through a private cp.async ring (no cross-lane dependency, no barriers); the
+// code is a single compact loop -- an unrolled variant overflowed the instruction cache.  The
+// slice-independent constant sums A, B are accumulated on the first pass (with_const).
+__device__ __forceinline__ void slice_pass(const D2Params& p, int e0, int rt, int kw0, int kw1, const __half* x16,
+                                        const float* xsum, const float* es_s, const float2* gcs, uint4* ring,
+                                        int lane, bool with_const, float (&ys)[2][4], float (&A)[2][4],
+                                        float (&B)[2][4]) {
+    const int g = lane >> 2, c = lane & 3;
+    const int tg = g < p.T ? g : kD2MaxT;  // B-fragment token row (row kD2MaxT is zeros)
+    const int t0 = 2 * c, t1 = 2 * c + 1;  // this lane's D columns (tokens)
+    const float es0 = t0 < p.T ? es_s[t0] : 0.f, es1 = t1 < p.T ? es_s[t1] : 0.f;
+    const float fs = ldexpf(1.f, -2 * e0);  // S 4^(4-e) with S = s / 2^6 and e = e0 + 1
+    const uint4* src = p.dplanes + (((int64_t)e0 * p.n_rt32 + rt) * p.kblocks) * 32 + lane;
+    const __half* xr = x16 + (size_t)tg * p.xs_stride + 2 * c;
+    uint4* my = ring + lane;  // this lane's slots: my[s * 32]
+#pragma unroll
+    for (int i = 0; i < kD2Ring - 1; ++i) {
+        cp_async16(my + i * 32, src + (int64_t)(kw0 + i) * 32, kw0 + i < kw1);
+        cp_commit();
+    }
+    float D[2][4];
+#pragma unroll
+    for (int rg = 0; rg < 2; ++rg) D[rg][0] = D[rg][1] = D[rg][2] = D[rg][3] = 0.f;
+    float xg0 = 0.f, xg1 = 0.f;
+    int grp = 0;  // local group index into gcs
+    const int kpg = p.single_group ? (1 << 30) : (int)(p.gs / kKBlock);  // k-blocks per group
+#pragma unroll 1
+    for (int kb = kw0; kb < kw1; ++kb) {
+        const int it = kb - kw0;
+        cp_async16(my + ((it + kD2Ring - 1) % kD2Ring) * 32, src + (int64_t)(kb + kD2Ring - 1) * 32, kb + kD2Ring - 1 < kw1);
+        cp_commit();
+        cp_wait<kD2Ring - 1>();
+        const uint4 q = my[(it % kD2Ring) * 32];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int ss = 0; ss < 4; ++ss) {
+            const __half* xk = xr + (size_t)kb * kKBlock + 16 * ss;
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xk);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xk + 8);
+#pragma unroll
+            for (int rg = 0; rg < 2; ++rg) {
+                const uint32_t W = w[rg * 2 + ss / 2];
+                const int i0 = (ss & 1) * 4;
+                mma_f16_acc(D[rg], frag(W, i0), frag(W, i0 + 1), frag(W, i0 + 2), frag(W, i0 + 3), b0, b1);
+            }
+        }
+        xg0 += t0 < p.T ? xsum[t0 * p.kblocks + kb] : 0.f;
+        xg1 += t1 < p.T ? xsum[t1 * p.kblocks + kb] : 0.f;
+        const bool grp_end = kb + 1 == kw1 || (kb + 1) % kpg == 0;
+        if (grp_end) {
+#pragma unroll
+            for (int rg = 0; rg < 2; ++rg) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {  // rows g and g+8 of the row group
+                    const float2 sc = gcs[grp * 32 + 16 * rg + g + 8 * h];
+                    const float m0 = sc.x * fs * es0, m1 = sc.x * fs * es1;
+                    ys[rg][2 * h] = fmaf(D[rg][2 * h] - 1024.f * xg0, m0, ys[rg][2 * h]);
+                    ys[rg][2 * h + 1] = fmaf(D[rg][2 * h + 1] - 1024.f * xg1, m1, ys[rg][2 * h + 1]);
+                    if (with_const) {
+                        A[rg][2 * h] = fmaf(sc.x, xg0 * es0, A[rg][2 * h]);
+                        A[rg][2 * h + 1] = fmaf(sc.x, xg1 * es1, A[rg][2 * h + 1]);
+                        B[rg][2 * h] = fmaf(sc.y, xg0 * es0, B[rg][2 * h]);
+                        B[rg][2 * h + 1] = fmaf(sc.y, xg1 * es1, B[rg][2 * h + 1]);
+                    }
+                }
+                D[rg][0] = D[rg][1] = D[rg][2] = D[rg][3] = 0.f;
+            }
+            xg0 = xg1 = 0.f;
+            ++grp;
+        }
+    }
+    cp_wait<0>();
+}
+
+__global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __grid_constant__ D2Params p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __half* x16 = reinterpret_cast<__half*>(smem);                                   // [kD2MaxT + 1][xs_stride]
+    float* xsum = reinterpret_cast<float*>(smem + (size_t)(kD2MaxT + 1) * p.xs_stride * 2);  // [T][kblocks]
+    float* red = reinterpret_cast<float*>(smem);  // [warps][kD2Acc][32], aliases x16 after the passes
+    __shared__ float es_s[kD2Warps][kD2MaxT];
+    __shared__ float s_score[kD2MaxT][MOBI_MAX_SLICES - 1];
+    __shared__ int s_mask[kD2MaxT];
+    const int tid = threadIdx.x, warp = warp_idx_uniform(), lane = tid & 31;
+    float2* gcs = reinterpret_cast<float2*>(smem + p.gcs_off) + (size_t)warp * p.gpw * 32;  // [groups][32 rows]
+    uint4* ring = reinterpret_cast<uint4*>(smem + p.ring_off) + (size_t)warp * kD2Ring * 32;   // [slots][32 lanes]
+    const int rt = blockIdx.x;
+    auto TRM = [&](int i) {
+        if (p.trace && tid == 0) p.trace[(size_t)(2048 + rt) * 8 + i] = gtimer2();
+    };
+    TRM(0);
+    const int T = p.T;
+    const int kw0 = (int)((int64_t)warp * p.kblocks / kD2Warps), kw1 = (int)((int64_t)(warp + 1) * p.kblocks / kD2Warps);
+
+    // (1) this warp's k range of X: bf16 -> per-token 2^-e scale (max over the range) -> fp16 in smem,
+    //     and per-(token, k-block) sums of the fp16 values
+    constexpr int XV = 2;  // 16-byte vectors per lane per token held in registers (k range <= 512)
+    const int64_t k_lo = (int64_t)kw0 * kKBlock, k_hi = (int64_t)kw1 * kKBlock;
+    uint4 xv[kD2MaxT][XV];  // every token's first vectors in flight at once
+#pragma unroll
+    for (int t = 0; t < kD2MaxT; ++t)
+#pragma unroll
+        for (int j = 0; j < XV; ++j) {
+            const int64_t k = k_lo + lane * 8 + 256 * j;
+            xv[t][j] = (t < T && k < k_hi && k < p.in)
+                           ? __ldg(reinterpret_cast<const uint4*>(p.x + (int64_t)t * p.in + k)) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+    for (int t = 0; t < kD2MaxT; ++t) {
+        if (t >= T) break;
+        const __nv_bfloat16* xt = p.x + (int64_t)t * p.in;
+        float m = 0.f;
+        auto vmax = [&](const uint4& q) {
+            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f2 = __bfloat1622float2(b[j]);
+                m = fmaxf(m, fmaxf(fabsf(f2.x), fabsf(f2.y)));
+            }
+        };
+#pragma unroll
+        for (int j = 0; j < XV; ++j) vmax(xv[t][j]);
+        for (int64_t k = k_lo + lane * 8 + 256 * XV; k < k_hi && k < p.in; k += 256)
+            vmax(__ldg(reinterpret_cast<const uint4*>(xt + k)));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        int e = 0;
+        if (m > 0.f && isfinite(m)) e = ilogbf(m) - 14;
+        const float sc = ldexpf(1.f, -e);
+        if (lane == 0) es_s[warp][t] = ldexpf(1.f, e);
+        auto conv = [&](const uint4& q) {
+            uint4 o;
+            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+            __half2* hh = reinterpret_cast<__half2*>(&o);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f2 = __bfloat1622float2(b[j]);
+                hh[j] = __floats2half2_rn(f2.x * sc, f2.y * sc);
+            }
+            return o;
+        };
+        // store fp16 and sum each k-block's 64 fp16 values: 8 lanes x 8 values, fixed butterfly
+        auto store_sum = [&](int64_t k, const uint4& q) {
+            const uint4 o = conv(q);
+            const __half2* hh = reinterpret_cast<const __half2*>(&o);
+            float sacc = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f2 = __half22float2(hh[j]);
+                sacc += f2.x + f2.y;
+            }
+            sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+            sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+            sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
+            if (k < k_hi) {
+                *reinterpret_cast<uint4*>(x16 + (size_t)t * p.xs_stride + k) = o;
+                if ((lane & 7) == 0) xsum[t * p.kblocks + k / kKBlock] = sacc;
+            }
+        };
+#pragma unroll
+        for (int j = 0; j < XV; ++j) store_sum(k_lo + lane * 8 + 256 * j, xv[t][j]);
+        for (int64_t k0 = k_lo + 256 * XV; k0 < k_hi; k0 += 256) {  // warp-uniform trip count
+            const int64_t k = k0 + lane * 8;
+            const uint4 q = (k < k_hi && k < p.in) ? __ldg(reinterpret_cast<const uint4*>(xt + k)) : make_uint4(0, 0, 0, 0);
+            store_sum(k, q);
+        }
+    }
+    for (int64_t k = (int64_t)kw0 * kKBlock + lane * 8; k < (int64_t)kw1 * kKBlock; k += 256)
+        *reinterpret_cast<uint4*>(x16 + (size_t)kD2MaxT * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+
+    {   // the group constants (s, s*z) of this warp's groups for the tile's 32 rows, read once for all slices
+        const int64_t g0 = p.single_group ? 0 : (int64_t)kw0 * kKBlock / p.gs;
+        const int64_t g1 = p.single_group ? 1 : ((int64_t)kw1 * kKBlock + p.gs - 1) / p.gs;
+        for (int i = lane; i < (int)(g1 - g0) * 32; i += 32)
+            gcs[i] = __ldg(p.gconst + (g0 + i / 32) * p.out_pad + (int64_t)rt * 32 + i % 32);
+    }
+    __syncwarp();
+    // yt: this lane's outputs (rows g/g+8 of both row groups, tokens 2c/2c+1) over the slices each
+    // token uses; ys: one slice pass
+    float yt[2][4], ys[2][4], A[2][4], B[2][4];
+#pragma unroll
+    for (int rg = 0; rg < 2; ++rg)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) yt[rg][j] = ys[rg][j] = A[rg][j] = B[rg][j] = 0.f;
+    TRM(1);
+    // (2) slice 1 is always on: stream it while the router may still be running
+    slice_pass(p, 0, rt, kw0, kw1, x16, xsum, es_s[warp], gcs, ring, lane, true, yt, A, B);
+    TRM(2);
+    // (3) slice masks: gate_hard(delta) on S = sum over hidden tiles + b2 (router.hpp:92-103)
+    grid_dep_wait2();
+    TRM(3);
+    if (p.masks) {
+        if (tid < T) s_mask[tid] = (p.masks[tid] & p.vmask) | 1;
+    } else {
+        for (int i = warp; i < T * p.nr; i += kD2Warps) {
+            const int t = i / p.nr, k = i % p.nr;
+            float sc = 0.f;
+            for (int q = lane; q < p.n_mt; q += 32) sc += __ldcg(p.spart + ((int64_t)q * T + t) * p.nr + k);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+            if (lane == 0) s_score[t][k] = sc + __ldg(p.b2 + k);
+        }
+        __syncthreads();
+        if (tid < T) {
+            int m = 1;
+            for (int k = 0; k < p.nr; ++k) {
+                if ((s_score[tid][k] - p.delta) > 0.f) m |= 1 << (k + 1);
+                if (rt == 0 && p.scores_out) p.scores_out[tid * p.nr + k] = s_score[tid][k];
+            }
+            s_mask[tid] = m;
+            if (rt == 0) {
+                p.masks_dev[tid] = (uint8_t)m;
+                if (p.masks_out) p.masks_out[tid] = (uint8_t)m;
+            }
+        }
+    }
+    __syncthreads();
+    int uni = 0;
+    for (int t = 0; t < T; ++t) uni |= s_mask[t];
+    // (4) the other slices of the batch's union only; a slice's partials go to the tokens that use it
+    const int mt0 = 2 * (lane & 3) < T ? s_mask[2 * (lane & 3)] : 0, mt1 = 2 * (lane & 3) + 1 < T ? s_mask[2 * (lane & 3) + 1] : 0;
+    for (int e0 = 1; e0 < p.E; ++e0) {
+        if (!(uni >> e0 & 1)) continue;
+#pragma unroll
+        for (int rg = 0; rg < 2; ++rg)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ys[rg][j] = 0.f;
+        slice_pass(p, e0, rt, kw0, kw1, x16, xsum, es_s[warp], gcs, ring, lane, false, ys, A, B);
+        const bool u0 = mt0 >> e0 & 1, u1 = mt1 >> e0 & 1;
+#pragma unroll
+        for (int rg = 0; rg < 2; ++rg) {
+            if (u0) yt[rg][0] += ys[rg][0], yt[rg][2] += ys[rg][2];
+            if (u1) yt[rg][1] += ys[rg][1], yt[rg][3] += ys[rg][3];
+        }
+    }
+    TRM(4);
+    __syncthreads();  // x16 is dead: the reduction buffer aliases it
+
+    // (5) warps' partials -> smem, then each (row, token) combines its slices in warp order
+    {
+        float* r = red + (size_t)warp * kD2Acc * 32 + lane;
+        int i = 0;
+#pragma unroll
+        for (int rg = 0; rg < 2; ++rg)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                r[(i++) * 32] = yt[rg][j];
+                r[(i++) * 32] = A[rg][j];
+                r[(i++) * 32] = B[rg][j];
+            }
+    }
+    __syncthreads();
+    if (tid < 32 * kD2MaxT) {
+        const int rl = tid % 32, t = tid / 32;
+        const int64_t row = (int64_t)rt * 32 + rl;
+        if (t < T && row < p.out) {
+            const int rg = rl / 16, rr = rl % 16, g = rr % 8, hi = rr / 8;
+            const int ln = g * 4 + t / 2, j = hi * 2 + (t & 1);
+            const int base = (rg * 4 + j) * 3;
+            const float kc = p.mt.kc[s_mask[t]];
+            float acc = 0.f;
+            for (int w = 0; w < kD2Warps; ++w) {
+                const float* r = red + (size_t)w * kD2Acc * 32 + ln;
+                acc += r[(base + 0) * 32] + (kc * r[(base + 1) * 32] - r[(base + 2) * 32]);
+            }
+            p.y[(int64_t)t * p.out + row] = __float2bfloat16_rn(acc);
+        }
+    }
+    TRM(5);
+}
+
+}  // namespace
+
+int d2_groups_per_warp(const mobi_layer* L) {
+    if (L->single_group) return 1;
+    const int64_t kpw = cdiv(L->kblocks, (int64_t)kD2Warps) * kKBlock;  // k per warp (upper bound)
+    return (int)(kpw / L->gs + 2);
+}
+
+bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
+    if (T < 1 || T > kD2MaxT || !L->dplanes || L->E > 4) return false;
+    if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
+    if (!L->single_group && L->gs % kKBlock != 0) return false;
+    const size_t xs = (size_t)(kD2MaxT + 1) * (L->in_pad + 8) * 2 + (size_t)kD2MaxT * L->kblocks * 4;
+    const size_t sm = (std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16 +
+                      (size_t)kD2Warps * d2_groups_per_warp(L) * 32 * 8 + (size_t)kD2Warps * kD2Ring * 32 * 16;
+    return sm <= 200 * 1024;
+}
+
+int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
+                         uint8_t* masks_out, float* scores_out, __nv_bfloat16* y, bool pdl, cudaStream_t st,
+                         unsigned long long* trace) {
+    D2Params p{};
+    p.trace = trace;
+    p.dplanes = reinterpret_cast<const uint4*>(L->dplanes);
+    p.gconst = L->gconst;
+    p.x = x;
+    p.masks = given_masks;
+    p.spart = L->dec_spart;
+    p.b2 = L->b2;
+    p.masks_dev = L->masks;
+    p.masks_out = masks_out;
+    p.scores_out = scores_out;
+    p.y = y;
+    p.mt = L->mtab;
+    p.out = L->out;
+    p.out_pad = L->out_pad;
+    p.in = L->in;
+    p.in_pad = L->in_pad;
+    p.kblocks = L->kblocks;
+    p.gs = L->gs;
+    p.delta = delta;
+    p.single_group = L->single_group ? 1 : 0;
+    p.T = (int)T;
+    p.E = L->E;
+    p.nr = L->nr;
+    p.n_mt = (int)(L->h_pad / 16);
+    p.vmask = (1 << (L->nr + 1)) - 1;
+    p.n_rt32 = (int)(L->out_pad / 32);
+    p.xs_stride = (int)(L->in_pad + 8);
+    const size_t xs = (size_t)(kD2MaxT + 1) * p.xs_stride * 2 + (size_t)kD2MaxT * L->kblocks * 4;
+    p.gpw = d2_groups_per_warp(L);
+    p.gcs_off = (int64_t)((std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16);
+    p.ring_off = p.gcs_off + (int64_t)kD2Warps * p.gpw * 32 * 8;
+    const size_t smem = (size_t)p.ring_off + (size_t)kD2Warps * kD2Ring * 32 * 16;
+    static bool attr = false;
+    if (!attr) {
+        MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)cdiv(L->out, 32));
+    cfg.blockDim = dim3(kD2Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_planes_kernel, p));
+    ++L->last_launches;
+    return MOBI_OK;
+}
+
+}  // namespace mobi

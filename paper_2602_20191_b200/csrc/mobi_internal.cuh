@@ -85,6 +85,7 @@ struct mobi_layer {
 
     // device weights
     uint8_t* codes8 = nullptr;        // tiled merged codes [out_pad/128][kblocks][8192]
+    uint8_t* dplanes = nullptr;       // decode slice planes [E][out_pad/32][kblocks][32 lanes][16 B] (2-bit slices)
     float2* gconst = nullptr;         // [G][out_pad] (s, s*z) per group: coalesced across rows
     __nv_bfloat16* w1t = nullptr;     // [h_pad][in_pad] bf16, K-major (router B operand)
     float* b1 = nullptr;              // [h_pad]
@@ -154,6 +155,12 @@ int set_error(int code, const std::string& msg);
 
 // ---- launchers (each returns MOBI_OK or an error code; each counts its launches) ----
 // layer.cu
+int launch_pack_dplanes(mobi_layer* L, cudaStream_t st);
+// decode2.cu
+bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T);
+int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
+                         uint8_t* masks_out, float* scores_out, __nv_bfloat16* y, bool pdl, cudaStream_t st,
+                         unsigned long long* trace = nullptr);
 int check_codes_device(const uint8_t* codes_dev, int64_t n, int qmax, int64_t* bad);
 int launch_pack_codes(mobi_layer* L, const uint8_t* codes_dev, cudaStream_t st);
 int launch_pack_planes(mobi_layer* L, const uint64_t* planes_dev, int bits, int64_t wpr,

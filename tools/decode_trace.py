@@ -20,7 +20,19 @@ def main():
     for _ in range(5):
         layer.forward(x, delta)
     set_debug_impl(9)
-    layer.forward(x, delta)
+    # replay from a CUDA graph, as bench.py does at decode sizes: the PDL edge only overlaps the two
+    # kernels when the dependent launch is already queued on the device
+    y = torch.empty((x.shape[0], layer.out), dtype=torch.bfloat16, device=dev)
+    layer.forward(x, delta, y=y)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            layer.forward(x, delta, y=y)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g.replay()
     torch.cuda.synchronize()
     set_debug_impl(0)
     full = np.zeros(32 * 1024, np.uint64)
@@ -46,6 +58,7 @@ def main():
         if ok.any():
             print("gemm SM clock (GHz, median over CTAs):", float(np.median(cyc[ok] / ns[ok])))
     show("gemm", g, ["start", "x prep done", "grid dep resolved", "main loop done", "end"])
+    show("planes", g, ["start", "x prep done", "slice 1 done", "grid dep resolved", "union slices done", "end"])
     ft = full.astype(np.int64)[24576:24576 + 4 * 64].reshape(4, 64)
     for c in range(2):
         print(f"cta {c} warp7 full-wait start:", [int(v - t0) if v else -1 for v in ft[c, :16]])
