@@ -30,17 +30,22 @@ namespace {
 
 using namespace sm100;
 
-constexpr int NSTAGE = 8;
+#ifndef MOBI_TMA_CODES
+#define MOBI_TMA_CODES 0  // 1: a codes warp stages each k-block's codes + group constants in smem
+#endif
+constexpr int NSTAGE = MOBI_TMA_CODES ? 6 : 8;
 constexpr int kDqWarps = 16;
-constexpr int kThreads = 32 * (2 + kDqWarps + 4);
+constexpr int kThreads = 32 * (2 + kDqWarps + 4 + (MOBI_TMA_CODES ? 1 : 0));
 constexpr int kWarpDq0 = 0, kWarpEpi0 = kDqWarps, kWarpTma = kDqWarps + 4, kWarpMma = kDqWarps + 5;
+constexpr int kWarpCodes = kDqWarps + 6;  // MOBI_TMA_CODES: streams the codes + constants of each stage
 constexpr int kHalfRows = kTokTile / 2;                  // token rows per CTA per stage
 constexpr int kStageBytes = kHalfRows * kKBlock * 2;     // 16 KiB
 constexpr int kBoxRows = 16;
 constexpr int kBoxBytes = kBoxRows * kKBlock * 2;        // 2 KiB
 constexpr int kACol0 = 256;
 constexpr int kYStageBytes = kTokTile * kRowTile * 2;    // 64 KiB
-constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 + 512 + kYStageBytes + kTokTile * 4;
+constexpr int kCodeStage = MOBI_TMA_CODES ? kBlockBytes + 2 * kRowTile * 8 : 0;  // codes + 2 groups' (s, s*z)
+constexpr int kSmemBytes = NSTAGE * (kStageBytes + kCodeStage) + 1024 + 512 + kYStageBytes + kTokTile * 4;
 constexpr int kBigBoxRows = kHalfRows;  // one TMA box per full half-tile
 
 struct Params {
@@ -83,7 +88,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stage_b = smem;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * kStageBytes);
+    uint8_t* stage_c = smem + NSTAGE * kStageBytes;  // [NSTAGE][codes 8 KiB | (s, s*z) of 2 groups x 128 rows]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * (kStageBytes + kCodeStage));
     // one full barrier per stage, in the leader: both halves' TMA bytes (one expect_tx arrival) and the
     // 8 + 8 dequant warps of the pair (the peer's arrive remotely)
     uint64_t* full_b = bars;                 // [NSTAGE] leader: stage complete (A in both TMEMs, B in both smems)
@@ -91,8 +97,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* acc_full = bars + 3 * NSTAGE;  // each CTA
     uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1 + NSTAGE);
-    __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 512);
-    int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);
+    uint64_t* codes_full = bars + NSTAGE;    // [NSTAGE] each CTA: its codes + constants of the stage landed
+    __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * (kStageBytes + kCodeStage) + 512);
+    int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * (kStageBytes + kCodeStage) + 512 + kYStageBytes);
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
 
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
@@ -101,6 +108,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1 + kDqWarps);  // TMA expect_tx + 8 dequant warps per CTA x 2
             mbar_init(&empty[s], 1);
+            mbar_init(&codes_full[s], 1);
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 8);  // 4 epilogue warps x 2 CTAs
@@ -154,6 +162,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < nbox; ++j)
                             tma_load_2d_2sm(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, full_b_leader + s * 8,
                                             0, (int)(kb * p.tpad) + row_half + j * kBoxRows);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (MOBI_TMA_CODES && warp == kWarpCodes) {
+        // ---------------- codes producer: this CTA's code block + group constants per stage ----------------
+        uint32_t it = 0;
+        for (int pair = cid; pair < total; pair += ncl) {
+            TokTile tt;
+            int rt, nc;
+            tile_of(pair, tt, rt, nc);
+            for (int kb = 0; kb < kb_n; ++kb, ++it) {
+                const int s = it % NSTAGE;
+                mbar_wait(&empty[s], ((it / NSTAGE) & 1) ^ 1);
+                if (elect_one_sync()) {
+                    uint8_t* dc = stage_c + s * kCodeStage;
+                    const int64_t g0 = p.single_group ? 0 : ((int64_t)kb * kKBlock) / p.gs;
+                    const int64_t g1 = p.single_group ? 0 : ((int64_t)kb * kKBlock + 32) / p.gs;
+                    mbar_arrive_expect_tx(&codes_full[s], kCodeStage);
+                    bulk_g2s(dc, p.codes8 + ((int64_t)rt * p.kblocks + kb) * kBlockBytes, kBlockBytes, &codes_full[s]);
+                    bulk_g2s(dc + kBlockBytes, p.gconst + g0 * p.out_pad + (int64_t)rt * kRowTile, kRowTile * 8,
+                             &codes_full[s]);
+                    bulk_g2s(dc + kBlockBytes + kRowTile * 8, p.gconst + g1 * p.out_pad + (int64_t)rt * kRowTile,
+                             kRowTile * 8, &codes_full[s]);
                 }
                 __syncwarp();
             }
@@ -241,6 +273,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) dequant4(w1[u], mw, S2, C2, v[8 + 2 * u], v[8 + 2 * u + 1]);
             };
+#if MOBI_TMA_CODES
+            // codes and constants arrive in the stage's smem with the B tile: no register prefetch ring
+            uint32_t v[16];
+            for (int kb = par; kb < kb_n; kb += 2) {
+                const uint32_t itk = base + kb;
+                const int s = itk % NSTAGE;
+                const uint32_t ph = (itk / NSTAGE) & 1;
+                mbar_wait(&codes_full[s], ph);  // (issued after empty[s]: the A stage is free too)
+                if (warp == 0 || warp == 4) EV(4, kb, base);
+                const uint8_t* dc = stage_c + s * kCodeStage;
+                const uint4 c0 = *reinterpret_cast<const uint4*>(dc + ((hh * 2) * kRowTile + 32 * q + lane) * 16);
+                const uint4 c1 = *reinterpret_cast<const uint4*>(dc + ((hh * 2 + 1) * kRowTile + 32 * q + lane) * 16);
+                const float2 gc = reinterpret_cast<const float2*>(dc + kBlockBytes)[hh * kRowTile + 32 * q + lane];
+                dq(c0, c1, gc, v);
+                tc_fence_after();
+                tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (warp == 0 || warp == 4) EV(5, kb, base);
+                if (lane == 0) {
+                    if (rank == 0)
+                        mbar_arrive_relaxed(&full_b[s]);
+                    else
+                        mbar_arrive_relaxed_cluster(full_leader + s * 8);
+                }
+            }
+            (void)ld;
+            (void)ldc;
+            (void)rv;
+#else
             // Ring of three static slots (codes + group constants), unrolled so a slot is refilled
             // right after it was consumed and each load has two iterations of lead time; no
             // register moves touch a pending load.
@@ -302,6 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (!step(kb + 2, c10, c11, g1, c20, c21, g2)) break;
                 if (!step(kb + 4, c20, c21, g2, c00, c01, g0)) break;
             }
+#endif
         }
     } else {
         // ---------------- epilogue ----------------

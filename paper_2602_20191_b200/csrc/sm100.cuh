@@ -126,6 +126,13 @@ __device__ __forceinline__ void mbar_wait_relaxed(uint64_t* bar, uint32_t parity
         "r"(parity)
         : "memory");
 }
+// 1-D bulk copy global -> this CTA's smem, completion (complete_tx bytes) on a local mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 // 2-SM TMA: data lands in the issuing CTA's smem, complete_tx goes to the barrier at cluster
 // address `bar_cluster` (the leader CTA's)
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
