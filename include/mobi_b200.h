@@ -90,6 +90,13 @@ MOBI_API int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_lay
  * no host staging.  Every other descriptor array stays on the host.  No reference counterpart: it is
  * the device-resident ingest for model-scale stacks (hundreds of matrices). */
 MOBI_API int mobi_layer_create_device(const mobi_layer_desc* desc, int device, mobi_layer_t* out);
+/* Column-parallel shard: a layer holding weight rows [row0, row1) of `desc` (every slice or
+ * bit-plane and the rows' group parameters -- groups never span rows, qcore.hpp:30-34) and the full
+ * router, so every rank decides the same masks.  Rank p of P creates rows [p*ceil(out/P), ...) and
+ * all-gathers the [T, row1-row0] outputs (NCCL) into [T, out]; the shards' outputs are bit-identical
+ * to the corresponding columns of the unsharded layer's.  No reference counterpart (single process). */
+MOBI_API int mobi_layer_create_rows(const mobi_layer_desc* desc, int64_t row0, int64_t row1, int device,
+                                    mobi_layer_t* out);
 MOBI_API int mobi_layer_destroy(mobi_layer_t layer);
 /* Pre-size the internal workspace for up to max_tokens tokens (avoids allocation inside
  * forward, required before stream capture into a CUDA graph). */

@@ -49,8 +49,18 @@ inline double from_bf16(uint16_t b) {
 // Device-resident MoBi layer built from the reference's SliceStack + RouterState.
 class Layer {
 public:
+    // Column-parallel shard: weight rows [row0, row1) of the stack (and their group parameters), full router.
     template <class SliceStack, class RouterState>
-    Layer(const SliceStack& st, const RouterState& rs, int device = 0) : device_(device) {
+    Layer(const SliceStack& st, const RouterState& rs, int device, int64_t row0, int64_t row1)
+        : Layer(st, rs, device, row0, row1, 0) {}
+
+    template <class SliceStack, class RouterState>
+    Layer(const SliceStack& st, const RouterState& rs, int device = 0) : Layer(st, rs, device, -1, -1, 0) {}
+
+private:
+    template <class SliceStack, class RouterState>
+    Layer(const SliceStack& st, const RouterState& rs, int device, int64_t row0, int64_t row1, int)
+        : device_(device) {
         mobi_layer_desc d{};
         d.out = static_cast<int64_t>(st.rows());
         d.in = static_cast<int64_t>(st.cols());
@@ -69,13 +79,20 @@ public:
         d.b1 = rs.b1.data();
         d.w2 = rs.w2.data();
         d.b2 = rs.b2.data();
-        check(mobi_layer_create(&d, device, &h_));
+        if (row0 >= 0) {
+            check(mobi_layer_create_rows(&d, row0, row1, device, &h_));
+            d.out = row1 - row0;
+        } else {
+            check(mobi_layer_create(&d, device, &h_));
+        }
         out_ = d.out;
         in_ = d.in;
         nr_ = d.n_slices - 1;
         codes_.clear();
         codes_.shrink_to_fit();
     }
+
+public:
     ~Layer() { mobi_layer_destroy(h_); }
     Layer(const Layer&) = delete;
     Layer& operator=(const Layer&) = delete;

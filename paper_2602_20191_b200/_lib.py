@@ -38,6 +38,7 @@ class LayerDesc(C.Structure):
 _SIGS = {
     "mobi_layer_create": [C.POINTER(LayerDesc), C.c_int, C.POINTER(_p)],
     "mobi_layer_create_device": [C.POINTER(LayerDesc), C.c_int, C.POINTER(_p)],
+    "mobi_layer_create_rows": [C.POINTER(LayerDesc), _i64, _i64, C.c_int, C.POINTER(_p)],
     "mobi_layer_destroy": [_p],
     "mobi_layer_reserve": [_p, _i64],
     "mobi_layer_info": [_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i32), C.POINTER(_i64), C.POINTER(_i64)],

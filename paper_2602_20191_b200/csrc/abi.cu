@@ -476,6 +476,42 @@ int mobi_layer_create(const mobi_layer_desc* desc, int device, mobi_layer_t* out
     return create_impl(desc, device, out, false);
 }
 
+int mobi_layer_create_rows(const mobi_layer_desc* desc, int64_t row0, int64_t row1, int device, mobi_layer_t* out) {
+    CHECK_ARG(desc != nullptr && out != nullptr, "mobi_layer_create_rows: null argument");
+    CHECK_ARG(0 <= row0 && row0 < row1 && row1 <= desc->out,
+              "mobi_layer_create_rows: rows [" << row0 << "," << row1 << ") outside [0," << desc->out << ")");
+    CHECK_ARG(desc->group_size >= 1 && desc->scale && desc->zero, "QuantParams: missing scales/zeros");
+    CHECK_ARG((desc->codes != nullptr) != (desc->planes != nullptr),
+              "mobi_layer_create: give exactly one of codes (SliceStack) or planes (LayerRecord)");
+    // column-parallel shard: rows [row0, row1) of every slice and their groups (groups never span rows,
+    // qcore.hpp:30-34); the router is the full one (replicated on every rank)
+    const int64_t n = row1 - row0, G = cdiv(desc->in, desc->group_size);
+    mobi_layer_desc d = *desc;
+    d.out = n;
+    std::vector<double> sc(desc->scale + row0 * G, desc->scale + row1 * G), ze(desc->zero + row0 * G, desc->zero + row1 * G);
+    d.scale = sc.data();
+    d.zero = ze.data();
+    std::vector<uint8_t> codes;
+    std::vector<uint64_t> planes;
+    if (desc->codes) {
+        CHECK_ARG(desc->n_slices >= 1, "mobi_layer_create: bad slice count");
+        codes.resize((size_t)(desc->n_slices * n * desc->in));
+        for (int e = 0; e < desc->n_slices; ++e)
+            std::memcpy(codes.data() + (size_t)e * n * desc->in, desc->codes + ((int64_t)e * desc->out + row0) * desc->in,
+                        (size_t)(n * desc->in));
+        d.codes = codes.data();
+    } else {
+        CHECK_ARG(desc->plane_bits >= 1 && desc->words_per_row >= 1, "bitplane: bad plane geometry");
+        planes.resize((size_t)(desc->plane_bits * n * desc->words_per_row));
+        for (int b = 0; b < desc->plane_bits; ++b)
+            std::memcpy(planes.data() + (size_t)b * n * desc->words_per_row,
+                        desc->planes + ((int64_t)b * desc->out + row0) * desc->words_per_row,
+                        (size_t)(n * desc->words_per_row) * 8);
+        d.planes = planes.data();
+    }
+    return create_impl(&d, device, out, false);
+}
+
 int mobi_layer_create_device(const mobi_layer_desc* desc, int device, mobi_layer_t* out) {
     CHECK_ARG(desc && desc->codes && !desc->planes, "mobi_layer_create_device: give device slice codes");
     return create_impl(desc, device, out, true);

@@ -89,7 +89,18 @@ class MobiLayer:
                            None, planes, rec.plane_bits, planes.shape[2], rec.w1, rec.b1, rec.w2, rec.b2, device)
 
     @classmethod
-    def _create(cls, out, inn, gs, slice_bits, scale, zero, codes, planes, plane_bits, wpr, w1, b1, w2, b2, device):
+    def from_stack_rows(cls, codes, slice_bits, scale, zero, group_size, w1, b1, w2, b2, row0: int, row1: int,
+                        device: int = 0):
+        """Column-parallel shard: weight rows [row0, row1) of the SliceStack + the full router
+        (mobi_layer_create_rows)."""
+        codes = _arr(codes, np.uint8)
+        E, out, inn = codes.shape
+        return cls._create(out, inn, group_size, slice_bits, scale, zero, codes, None, 0, 0, w1, b1, w2, b2, device,
+                           rows=(row0, row1))
+
+    @classmethod
+    def _create(cls, out, inn, gs, slice_bits, scale, zero, codes, planes, plane_bits, wpr, w1, b1, w2, b2, device,
+                rows=None):
         sb = _arr(slice_bits, np.int32)
         dev_codes = isinstance(codes, torch.Tensor)
         scale, zero = _arr(scale, np.float64), _arr(zero, np.float64)
@@ -106,6 +117,9 @@ class MobiLayer:
                       router_hidden=w1.shape[1], w1=_ptr(w1, _f64), b1=_ptr(b1, _f64), w2=_ptr(w2, _f64),
                       b2=_ptr(b2, _f64))
         h = C.c_void_p()
+        if rows is not None:
+            check(lib().mobi_layer_create_rows(C.byref(d), rows[0], rows[1], device, C.byref(h)))
+            return cls(h.value, sb.tolist(), rows[1] - rows[0], inn, w1.shape[1], device)
         create = lib().mobi_layer_create_device if dev_codes else lib().mobi_layer_create
         check(create(C.byref(d), device, C.byref(h)))
         return cls(h.value, sb.tolist(), out, inn, w1.shape[1], device)

@@ -81,8 +81,8 @@ class ColumnParallelMobiLayer:
         self.r0, self.r1 = ranges[rank]
         if self.r1 <= self.r0:
             raise ValueError(f"column-parallel: rank {rank} of {world} owns no rows of {self.out}")
-        c, s, z = shard_stack_rows(codes, scale, zero, group_size, self.r0, self.r1)
-        self.local = MobiLayer.from_stack(c, slice_bits, s, z, group_size, w1, b1, w2, b2, device=device)
+        self.local = MobiLayer.from_stack_rows(codes, slice_bits, scale, zero, group_size, w1, b1, w2, b2,
+                                               self.r0, self.r1, device=device)
         self.rank, self.world, self.group = rank, world, group
 
     def reserve(self, max_tokens: int):

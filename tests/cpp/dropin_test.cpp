@@ -83,6 +83,18 @@ int run_case(size_t out, size_t in, size_t gs, size_t T, unsigned seed) {
         worst = std::max(worst, std::max(rel, rel2));
         EXPECT(rel <= 1e-2 && rel2 <= 1e-2, "token %zu rel-L2 %g / %g", t, rel, rel2);
     }
+    // column-parallel shards (mobi_layer_create_rows): two halves of the rows concatenate to the full
+    // layer's output bit-for-bit (same kernels, same per-row arithmetic)
+    if (out >= 64) {
+        const int64_t half = static_cast<int64_t>(out / 2);
+        mobi_b200::Layer s0(st, rs, 0, 0, half), s1(st, rs, 0, half, static_cast<int64_t>(out));
+        Matrix y0 = s0.forward_elastic(x, g_gpu), y1 = s1.forward_elastic(x, g_gpu);
+        for (size_t t = 0; t < T; ++t)
+            for (size_t r = 0; r < out; ++r) {
+                const double v = r < static_cast<size_t>(half) ? y0(t, r) : y1(t, r - half);
+                EXPECT(v == y_gpu(t, r), "shard output (%zu,%zu) %g != %g", t, r, v, y_gpu(t, r));
+            }
+    }
     // error behaviour mirrors MOBI_CHECK
     bool threw = false;
     try {

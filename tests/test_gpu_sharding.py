@@ -58,6 +58,23 @@ def test_column_shards_concat_equals_full(T, world):
         assert d <= 2e-2 * y_full.float().abs().max().item()
 
 
+def test_create_rows_equals_sliced_stack():
+    from paper_2602_20191_b200 import MobiInvalidArgument, MobiLayer, calibrate_threshold
+    from paper_2602_20191_b200.sharding import shard_stack_rows
+    L = O.synthetic_layer(600, 320, seed=12, group_size=64)
+    args = (L["slice_bits"], L["scale"], L["zero"], 64, L["w1"], L["b1"], L["w2"], L["b2"])
+    r0, r1 = 128, 472
+    a = MobiLayer.from_stack_rows(L["codes"], *args, r0, r1)
+    c, s, z = shard_stack_rows(L["codes"], L["scale"], L["zero"], 64, r0, r1)
+    b = MobiLayer.from_stack(c, L["slice_bits"], s, z, 64, L["w1"], L["b1"], L["w2"], L["b2"])
+    assert a.out == r1 - r0 and np.array_equal(a.unpack_codes(), b.unpack_codes())
+    xb, _ = make_x(200, 320, seed=3)
+    delta = calibrate_threshold(a.score(xb), 1 / 6)
+    assert torch.equal(a.forward(xb, delta), b.forward(xb, delta))
+    with pytest.raises(MobiInvalidArgument):
+        MobiLayer.from_stack_rows(L["codes"], *args, 500, 700)
+
+
 def test_column_parallel_layer_nccl_world1():
     import torch.distributed as dist
     from paper_2602_20191_b200 import calibrate_threshold
