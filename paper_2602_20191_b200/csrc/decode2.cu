@@ -24,7 +24,7 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kD2Warps = 8, kD2Threads = 32 * kD2Warps;
+constexpr int kD2Warps = 16, kD2Threads = 32 * kD2Warps;  // 16 warps: 4 per scheduler (latency hiding)
 constexpr int kD2MaxT = 4;
 constexpr int kD2Acc = 3 * 2 * 4;  // per lane: y over the token's slices, A, B  ([2][4] each)
 
@@ -75,81 +75,27 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kD2Ring = 8;  // k-blocks in flight per lane (16 B each)
+constexpr int kD2Ring = 8;  // (slice, k-block) items in flight per lane (16 B each): 64 KiB per CTA
 
-// One slice over the warp's k-blocks [kw0, kw1), folded per group into ys.  Each lane streams its own
-// 16-byte fragment words through a private cp.async ring (no cross-lane dependency, no barriers); the
-// code is a single compact loop -- an unrolled variant overflowed the instruction cache.  The
-// slice-independent constant sums A, B are accumulated on the first pass (with_const).
-__device__ __forceinline__ void slice_pass(const D2Params& p, int e0, int rt, int kw0, int kw1, const __half* x16,
-                                        const float* xsum, const float* es_s, const float2* gcs, uint4* ring,
-                                        int lane, bool with_const, float (&ys)[2][4], float (&A)[2][4],
-                                        float (&B)[2][4]) {
-    const int g = lane >> 2, c = lane & 3;
-    const int tg = g < p.T ? g : kD2MaxT;  // B-fragment token row (row kD2MaxT is zeros)
-    const int t0 = 2 * c, t1 = 2 * c + 1;  // this lane's D columns (tokens)
-    const float es0 = t0 < p.T ? es_s[t0] : 0.f, es1 = t1 < p.T ? es_s[t1] : 0.f;
-    const float fs = ldexpf(1.f, -2 * e0);  // S 4^(4-e) with S = s / 2^6 and e = e0 + 1
-    const uint4* src = p.dplanes + (((int64_t)e0 * p.n_rt32 + rt) * p.kblocks) * 32 + lane;
-    const __half* xr = x16 + (size_t)tg * p.xs_stride + 2 * c;
-    uint4* my = ring + lane;  // this lane's slots: my[s * 32]
-#pragma unroll
-    for (int i = 0; i < kD2Ring - 1; ++i) {
-        cp_async16(my + i * 32, src + (int64_t)(kw0 + i) * 32, kw0 + i < kw1);
-        cp_commit();
+// cp.async.wait_group with a runtime count (<= kD2Ring - 1)
+__device__ __forceinline__ void cp_wait_dyn(int n) {
+    switch (n) {
+        case 0: cp_wait<0>(); break;
+        case 1: cp_wait<1>(); break;
+        case 2: cp_wait<2>(); break;
+        case 3: cp_wait<3>(); break;
+        case 4: cp_wait<4>(); break;
+        case 5: cp_wait<5>(); break;
+        case 6: cp_wait<6>(); break;
+        case 7: cp_wait<7>(); break;
+        case 8: cp_wait<8>(); break;
+        case 9: cp_wait<9>(); break;
+        case 10: cp_wait<10>(); break;
+        case 11: cp_wait<11>(); break;
+        case 12: cp_wait<12>(); break;
+        case 13: cp_wait<13>(); break;
+        default: cp_wait<14>(); break;
     }
-    float D[2][4];
-#pragma unroll
-    for (int rg = 0; rg < 2; ++rg) D[rg][0] = D[rg][1] = D[rg][2] = D[rg][3] = 0.f;
-    float xg0 = 0.f, xg1 = 0.f;
-    int grp = 0;  // local group index into gcs
-    const int kpg = p.single_group ? (1 << 30) : (int)(p.gs / kKBlock);  // k-blocks per group
-#pragma unroll 1
-    for (int kb = kw0; kb < kw1; ++kb) {
-        const int it = kb - kw0;
-        cp_async16(my + ((it + kD2Ring - 1) % kD2Ring) * 32, src + (int64_t)(kb + kD2Ring - 1) * 32, kb + kD2Ring - 1 < kw1);
-        cp_commit();
-        cp_wait<kD2Ring - 1>();
-        const uint4 q = my[(it % kD2Ring) * 32];
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int ss = 0; ss < 4; ++ss) {
-            const __half* xk = xr + (size_t)kb * kKBlock + 16 * ss;
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xk);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xk + 8);
-#pragma unroll
-            for (int rg = 0; rg < 2; ++rg) {
-                const uint32_t W = w[rg * 2 + ss / 2];
-                const int i0 = (ss & 1) * 4;
-                mma_f16_acc(D[rg], frag(W, i0), frag(W, i0 + 1), frag(W, i0 + 2), frag(W, i0 + 3), b0, b1);
-            }
-        }
-        xg0 += t0 < p.T ? xsum[t0 * p.kblocks + kb] : 0.f;
-        xg1 += t1 < p.T ? xsum[t1 * p.kblocks + kb] : 0.f;
-        const bool grp_end = kb + 1 == kw1 || (kb + 1) % kpg == 0;
-        if (grp_end) {
-#pragma unroll
-            for (int rg = 0; rg < 2; ++rg) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {  // rows g and g+8 of the row group
-                    const float2 sc = gcs[grp * 32 + 16 * rg + g + 8 * h];
-                    const float m0 = sc.x * fs * es0, m1 = sc.x * fs * es1;
-                    ys[rg][2 * h] = fmaf(D[rg][2 * h] - 1024.f * xg0, m0, ys[rg][2 * h]);
-                    ys[rg][2 * h + 1] = fmaf(D[rg][2 * h + 1] - 1024.f * xg1, m1, ys[rg][2 * h + 1]);
-                    if (with_const) {
-                        A[rg][2 * h] = fmaf(sc.x, xg0 * es0, A[rg][2 * h]);
-                        A[rg][2 * h + 1] = fmaf(sc.x, xg1 * es1, A[rg][2 * h + 1]);
-                        B[rg][2 * h] = fmaf(sc.y, xg0 * es0, B[rg][2 * h]);
-                        B[rg][2 * h + 1] = fmaf(sc.y, xg1 * es1, B[rg][2 * h + 1]);
-                    }
-                }
-                D[rg][0] = D[rg][1] = D[rg][2] = D[rg][3] = 0.f;
-            }
-            xg0 = xg1 = 0.f;
-            ++grp;
-        }
-    }
-    cp_wait<0>();
 }
 
 __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __grid_constant__ D2Params p) {
@@ -170,6 +116,21 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
     TRM(0);
     const int T = p.T;
     const int kw0 = (int)((int64_t)warp * p.kblocks / kD2Warps), kw1 = (int)((int64_t)(warp + 1) * p.kblocks / kD2Warps);
+    // streamed items (see (2)-(4) below): item i = (slice slist[i / nk], k-block kw0 + i % nk); issued in
+    // order, one cp.async group each, into ring slot i % kD2Ring; slice 1's first items go out now so
+    // their latency hides behind the activation prologue
+    int pi = 0;
+    int slist[MOBI_MAX_SLICES] = {0, 0, 0, 0};  // the stream's slices: slice 1, then the union's others
+    int psi = 0, pkb = kw0;  // issue cursor: (slice index, k-block) of item pi
+    auto issue = [&](int i) {
+        const uint4* src = p.dplanes + (((int64_t)slist[psi] * p.n_rt32 + rt) * p.kblocks + pkb) * 32 + lane;
+        cp_async16(ring + (i % kD2Ring) * 32 + lane, src, true);
+        cp_commit();
+        if (++pkb == kw1) pkb = kw0, ++psi;
+    };
+    while (pi < kw1 - kw0 && pi < kD2Ring - 1) issue(pi++);
+    float xg0 = 0.f, xg1 = 0.f;
+    int grp = 0, gleft = 0;
 
     // (1) this warp's k range of X: bf16 -> per-token 2^-e scale (max over the range) -> fp16 in smem,
     //     and per-(token, k-block) sums of the fp16 values
@@ -256,63 +217,127 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
     }
     __syncwarp();
     // yt: this lane's outputs (rows g/g+8 of both row groups, tokens 2c/2c+1) over the slices each
-    // token uses; ys: one slice pass
-    float yt[2][4], ys[2][4], A[2][4], B[2][4];
+    // token uses; ys: the current slice's partials
+    float yt[2][4], ys[2][4], A[2][4], B[2][4], D[2][4];
 #pragma unroll
     for (int rg = 0; rg < 2; ++rg)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) yt[rg][j] = ys[rg][j] = A[rg][j] = B[rg][j] = 0.f;
+        for (int j = 0; j < 4; ++j) yt[rg][j] = ys[rg][j] = A[rg][j] = B[rg][j] = D[rg][j] = 0.f;
     TRM(1);
-    // (2) slice 1 is always on: stream it while the router may still be running
-    slice_pass(p, 0, rt, kw0, kw1, x16, xsum, es_s[warp], gcs, ring, lane, true, yt, A, B);
-    TRM(2);
-    // (3) slice masks: gate_hard(delta) on S = sum over hidden tiles + b2 (router.hpp:92-103)
-    grid_dep_wait2();
-    TRM(3);
-    if (p.masks) {
-        if (tid < T) s_mask[tid] = (p.masks[tid] & p.vmask) | 1;
-    } else {
-        for (int i = warp; i < T * p.nr; i += kD2Warps) {
-            const int t = i / p.nr, k = i % p.nr;
-            float sc = 0.f;
-            for (int q = lane; q < p.n_mt; q += 32) sc += __ldcg(p.spart + ((int64_t)q * T + t) * p.nr + k);
+    const int g = lane >> 2, c = lane & 3;
+    const int tg = g < T ? g : kD2MaxT;  // B-fragment token row (row kD2MaxT is zeros)
+    const int t0 = 2 * c, t1 = 2 * c + 1;  // this lane's D columns (tokens)
+    const float es0 = t0 < T ? es_s[warp][t0] : 0.f, es1 = t1 < T ? es_s[warp][t1] : 0.f;
+    const __half* xr = x16 + (size_t)tg * p.xs_stride + 2 * c;
+    const int kpg = p.single_group ? (1 << 30) : (int)(p.gs / kKBlock);  // k-blocks per group
+    // (2)-(4) one stream of (slice, k-block) items: slice 1's k-blocks (already in flight since the
+    // prologue), then -- once the masks are known -- those of every other slice in the batch's union
+    const int nk = kw1 - kw0;
+    int n_items = nk, uni = 1, mt0 = 0, mt1 = 0;
+    int csi = 0, ckb = kw0;  // consume cursor
+    for (int ci = 0;; ++ci) {
+        if (ci == nk) {
+            TRM(2);
+            // slice masks: gate_hard(delta) on S = sum over hidden tiles + b2 (router.hpp:92-103)
+            grid_dep_wait2();
+            TRM(3);
+            if (p.masks) {
+                if (tid < T) s_mask[tid] = (p.masks[tid] & p.vmask) | 1;
+            } else {
+                for (int i = warp; i < T * p.nr; i += kD2Warps) {
+                    const int t = i / p.nr, k = i % p.nr;
+                    float sc = 0.f;
+                    for (int q = lane; q < p.n_mt; q += 32) sc += __ldcg(p.spart + ((int64_t)q * T + t) * p.nr + k);
 #pragma unroll
-            for (int o = 16; o; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-            if (lane == 0) s_score[t][k] = sc + __ldg(p.b2 + k);
-        }
-        __syncthreads();
-        if (tid < T) {
-            int m = 1;
-            for (int k = 0; k < p.nr; ++k) {
-                if ((s_score[tid][k] - p.delta) > 0.f) m |= 1 << (k + 1);
-                if (rt == 0 && p.scores_out) p.scores_out[tid * p.nr + k] = s_score[tid][k];
+                    for (int o = 16; o; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+                    if (lane == 0) s_score[t][k] = sc + __ldg(p.b2 + k);
+                }
+                __syncthreads();
+                if (tid < T) {
+                    int m = 1;
+                    for (int k = 0; k < p.nr; ++k) {
+                        if ((s_score[tid][k] - p.delta) > 0.f) m |= 1 << (k + 1);
+                        if (rt == 0 && p.scores_out) p.scores_out[tid * p.nr + k] = s_score[tid][k];
+                    }
+                    s_mask[tid] = m;
+                    if (rt == 0) {
+                        p.masks_dev[tid] = (uint8_t)m;
+                        if (p.masks_out) p.masks_out[tid] = (uint8_t)m;
+                    }
+                }
             }
-            s_mask[tid] = m;
-            if (rt == 0) {
-                p.masks_dev[tid] = (uint8_t)m;
-                if (p.masks_out) p.masks_out[tid] = (uint8_t)m;
+            __syncthreads();
+            for (int t = 0; t < T; ++t) uni |= s_mask[t];
+            mt0 = t0 < T ? s_mask[t0] : 0;
+            mt1 = t1 < T ? s_mask[t1] : 0;
+            int ns = 1;
+            for (int e0 = 1; e0 < p.E; ++e0)
+                if (uni >> e0 & 1) slist[ns++] = e0;
+            n_items = nk * ns;
+            // burst: the union's first items
+            while (pi < n_items && pi <= ci + kD2Ring - 1) issue(pi++);
+        }
+        if (ci >= n_items) break;
+        const int si = csi, kb = ckb, e0 = slist[si];
+        if (++ckb == kw1) ckb = kw0, ++csi;
+        cp_wait_dyn(pi - 1 - ci);
+        const uint4 q = ring[(ci % kD2Ring) * 32 + lane];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int ss = 0; ss < 4; ++ss) {
+            const __half* xk = xr + (size_t)kb * kKBlock + 16 * ss;
+            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xk);
+            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xk + 8);
+#pragma unroll
+            for (int rg = 0; rg < 2; ++rg) {
+                const uint32_t W = w[rg * 2 + ss / 2];
+                const int i0 = (ss & 1) * 4;
+                mma_f16_acc(D[rg], frag(W, i0), frag(W, i0 + 1), frag(W, i0 + 2), frag(W, i0 + 3), b0, b1);
+            }
+        }
+        // refill: item ci + R - 1 goes into the slot just consumed (its data is in registers)
+        if (pi < n_items && pi <= ci + kD2Ring - 1) issue(pi++);
+        xg0 += t0 < T ? xsum[t0 * p.kblocks + kb] : 0.f;
+        xg1 += t1 < T ? xsum[t1 * p.kblocks + kb] : 0.f;
+        if (kb == kw0) {  // a slice starts: its group cursor
+            grp = 0;
+            gleft = p.single_group ? (1 << 30) : kpg - (kw0 % kpg);
+        }
+        const bool slice_end = kb + 1 == kw1;
+        if (slice_end || --gleft == 0) {
+            const float fs = ldexpf(1.f, -2 * e0);  // S 4^(4-e) with S = s / 2^6 and e = e0 + 1
+#pragma unroll
+            for (int rg = 0; rg < 2; ++rg) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {  // rows g and g+8 of the row group
+                    const float2 sc = gcs[grp * 32 + 16 * rg + g + 8 * h];
+                    const float m0 = sc.x * fs * es0, m1 = sc.x * fs * es1;
+                    ys[rg][2 * h] = fmaf(D[rg][2 * h] - 1024.f * xg0, m0, ys[rg][2 * h]);
+                    ys[rg][2 * h + 1] = fmaf(D[rg][2 * h + 1] - 1024.f * xg1, m1, ys[rg][2 * h + 1]);
+                    if (si == 0) {
+                        A[rg][2 * h] = fmaf(sc.x, xg0 * es0, A[rg][2 * h]);
+                        A[rg][2 * h + 1] = fmaf(sc.x, xg1 * es1, A[rg][2 * h + 1]);
+                        B[rg][2 * h] = fmaf(sc.y, xg0 * es0, B[rg][2 * h]);
+                        B[rg][2 * h + 1] = fmaf(sc.y, xg1 * es1, B[rg][2 * h + 1]);
+                    }
+                }
+                D[rg][0] = D[rg][1] = D[rg][2] = D[rg][3] = 0.f;
+            }
+            xg0 = xg1 = 0.f;
+            ++grp;
+            gleft = kpg;
+        }
+        if (slice_end) {  // the slice's partials go to the tokens that use it (slice 1: every token)
+            const bool u0 = si == 0 || (mt0 >> e0 & 1), u1 = si == 0 || (mt1 >> e0 & 1);
+#pragma unroll
+            for (int rg = 0; rg < 2; ++rg) {
+                if (u0) yt[rg][0] += ys[rg][0], yt[rg][2] += ys[rg][2];
+                if (u1) yt[rg][1] += ys[rg][1], yt[rg][3] += ys[rg][3];
+                ys[rg][0] = ys[rg][1] = ys[rg][2] = ys[rg][3] = 0.f;
             }
         }
     }
-    __syncthreads();
-    int uni = 0;
-    for (int t = 0; t < T; ++t) uni |= s_mask[t];
-    // (4) the other slices of the batch's union only; a slice's partials go to the tokens that use it
-    const int mt0 = 2 * (lane & 3) < T ? s_mask[2 * (lane & 3)] : 0, mt1 = 2 * (lane & 3) + 1 < T ? s_mask[2 * (lane & 3) + 1] : 0;
-    for (int e0 = 1; e0 < p.E; ++e0) {
-        if (!(uni >> e0 & 1)) continue;
-#pragma unroll
-        for (int rg = 0; rg < 2; ++rg)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) ys[rg][j] = 0.f;
-        slice_pass(p, e0, rt, kw0, kw1, x16, xsum, es_s[warp], gcs, ring, lane, false, ys, A, B);
-        const bool u0 = mt0 >> e0 & 1, u1 = mt1 >> e0 & 1;
-#pragma unroll
-        for (int rg = 0; rg < 2; ++rg) {
-            if (u0) yt[rg][0] += ys[rg][0], yt[rg][2] += ys[rg][2];
-            if (u1) yt[rg][1] += ys[rg][1], yt[rg][3] += ys[rg][3];
-        }
-    }
+    cp_wait<0>();
     TRM(4);
     __syncthreads();  // x16 is dead: the reduction buffer aliases it
 
