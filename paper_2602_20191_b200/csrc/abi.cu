@@ -524,6 +524,10 @@ int mobi_layer_destroy(mobi_layer_t L) {
     free_ws(L);
     dfree(L->codes8);
     dfree(L->dplanes);
+    if (L->s_h2d) cudaStreamDestroy(L->s_h2d);
+    if (L->s_d2h) cudaStreamDestroy(L->s_d2h);
+    for (auto& e : L->ev_pipe)
+        if (e) cudaEventDestroy(e);
     dfree(L->gconst);
     dfree(L->gpart);
     dfree(L->hpart);
@@ -670,13 +674,50 @@ int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta
         std::memcpy(L->h_x, x_host, xb);
         xsrc = L->h_x;
     }
-    MOBI_CUDA(cudaMemcpyAsync(L->x_dev, xsrc, xb, cudaMemcpyHostToDevice, st));
     uint8_t* mdev = masks_host ? reinterpret_cast<uint8_t*>(L->x_dev) + xb : nullptr;
-    int rc = run_layer(L, L->x_dev, T, delta, nullptr, L->y_dev, mdev, st);
-    if (rc) return rc;
     void* ydst = yp ? y_host : L->h_y;
-    MOBI_CUDA(cudaMemcpyAsync(ydst, L->y_dev, yb, cudaMemcpyDeviceToHost, st));
-    if (masks_host) MOBI_CUDA(cudaMemcpyAsync(masks_host, mdev, (size_t)T, cudaMemcpyDeviceToHost, st));
+    // token chunks pipelined over three streams: the host->device copy of chunk i+1 and the
+    // device->host copy of chunk i-1 overlap the forward of chunk i (tokens are independent, so the
+    // chunked result is identical to the whole-batch one)
+    const int nch = T >= 2048 ? 4 : (T >= 1024 ? 2 : 1);
+    if (nch > 1 && !L->s_h2d) {
+        MOBI_CUDA(cudaStreamCreateWithFlags(&L->s_h2d, cudaStreamNonBlocking));
+        MOBI_CUDA(cudaStreamCreateWithFlags(&L->s_d2h, cudaStreamNonBlocking));
+        for (int i = 0; i < 8; ++i) MOBI_CUDA(cudaEventCreateWithFlags(&L->ev_pipe[i], cudaEventDisableTiming));
+    }
+    if (nch == 1) {
+        MOBI_CUDA(cudaMemcpyAsync(L->x_dev, xsrc, xb, cudaMemcpyHostToDevice, st));
+        int rc = run_layer(L, L->x_dev, T, delta, nullptr, L->y_dev, mdev, st);
+        if (rc) return rc;
+        MOBI_CUDA(cudaMemcpyAsync(ydst, L->y_dev, yb, cudaMemcpyDeviceToHost, st));
+        if (masks_host) MOBI_CUDA(cudaMemcpyAsync(masks_host, mdev, (size_t)T, cudaMemcpyDeviceToHost, st));
+    } else {
+        const int64_t step = round_up(cdiv(T, (int64_t)nch), 256);
+        cudaEvent_t* ev = L->ev_pipe;  // [0..3] copied in, [4..7] computed
+        MOBI_CUDA(cudaEventRecord(ev[7], st));  // prior work on the caller's stream
+        MOBI_CUDA(cudaStreamWaitEvent(L->s_h2d, ev[7], 0));
+        int c = 0;
+        for (int64_t t0 = 0; t0 < T; t0 += step, ++c) {
+            const int64_t n = std::min(step, T - t0);
+            const size_t xo = (size_t)(t0 * L->in * 2), yo = (size_t)(t0 * L->out * 2);
+            MOBI_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(L->x_dev) + xo,
+                                      reinterpret_cast<const uint8_t*>(xsrc) + xo, (size_t)(n * L->in * 2),
+                                      cudaMemcpyHostToDevice, L->s_h2d));
+            MOBI_CUDA(cudaEventRecord(ev[c], L->s_h2d));
+            MOBI_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
+            int rc = run_layer(L, reinterpret_cast<uint8_t*>(L->x_dev) + xo, n, delta, nullptr,
+                               reinterpret_cast<uint8_t*>(L->y_dev) + yo, mdev ? mdev + t0 : nullptr, st);
+            if (rc) return rc;
+            MOBI_CUDA(cudaEventRecord(ev[4 + c], st));
+            MOBI_CUDA(cudaStreamWaitEvent(L->s_d2h, ev[4 + c], 0));
+            MOBI_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ydst) + yo,
+                                      reinterpret_cast<const uint8_t*>(L->y_dev) + yo, (size_t)(n * L->out * 2),
+                                      cudaMemcpyDeviceToHost, L->s_d2h));
+            if (masks_host)
+                MOBI_CUDA(cudaMemcpyAsync(masks_host + t0, mdev + t0, (size_t)n, cudaMemcpyDeviceToHost, L->s_d2h));
+        }
+        MOBI_CUDA(cudaStreamSynchronize(L->s_d2h));
+    }
     MOBI_CUDA(cudaStreamSynchronize(st));
     if (!yp) std::memcpy(y_host, L->h_y, yb);
     return MOBI_OK;

@@ -231,3 +231,21 @@ def test_router_tcgen05_matches_cuda_core_router(orc, inn, h, T):
     s_ref = oracle_scores(orc, layer, x64)
     for s in (s_tc, s_cc):
         assert np.all(np.abs(s - s_ref) <= SCORE_ATOL + SCORE_RTOL * np.abs(s_ref))
+
+
+@pytest.mark.parametrize("T", [1100, 2100])
+def test_forward_host_chunked_pipeline_equals_device_forward(T):
+    """mobi_forward_host splits large batches into token chunks pipelined over copy/compute streams;
+    tokens are independent, so outputs and masks must equal the single device-side call exactly."""
+    from paper_2602_20191_b200 import calibrate_threshold
+    L, layer = make_layer(512, 384, gs=128, seed=T)
+    xb, _ = make_x(T, 384, seed=T + 1)
+    delta = calibrate_threshold(layer.score(xb), 1 / 6)
+    y, m = layer.forward(xb, delta, return_masks=True)
+    xh = xb.cpu().pin_memory()
+    yh = torch.empty((T, 512), dtype=torch.bfloat16).pin_memory()
+    mh = torch.empty(T, dtype=torch.uint8).pin_memory()
+    layer.forward_host(xh, delta, y_host=yh, masks_host=mh)
+    assert torch.equal(yh, y.cpu()) and torch.equal(mh, m.cpu())
+    y2 = layer.forward_host(xb.cpu(), delta)  # pageable buffers take the staging path
+    assert torch.equal(y2, y.cpu())
