@@ -394,7 +394,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     }
     {
         ProfScope p(L, 2, st);
-        if ((rc = launch_gather(L, xb, T, st, fused))) return rc;
+        if ((rc = launch_gather(L, xb, T, st, fused, fused && !L->prof))) return rc;
     }
     __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
     if (fused && g_impl_override != 0 && g_impl_override != 3 && g_impl_override != 5)  // the tcgen05 GEMMs clear them
@@ -414,7 +414,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     // production: the CTA-pair kernel (B split across the pair: half the smem operand traffic per SM);
     // the 1-CTA kernel for batches small enough to need split-K
     if (T <= 64) return launch_gemm_tc(L, yb, T, st);
-    return launch_gemm_tc2(L, yb, T, st);
+    return launch_gemm_tc2(L, yb, T, st, nullptr, !L->prof);
 }
 
 }  // namespace

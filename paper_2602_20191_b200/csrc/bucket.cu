@@ -15,6 +15,7 @@
 // by a per-row power of two 2^-e (max|x| lands in [2^14, 2^15)); the GEMM epilogue multiplies
 // by 2^e.  The scaling is exact, so fp16 operands lose nothing against the bf16 input.
 #include "mobi_internal.cuh"
+#include "sm100.cuh"
 
 namespace mobi {
 namespace {
@@ -220,6 +221,8 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
     __shared__ float red[4];
     __shared__ int s_row;
     const int64_t src = blockIdx.x;
+    sm100::pdl_trigger();
+    sm100::pdl_wait();  // the router's masks / histogram (PDL launch; a no-op otherwise)
     if (hist) {
         // fused bucketing (the router decided the masks and counted the buckets): claim the next slot
         // of this token's bucket.  The slot order inside a bucket is arbitrary, which cannot change
@@ -308,10 +311,20 @@ int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* 
     return MOBI_OK;
 }
 
-int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st, bool claim) {
+int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st, bool claim, bool pdl) {
     const bool vec = (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    gather_kernel<<<(unsigned)T, 128, 0, st>>>(x, L->in, L->in_pad, L->tpad_max, L->pinv, L->xperm, L->escale, vec,
-                                               L->masks, claim ? L->bk_hist : nullptr, L->bk_hist + 32, L->perm, L->tiles, L->meta);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)T);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    MOBI_CUDA(cudaLaunchKernelEx(&cfg, gather_kernel, x, L->in, L->in_pad, L->tpad_max, L->pinv, L->xperm, L->escale,
+                                 vec, (const uint8_t*)L->masks, claim ? (const int*)L->bk_hist : (const int*)nullptr,
+                                 L->bk_hist + 32, L->perm, L->tiles, L->meta));
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

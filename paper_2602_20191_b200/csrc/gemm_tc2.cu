@@ -117,6 +117,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         prefetch_tmap(&tmap_big);
     }
     if (warp == kWarpMma) tmem_alloc_2sm(tmem_slot, 512);
+    pdl_wait();  // PDL launch: everything above overlapped the gather; its outputs are visible from here
     if (blockIdx.x == 0 && threadIdx.x < 48 && p.bk_hist) p.bk_hist[threadIdx.x] = 0;  // gather consumed it
     tc_fence_before();
     __syncthreads();
@@ -444,7 +445,8 @@ int sm_count() {
 
 }  // namespace
 
-int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace) {
+int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace,
+                    bool pdl) {
     static bool attr = false;
     if (!attr) {
         MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -486,10 +488,20 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
     p.trace = trace;
     p.bk_hist = L->bk_hist;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];  // (cluster shape from __cluster_dims__)
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
     if (trace)
-        mobi_gemm_tc2_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(L->tmap_x2[0], L->tmap_x2[1], p);
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, mobi_gemm_tc2_kernel<true>, *(&L->tmap_x2[0]), *(&L->tmap_x2[1]), p));
     else
-        mobi_gemm_tc2_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(L->tmap_x2[0], L->tmap_x2[1], p);
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, mobi_gemm_tc2_kernel<false>, *(&L->tmap_x2[0]), *(&L->tmap_x2[1]), p));
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

@@ -179,13 +179,14 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
 int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks,
                   float* scores_out, uint8_t* masks_out, int32_t* cperm_out,
                   int32_t* inverse_out, int32_t* counts_out, cudaStream_t st, bool sanitize = true);
-int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st, bool claim = false);
+int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st, bool claim = false,
+                  bool pdl = false);
 // gemm_tc.cu (tcgen05) / gemm_simt.cu (reference kernel, tests only)
 int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
                    unsigned long long* trace = nullptr);
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
-int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
-                    unsigned long long* trace = nullptr);  // gemm_tc2.cu (CTA pairs)
+int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace = nullptr,
+                    bool pdl = false);  // gemm_tc2.cu (CTA pairs)
 // decode.cu (T <= kDecMaxT: router GEMV + stream-K decode GEMM, PDL-chained)
 bool decode_supported(const mobi_layer* L, const void* x, int64_t T);
 int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, uint8_t* masks_out,

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
+    pdl_trigger();  // the gather may launch and start loading its rows
     const long long t_start = clock64();
     auto TR = [&](int i) {
         if (p.trace && blockIdx.x == 0 && (threadIdx.x % 32) == 0) p.trace[i] = (unsigned long long)(clock64() - t_start);
