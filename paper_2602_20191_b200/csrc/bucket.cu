@@ -222,6 +222,18 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
     __shared__ int s_row;
     const int64_t src = blockIdx.x;
     sm100::pdl_trigger();
+    // the row (an input, not a router output) is loaded before the grid dependency resolves; its
+    // vectors stay in registers between the max and the conversion (in <= 8192)
+    constexpr int kRV = 8;
+    const __nv_bfloat16* row = x + (int64_t)src * in;
+    uint4 rv[kRV];
+    if (vec) {
+#pragma unroll
+        for (int j = 0; j < kRV; ++j) {
+            const int64_t k = (int64_t)(threadIdx.x + 128 * j) * 8;
+            rv[j] = k < in ? __ldg(reinterpret_cast<const uint4*>(row + k)) : make_uint4(0, 0, 0, 0);
+        }
+    }
     sm100::pdl_wait();  // the router's masks / histogram (PDL launch; a no-op otherwise)
     if (hist) {
         // fused bucketing (the router decided the masks and counted the buckets): claim the next slot
@@ -229,56 +241,63 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
         // any output: a token's result depends only on its own row and its bucket's effective weight.
         if (threadIdx.x == 0) {
             if (src == 0) build_tiles(hist, tiles, meta);
-            const int m = masks[src];
-            const int i = bucket_start(hist, m) + atomicAdd(&fill[m], 1);
+            const int mk = masks[src];
+            const int i = bucket_start(hist, mk) + atomicAdd(&fill[mk], 1);
             perm[i] = (int32_t)src;
             pinv[src] = i;
             s_row = i;
         }
-        __syncthreads();
     }
-    const int64_t i = hist ? s_row : pinv[src];
-    // k-block slab layout [in_pad/64][tpad][64]: element k of permuted row i at (k/64*tpad + i)*64 + k%64
-    __half* dst = xperm + i * kKBlock;
-    auto at = [&](int64_t k) { return dst + (k / kKBlock) * tpad * kKBlock + (k % kKBlock); };
-    const __nv_bfloat16* row = x + (int64_t)src * in;
     float m = 0.f;
-    if (vec) {
-        for (int64_t k = threadIdx.x * 8; k < in; k += 128 * 8) {
-            uint4 q = __ldg(reinterpret_cast<const uint4*>(row + k));
-            const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&q);
+    auto vmax = [&](const uint4& q) {
+        const __nv_bfloat162* pp = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                float2 f = __bfloat1622float2(p[j]);
-                m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
-            }
+        for (int j = 0; j < 4; ++j) {
+            float2 f = __bfloat1622float2(pp[j]);
+            m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
         }
+    };
+    if (vec) {
+#pragma unroll
+        for (int j = 0; j < kRV; ++j) vmax(rv[j]);
+        for (int64_t k = (int64_t)(threadIdx.x + 128 * kRV) * 8; k < in; k += 128 * 8)
+            vmax(__ldg(reinterpret_cast<const uint4*>(row + k)));
     } else {
         for (int64_t k = threadIdx.x; k < in; k += 128) m = fmaxf(m, fabsf(__bfloat162float(row[k])));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
+    __syncthreads();  // also publishes s_row
     m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    const int64_t i = hist ? s_row : pinv[src];
+    // k-block slab layout [in_pad/64][tpad][64]: element k of permuted row i at (k/64*tpad + i)*64 + k%64
+    __half* dst = xperm + i * kKBlock;
+    auto at = [&](int64_t k) { return dst + (k / kKBlock) * tpad * kKBlock + (k % kKBlock); };
     int e = 0;
     if (m > 0.f && isfinite(m)) e = ilogbf(m) - 14;
     const float sc = ldexpf(1.f, -e);
     if (threadIdx.x == 0) escale[i] = ldexpf(1.f, e);
     if (vec) {
-        for (int64_t k = threadIdx.x * 8; k < in_pad; k += 128 * 8) {
-            uint4 o = make_uint4(0, 0, 0, 0);
-            if (k < in) {
-                uint4 q = __ldg(reinterpret_cast<const uint4*>(row + k));
-                const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&q);
-                __half2* h = reinterpret_cast<__half2*>(&o);
+        auto conv = [&](const uint4& q) {
+            uint4 o;
+            const __nv_bfloat162* pp = reinterpret_cast<const __nv_bfloat162*>(&q);
+            __half2* h = reinterpret_cast<__half2*>(&o);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    float2 f = __bfloat1622float2(p[j]);
-                    h[j] = __floats2half2_rn(f.x * sc, f.y * sc);
-                }
+            for (int j = 0; j < 4; ++j) {
+                float2 f = __bfloat1622float2(pp[j]);
+                h[j] = __floats2half2_rn(f.x * sc, f.y * sc);
             }
-            *reinterpret_cast<uint4*>(at(k)) = o;
+            return o;
+        };
+#pragma unroll
+        for (int j = 0; j < kRV; ++j) {  // rv[j] is zero past `in`: the in..in_pad tail is written as zeros
+            const int64_t k = (int64_t)(threadIdx.x + 128 * j) * 8;
+            if (k < in_pad) *reinterpret_cast<uint4*>(at(k)) = conv(rv[j]);
+        }
+        for (int64_t k = (int64_t)(threadIdx.x + 128 * kRV) * 8; k < in_pad; k += 128 * 8) {
+            const uint4 q = k < in ? __ldg(reinterpret_cast<const uint4*>(row + k)) : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(at(k)) = conv(q);
         }
     } else {
         for (int64_t k = threadIdx.x; k < in_pad; k += 128)
