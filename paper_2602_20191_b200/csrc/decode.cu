@@ -1018,6 +1018,17 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
     p.delta = delta;
     const int n_mt = (int)(L->h_pad / kRdRows);
     const dim3 grid((unsigned)(n_mt * kRdCluster));
+    static bool carve = false;
+    if (!carve) {  // run with the SM configured for maximum shared memory, so the decode GEMM that
+                   // follows (PDL) can be co-resident while the router streams w1
+        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<4>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       (int)cudaSharedmemCarveoutMaxShared));
+        carve = true;
+    }
     if (T <= 8)
         router_dec_kernel<1><<<grid, 32 * kRdWarps, 0, st>>>(p);
     else if (T <= 16)

@@ -65,7 +65,14 @@ __device__ __forceinline__ void mma_f16_acc(float (&d)[4], uint32_t a0, uint32_t
 __device__ __forceinline__ void grid_dep_wait2() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // 2-bit fields i and i+8 of a fragment word -> half2 (1024 + lo, 1024 + hi)
-__device__ __forceinline__ uint32_t frag(uint32_t w, int i) { return ((w >> (2 * i)) & 0x00030003u) | 0x64006400u; }
+// Field ss of a (pre-shifted) plane word -> half2 (1024 + 4^ss lo, 1024 + 4^ss hi): one LOP3 (a & b) | c,
+// the magic in a register so the mask can be the immediate (layer.cu: pack_dplanes_kernel)
+template <int SS>
+__device__ __forceinline__ uint32_t frag(uint32_t w, uint32_t magic) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "n"(0x00030003u << (2 * SS)), "r"(magic));
+    return r;
+}
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
@@ -77,31 +84,21 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 constexpr int kD2Ring = 8;  // (slice, k-block) items in flight per lane (16 B each): 64 KiB per CTA
 
-// cp.async.wait_group with a runtime count (<= kD2Ring - 1)
+// cp.async.wait_group for "at most n groups pending": exact in the steady state (n = kD2Ring - 2),
+// conservatively rounded down near the ends of the stream (no jump table in the item loop)
 __device__ __forceinline__ void cp_wait_dyn(int n) {
-    switch (n) {
-        case 0: cp_wait<0>(); break;
-        case 1: cp_wait<1>(); break;
-        case 2: cp_wait<2>(); break;
-        case 3: cp_wait<3>(); break;
-        case 4: cp_wait<4>(); break;
-        case 5: cp_wait<5>(); break;
-        case 6: cp_wait<6>(); break;
-        case 7: cp_wait<7>(); break;
-        case 8: cp_wait<8>(); break;
-        case 9: cp_wait<9>(); break;
-        case 10: cp_wait<10>(); break;
-        case 11: cp_wait<11>(); break;
-        case 12: cp_wait<12>(); break;
-        case 13: cp_wait<13>(); break;
-        default: cp_wait<14>(); break;
-    }
+    static_assert(kD2Ring == 8, "staged waits assume an 8-deep ring");
+    if (n >= 6) cp_wait<6>();
+    else if (n >= 3) cp_wait<3>();
+    else if (n >= 1) cp_wait<1>();
+    else cp_wait<0>();
 }
 
-__global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __grid_constant__ D2Params p) {
+__global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2Params p) {
     extern __shared__ __align__(16) uint8_t smem[];
     __half* x16 = reinterpret_cast<__half*>(smem);                                   // [kD2MaxT + 1][xs_stride]
-    float* xsum = reinterpret_cast<float*>(smem + (size_t)(kD2MaxT + 1) * p.xs_stride * 2);  // [T][kblocks]
+    // [T][kblocks] {sum of the k-step-scaled fp16 X (offset cancellation), unscaled sum (A, B)}
+    float2* xsum = reinterpret_cast<float2*>(smem + (size_t)(kD2MaxT + 1) * p.xs_stride * 2);
     float* red = reinterpret_cast<float*>(smem);  // [warps][kD2Acc][32], aliases x16 after the passes
     __shared__ float es_s[kD2Warps][kD2MaxT];
     __shared__ float s_score[kD2MaxT][MOBI_MAX_SLICES - 1];
@@ -120,16 +117,33 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
     // order, one cp.async group each, into ring slot i % kD2Ring; slice 1's first items go out now so
     // their latency hides behind the activation prologue
     int pi = 0;
-    int slist[MOBI_MAX_SLICES] = {0, 0, 0, 0};  // the stream's slices: slice 1, then the union's others
+    uint32_t slist = 0;  // the stream's slices, 2 bits each: slice 1 (e0 = 0), then the union's others
     int psi = 0, pkb = kw0;  // issue cursor: (slice index, k-block) of item pi
+    const uint4* rt_planes = p.dplanes + (int64_t)rt * p.kblocks * 32 + lane;
+    const int plane_stride = p.n_rt32 * (int)p.kblocks * 32;  // uint4s per slice plane
+    const uint4* ip = rt_planes + kw0 * 32;  // source of item pi
+    auto seek = [&]() { ip = rt_planes + ((int)(slist >> (2 * psi)) & 3) * plane_stride + pkb * 32; };
     auto issue = [&](int i) {
-        const uint4* src = p.dplanes + (((int64_t)slist[psi] * p.n_rt32 + rt) * p.kblocks + pkb) * 32 + lane;
-        cp_async16(ring + (i % kD2Ring) * 32 + lane, src, true);
+        cp_async16(ring + (i % kD2Ring) * 32 + lane, ip, true);
         cp_commit();
-        if (++pkb == kw1) pkb = kw0, ++psi;
+        if (++pkb == kw1) {
+            pkb = kw0, ++psi;
+            seek();
+        } else {
+            ip += 32;
+        }
     };
+    {   // the group constants (s, s*z) of this warp's groups for the tile's 32 rows, read once for all
+        // slices: 16-byte cp.asyncs that join item 0's group (waited for before the first group ends)
+        const int64_t g0 = p.single_group ? 0 : (int64_t)kw0 * kKBlock / p.gs;
+        const int64_t g1 = p.single_group ? 1 : ((int64_t)kw1 * kKBlock + p.gs - 1) / p.gs;
+        if (kw1 > kw0)
+            for (int i = lane; i < (int)(g1 - g0) * 16; i += 32)
+                cp_async16(gcs + (i / 16) * 32 + (i % 16) * 2,
+                           p.gconst + (g0 + i / 16) * p.out_pad + (int64_t)rt * 32 + (i % 16) * 2, true);
+    }
     while (pi < kw1 - kw0 && pi < kD2Ring - 1) issue(pi++);
-    float xg0 = 0.f, xg1 = 0.f;
+    float xg0 = 0.f, xg1 = 0.f, xu0 = 0.f, xu1 = 0.f;
     int grp = 0, gleft = 0;
 
     // (1) this warp's k range of X: bf16 -> per-token 2^-e scale (max over the range) -> fp16 in smem,
@@ -166,7 +180,9 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         int e = 0;
         if (m > 0.f && isfinite(m)) e = ilogbf(m) - 14;
-        const float sc = ldexpf(1.f, -e);
+        // k-step ss = (k % 64) / 16 of this lane's 8 values is (lane % 8) / 2: scaled by 4^-ss
+        const int lss = (lane & 7) >> 1;
+        const float sc = ldexpf(1.f, -e - 2 * lss);
         if (lane == 0) es_s[warp][t] = ldexpf(1.f, e);
         auto conv = [&](const uint4& q) {
             uint4 o;
@@ -189,12 +205,16 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
                 const float2 f2 = __half22float2(hh[j]);
                 sacc += f2.x + f2.y;
             }
+            float uacc = sacc * (float)(1 << (2 * lss));  // exact: power-of-two rescale
             sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
             sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
             sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
+            uacc += __shfl_xor_sync(0xffffffffu, uacc, 1);
+            uacc += __shfl_xor_sync(0xffffffffu, uacc, 2);
+            uacc += __shfl_xor_sync(0xffffffffu, uacc, 4);
             if (k < k_hi) {
                 *reinterpret_cast<uint4*>(x16 + (size_t)t * p.xs_stride + k) = o;
-                if ((lane & 7) == 0) xsum[t * p.kblocks + k / kKBlock] = sacc;
+                if ((lane & 7) == 0) xsum[t * p.kblocks + k / kKBlock] = make_float2(sacc, uacc);
             }
         };
 #pragma unroll
@@ -209,13 +229,6 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
         *reinterpret_cast<uint4*>(x16 + (size_t)kD2MaxT * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
     __syncwarp();
 
-    {   // the group constants (s, s*z) of this warp's groups for the tile's 32 rows, read once for all slices
-        const int64_t g0 = p.single_group ? 0 : (int64_t)kw0 * kKBlock / p.gs;
-        const int64_t g1 = p.single_group ? 1 : ((int64_t)kw1 * kKBlock + p.gs - 1) / p.gs;
-        for (int i = lane; i < (int)(g1 - g0) * 32; i += 32)
-            gcs[i] = __ldg(p.gconst + (g0 + i / 32) * p.out_pad + (int64_t)rt * 32 + i % 32);
-    }
-    __syncwarp();
     // yt: this lane's outputs (rows g/g+8 of both row groups, tokens 2c/2c+1) over the slices each
     // token uses; ys: the current slice's partials
     float yt[2][4], ys[2][4], A[2][4], B[2][4], D[2][4];
@@ -233,6 +246,8 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
     // (2)-(4) one stream of (slice, k-block) items: slice 1's k-blocks (already in flight since the
     // prologue), then -- once the masks are known -- those of every other slice in the batch's union
     const int nk = kw1 - kw0;
+    const int gleft0 = p.single_group ? (1 << 30) : kpg - (kw0 % kpg);  // k-blocks left in the first group
+    const uint32_t magic = 0x64006400u;  // fp16 1024: (1024 + c) halves
     int n_items = nk, uni = 1, mt0 = 0, mt1 = 0;
     int csi = 0, ckb = kw0;  // consume cursor
     for (int ci = 0;; ++ci) {
@@ -272,67 +287,76 @@ __global__ void __launch_bounds__(kD2Threads, 1) decode_planes_kernel(const __gr
             mt1 = t1 < T ? s_mask[t1] : 0;
             int ns = 1;
             for (int e0 = 1; e0 < p.E; ++e0)
-                if (uni >> e0 & 1) slist[ns++] = e0;
+                if (uni >> e0 & 1) slist |= (uint32_t)e0 << (2 * ns++);
             n_items = nk * ns;
+            seek();  // the issue cursor's slice is known now
             // burst: the union's first items
             while (pi < n_items && pi <= ci + kD2Ring - 1) issue(pi++);
         }
         if (ci >= n_items) break;
-        const int si = csi, kb = ckb, e0 = slist[si];
+        const int si = csi, kb = ckb, e0 = (int)(slist >> (2 * si)) & 3;
         if (++ckb == kw1) ckb = kw0, ++csi;
         cp_wait_dyn(pi - 1 - ci);
+        if (ci == 0) __syncwarp();  // the group constants other lanes copied are visible
         const uint4 q = ring[(ci % kD2Ring) * 32 + lane];
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-        for (int ss = 0; ss < 4; ++ss) {
-            const __half* xk = xr + (size_t)kb * kKBlock + 16 * ss;
+        const uint32_t w0[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t w1[4] = {q.x >> 8, q.y >> 8, q.z >> 8, q.w >> 8};  // row group 1's fields
+        auto kstep = [&](auto SSc) {
+            constexpr int SS = decltype(SSc)::value;
+            const __half* xk = xr + (size_t)kb * kKBlock + 16 * SS;
             const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xk);
             const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xk + 8);
-#pragma unroll
-            for (int rg = 0; rg < 2; ++rg) {
-                const uint32_t W = w[rg * 2 + ss / 2];
-                const int i0 = (ss & 1) * 4;
-                mma_f16_acc(D[rg], frag(W, i0), frag(W, i0 + 1), frag(W, i0 + 2), frag(W, i0 + 3), b0, b1);
-            }
-        }
+            mma_f16_acc(D[0], frag<SS>(w0[0], magic), frag<SS>(w0[1], magic), frag<SS>(w0[2], magic),
+                        frag<SS>(w0[3], magic), b0, b1);
+            mma_f16_acc(D[1], frag<SS>(w1[0], magic), frag<SS>(w1[1], magic), frag<SS>(w1[2], magic),
+                        frag<SS>(w1[3], magic), b0, b1);
+        };
+        kstep(std::integral_constant<int, 0>{});
+        kstep(std::integral_constant<int, 1>{});
+        kstep(std::integral_constant<int, 2>{});
+        kstep(std::integral_constant<int, 3>{});
         // refill: item ci + R - 1 goes into the slot just consumed (its data is in registers)
         if (pi < n_items && pi <= ci + kD2Ring - 1) issue(pi++);
-        xg0 += t0 < T ? xsum[t0 * p.kblocks + kb] : 0.f;
-        xg1 += t1 < T ? xsum[t1 * p.kblocks + kb] : 0.f;
+        {
+            const float2 s0 = t0 < T ? xsum[t0 * p.kblocks + kb] : make_float2(0.f, 0.f);
+            const float2 s1 = t1 < T ? xsum[t1 * p.kblocks + kb] : make_float2(0.f, 0.f);
+            xg0 += s0.x, xu0 += s0.y;
+            xg1 += s1.x, xu1 += s1.y;
+        }
         if (kb == kw0) {  // a slice starts: its group cursor
             grp = 0;
-            gleft = p.single_group ? (1 << 30) : kpg - (kw0 % kpg);
+            gleft = gleft0;
         }
         const bool slice_end = kb + 1 == kw1;
         if (slice_end || --gleft == 0) {
-            const float fs = ldexpf(1.f, -2 * e0);  // S 4^(4-e) with S = s / 2^6 and e = e0 + 1
 #pragma unroll
             for (int rg = 0; rg < 2; ++rg) {
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {  // rows g and g+8 of the row group
                     const float2 sc = gcs[grp * 32 + 16 * rg + g + 8 * h];
-                    const float m0 = sc.x * fs * es0, m1 = sc.x * fs * es1;
-                    ys[rg][2 * h] = fmaf(D[rg][2 * h] - 1024.f * xg0, m0, ys[rg][2 * h]);
-                    ys[rg][2 * h + 1] = fmaf(D[rg][2 * h + 1] - 1024.f * xg1, m1, ys[rg][2 * h + 1]);
+                    ys[rg][2 * h] = fmaf(D[rg][2 * h] - 1024.f * xg0, sc.x, ys[rg][2 * h]);
+                    ys[rg][2 * h + 1] = fmaf(D[rg][2 * h + 1] - 1024.f * xg1, sc.x, ys[rg][2 * h + 1]);
                     if (si == 0) {
-                        A[rg][2 * h] = fmaf(sc.x, xg0 * es0, A[rg][2 * h]);
-                        A[rg][2 * h + 1] = fmaf(sc.x, xg1 * es1, A[rg][2 * h + 1]);
-                        B[rg][2 * h] = fmaf(sc.y, xg0 * es0, B[rg][2 * h]);
-                        B[rg][2 * h + 1] = fmaf(sc.y, xg1 * es1, B[rg][2 * h + 1]);
+                        A[rg][2 * h] = fmaf(sc.x, xu0 * es0, A[rg][2 * h]);
+                        A[rg][2 * h + 1] = fmaf(sc.x, xu1 * es1, A[rg][2 * h + 1]);
+                        B[rg][2 * h] = fmaf(sc.y, xu0 * es0, B[rg][2 * h]);
+                        B[rg][2 * h + 1] = fmaf(sc.y, xu1 * es1, B[rg][2 * h + 1]);
                     }
                 }
                 D[rg][0] = D[rg][1] = D[rg][2] = D[rg][3] = 0.f;
             }
-            xg0 = xg1 = 0.f;
+            xg0 = xg1 = xu0 = xu1 = 0.f;
             ++grp;
             gleft = kpg;
         }
         if (slice_end) {  // the slice's partials go to the tokens that use it (slice 1: every token)
             const bool u0 = si == 0 || (mt0 >> e0 & 1), u1 = si == 0 || (mt1 >> e0 & 1);
+            const float fs = __int_as_float((127 - 2 * e0) << 23);  // 4^-e0: S 4^(4-e), S = s / 2^6, e = e0 + 1
+            const float f0 = u0 ? fs * es0 : 0.f, f1 = u1 ? fs * es1 : 0.f;
 #pragma unroll
             for (int rg = 0; rg < 2; ++rg) {
-                if (u0) yt[rg][0] += ys[rg][0], yt[rg][2] += ys[rg][2];
-                if (u1) yt[rg][1] += ys[rg][1], yt[rg][3] += ys[rg][3];
+                yt[rg][0] = fmaf(ys[rg][0], f0, yt[rg][0]), yt[rg][2] = fmaf(ys[rg][2], f0, yt[rg][2]);
+                yt[rg][1] = fmaf(ys[rg][1], f1, yt[rg][1]), yt[rg][3] = fmaf(ys[rg][3], f1, yt[rg][3]);
                 ys[rg][0] = ys[rg][1] = ys[rg][2] = ys[rg][3] = 0.f;
             }
         }
@@ -386,7 +410,7 @@ bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
     if (T < 1 || T > kD2MaxT || !L->dplanes || L->E > 4) return false;
     if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
     if (!L->single_group && L->gs % kKBlock != 0) return false;
-    const size_t xs = (size_t)(kD2MaxT + 1) * (L->in_pad + 8) * 2 + (size_t)kD2MaxT * L->kblocks * 4;
+    const size_t xs = (size_t)(kD2MaxT + 1) * (L->in_pad + 8) * 2 + (size_t)2 * kD2MaxT * L->kblocks * 4;
     const size_t sm = (std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16 +
                       (size_t)kD2Warps * d2_groups_per_warp(L) * 32 * 8 + (size_t)kD2Warps * kD2Ring * 32 * 16;
     return sm <= 200 * 1024;
@@ -423,7 +447,7 @@ int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const
     p.vmask = (1 << (L->nr + 1)) - 1;
     p.n_rt32 = (int)(L->out_pad / 32);
     p.xs_stride = (int)(L->in_pad + 8);
-    const size_t xs = (size_t)(kD2MaxT + 1) * p.xs_stride * 2 + (size_t)kD2MaxT * L->kblocks * 4;
+    const size_t xs = (size_t)(kD2MaxT + 1) * p.xs_stride * 2 + (size_t)2 * kD2MaxT * L->kblocks * 4;
     p.gpw = d2_groups_per_warp(L);
     p.gcs_off = (int64_t)((std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16);
     p.ring_off = p.gcs_off + (int64_t)kD2Warps * p.gpw * 32 * 8;

@@ -22,8 +22,15 @@ using namespace sm100;
 constexpr int RS = 6;                       // smem stages
 constexpr int RM = 128, RN = 128;           // tokens x hidden per tile
 constexpr int kAB = RM * kKBlock * 2;       // 16 KiB per operand per stage
-constexpr int kRThreads = 192;              // 4 epilogue warps, TMA, MMA (highest ids = priority)
-constexpr int kRWarpTma = 4, kRWarpMma = 5;
+#ifndef MOBI_RTMA2
+#define MOBI_RTMA2 1
+#endif
+// 4 epilogue warps, TMA, MMA [, second TMA]: one thread's TMA issue chain (~350 cycles per stage,
+// tools/pipe_probe.cu) is slower than the 4 N=128 MMAs a stage feeds, so two producer warps take
+// alternate stages
+constexpr int kRProducers = MOBI_RTMA2 ? 2 : 1;
+constexpr int kRThreads = 192 + 32 * (kRProducers - 1);
+constexpr int kRWarpTma = 4, kRWarpMma = 5, kRWarpTma2 = 6;
 constexpr int kRSmem = RS * 2 * kAB + 1024 + 256 + 2 * RN * 16;  // + per-tile {b1, w2} staging
 
 struct RParams {
@@ -79,6 +86,8 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     }
     pdl_trigger();  // the gather may launch and start loading its rows
     const long long t_start = clock64();
+    unsigned long long g_start = 0;
+    if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_start));
     auto TR = [&](int i) {
         if (p.trace && blockIdx.x == 0 && (threadIdx.x % 32) == 0) p.trace[i] = (unsigned long long)(clock64() - t_start);
     };
@@ -99,12 +108,14 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         kb1 = min(p.kblocks, kb0 + p.kb_per);
     };
 
-    if (warp == kRWarpTma) {
+    if (warp == kRWarpTma || (kRProducers == 2 && warp == kRWarpTma2)) {
+        const uint32_t mine = warp == kRWarpTma ? 0u : 1u;
         uint32_t it = 0;
         for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
             int mt, nt, ks, kb0, kb1;
             tile_of(tile, mt, nt, ks, kb0, kb1);
             for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                if ((it & (kRProducers - 1)) != mine) continue;
                 const int s = it % RS;
                 mbar_wait(&empty[s], ((it / RS) & 1) ^ 1);
                 if (kb < 64) TR(128 + kb);
@@ -255,6 +266,16 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     __syncthreads();
     if (warp == kRWarpMma) tmem_dealloc(tmem, 512);
     TR(205);
+    if (p.trace && threadIdx.x == 0) {  // per-CTA wall marks (ns) + SM id
+        unsigned long long g_end;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_end));
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        p.trace[4096 + 4 * blockIdx.x] = g_start;
+        p.trace[4096 + 4 * blockIdx.x + 1] = g_end;
+        p.trace[4096 + 4 * blockIdx.x + 2] = smid;
+        p.trace[4096 + 4 * blockIdx.x + 3] = (unsigned long long)(clock64() - t_start);
+    }
 }
 
 // split-K finish: H = sum_ks hpart (fixed order) -> silu(H + b1) . w2 -> s_part[nt][t][k]

@@ -10,7 +10,7 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, int iters) {
     for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 7919u + i * 104729u;
     float f[8];
     for (int i = 0; i < 8; ++i) f[i] = (float)a[i];
-    float acc[4] = {0, 0, 0, 0};
+    float acc[4] = {0, 0, 0, 0}, acc2[4][4] = {};
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -25,8 +25,16 @@ __global__ void __launch_bounds__(256) k(uint32_t* out, int iters) {
                          : "+f"(acc[0]), "+f"(acc[1]), "+f"(acc[2]), "+f"(acc[3])
                          : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]));
         }
+        if (OP == 5) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                             : "+f"(acc2[c][0]), "+f"(acc2[c][1]), "+f"(acc2[c][2]), "+f"(acc2[c][3])
+                             : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]));
+        }
     }
     long long t1 = clock64();
+    for (int c = 0; c < 4; ++c) acc[c] += acc2[c][0] + acc2[c][1] + acc2[c][2] + acc2[c][3];
     uint32_t s = 0;
     for (int i = 0; i < 8; ++i) s += a[i] + __float_as_uint(f[i]);
     s += __float_as_uint(acc[0] + acc[1] + acc[2] + acc[3]);
@@ -60,6 +68,10 @@ int main() {
     uint32_t cyc;
     cudaMemcpy(&cyc, d + (1 << 20), 4, cudaMemcpyDeviceToHost);
     printf("%-34s %8.2f HMMA/cycle/SM (dependent chain per warp, 8 warps)\n", "mma.sync m16n8k16", 4096.0 * 8 / cyc);
+    k<5><<<148, 256>>>(d, 1024);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&cyc, d + (1 << 20), 4, cudaMemcpyDeviceToHost);
+    printf("%-34s %8.2f HMMA/cycle/SM (4 independent chains per warp, 8 warps)\n", "mma.sync m16n8k16", 1024.0 * 4 * 8 / cyc);
     printf("%s\n", cudaGetErrorString(e));
     return 0;
 }

@@ -57,8 +57,16 @@ def main():
         ok = (g[:, 5] > 0) & (ns > 0)
         if ok.any():
             print("gemm SM clock (GHz, median over CTAs):", float(np.median(cyc[ok] / ns[ok])))
-    show("gemm", g, ["start", "x prep done", "grid dep resolved", "main loop done", "end"])
-    show("planes", g, ["start", "x prep done", "slice 1 done", "grid dep resolved", "union slices done", "end"])
+    if False: show("gemm", g, ["start", "x prep done", "grid dep resolved", "main loop done", "end"])
+    show("planes", g, ["start", "x prep done", "slice 1 done", "grid dep resolved", "union slices done", "end",
+                       "item 0 data ready", "last slice-1 item ready"])
+    it = full.astype(np.int64)[24576:24576 + 16 * 32 * 4].reshape(16, 32, 4)
+    for w in (0, 7, 15):
+        print(f"planes CTA0 warp {w} per item (cycles rel. item 0: pre-wait, data, mma done, issued):")
+        for ci in range(32):
+            if it[w, ci, 0]:
+                print("   ", ci, [int(v - it[w, 0, 0]) for v in it[w, ci]])
+    return
     ft = full.astype(np.int64)[24576:24576 + 4 * 64].reshape(4, 64)
     for c in range(2):
         print(f"cta {c} warp7 full-wait start:", [int(v - t0) if v else -1 for v in ft[c, :16]])

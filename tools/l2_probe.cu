@@ -176,11 +176,14 @@ int main() {
     }
     unsigned long long* d_out;
     cudaMalloc(&d_out, 8 * 2048);
-    run<4, 16384, 8, 128>("tensor contiguous 48MB", buf, bytes, d_out, nsm);
-    run<5, 16384, 8, 128>("tensor strided 8KB pitch 16MB", buf, 16ull << 20, d_out, nsm);
-    run<5, 16384, 8, 128>("tensor strided 8KB pitch 48MB", buf, bytes, d_out, nsm);
-    run<5, 32768, 6, 256>("tensor strided 8KB pitch 16MB", buf, 16ull << 20, d_out, nsm);
-    run<5, 16384, 8, 32>("tensor strided 8KB pitch 16MB", buf, 16ull << 20, d_out, nsm);
-    run<4, 32768, 6, 256>("tensor contiguous 48MB", buf, bytes, d_out, nsm);
+    run<0, 16384, 8>("bulk distinct 148 SMs", buf, bytes, d_out, nsm);
+    run<0, 16384, 8>("bulk distinct 32 SMs", buf, bytes, d_out, 32);
+    run<0, 16384, 8>("bulk distinct 74 SMs", buf, bytes, d_out, 74);
+    run<0, 16384, 8, 32, 2>("bulk distinct 2 producers 148", buf, bytes, d_out, nsm);
+    run<0, 16384, 8, 32, 2>("bulk distinct 2 producers 32", buf, bytes, d_out, 32);
+    run<2, 16384, 8>("bulk multicast pairs 148", buf, bytes, d_out, nsm);
+    run<3, 16384, 8>("bulk all-same 148", buf, bytes, d_out, nsm);
+    run<4, 32768, 6, 256>("tensor contiguous 148", buf, bytes, d_out, nsm);
+    run<4, 32768, 6, 256>("tensor contiguous 32", buf, bytes, d_out, 32);
     return 0;
 }

@@ -30,6 +30,12 @@ def main():
     print("kb  tma:empty-ok  mma:full-ok")
     for kb in range(64):
         print(f"{kb:3d} {t[128 + kb]:10d} {t[kb]:10d}")
+    g = t[4096:4096 + 4 * 148].reshape(-1, 4)
+    g = g[g[:, 1] > 0]
+    t0 = g[:, 0].min()
+    print(f"CTAs {len(g)}: start spread {(g[:, 0].max() - t0) / 1e3:.2f} us, end min/med/max "
+          f"{(g[:, 1].min() - t0) / 1e3:.2f}/{(np.median(g[:, 1]) - t0) / 1e3:.2f}/{(g[:, 1].max() - t0) / 1e3:.2f} us, "
+          f"cycles min/max {g[:, 3].min()}/{g[:, 3].max()}, clock {np.median(g[:, 3] / ((g[:, 1] - g[:, 0]) + 1)):.3f} GHz")
     print("epi acc_full", t[200], "epi drained", t[201], "end epi/mma/tma", t[202], t[203], t[204], "exit", t[205])
 
 
