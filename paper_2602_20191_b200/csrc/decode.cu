@@ -116,9 +116,15 @@ struct RDParams {
 // shared memory (rank 0 + rank 1, fixed order), then silu(H + b1) . w2 over the tile's 16 hidden
 // units gives the tile's partial scores spart[mt][t][k] (router.hpp:63-76).  The decode GEMM sums
 // the tiles in order, adds b2 and applies gate_hard(delta).
+constexpr int kRdRing = 6;  // router: 32-k chunks in flight per lane
+__device__ __forceinline__ void rd_cp16(void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+}
 template <int NT>
 __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWarps)
     router_dec_kernel(const __grid_constant__ RDParams p) {
+    extern __shared__ __align__(16) uint8_t rd_ring[];  // [warps][kRdRing][32 lanes][2 + NT] x 16 B
     grid_dep_launch();  // the decode GEMM may start prefetching codes right away
     const int tcta = blockIdx.x;
     auto TRM = [&](int i) {
@@ -128,9 +134,14 @@ __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWar
     __shared__ float red[kRdWarps][kRdRows][8 * NT + 1];
     __shared__ float hsum[8 * NT][kRdRows];
     __shared__ float act[8 * NT][kRdRows];
+    __shared__ float sb1[kRdRows], sw2[kRdRows * (MOBI_MAX_SLICES - 1)];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, c = lane & 3;
     const uint32_t rank = cluster_ctarank();
     const int mt = blockIdx.x / kRdCluster;
+    // the tile's b1 and w2 go out first: the epilogue must not wait on dependent global loads
+    float pb1 = 0.f, pw2 = 0.f;
+    if (tid < kRdRows) pb1 = __ldg(p.b1 + (int64_t)mt * kRdRows + tid);
+    if (tid < kRdRows * p.nr) pw2 = __ldg(p.w2 + (int64_t)mt * kRdRows * p.nr + tid);
     const int64_t nchunks = p.in_pad / 32;
     const int64_t per_cta = (nchunks + kRdCluster - 1) / kRdCluster;
     const int64_t per_warp = (per_cta + kRdWarps - 1) / kRdWarps;
@@ -144,32 +155,50 @@ __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWar
         for (int n = 0; n < NT; ++n) acc4[a][n][0] = acc4[a][n][1] = acc4[a][n][2] = acc4[a][n][3] = 0.f;
     const __nv_bfloat16* ar0 = p.w1t + ((int64_t)mt * kRdRows + g) * p.in_pad + 8 * c;
     const __nv_bfloat16* ar1 = ar0 + 8 * p.in_pad;
-    constexpr int U = NT == 1 ? 8 : NT == 2 ? 4 : 2;
-    for (int64_t q = q0; q < q1; q += U) {
-        uint4 a0[U], a1[U], b[U][NT];
+    // Per-lane cp.async ring: chunk q's two w1 vectors (rows g, g+8) and the X vectors of the lane's
+    // tokens (8n + g) go into the lane's own slot, so kRdRing chunks are in flight per lane whatever
+    // the register budget (the kernel shares the SM with the decode GEMM) and no lane reads another's.
+    constexpr int kSlot = 2 + NT;  // 16-byte vectors per lane per chunk
+    uint4* ring = reinterpret_cast<uint4*>(rd_ring) + ((size_t)warp * kRdRing * 32 + lane) * kSlot;
+    int64_t qi = q0;  // next chunk to issue
+    auto issue = [&]() {
+        uint4* d = ring + (size_t)((qi - q0) % kRdRing) * 32 * kSlot;
+        const int64_t k = qi * 32;
+        rd_cp16(d, ar0 + k, true);
+        rd_cp16(d + 1, ar1 + k, true);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t k = (q + u) * 32;
-            const bool ok = q + u < q1;
-            a0[u] = ok ? ldg_stream(ar0 + k) : make_uint4(0, 0, 0, 0);
-            a1[u] = ok ? ldg_stream(ar1 + k) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-            for (int n = 0; n < NT; ++n) {
-                const int tok = 8 * n + g;
-                b[u][n] = (ok && tok < p.T && k + 8 * c < p.in)
-                              ? __ldg(reinterpret_cast<const uint4*>(p.x + (int64_t)tok * p.in + k + 8 * c))
-                              : make_uint4(0, 0, 0, 0);
-            }
+        for (int n = 0; n < NT; ++n) {
+            const int tok = 8 * n + g;
+            const bool ok = tok < p.T && k + 8 * c < p.in;
+            rd_cp16(d + 2 + n, ok ? (const void*)(p.x + (int64_t)tok * p.in + k + 8 * c) : (const void*)p.x, ok);
         }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        ++qi;
+    };
+    while (qi < q1 && qi < q0 + kRdRing - 1) issue();
+    for (int64_t q = q0; q < q1; ++q) {
+        const int64_t pend = qi - 1 - q;  // groups allowed to stay in flight
+        if (pend >= kRdRing - 2) asm volatile("cp.async.wait_group %0;" ::"n"(kRdRing - 2) : "memory");
+        else if (pend >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+        else if (pend >= 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+        const uint4* d = ring + (size_t)((q - q0) % kRdRing) * 32 * kSlot;
+        const uint4 a0 = d[0], a1 = d[1];
+        auto step = [&](float (&c0)[NT][4], float (&c1)[NT][4]) {
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
-                mma_bf16(acc4[(u & 1) * 2][n], a0[u].x, a1[u].x, a0[u].y, a1[u].y, b[u][n].x, b[u][n].y);
-                mma_bf16(acc4[(u & 1) * 2 + 1][n], a0[u].z, a1[u].z, a0[u].w, a1[u].w, b[u][n].z, b[u][n].w);
+                const uint4 b = d[2 + n];
+                mma_bf16(c0[n], a0.x, a1.x, a0.y, a1.y, b.x, b.y);
+                mma_bf16(c1[n], a0.z, a1.z, a0.w, a1.w, b.z, b.w);
             }
+        };
+        if (((q - q0) & 1) == 0) step(acc4[0], acc4[1]);
+        else step(acc4[2], acc4[3]);
+        if (qi < q1) issue();  // refills the slot just read (its data is in registers)
     }
     TRM(1);
+    if (tid < kRdRows) sb1[tid] = pb1;
+    if (tid < kRdRows * p.nr) sw2[tid] = pw2;
     float acc[NT][4];
 #pragma unroll
     for (int n = 0; n < NT; ++n)
@@ -200,7 +229,7 @@ __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWar
             const int64_t j = (int64_t)mt * kRdRows + row;
             float v = 0.f;
             if (j < p.h && tok < p.T) {
-                const float a = hsum[tok][row] + other + p.b1[j];
+                const float a = hsum[tok][row] + other + sb1[row];
                 v = a * __fdividef(1.f, 1.f + __expf(-a));
             }
             act[tok][row] = v;
@@ -212,7 +241,7 @@ __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWar
         const int tok = i / p.nr, k = i % p.nr;
         float s = 0.f;
 #pragma unroll
-        for (int row = 0; row < kRdRows; ++row) s += act[tok][row] * p.w2[((int64_t)mt * kRdRows + row) * p.nr + k];
+        for (int row = 0; row < kRdRows; ++row) s += act[tok][row] * sw2[row * p.nr + k];
         p.spart[((int64_t)mt * p.T + tok) * p.nr + k] = s;
     }
     TRM(2);
@@ -1019,6 +1048,7 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
     const int n_mt = (int)(L->h_pad / kRdRows);
     const dim3 grid((unsigned)(n_mt * kRdCluster));
     static bool carve = false;
+    auto smem_of = [](int nt) { return (size_t)kRdWarps * kRdRing * 32 * (2 + nt) * 16; };
     if (!carve) {  // run with the SM configured for maximum shared memory, so the decode GEMM that
                    // follows (PDL) can be co-resident while the router streams w1
         MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -1027,14 +1057,17 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
                                        (int)cudaSharedmemCarveoutMaxShared));
         MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<4>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                        (int)cudaSharedmemCarveoutMaxShared));
+        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(1)));
+        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(2)));
+        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(4)));
         carve = true;
     }
     if (T <= 8)
-        router_dec_kernel<1><<<grid, 32 * kRdWarps, 0, st>>>(p);
+        router_dec_kernel<1><<<grid, 32 * kRdWarps, smem_of(1), st>>>(p);
     else if (T <= 16)
-        router_dec_kernel<2><<<grid, 32 * kRdWarps, 0, st>>>(p);
+        router_dec_kernel<2><<<grid, 32 * kRdWarps, smem_of(2), st>>>(p);
     else
-        router_dec_kernel<4><<<grid, 32 * kRdWarps, 0, st>>>(p);
+        router_dec_kernel<4><<<grid, 32 * kRdWarps, smem_of(4), st>>>(p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

@@ -133,8 +133,17 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
             ip += 32;
         }
     };
-    {   // the group constants (s, s*z) of this warp's groups for the tile's 32 rows, read once for all
-        // slices: 16-byte cp.asyncs that join item 0's group (waited for before the first group ends)
+    // (0) stage, as one cp.async group: this warp's k range of every token's bf16 X into its x16 rows
+    //     (converted in place below) and the group constants (s, s*z) of the warp's groups for the
+    //     tile's 32 rows (read once for all slices); slice 1's first items follow as their own groups
+    const int64_t k_lo = (int64_t)kw0 * kKBlock, k_hi = (int64_t)kw1 * kKBlock;
+    for (int t = 0; t < T; ++t)
+        for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256) {
+            const bool ok = k < p.in;
+            cp_async16(x16 + (size_t)t * p.xs_stride + k, ok ? (const void*)(p.x + (int64_t)t * p.in + k) : (const void*)p.x,
+                       ok);
+        }
+    {
         const int64_t g0 = p.single_group ? 0 : (int64_t)kw0 * kKBlock / p.gs;
         const int64_t g1 = p.single_group ? 1 : ((int64_t)kw1 * kKBlock + p.gs - 1) / p.gs;
         if (kw1 > kw0)
@@ -142,68 +151,60 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
                 cp_async16(gcs + (i / 16) * 32 + (i % 16) * 2,
                            p.gconst + (g0 + i / 16) * p.out_pad + (int64_t)rt * 32 + (i % 16) * 2, true);
     }
+    cp_commit();
     while (pi < kw1 - kw0 && pi < kD2Ring - 1) issue(pi++);
+    switch (pi) {  // the staging group has landed (slice 1's items may still be in flight)
+        case 0: cp_wait<0>(); break;
+        case 1: cp_wait<1>(); break;
+        case 2: cp_wait<2>(); break;
+        case 3: cp_wait<3>(); break;
+        case 4: cp_wait<4>(); break;
+        case 5: cp_wait<5>(); break;
+        case 6: cp_wait<6>(); break;
+        default: cp_wait<7>(); break;
+    }
+    __syncwarp();
     float xg0 = 0.f, xg1 = 0.f, xu0 = 0.f, xu1 = 0.f;
     int grp = 0, gleft = 0;
 
-    // (1) this warp's k range of X: bf16 -> per-token 2^-e scale (max over the range) -> fp16 in smem,
-    //     and per-(token, k-block) sums of the fp16 values
-    constexpr int XV = 2;  // 16-byte vectors per lane per token held in registers (k range <= 512)
-    const int64_t k_lo = (int64_t)kw0 * kKBlock, k_hi = (int64_t)kw1 * kKBlock;
-    uint4 xv[kD2MaxT][XV];  // every token's first vectors in flight at once
-#pragma unroll
-    for (int t = 0; t < kD2MaxT; ++t)
-#pragma unroll
-        for (int j = 0; j < XV; ++j) {
-            const int64_t k = k_lo + lane * 8 + 256 * j;
-            xv[t][j] = (t < T && k < k_hi && k < p.in)
-                           ? __ldg(reinterpret_cast<const uint4*>(p.x + (int64_t)t * p.in + k)) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-    for (int t = 0; t < kD2MaxT; ++t) {
-        if (t >= T) break;
-        const __nv_bfloat16* xt = p.x + (int64_t)t * p.in;
+    // (1) X in place: bf16 -> per-token 2^-e scale (max over the warp's range) x 4^-ss per k-step ->
+    //     fp16, and per-(token, k-block) sums of the fp16 values (scaled, and rescaled by 4^ss)
+    const int lss = (lane & 7) >> 1;  // k-step ss = (k % 64) / 16 of this lane's 8 values
+    for (int t = 0; t < T; ++t) {
+        __half* xrow = x16 + (size_t)t * p.xs_stride;
         float m = 0.f;
-        auto vmax = [&](const uint4& q) {
+        for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256) {
+            const uint4 q = *reinterpret_cast<const uint4*>(xrow + k);
             const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const float2 f2 = __bfloat1622float2(b[j]);
                 m = fmaxf(m, fmaxf(fabsf(f2.x), fabsf(f2.y)));
             }
-        };
-#pragma unroll
-        for (int j = 0; j < XV; ++j) vmax(xv[t][j]);
-        for (int64_t k = k_lo + lane * 8 + 256 * XV; k < k_hi && k < p.in; k += 256)
-            vmax(__ldg(reinterpret_cast<const uint4*>(xt + k)));
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (t == 0) TRM(6);
         int e = 0;
         if (m > 0.f && isfinite(m)) e = ilogbf(m) - 14;
-        // k-step ss = (k % 64) / 16 of this lane's 8 values is (lane % 8) / 2: scaled by 4^-ss
-        const int lss = (lane & 7) >> 1;
         const float sc = ldexpf(1.f, -e - 2 * lss);
         if (lane == 0) es_s[warp][t] = ldexpf(1.f, e);
-        auto conv = [&](const uint4& q) {
-            uint4 o;
-            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
-            __half2* hh = reinterpret_cast<__half2*>(&o);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float2 f2 = __bfloat1622float2(b[j]);
-                hh[j] = __floats2half2_rn(f2.x * sc, f2.y * sc);
-            }
-            return o;
-        };
-        // store fp16 and sum each k-block's 64 fp16 values: 8 lanes x 8 values, fixed butterfly
-        auto store_sum = [&](int64_t k, const uint4& q) {
-            const uint4 o = conv(q);
-            const __half2* hh = reinterpret_cast<const __half2*>(&o);
+        for (int64_t k0 = k_lo; k0 < k_hi; k0 += 256) {  // warp-uniform trip count
+            const int64_t k = k0 + lane * 8;
+            uint4 o = make_uint4(0, 0, 0, 0);
             float sacc = 0.f;
+            if (k < k_hi) {
+                const uint4 q = *reinterpret_cast<const uint4*>(xrow + k);
+                const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+                __half2* hh = reinterpret_cast<__half2*>(&o);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float2 f2 = __half22float2(hh[j]);
-                sacc += f2.x + f2.y;
+                for (int j = 0; j < 4; ++j) {
+                    const float2 f2 = __bfloat1622float2(b[j]);
+                    hh[j] = __floats2half2_rn(f2.x * sc, f2.y * sc);
+                    const float2 h2 = __half22float2(hh[j]);
+                    sacc += h2.x + h2.y;
+                }
+                *reinterpret_cast<uint4*>(xrow + k) = o;
             }
             float uacc = sacc * (float)(1 << (2 * lss));  // exact: power-of-two rescale
             sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
@@ -212,18 +213,9 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
             uacc += __shfl_xor_sync(0xffffffffu, uacc, 1);
             uacc += __shfl_xor_sync(0xffffffffu, uacc, 2);
             uacc += __shfl_xor_sync(0xffffffffu, uacc, 4);
-            if (k < k_hi) {
-                *reinterpret_cast<uint4*>(x16 + (size_t)t * p.xs_stride + k) = o;
-                if ((lane & 7) == 0) xsum[t * p.kblocks + k / kKBlock] = make_float2(sacc, uacc);
-            }
-        };
-#pragma unroll
-        for (int j = 0; j < XV; ++j) store_sum(k_lo + lane * 8 + 256 * j, xv[t][j]);
-        for (int64_t k0 = k_lo + 256 * XV; k0 < k_hi; k0 += 256) {  // warp-uniform trip count
-            const int64_t k = k0 + lane * 8;
-            const uint4 q = (k < k_hi && k < p.in) ? __ldg(reinterpret_cast<const uint4*>(xt + k)) : make_uint4(0, 0, 0, 0);
-            store_sum(k, q);
+            if (k < k_hi && (lane & 7) == 0) xsum[t * p.kblocks + k / kKBlock] = make_float2(sacc, uacc);
         }
+        if (t == T - 1) TRM(7);
     }
     for (int64_t k = (int64_t)kw0 * kKBlock + lane * 8; k < (int64_t)kw1 * kKBlock; k += 256)
         *reinterpret_cast<uint4*>(x16 + (size_t)kD2MaxT * p.xs_stride + k) = make_uint4(0, 0, 0, 0);

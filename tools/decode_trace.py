@@ -59,7 +59,7 @@ def main():
             print("gemm SM clock (GHz, median over CTAs):", float(np.median(cyc[ok] / ns[ok])))
     if False: show("gemm", g, ["start", "x prep done", "grid dep resolved", "main loop done", "end"])
     show("planes", g, ["start", "x prep done", "slice 1 done", "grid dep resolved", "union slices done", "end",
-                       "item 0 data ready", "last slice-1 item ready"])
+                       "x token 0 loaded", "x last token loaded"])
     it = full.astype(np.int64)[24576:24576 + 16 * 32 * 4].reshape(16, 32, 4)
     for w in (0, 7, 15):
         print(f"planes CTA0 warp {w} per item (cycles rel. item 0: pre-wait, data, mma done, issued):")
