@@ -125,7 +125,6 @@ template <int NT>
 __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWarps)
     router_dec_kernel(const __grid_constant__ RDParams p) {
     extern __shared__ __align__(16) uint8_t rd_ring[];  // [warps][kRdRing][32 lanes][2 + NT] x 16 B
-    grid_dep_launch();  // the decode GEMM may start prefetching codes right away
     const int tcta = blockIdx.x;
     auto TRM = [&](int i) {
         if (p.trace && threadIdx.x == 0) p.trace[(size_t)tcta * 8 + i] = gtimer();
@@ -161,21 +160,40 @@ __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWar
     constexpr int kSlot = 2 + NT;  // 16-byte vectors per lane per chunk
     uint4* ring = reinterpret_cast<uint4*>(rd_ring) + ((size_t)warp * kRdRing * 32 + lane) * kSlot;
     int64_t qi = q0;  // next chunk to issue
-    auto issue = [&]() {
-        uint4* d = ring + (size_t)((qi - q0) % kRdRing) * 32 * kSlot;
-        const int64_t k = qi * 32;
-        rd_cp16(d, ar0 + k, true);
-        rd_cp16(d + 1, ar1 + k, true);
+    auto issue_w = [&](int64_t qq) {
+        uint4* d = ring + (size_t)((qq - q0) % kRdRing) * 32 * kSlot;
+        rd_cp16(d, ar0 + qq * 32, true);
+        rd_cp16(d + 1, ar1 + qq * 32, true);
+    };
+    auto issue_x = [&](int64_t qq) {
+        uint4* d = ring + (size_t)((qq - q0) % kRdRing) * 32 * kSlot;
+        const int64_t k = qq * 32;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
             const int tok = 8 * n + g;
             const bool ok = tok < p.T && k + 8 * c < p.in;
             rd_cp16(d + 2 + n, ok ? (const void*)(p.x + (int64_t)tok * p.in + k + 8 * c) : (const void*)p.x, ok);
         }
+    };
+    auto issue = [&]() {
+        issue_w(qi);
+        issue_x(qi);
         asm volatile("cp.async.commit_group;" ::: "memory");
         ++qi;
     };
-    while (qi < q1 && qi < q0 + kRdRing - 1) issue();
+    // w1 is a constant: the first chunks stream in before the previous kernel in the stream has
+    // finished (PDL); X -- possibly that kernel's output -- and every write wait for it
+    while (qi < q1 && qi < q0 + kRdRing - 1) {
+        issue_w(qi++);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    grid_dep_wait();
+    // only now may the decode GEMM launch: it reads X before its own wait, and X may be the output of
+    // the kernel this one just waited for
+    grid_dep_launch();
+    for (int64_t qq = q0; qq < qi; ++qq) issue_x(qq);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // the prologue chunks (w1 + X) have landed
     for (int64_t q = q0; q < q1; ++q) {
         const int64_t pend = qi - 1 - q;  // groups allowed to stay in flight
         if (pend >= kRdRing - 2) asm volatile("cp.async.wait_group %0;" ::"n"(kRdRing - 2) : "memory");
@@ -1062,12 +1080,27 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
         MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(4)));
         carve = true;
     }
-    if (T <= 8)
-        router_dec_kernel<1><<<grid, 32 * kRdWarps, smem_of(1), st>>>(p);
-    else if (T <= 16)
-        router_dec_kernel<2><<<grid, 32 * kRdWarps, smem_of(2), st>>>(p);
-    else
-        router_dec_kernel<4><<<grid, 32 * kRdWarps, smem_of(4), st>>>(p);
+    // PDL: the router's CTAs may launch while the previous kernel (e.g. the last layer's decode GEMM)
+    // drains and prefetch their first w1 chunks; griddepcontrol.wait guards X and every write
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(32 * kRdWarps);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (T <= 8) {
+        cfg.dynamicSmemBytes = smem_of(1);
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_dec_kernel<1>, p));
+    } else if (T <= 16) {
+        cfg.dynamicSmemBytes = smem_of(2);
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_dec_kernel<2>, p));
+    } else {
+        cfg.dynamicSmemBytes = smem_of(4);
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_dec_kernel<4>, p));
+    }
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     return MOBI_OK;

@@ -111,6 +111,7 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
         if (p.trace && tid == 0) p.trace[(size_t)(2048 + rt) * 8 + i] = gtimer2();
     };
     TRM(0);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next router may prefetch its w1
     const int T = p.T;
     const int kw0 = (int)((int64_t)warp * p.kblocks / kD2Warps), kw1 = (int)((int64_t)(warp + 1) * p.kblocks / kD2Warps);
     // streamed items (see (2)-(4) below): item i = (slice slist[i / nk], k-block kw0 + i % nk); issued in
@@ -170,53 +171,75 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
     // (1) X in place: bf16 -> per-token 2^-e scale (max over the warp's range) x 4^-ss per k-step ->
     //     fp16, and per-(token, k-block) sums of the fp16 values (scaled, and rescaled by 4^ss)
     const int lss = (lane & 7) >> 1;  // k-step ss = (k % 64) / 16 of this lane's 8 values
-    for (int t = 0; t < T; ++t) {
-        __half* xrow = x16 + (size_t)t * p.xs_stride;
-        float m = 0.f;
-        for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256) {
-            const uint4 q = *reinterpret_cast<const uint4*>(xrow + k);
-            const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+    // every token's max-reduction and conversion proceed side by side (independent shuffle chains)
+    float sc[kD2MaxT];
+    {
+        float m[kD2MaxT];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float2 f2 = __bfloat1622float2(b[j]);
-                m = fmaxf(m, fmaxf(fabsf(f2.x), fabsf(f2.y)));
-            }
+        for (int t = 0; t < kD2MaxT; ++t) {
+            m[t] = 0.f;
+            if (t < T)
+                for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256) {
+                    const uint4 q = *reinterpret_cast<const uint4*>(x16 + (size_t)t * p.xs_stride + k);
+                    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float2 f2 = __bfloat1622float2(b[j]);
+                        m[t] = fmaxf(m[t], fmaxf(fabsf(f2.x), fabsf(f2.y)));
+                    }
+                }
         }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (t == 0) TRM(6);
-        int e = 0;
-        if (m > 0.f && isfinite(m)) e = ilogbf(m) - 14;
-        const float sc = ldexpf(1.f, -e - 2 * lss);
-        if (lane == 0) es_s[warp][t] = ldexpf(1.f, e);
-        for (int64_t k0 = k_lo; k0 < k_hi; k0 += 256) {  // warp-uniform trip count
-            const int64_t k = k0 + lane * 8;
-            uint4 o = make_uint4(0, 0, 0, 0);
-            float sacc = 0.f;
-            if (k < k_hi) {
-                const uint4 q = *reinterpret_cast<const uint4*>(xrow + k);
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int t = 0; t < kD2MaxT; ++t) m[t] = fmaxf(m[t], __shfl_xor_sync(0xffffffffu, m[t], o));
+        TRM(6);
+#pragma unroll
+        for (int t = 0; t < kD2MaxT; ++t) {
+            // e = exponent(max) - 14 (the max lands in [2^14, 2^15)), clamped so 2^-e stays a normal
+            // float for tiny activations; powers of two built from exponent bits (no libm calls)
+            int e = 0;
+            if (m[t] > 0.f && m[t] <= 3.0e38f) e = max(((__float_as_int(m[t]) >> 23) & 0xff) - 127 - 14, -100);
+            sc[t] = __int_as_float((127 - e - 2 * lss) << 23);
+            if (lane == 0 && t < T) es_s[warp][t] = __int_as_float((127 + e) << 23);
+        }
+    }
+    for (int64_t k0 = k_lo; k0 < k_hi; k0 += 256) {  // warp-uniform trip count
+        const int64_t k = k0 + lane * 8;
+        float sacc[kD2MaxT], uacc[kD2MaxT];
+#pragma unroll
+        for (int t = 0; t < kD2MaxT; ++t) {
+            sacc[t] = 0.f;
+            if (t < T && k < k_hi) {
+                __half* xp = x16 + (size_t)t * p.xs_stride + k;
+                const uint4 q = *reinterpret_cast<const uint4*>(xp);
                 const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+                uint4 o;
                 __half2* hh = reinterpret_cast<__half2*>(&o);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const float2 f2 = __bfloat1622float2(b[j]);
-                    hh[j] = __floats2half2_rn(f2.x * sc, f2.y * sc);
+                    hh[j] = __floats2half2_rn(f2.x * sc[t], f2.y * sc[t]);
                     const float2 h2 = __half22float2(hh[j]);
-                    sacc += h2.x + h2.y;
+                    sacc[t] += h2.x + h2.y;
                 }
-                *reinterpret_cast<uint4*>(xrow + k) = o;
+                *reinterpret_cast<uint4*>(xp) = o;
             }
-            float uacc = sacc * (float)(1 << (2 * lss));  // exact: power-of-two rescale
-            sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
-            sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
-            sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
-            uacc += __shfl_xor_sync(0xffffffffu, uacc, 1);
-            uacc += __shfl_xor_sync(0xffffffffu, uacc, 2);
-            uacc += __shfl_xor_sync(0xffffffffu, uacc, 4);
-            if (k < k_hi && (lane & 7) == 0) xsum[t * p.kblocks + k / kKBlock] = make_float2(sacc, uacc);
+            uacc[t] = sacc[t] * (float)(1 << (2 * lss));  // exact: power-of-two rescale
         }
-        if (t == T - 1) TRM(7);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1)
+#pragma unroll
+            for (int t = 0; t < kD2MaxT; ++t) {
+                sacc[t] += __shfl_xor_sync(0xffffffffu, sacc[t], o);
+                uacc[t] += __shfl_xor_sync(0xffffffffu, uacc[t], o);
+            }
+        if (k < k_hi && (lane & 7) == 0)
+#pragma unroll
+            for (int t = 0; t < kD2MaxT; ++t)
+                if (t < T) xsum[t * p.kblocks + k / kKBlock] = make_float2(sacc[t], uacc[t]);
     }
+    TRM(7);
     for (int64_t k = (int64_t)kw0 * kKBlock + lane * 8; k < (int64_t)kw1 * kKBlock; k += 256)
         *reinterpret_cast<uint4*>(x16 + (size_t)kD2MaxT * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
     __syncwarp();
