@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -679,11 +680,16 @@ int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta
     // token chunks pipelined over three streams: the host->device copy of chunk i+1 and the
     // device->host copy of chunk i-1 overlap the forward of chunk i (tokens are independent, so the
     // chunked result is identical to the whole-batch one)
-    const int nch = T >= 2048 ? 4 : (T >= 1024 ? 2 : 1);
+    static const int nch_env = [] {  // development knob: MOBI_E2E_CHUNKS overrides the chunk count
+        const char* e = std::getenv("MOBI_E2E_CHUNKS");
+        return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
+    }();
+    const int nch = nch_env ? (int)std::min<int64_t>(nch_env, std::max<int64_t>(1, T / 256))
+                            : (T >= 2048 ? 4 : (T >= 1024 ? 2 : 1));
     if (nch > 1 && !L->s_h2d) {
         MOBI_CUDA(cudaStreamCreateWithFlags(&L->s_h2d, cudaStreamNonBlocking));
         MOBI_CUDA(cudaStreamCreateWithFlags(&L->s_d2h, cudaStreamNonBlocking));
-        for (int i = 0; i < 8; ++i) MOBI_CUDA(cudaEventCreateWithFlags(&L->ev_pipe[i], cudaEventDisableTiming));
+        for (int i = 0; i < 17; ++i) MOBI_CUDA(cudaEventCreateWithFlags(&L->ev_pipe[i], cudaEventDisableTiming));
     }
     if (nch == 1) {
         MOBI_CUDA(cudaMemcpyAsync(L->x_dev, xsrc, xb, cudaMemcpyHostToDevice, st));
@@ -693,9 +699,9 @@ int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta
         if (masks_host) MOBI_CUDA(cudaMemcpyAsync(masks_host, mdev, (size_t)T, cudaMemcpyDeviceToHost, st));
     } else {
         const int64_t step = round_up(cdiv(T, (int64_t)nch), 256);
-        cudaEvent_t* ev = L->ev_pipe;  // [0..3] copied in, [4..7] computed
-        MOBI_CUDA(cudaEventRecord(ev[7], st));  // prior work on the caller's stream
-        MOBI_CUDA(cudaStreamWaitEvent(L->s_h2d, ev[7], 0));
+        cudaEvent_t* ev = L->ev_pipe;  // [0..7] copied in, [8..15] computed, [16] prior work
+        MOBI_CUDA(cudaEventRecord(ev[16], st));  // prior work on the caller's stream
+        MOBI_CUDA(cudaStreamWaitEvent(L->s_h2d, ev[16], 0));
         int c = 0;
         for (int64_t t0 = 0; t0 < T; t0 += step, ++c) {
             const int64_t n = std::min(step, T - t0);
@@ -708,8 +714,8 @@ int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta
             int rc = run_layer(L, reinterpret_cast<uint8_t*>(L->x_dev) + xo, n, delta, nullptr,
                                reinterpret_cast<uint8_t*>(L->y_dev) + yo, mdev ? mdev + t0 : nullptr, st);
             if (rc) return rc;
-            MOBI_CUDA(cudaEventRecord(ev[4 + c], st));
-            MOBI_CUDA(cudaStreamWaitEvent(L->s_d2h, ev[4 + c], 0));
+            MOBI_CUDA(cudaEventRecord(ev[8 + c], st));
+            MOBI_CUDA(cudaStreamWaitEvent(L->s_d2h, ev[8 + c], 0));
             MOBI_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ydst) + yo,
                                       reinterpret_cast<const uint8_t*>(L->y_dev) + yo, (size_t)(n * L->out * 2),
                                       cudaMemcpyDeviceToHost, L->s_d2h));
