@@ -25,7 +25,7 @@ namespace {
 using namespace sm100;
 
 constexpr int kD2Warps = 16, kD2Threads = 32 * kD2Warps;  // 16 warps: 4 per scheduler (latency hiding)
-constexpr int kD2MaxT = 4;
+constexpr int kD2MaxT = 8;  // the m16n8k16 N dimension: one token per column
 constexpr int kD2Acc = 3 * 2 * 4;  // per lane: y over the token's slices, A, B  ([2][4] each)
 
 struct D2Params {
@@ -82,14 +82,15 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-constexpr int kD2Ring = 8;  // (slice, k-block) items in flight per lane (16 B each): 64 KiB per CTA
+constexpr int kD2Ring = 6;  // (slice, k-block) items in flight per lane (16 B each): 48 KiB per CTA
+                            // (sized so the router's ring fits on the same SM at T = 8)
 
 // cp.async.wait_group for "at most n groups pending": exact in the steady state (n = kD2Ring - 2),
 // conservatively rounded down near the ends of the stream (no jump table in the item loop)
 __device__ __forceinline__ void cp_wait_dyn(int n) {
-    static_assert(kD2Ring == 8, "staged waits assume an 8-deep ring");
-    if (n >= 6) cp_wait<6>();
-    else if (n >= 3) cp_wait<3>();
+    static_assert(kD2Ring == 6, "staged waits assume a 6-deep ring");
+    if (n >= 4) cp_wait<4>();
+    else if (n >= 2) cp_wait<2>();
     else if (n >= 1) cp_wait<1>();
     else cp_wait<0>();
 }
@@ -98,7 +99,7 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
     extern __shared__ __align__(16) uint8_t smem[];
     __half* x16 = reinterpret_cast<__half*>(smem);                                   // [kD2MaxT + 1][xs_stride]
     // [T][kblocks] {sum of the k-step-scaled fp16 X (offset cancellation), unscaled sum (A, B)}
-    float2* xsum = reinterpret_cast<float2*>(smem + (size_t)(kD2MaxT + 1) * p.xs_stride * 2);
+    float2* xsum = reinterpret_cast<float2*>(smem + (size_t)(p.T + 1) * p.xs_stride * 2);  // rows 0..T-1 + zeros
     float* red = reinterpret_cast<float*>(smem);  // [warps][kD2Acc][32], aliases x16 after the passes
     __shared__ float es_s[kD2Warps][kD2MaxT];
     __shared__ float s_score[kD2MaxT][MOBI_MAX_SLICES - 1];
@@ -160,9 +161,7 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
         case 2: cp_wait<2>(); break;
         case 3: cp_wait<3>(); break;
         case 4: cp_wait<4>(); break;
-        case 5: cp_wait<5>(); break;
-        case 6: cp_wait<6>(); break;
-        default: cp_wait<7>(); break;
+        default: cp_wait<5>(); break;
     }
     __syncwarp();
     float xg0 = 0.f, xg1 = 0.f, xu0 = 0.f, xu1 = 0.f;
@@ -171,77 +170,82 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
     // (1) X in place: bf16 -> per-token 2^-e scale (max over the warp's range) x 4^-ss per k-step ->
     //     fp16, and per-(token, k-block) sums of the fp16 values (scaled, and rescaled by 4^ss)
     const int lss = (lane & 7) >> 1;  // k-step ss = (k % 64) / 16 of this lane's 8 values
-    // every token's max-reduction and conversion proceed side by side (independent shuffle chains)
-    float sc[kD2MaxT];
-    {
-        float m[kD2MaxT];
+    // four tokens at a time: their max-reductions and conversions proceed side by side
+    // (independent shuffle chains)
+    for (int tb = 0; tb < T; tb += 4) {
+        float sc[4];
+        {
+            float m[4];
 #pragma unroll
-        for (int t = 0; t < kD2MaxT; ++t) {
-            m[t] = 0.f;
-            if (t < T)
-                for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256) {
-                    const uint4 q = *reinterpret_cast<const uint4*>(x16 + (size_t)t * p.xs_stride + k);
+            for (int i = 0; i < 4; ++i) {
+                const int t = tb + i;
+                m[i] = 0.f;
+                if (t < T)
+                    for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256) {
+                        const uint4 q = *reinterpret_cast<const uint4*>(x16 + (size_t)t * p.xs_stride + k);
+                        const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float2 f2 = __bfloat1622float2(b[j]);
+                            m[i] = fmaxf(m[i], fmaxf(fabsf(f2.x), fabsf(f2.y)));
+                        }
+                    }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) m[i] = fmaxf(m[i], __shfl_xor_sync(0xffffffffu, m[i], o));
+            if (tb == 0) TRM(6);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                // e = exponent(max) - 14 (the max lands in [2^14, 2^15)), clamped so 2^-e stays a
+                // normal float for tiny activations; powers of two from exponent bits (no libm calls)
+                int e = 0;
+                if (m[i] > 0.f && m[i] <= 3.0e38f) e = max(((__float_as_int(m[i]) >> 23) & 0xff) - 127 - 14, -100);
+                sc[i] = __int_as_float((127 - e - 2 * lss) << 23);
+                if (lane == 0 && tb + i < T) es_s[warp][tb + i] = __int_as_float((127 + e) << 23);
+            }
+        }
+        for (int64_t k0 = k_lo; k0 < k_hi; k0 += 256) {  // warp-uniform trip count
+            const int64_t k = k0 + lane * 8;
+            float sacc[4], uacc[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int t = tb + i;
+                sacc[i] = 0.f;
+                if (t < T && k < k_hi) {
+                    __half* xp = x16 + (size_t)t * p.xs_stride + k;
+                    const uint4 q = *reinterpret_cast<const uint4*>(xp);
                     const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+                    uint4 o;
+                    __half2* hh = reinterpret_cast<__half2*>(&o);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const float2 f2 = __bfloat1622float2(b[j]);
-                        m[t] = fmaxf(m[t], fmaxf(fabsf(f2.x), fabsf(f2.y)));
+                        hh[j] = __floats2half2_rn(f2.x * sc[i], f2.y * sc[i]);
+                        const float2 h2 = __half22float2(hh[j]);
+                        sacc[i] += h2.x + h2.y;
                     }
+                    *reinterpret_cast<uint4*>(xp) = o;
                 }
-        }
+                uacc[i] = sacc[i] * (float)(1 << (2 * lss));  // exact: power-of-two rescale
+            }
 #pragma unroll
-        for (int o = 16; o; o >>= 1)
+            for (int o = 1; o < 8; o <<= 1)
 #pragma unroll
-            for (int t = 0; t < kD2MaxT; ++t) m[t] = fmaxf(m[t], __shfl_xor_sync(0xffffffffu, m[t], o));
-        TRM(6);
-#pragma unroll
-        for (int t = 0; t < kD2MaxT; ++t) {
-            // e = exponent(max) - 14 (the max lands in [2^14, 2^15)), clamped so 2^-e stays a normal
-            // float for tiny activations; powers of two built from exponent bits (no libm calls)
-            int e = 0;
-            if (m[t] > 0.f && m[t] <= 3.0e38f) e = max(((__float_as_int(m[t]) >> 23) & 0xff) - 127 - 14, -100);
-            sc[t] = __int_as_float((127 - e - 2 * lss) << 23);
-            if (lane == 0 && t < T) es_s[warp][t] = __int_as_float((127 + e) << 23);
-        }
-    }
-    for (int64_t k0 = k_lo; k0 < k_hi; k0 += 256) {  // warp-uniform trip count
-        const int64_t k = k0 + lane * 8;
-        float sacc[kD2MaxT], uacc[kD2MaxT];
-#pragma unroll
-        for (int t = 0; t < kD2MaxT; ++t) {
-            sacc[t] = 0.f;
-            if (t < T && k < k_hi) {
-                __half* xp = x16 + (size_t)t * p.xs_stride + k;
-                const uint4 q = *reinterpret_cast<const uint4*>(xp);
-                const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
-                uint4 o;
-                __half2* hh = reinterpret_cast<__half2*>(&o);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float2 f2 = __bfloat1622float2(b[j]);
-                    hh[j] = __floats2half2_rn(f2.x * sc[t], f2.y * sc[t]);
-                    const float2 h2 = __half22float2(hh[j]);
-                    sacc[t] += h2.x + h2.y;
+                for (int i = 0; i < 4; ++i) {
+                    sacc[i] += __shfl_xor_sync(0xffffffffu, sacc[i], o);
+                    uacc[i] += __shfl_xor_sync(0xffffffffu, uacc[i], o);
                 }
-                *reinterpret_cast<uint4*>(xp) = o;
-            }
-            uacc[t] = sacc[t] * (float)(1 << (2 * lss));  // exact: power-of-two rescale
+            if (k < k_hi && (lane & 7) == 0)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (tb + i < T) xsum[(tb + i) * p.kblocks + k / kKBlock] = make_float2(sacc[i], uacc[i]);
         }
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1)
-#pragma unroll
-            for (int t = 0; t < kD2MaxT; ++t) {
-                sacc[t] += __shfl_xor_sync(0xffffffffu, sacc[t], o);
-                uacc[t] += __shfl_xor_sync(0xffffffffu, uacc[t], o);
-            }
-        if (k < k_hi && (lane & 7) == 0)
-#pragma unroll
-            for (int t = 0; t < kD2MaxT; ++t)
-                if (t < T) xsum[t * p.kblocks + k / kKBlock] = make_float2(sacc[t], uacc[t]);
     }
     TRM(7);
     for (int64_t k = (int64_t)kw0 * kKBlock + lane * 8; k < (int64_t)kw1 * kKBlock; k += 256)
-        *reinterpret_cast<uint4*>(x16 + (size_t)kD2MaxT * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(x16 + (size_t)T * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
     __syncwarp();
 
     // yt: this lane's outputs (rows g/g+8 of both row groups, tokens 2c/2c+1) over the slices each
@@ -253,7 +257,7 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
         for (int j = 0; j < 4; ++j) yt[rg][j] = ys[rg][j] = A[rg][j] = B[rg][j] = D[rg][j] = 0.f;
     TRM(1);
     const int g = lane >> 2, c = lane & 3;
-    const int tg = g < T ? g : kD2MaxT;  // B-fragment token row (row kD2MaxT is zeros)
+    const int tg = g < T ? g : T;  // B-fragment token row (row T is zeros)
     const int t0 = 2 * c, t1 = 2 * c + 1;  // this lane's D columns (tokens)
     const float es0 = t0 < T ? es_s[warp][t0] : 0.f, es1 = t1 < T ? es_s[warp][t1] : 0.f;
     const __half* xr = x16 + (size_t)tg * p.xs_stride + 2 * c;
@@ -421,14 +425,25 @@ int d2_groups_per_warp(const mobi_layer* L) {
     return (int)(kpw / L->gs + 2);
 }
 
+// dynamic shared memory: x16 rows 0..T (row T zeros) + per-(token, k-block) sums, aliased after the
+// item loop by the warps' reduction buffer; then the staged group constants and the per-lane rings
+struct D2Smem {
+    size_t gcs_off, ring_off, total;
+};
+static D2Smem d2_smem(const mobi_layer* L, int64_t T) {
+    const size_t xs = (size_t)(T + 1) * (L->in_pad + 8) * 2 + (size_t)T * L->kblocks * 8;
+    D2Smem m;
+    m.gcs_off = (std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16;
+    m.ring_off = m.gcs_off + (size_t)kD2Warps * d2_groups_per_warp(L) * 32 * 8;
+    m.total = m.ring_off + (size_t)kD2Warps * kD2Ring * 32 * 16;
+    return m;
+}
+
 bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
     if (T < 1 || T > kD2MaxT || !L->dplanes || L->E > 4) return false;
     if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
     if (!L->single_group && L->gs % kKBlock != 0) return false;
-    const size_t xs = (size_t)(kD2MaxT + 1) * (L->in_pad + 8) * 2 + (size_t)2 * kD2MaxT * L->kblocks * 4;
-    const size_t sm = (std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16 +
-                      (size_t)kD2Warps * d2_groups_per_warp(L) * 32 * 8 + (size_t)kD2Warps * kD2Ring * 32 * 16;
-    return sm <= 200 * 1024;
+    return d2_smem(L, T).total <= 200 * 1024;
 }
 
 int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
@@ -462,11 +477,11 @@ int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const
     p.vmask = (1 << (L->nr + 1)) - 1;
     p.n_rt32 = (int)(L->out_pad / 32);
     p.xs_stride = (int)(L->in_pad + 8);
-    const size_t xs = (size_t)(kD2MaxT + 1) * p.xs_stride * 2 + (size_t)2 * kD2MaxT * L->kblocks * 4;
     p.gpw = d2_groups_per_warp(L);
-    p.gcs_off = (int64_t)((std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16);
-    p.ring_off = p.gcs_off + (int64_t)kD2Warps * p.gpw * 32 * 8;
-    const size_t smem = (size_t)p.ring_off + (size_t)kD2Warps * kD2Ring * 32 * 16;
+    const D2Smem sm = d2_smem(L, T);
+    p.gcs_off = (int64_t)sm.gcs_off;
+    p.ring_off = (int64_t)sm.ring_off;
+    const size_t smem = sm.total;
     static bool attr = false;
     if (!attr) {
         MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));

@@ -48,6 +48,8 @@ DEC_SHAPES = [  # (out, in, gs, hidden, T)
     (130, 200, 256, 50, 3),     # single group (gs > in), in not a multiple of 64
     (300, 136, 136, 24, 31),    # single group, in % 64 != 0, partial last row tile
     (14336 // 4, 4096, 128, 0, 4),  # more row tiles than SMs' worth of k-blocks per tile
+    (4096, 4096, 128, 0, 8),    # slice-plane kernel at its 8-token limit
+    (1024, 14336, 128, 0, 6),   # in = 14336 (down projection), planes kernel
 ]
 
 
