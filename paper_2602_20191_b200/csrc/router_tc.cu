@@ -8,6 +8,7 @@
 // E-1 partial scores, written to s_part[hidden tile][token][j] and summed in a fixed order by the
 // bucket kernel (deterministic, no atomics).
 #include <algorithm>
+#include <cstdlib>
 
 #include "mobi_internal.cuh"
 #include "sm100.cuh"
@@ -32,11 +33,16 @@ constexpr int kRProducers = MOBI_RTMA2 ? 2 : 1;
 constexpr int kRThreads = 192 + 32 * (kRProducers - 1);
 constexpr int kRWarpTma = 4, kRWarpMma = 5, kRWarpTma2 = 6;
 constexpr int kRSmem = RS * 2 * kAB + 1024 + 256 + 2 * RN * 16;  // + per-tile {b1, w2} staging
+constexpr int kRecvBytes = RM * RN * 4;  // one peer's partial H tile, [RN/4][RM][4] floats
+constexpr int kMaxCsplit = 1 + (RS * 2 * kAB) / kRecvBytes;  // the peers' partials fit rank 0's ring
+static_assert(kMaxCsplit >= 3, "ring too small for a 3-way cluster split");
 
 struct RParams {
     int64_t T, h, h_pad;
     int kblocks, n_mt, n_nt, nr;
     int nsplit, kb_per;  // split-K (decode-size T): raw hidden partials to hpart, reduced below
+    int csplit;          // > 1: the nsplit (= csplit) CTAs of a tile form a cluster; ranks 1.. ship their
+                         // partial H to rank 0 through DSMEM and rank 0 runs the fused epilogue
     const float* b1;
     const float* w2;
     float* s_part;
@@ -66,6 +72,8 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     uint64_t* acc_full = bars + 2 * RS; // [2]
     uint64_t* acc_empty = acc_full + 2; // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* peer_go = acc_empty + 4;    // cluster split-K: rank 0's ring is free for the peers' partials
+    uint64_t* recv_full = acc_empty + 5;  // cluster split-K (rank 0): the peers' partials have landed
     // [2][RN] {b1[j], w2[j][0..2]} of the tile's hidden units, staged by the epilogue warps while the
     // mainloop runs so the SiLU.w2 epilogue reads them as smem broadcasts (not dependent global loads)
     float4* cst = reinterpret_cast<float4*>(smem + RS * 2 * kAB + 256);
@@ -80,7 +88,11 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 4);
         }
+        mbar_init(peer_go, 1);
+        mbar_init(recv_full, 1);
         fence_barrier_init();
+        // rank 0 expects the peers' partials as bulk-copy bytes (complete_tx may land before or after)
+        if (p.csplit > 1 && cluster_ctarank() == 0) mbar_arrive_expect_tx(recv_full, (p.csplit - 1) * kRecvBytes);
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
@@ -89,12 +101,14 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     unsigned long long g_start = 0;
     if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_start));
     auto TR = [&](int i) {
-        if (p.trace && blockIdx.x == 0 && (threadIdx.x % 32) == 0) p.trace[i] = (unsigned long long)(clock64() - t_start);
+        if (p.trace && blockIdx.x < 2 && (threadIdx.x % 32) == 0)
+            p.trace[blockIdx.x * 1024 + i] = (unsigned long long)(clock64() - t_start);
     };
     if (warp == kRWarpMma) tmem_alloc(tmem_slot, 512);  // all columns: base is the constant 0
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (p.csplit > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
     if (*tmem_slot != 0) __trap();
     constexpr uint32_t tmem = 0;
     const int total = p.n_mt * p.n_nt * p.nsplit;
@@ -174,7 +188,9 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             const int64_t t = (int64_t)mt * RM + 32 * q + lane;
             const int64_t h0 = (int64_t)nt * RN;
             const int nh = (int)std::min<int64_t>(RN, p.h - h0);
-            if (p.nsplit == 1) {
+            const bool clus = p.csplit > 1;
+            const uint32_t crank = clus ? cluster_ctarank() : 0u;
+            if (p.nsplit == 1 || (clus && crank == 0)) {
                 const int et = 32 * q + lane;  // epilogue warps are 0..3
                 float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (et < nh) {
@@ -190,7 +206,44 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             mbar_wait(&acc_full[buf], (tc >> 1) & 1);
             if (q == 0) TR(200);
             tc_fence_after();
-            if (p.nsplit > 1) {  // raw hidden partial H[t, h0..h0+nh) for this k-split
+            // cluster split-K receive buffer: rank 0's (idle) stage ring, [peer][column / 4][token row][4]
+            const uint32_t recv0 = smem_u32(smem);
+            if (clus && crank != 0) {  // peer: ship this K-range's H[128 x RN] to rank 0
+                // stage it in this CTA's own (idle) ring as [column / 4][token row][4] floats, then one
+                // bulk copy into rank 0's ring once rank 0 has released it
+                for (int c0 = 0; c0 < RN; c0 += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(tmem + lane_base + buf * RN + c0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        *reinterpret_cast<uint4*>(smem + ((size_t)((c0 + j) / 4) * RM + 32 * q + lane) * 16) =
+                            make_uint4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                }
+                tc_fence_before();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> bulk copy
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (q == 0) TR(210);
+                if (q == 0 && lane == 0) {
+                    mbar_arrive(&acc_empty[buf]);
+                    mbar_wait_cluster(peer_go, 0);
+                    TR(211);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            mapa_shared(recv0 + (crank - 1) * (uint32_t)kRecvBytes, 0)),
+                        "r"(recv0), "r"((uint32_t)kRecvBytes), "r"(mapa_shared(smem_u32(recv_full), 0))
+                        : "memory");
+                }
+                continue;
+            }
+            if (clus) {  // rank 0: every MMA of this CTA has completed (acc_full), so no stage of the ring
+                         // is read or written any more -- hand it to the peers, wait for their partials
+                if (q == 0 && lane > 0 && lane < p.csplit)
+                    mbar_arrive_cluster(mapa_shared(smem_u32(peer_go), (uint32_t)lane));
+                mbar_wait_cluster(recv_full, 0);
+                if (q == 0) TR(212);
+            }
+            if (p.nsplit > 1 && !clus) {  // raw hidden partial H[t, h0..h0+nh) for this k-split
                 for (int c0 = 0; c0 < nh; c0 += 32) {
                     uint32_t v[32];
                     tmem_ld32(tmem + lane_base + buf * RN + c0, v);
@@ -212,10 +265,23 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
                 uint32_t v[32];
                 tmem_ld32(tmem + lane_base + buf * RN + c0, v);
                 tmem_ld_wait();
+                for (int r = 1; r < p.csplit; ++r) {  // H = rank 0 + rank 1 + ... (fixed order)
+                    const uint8_t* src = smem + (size_t)(r - 1) * kRecvBytes;
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        const float4 f = *reinterpret_cast<const float4*>(
+                            src + ((size_t)((c0 + j) / 4) * RM + 32 * q + lane) * 16);
+                        v[j] = __float_as_uint(__uint_as_float(v[j]) + f.x);
+                        v[j + 1] = __float_as_uint(__uint_as_float(v[j + 1]) + f.y);
+                        v[j + 2] = __float_as_uint(__uint_as_float(v[j + 2]) + f.z);
+                        v[j + 3] = __float_as_uint(__uint_as_float(v[j + 3]) + f.w);
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const float4 c = cst[buf * RN + c0 + j];  // zero beyond nh: contributes nothing
-                    const float a = __uint_as_float(v[j]) + c.x;
+                    const float4 c = cst[buf * RN + c0 + j];
+                    // TMEM columns past the tile's hidden units are undefined: clamp them to 0
+                    const float a = (c0 + j < nh ? __uint_as_float(v[j]) : 0.f) + c.x;
                     const float sv = a * __fdividef(1.f, 1.f + __expf(-a));
                     part0 = fmaf(sv, c.y, part0);
                     part1 = fmaf(sv, c.z, part1);
@@ -264,6 +330,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     TR(202 + (warp == kRWarpMma) + 2 * (warp == kRWarpTma));
     tc_fence_before();
     __syncthreads();
+    if (p.csplit > 1) cluster_sync();  // no CTA leaves while a peer may still address its shared memory
     if (warp == kRWarpMma) tmem_dealloc(tmem, 512);
     TR(205);
     if (p.trace && threadIdx.x == 0) {  // per-CTA wall marks (ns) + SM id
@@ -321,6 +388,12 @@ bool router_tc_supported(const mobi_layer* L, const void* x) {
     return (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 }
 
+// development switch (MOBI_ROUTER_CSPLIT): 0 = no cluster split-K in the prefill router, 1 = by tile count
+int g_router_csplit = [] {
+    const char* e = std::getenv("MOBI_ROUTER_CSPLIT");
+    return e ? std::atoi(e) : 1;
+}();
+
 int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, float* scores_out,
                      uint8_t* masks_out, bool* masks_ready, cudaStream_t st, unsigned long long* trace,
                      bool fuse_bucket) {
@@ -364,13 +437,45 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
     L->htiles = p.n_nt;
     // split K when the tile grid cannot fill the SMs (decode-size T)
     p.nsplit = 1;
-    if (T <= 64 && L->hpart) p.nsplit = std::max(1, std::min(16, sm_count() / (p.n_mt * p.n_nt)));
+    p.csplit = 1;
+    const int tiles = p.n_mt * p.n_nt;
+    if (T <= 64 && L->hpart) {
+        p.nsplit = std::max(1, std::min(16, sm_count() / tiles));
+    } else if (g_router_csplit == 2 && p.kblocks >= 8) {  // experiment: fixed 2-way split at every T
+        p.csplit = 2;
+        p.nsplit = 2;
+    } else if (g_router_csplit == 1 && 2 * tiles <= sm_count() && p.kblocks >= 8) {
+        // too few tiles to fill the SMs: split K over a cluster of 2-3 CTAs per tile (DSMEM reduction
+        // into rank 0, which keeps the fused gate/histogram epilogue).  The split depends on the tile
+        // count only, so outputs are identical for every T of the same regime.
+        p.csplit = std::min(kMaxCsplit, std::min(3, sm_count() / tiles));
+        p.nsplit = p.csplit;
+    }
     p.kb_per = (p.kblocks + p.nsplit - 1) / p.nsplit;
     p.nsplit = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty splits
-    const int total = p.n_mt * p.n_nt * p.nsplit;
+    if (p.csplit > 1) p.csplit = p.nsplit;
+    const int total = tiles * p.nsplit;
+    const bool clus = p.csplit > 1;
+    if (masks_ready) *masks_ready = p.nsplit == 1 || clus;
+    if (p.nsplit != 1 && !clus) p.hist = nullptr;
+    if (clus) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)total);
+        cfg.blockDim = dim3(kRThreads);
+        cfg.dynamicSmemBytes = kRSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)p.csplit;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_tc_kernel, tmap_x, *L->tmap_w1, p));
+        ++L->last_launches;
+        return MOBI_OK;
+    }
     const int grid = std::min(total, sm_count());
-    if (masks_ready) *masks_ready = p.nsplit == 1;
-    if (p.nsplit != 1) p.hist = nullptr;
     router_tc_kernel<<<grid, kRThreads, kRSmem, st>>>(tmap_x, *L->tmap_w1, p);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;

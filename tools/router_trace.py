@@ -36,6 +36,8 @@ def main():
     print(f"CTAs {len(g)}: start spread {(g[:, 0].max() - t0) / 1e3:.2f} us, end min/med/max "
           f"{(g[:, 1].min() - t0) / 1e3:.2f}/{(np.median(g[:, 1]) - t0) / 1e3:.2f}/{(g[:, 1].max() - t0) / 1e3:.2f} us, "
           f"cycles min/max {g[:, 3].min()}/{g[:, 3].max()}, clock {np.median(g[:, 3] / ((g[:, 1] - g[:, 0]) + 1)):.3f} GHz")
+    print("cluster: rank0 recv_full", t[212], " rank1 acc_full", t[1024 + 200], "staged", t[1024 + 210],
+          "peer_go", t[1024 + 211], "rank1 mma end", t[1024 + 203], "tma end", t[1024 + 204])
     print("epi acc_full", t[200], "epi drained", t[201], "end epi/mma/tma", t[202], t[203], t[204], "exit", t[205])
 
 
