@@ -540,6 +540,7 @@ int mobi_layer_destroy(mobi_layer_t L) {
     dfree(L->w2);
     dfree(L->b2);
     if (L->tmap_w1) delete L->tmap_w1;
+    if (L->tmap_w1_64) delete L->tmap_w1_64;
     if (L->x_dev) cudaFree(L->x_dev);
     if (L->y_dev) cudaFree(L->y_dev);
     if (L->h_x) cudaFreeHost(L->h_x);

@@ -123,7 +123,8 @@ struct mobi_layer {
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // mobi_forward_host pipeline (created on first use)
     cudaEvent_t ev_pipe[17] = {};  // e2e pipeline: [0..7] chunk copied in, [8..15] computed, [16] prior work
     CUtensorMap* tmap_x = nullptr;  // host copies, rebuilt when the workspace changes
-    CUtensorMap* tmap_w1 = nullptr; // router w1t (fixed for the layer's lifetime)
+    CUtensorMap* tmap_w1 = nullptr; // router w1t (fixed for the layer's lifetime), 128-row boxes
+    CUtensorMap* tmap_w1_64 = nullptr;  // the same with 64-row boxes (CTA-pair router, N = 128)
     CUtensorMap* tmap_x2 = nullptr; // xperm, 16-row boxes (CTA-pair GEMM)
     int32_t last_launches = 0;
     int64_t device_bytes = 0;

@@ -345,6 +345,192 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     }
 }
 
+// CTA-pair router tile (cta_group::2): M = 256 tokens (128 per CTA, each CTA TMA-loads its own X
+// rows) x N = PN hidden units (each CTA TMA-loads PN/2 rows of w1, the tensor cores exchange the
+// halves), fp32 D in each CTA's TMEM for its own 128 tokens.  Per k-block a CTA takes in 16 KiB of X
+// + PN/4 KiB of w1 for 128 x PN outputs, against 32 KiB for 128 x 128 in the 1-CTA kernel, whose
+// tiles sit at the measured ~71 B/cycle/SM L2->SMEM limit.  The leader's MMA thread issues for the
+// pair; both CTAs run the same fused SiLU.w2 / gate / histogram epilogue on their own tokens.
+template <int PN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    router_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                      const RParams p) {
+    constexpr int kBB = PN / 2 * kKBlock * 2;  // w1 half per stage
+    constexpr int kStg = kAB + kBB;
+    constexpr int NS = (RS * 2 * kAB) / kStg;   // stages in the same ring footprint
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RS * 2 * kAB);
+    uint64_t* full = bars;                 // [NS] leader: both CTAs' bytes of the stage
+    uint64_t* empty = bars + NS;           // [NS] each CTA: the pair's MMAs are done with the stage
+    uint64_t* acc_full = bars + 2 * NS;    // [2] each CTA
+    uint64_t* acc_empty = acc_full + 2;    // [2] leader: 4 epilogue warps x 2 CTAs drained the buffer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    float4* cst = reinterpret_cast<float4*>(smem + RS * 2 * kAB + 1024);  // [2][PN] {b1, w2[0..2]}
+    const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 8);
+        }
+        fence_barrier_init();
+        prefetch_tmap(&tmap_a);
+        prefetch_tmap(&tmap_b);
+    }
+    pdl_trigger();  // the gather may launch and start loading its rows
+    if (warp == kRWarpMma) tmem_alloc_2sm(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    if (*tmem_slot != 0) __trap();
+    constexpr uint32_t tmem = 0;
+    const int n_mp = (p.n_mt + 1) / 2;
+    const int total = n_mp * p.n_nt;
+    const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+    auto tile_of = [&](int pair, int& mp, int& nt) {
+        mp = pair % n_mp;
+        nt = pair / n_mp;
+    };
+    if (warp == kRWarpTma) {
+        const uint32_t full_leader = mapa_shared(smem_u32(full), 0);
+        uint32_t it = 0;
+        for (int pair = cid; pair < total; pair += ncl) {
+            int mp, nt;
+            tile_of(pair, mp, nt);
+            for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+                const int s = it % NS;
+                mbar_wait(&empty[s], ((it / NS) & 1) ^ 1);
+                if (elect_one_sync()) {
+                    uint8_t* a = smem + s * kStg;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * kStg);
+                    tma_load_2d_2sm(a, &tmap_a, full_leader + s * 8, kb * kKBlock, (2 * mp + (int)rank) * RM);
+                    tma_load_2d_2sm(a + kAB, &tmap_b, full_leader + s * 8, kb * kKBlock,
+                                    nt * PN + (int)rank * (PN / 2));
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == kRWarpMma) {
+        if (rank == 0) {
+            uint32_t it = 0, tc = 0;
+            constexpr uint32_t idesc = idesc_f16(2 * RM, PN, 1);
+            for (int pair = cid; pair < total; pair += ncl, ++tc) {
+                const int buf = tc & 1;
+                mbar_wait_cluster(&acc_empty[buf], ((tc >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
+                    const int s = it % NS;
+                    mbar_wait_cluster(&full[s], (it / NS) & 1);
+                    tc_fence_after();
+                    if (elect_one_sync()) {
+                        const uint32_t a = smem_u32(smem + s * kStg);
+                        const uint64_t adesc = sdesc_sw128(a), bdesc = sdesc_sw128(a + kAB);
+#pragma unroll
+                        for (int j = 0; j < kKBlock / 16; ++j)
+                            mma_ss_f16_2sm(tmem + buf * PN, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc,
+                                           (kb != 0) || (j != 0));
+                        mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
+                        if (kb == p.kblocks - 1) mma_commit_2sm_mc(&acc_full[buf], (uint16_t)0x3);
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        const int q = warp % 4;
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
+        uint32_t tc = 0;
+        for (int pair = cid; pair < total; pair += ncl, ++tc) {
+            int mp, nt;
+            tile_of(pair, mp, nt);
+            const int mt = 2 * mp + (int)rank;
+            const int buf = tc & 1;
+            const int64_t t = (int64_t)mt * RM + 32 * q + lane;
+            const int64_t h0 = (int64_t)nt * PN;
+            for (int et = 32 * q + lane; et < PN; et += 128) {
+                float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int64_t hj = h0 + et;
+                c.x = __ldg(p.b1 + hj);
+                c.y = __ldg(p.w2 + hj * p.nr);
+                if (p.nr > 1) c.z = __ldg(p.w2 + hj * p.nr + 1);
+                if (p.nr > 2) c.w = __ldg(p.w2 + hj * p.nr + 2);
+                cst[buf * PN + et] = c;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(&acc_full[buf], (tc >> 1) & 1);
+            tc_fence_after();
+            float part0 = 0.f, part1 = 0.f, part2 = 0.f;
+            for (int c0 = 0; c0 < PN; c0 += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + buf * PN + c0, v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float4 c = cst[buf * PN + c0 + j];
+                    const float a = __uint_as_float(v[j]) + c.x;
+                    const float sv = a * __fdividef(1.f, 1.f + __expf(-a));
+                    part0 = fmaf(sv, c.y, part0);
+                    part1 = fmaf(sv, c.z, part1);
+                    part2 = fmaf(sv, c.w, part2);
+                }
+            }
+            const float part[3] = {part0, part1, part2};
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0)
+                    mbar_arrive(&acc_empty[buf]);
+                else
+                    mbar_arrive_cluster(acc_empty_leader + buf * 8);
+            }
+            if (t < p.T) {
+#pragma unroll
+                for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
+                    if (k < p.nr) p.s_part[((int64_t)nt * p.T + t) * p.nr + k] = part[k];
+            }
+            // last hidden tile of token tile mt: scores and slice masks for its tokens
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (q == 0 && lane == 0) s_last = (int64_t)mt * RM < p.T && atomicAdd(&p.cnt[mt], 1) == p.n_nt - 1;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (s_last) {
+                __threadfence();
+                int mk = 2 * kMaxBuckets;  // no token
+                if (t < p.T) {
+                    int m = 1;
+                    for (int k = 0; k < p.nr; ++k) {
+                        float sc = 0.f;
+                        for (int j = 0; j < p.n_nt; ++j) sc += __ldcg(p.s_part + ((int64_t)j * p.T + t) * p.nr + k);
+                        sc += __ldg(p.b2 + k);
+                        if (p.scores_out) p.scores_out[t * p.nr + k] = sc;
+                        if ((sc - p.delta) > 0.f) m |= 1 << (k + 1);
+                    }
+                    p.masks[t] = (uint8_t)m;
+                    if (p.masks_out) p.masks_out[t] = (uint8_t)m;
+                    mk = m;
+                }
+                if (q == 0 && lane == 0) p.cnt[mt] = 0;
+                if (p.hist) {
+                    const unsigned peers = __match_any_sync(0xffffffffu, mk);
+                    if (mk < 2 * kMaxBuckets && lane == __ffs(peers) - 1) atomicAdd(&p.hist[mk], __popc(peers));
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();  // the peer's remote arrivals and TMEM use are over before either CTA releases it
+    if (warp == kRWarpMma) tmem_dealloc_2sm(tmem, 512);
+}
+
 // split-K finish: H = sum_ks hpart (fixed order) -> silu(H + b1) . w2 -> s_part[nt][t][k]
 __global__ void __launch_bounds__(RN) router_reduce_kernel(const float* __restrict__ hpart, int nsplit, int64_t T,
                                                            int64_t h, int64_t h_pad, const float* __restrict__ b1,
@@ -387,6 +573,13 @@ int sm_count() {
 bool router_tc_supported(const mobi_layer* L, const void* x) {
     return (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 }
+
+// development switch (MOBI_ROUTER_PAIR): 0 = never use the CTA-pair router
+int g_router_pair = [] {
+    const char* e = std::getenv("MOBI_ROUTER_PAIR");
+    return e ? std::atoi(e) : 1;
+}();
+constexpr int r2_smem(int pn) { return RS * 2 * kAB + 1024 + 1024 + 2 * pn * 16; }
 
 // development switch (MOBI_ROUTER_CSPLIT): 0 = no cluster split-K in the prefill router, 1 = by tile count
 int g_router_csplit = [] {
@@ -438,6 +631,48 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
     // split K when the tile grid cannot fill the SMs (decode-size T)
     p.nsplit = 1;
     p.csplit = 1;
+    // CTA-pair tiles when they alone fill the SMs (fewer w1 bytes per SM per flop, see the kernel)
+    const int n_mp = (int)cdiv(T, 2 * RM);
+    int pn = 0;
+    if (g_router_pair && T > 64 && L->h % 256 == 0 && n_mp * (int)(L->h / 256) * 2 >= sm_count())
+        pn = 256;
+    else if (g_router_pair && T > 64 && L->h % 128 == 0 && n_mp * (int)(L->h / 128) * 2 >= sm_count() * 3 / 4)
+        pn = 128;
+    if (pn == 128 && !L->tmap_w1_64) {
+        L->tmap_w1_64 = new CUtensorMap;
+        int rc2 = make_tmap_2d(L->tmap_w1_64, L->w1t, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L->h_pad, L->in_pad, 64);
+        if (rc2) {
+            delete L->tmap_w1_64;
+            L->tmap_w1_64 = nullptr;
+            return rc2;
+        }
+    }
+    if (pn) {
+        p.n_nt = (int)(L->h / pn);
+        L->htiles = p.n_nt;
+        if (masks_ready) *masks_ready = true;
+        const int grid = 2 * std::min(n_mp * p.n_nt, sm_count() / 2);
+        if (pn == 256) {
+            static bool a256 = false;
+            if (!a256) {
+                MOBI_CUDA(cudaFuncSetAttribute(router_tc2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               r2_smem(256)));
+                a256 = true;
+            }
+            router_tc2_kernel<256><<<grid, 192, r2_smem(256), st>>>(tmap_x, *L->tmap_w1, p);
+        } else {
+            static bool a128 = false;
+            if (!a128) {
+                MOBI_CUDA(cudaFuncSetAttribute(router_tc2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               r2_smem(128)));
+                a128 = true;
+            }
+            router_tc2_kernel<128><<<grid, 192, r2_smem(128), st>>>(tmap_x, *L->tmap_w1_64, p);
+        }
+        MOBI_LAUNCH_CHECK();
+        ++L->last_launches;
+        return MOBI_OK;
+    }
     const int tiles = p.n_mt * p.n_nt;
     if (T <= 64 && L->hpart) {
         p.nsplit = std::max(1, std::min(16, sm_count() / tiles));
