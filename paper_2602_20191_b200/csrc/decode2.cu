@@ -25,7 +25,9 @@ namespace {
 using namespace sm100;
 
 constexpr int kD2Warps = 16, kD2Threads = 32 * kD2Warps;  // 16 warps: 4 per scheduler (latency hiding)
-constexpr int kD2MaxT = 8;  // the m16n8k16 N dimension: one token per column
+constexpr int kD2MaxT = 8;  // tokens per launch: the m16n8k16 N dimension, one token per column
+constexpr int kD2MaxLaunchT = 16;  // 9..16 tokens: two launches of up to kD2MaxT tokens (measured ~7% faster
+                                   // than the merged-code kernel; beyond 16 the merged-code kernel wins)
 constexpr int kD2Acc = 3 * 2 * 4;  // per lane: y over the token's slices, A, B  ([2][4] each)
 
 struct D2Params {
@@ -43,6 +45,7 @@ struct D2Params {
     int64_t out, out_pad, in, in_pad, kblocks, gs;
     float delta;
     int single_group, T, E, nr, n_mt, vmask, n_rt32, xs_stride;
+    int t0, t_all;    // this launch's first token and the batch size (router partials are [n_mt][t_all][nr])
     int gpw;          // groups per warp (bound) for the staged constants
     int64_t gcs_off;  // byte offset of the staged constants in dynamic smem
     int64_t ring_off; // byte offset of the per-lane cp.async rings
@@ -281,7 +284,8 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
                 for (int i = warp; i < T * p.nr; i += kD2Warps) {
                     const int t = i / p.nr, k = i % p.nr;
                     float sc = 0.f;
-                    for (int q = lane; q < p.n_mt; q += 32) sc += __ldcg(p.spart + ((int64_t)q * T + t) * p.nr + k);
+                    for (int q = lane; q < p.n_mt; q += 32)
+                        sc += __ldcg(p.spart + ((int64_t)q * p.t_all + p.t0 + t) * p.nr + k);
 #pragma unroll
                     for (int o = 16; o; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
                     if (lane == 0) s_score[t][k] = sc + __ldg(p.b2 + k);
@@ -440,65 +444,72 @@ static D2Smem d2_smem(const mobi_layer* L, int64_t T) {
 }
 
 bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
-    if (T < 1 || T > kD2MaxT || !L->dplanes || L->E > 4) return false;
+    if (T < 1 || T > kD2MaxLaunchT || !L->dplanes || L->E > 4) return false;
     if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
     if (!L->single_group && L->gs % kKBlock != 0) return false;
-    return d2_smem(L, T).total <= 200 * 1024;
+    return d2_smem(L, std::min<int64_t>(T, kD2MaxT)).total <= 200 * 1024;
 }
 
 int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
                          uint8_t* masks_out, float* scores_out, __nv_bfloat16* y, bool pdl, cudaStream_t st,
                          unsigned long long* trace) {
-    D2Params p{};
-    p.trace = trace;
-    p.dplanes = reinterpret_cast<const uint4*>(L->dplanes);
-    p.gconst = L->gconst;
-    p.x = x;
-    p.masks = given_masks;
-    p.spart = L->dec_spart;
-    p.b2 = L->b2;
-    p.masks_dev = L->masks;
-    p.masks_out = masks_out;
-    p.scores_out = scores_out;
-    p.y = y;
-    p.mt = L->mtab;
-    p.out = L->out;
-    p.out_pad = L->out_pad;
-    p.in = L->in;
-    p.in_pad = L->in_pad;
-    p.kblocks = L->kblocks;
-    p.gs = L->gs;
-    p.delta = delta;
-    p.single_group = L->single_group ? 1 : 0;
-    p.T = (int)T;
-    p.E = L->E;
-    p.nr = L->nr;
-    p.n_mt = (int)(L->h_pad / 16);
-    p.vmask = (1 << (L->nr + 1)) - 1;
-    p.n_rt32 = (int)(L->out_pad / 32);
-    p.xs_stride = (int)(L->in_pad + 8);
-    p.gpw = d2_groups_per_warp(L);
-    const D2Smem sm = d2_smem(L, T);
-    p.gcs_off = (int64_t)sm.gcs_off;
-    p.ring_off = (int64_t)sm.ring_off;
-    const size_t smem = sm.total;
+    // one launch per group of <= kD2MaxT tokens (the m16n8k16 N width); each decides its tokens' masks
+    // from the router partials and streams only its own union of slices.  Under PDL the later groups'
+    // prologue (activation staging, slice 1) overlaps the previous group's tail.
     static bool attr = false;
     if (!attr) {
         MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr = true;
     }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)cdiv(L->out, 32));
-    cfg.blockDim = dim3(kD2Threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
-    MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_planes_kernel, p));
-    ++L->last_launches;
+    for (int64_t t0 = 0; t0 < T; t0 += kD2MaxT) {
+        const int64_t Tg = std::min<int64_t>(kD2MaxT, T - t0);
+        D2Params p{};
+        p.trace = t0 == 0 ? trace : nullptr;
+        p.dplanes = reinterpret_cast<const uint4*>(L->dplanes);
+        p.gconst = L->gconst;
+        p.x = x + t0 * L->in;
+        p.masks = given_masks ? given_masks + t0 : nullptr;
+        p.spart = L->dec_spart;
+        p.b2 = L->b2;
+        p.masks_dev = L->masks + t0;
+        p.masks_out = masks_out ? masks_out + t0 : nullptr;
+        p.scores_out = scores_out ? scores_out + t0 * L->nr : nullptr;
+        p.y = y + t0 * L->out;
+        p.mt = L->mtab;
+        p.out = L->out;
+        p.out_pad = L->out_pad;
+        p.in = L->in;
+        p.in_pad = L->in_pad;
+        p.kblocks = L->kblocks;
+        p.gs = L->gs;
+        p.delta = delta;
+        p.single_group = L->single_group ? 1 : 0;
+        p.T = (int)Tg;
+        p.t0 = (int)t0;
+        p.t_all = (int)T;
+        p.E = L->E;
+        p.nr = L->nr;
+        p.n_mt = (int)(L->h_pad / 16);
+        p.vmask = (1 << (L->nr + 1)) - 1;
+        p.n_rt32 = (int)(L->out_pad / 32);
+        p.xs_stride = (int)(L->in_pad + 8);
+        p.gpw = d2_groups_per_warp(L);
+        const D2Smem sm = d2_smem(L, Tg);
+        p.gcs_off = (int64_t)sm.gcs_off;
+        p.ring_off = (int64_t)sm.ring_off;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)cdiv(L->out, 32));
+        cfg.blockDim = dim3(kD2Threads);
+        cfg.dynamicSmemBytes = sm.total;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = pdl ? 1 : 0;
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_planes_kernel, p));
+        ++L->last_launches;
+    }
     return MOBI_OK;
 }
 
