@@ -388,7 +388,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 src_r[c] = ok ? __ldg(p.perm + tt.row0 + 32 * c + lane) : -1;
                 es_r[c] = ok ? __ldg(p.escale + tt.row0 + 32 * c + lane) : 0.f;
             }
-            mbar_wait_cluster(acc_full, tc & 1);
+            // CTA-scope wait: the arrival is the tensor core's commit and TMEM visibility comes from
+            // tcgen05.fence (a cluster-scope acquire would invalidate L1 on every poll)
+            mbar_wait(acc_full, tc & 1);
             tc_fence_after();
             epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
             uint32_t va[16], vb[16];
