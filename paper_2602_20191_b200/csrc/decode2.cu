@@ -445,6 +445,14 @@ static D2Smem d2_smem(const mobi_layer* L, int64_t T) {
 
 bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
     if (T < 1 || T > kD2MaxLaunchT || !L->dplanes || L->E > 4) return false;
+    // several launches only pay while each is a single wave of row tiles (gate/up: 448 tiles, not)
+    static const int n_sm = [] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+    }();
+    if (T > kD2MaxT && cdiv(L->out, (int64_t)32) > n_sm) return false;
     if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
     if (!L->single_group && L->gs % kKBlock != 0) return false;
     return d2_smem(L, std::min<int64_t>(T, kD2MaxT)).total <= 200 * 1024;

@@ -11,6 +11,6 @@ for args in "--tokens 1" "--tokens 2" "--tokens 4" "--tokens 8" "--tokens 16" "-
 done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 30 -c 30 --csv --log-file gpurun_out/p_launches.csv python bench.py --steps 12 --warmup 3 --no-cpu-baseline --no-e2e --ring 1 > /dev/null 2>&1; echo launches rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:mobi_gemm_tc2 -s 3 -c 1 -o gpurun_out/p_gemm python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e --ring 1 > /dev/null 2>&1; echo gemm rc=$?
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:router_tc -s 3 -c 1 -o gpurun_out/p_router python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e --ring 1 > /dev/null 2>&1; echo router rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:router_tc2 -s 3 -c 1 -o gpurun_out/p_router python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-e2e --ring 1 > /dev/null 2>&1; echo router rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"decode_planes|router_dec" -s 4 -c 2 -o gpurun_out/p_decode python bench.py --tokens 1 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e --ring 1 > /dev/null 2>&1; echo decode rc=$?
 timeout 900 python tools/stack_sweep.py --blocks 32 --tokens 2048 --steps 5 > gpurun_out/p_stack_sweep.jsonl 2> gpurun_out/p_stack_sweep.err; echo stack rc=$?
