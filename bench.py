@@ -351,6 +351,22 @@ def main():
                 "flops_per_launch": gemm_flops(args),
                 "flops_basis": "dense 2*T*in*out (bucket slices folded into one effective weight per MMA)",
                 "peak_source": f"{pk_src} burst bf16 (MEASURED_PEAKS.json bf16_tflops)"}
+    # whole step: router + GEMM flops and the step's bytes against both roofs;
+    # time_lb = max(F / P_tc, B / P_hbm), achieved = time_lb / measured step time
+    step_ms = ms / args.steps
+    f_step = gemm_flops(args) + router_flops(args)
+    G = math.ceil(args.inn / args.group_size)
+    h_s = args.hidden or args.inn // 4
+    b_step = (args.out * args.inn * 2 * 4 / 8 + args.out * G * 8 + args.inn * h_s * 2
+              + args.tokens * (args.inn + args.out) * 2)
+    t_tc = f_step / (peak_tf * 1e12) * 1e3
+    t_hbm = b_step / (pk.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"]) * 1e9) * 1e3
+    roofline["step"] = {"flops": f_step, "bytes": b_step, "ms": round(step_ms, 5),
+                        "tflops": round(f_step / (step_ms * 1e-3) / 1e12, 1),
+                        "time_lb_ms": round(max(t_tc, t_hbm), 5), "binds": "tensor" if t_tc >= t_hbm else "hbm",
+                        "achieved": round(max(t_tc, t_hbm) / step_ms, 4),
+                        "basis": "router 2*T*(in*h+3h) + dense GEMM 2*T*in*out flops; bytes = all 4 slices' codes "
+                                 "(2 bit each) + group constants + router w1 + X/Y"}
     hbm = pk.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
     if args.tokens <= DECODE_MAX_T:
         # decode sizes are HBM-bound: algorithmic bytes = the union of the batch's active

@@ -5,7 +5,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gp
 timeout 600 python bench.py > gpurun_out/p_bench_default.json 2> gpurun_out/p_bench_default.err; echo bench rc=$?
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/p_bench_reference.json 2>&1; echo ref rc=$?
 : > gpurun_out/p_sweep.jsonl
-for args in "--tokens 1" "--tokens 2" "--tokens 4" "--tokens 8" "--tokens 16" "--tokens 32" "--tokens 64" "--tokens 128" "--tokens 512" "--tokens 2048 --target-bits 2" "--tokens 2048 --target-bits 2.5" "--tokens 2048 --target-bits 3.5" "--tokens 2048 --target-bits 4" \
+for args in "--tokens 1" "--tokens 2" "--tokens 4" "--tokens 8" "--tokens 16" "--tokens 32" "--tokens 64" "--tokens 128" "--tokens 512" "--tokens 2048 --target-bits 2" "--tokens 2048 --target-bits 2.5" "--tokens 2048 --target-bits 3.5" "--tokens 2048 --target-bits 4" "--tokens 2048 --hidden 256" \
             "--out 1024 --in 4096 --tokens 2048" "--out 14336 --in 4096 --tokens 1" "--out 14336 --in 4096 --tokens 16" "--out 14336 --in 4096 --tokens 64" "--out 4096 --in 14336 --tokens 1" "--out 4096 --in 14336 --tokens 64" "--out 14336 --in 4096 --tokens 8192" "--out 4096 --in 14336 --tokens 8192"; do
   timeout 300 python bench.py $args --no-cpu-baseline --no-e2e --steps 100 2>>gpurun_out/p_sweep.err | python -c "import json,sys; d=json.loads(sys.stdin.read()); d['args']='$args'; print(json.dumps(d))" >> gpurun_out/p_sweep.jsonl
 done
