@@ -25,9 +25,8 @@ namespace {
 using namespace sm100;
 
 constexpr int kD2Warps = 16, kD2Threads = 32 * kD2Warps;  // 16 warps: 4 per scheduler (latency hiding)
-constexpr int kD2MaxT = 8;  // tokens per launch: the m16n8k16 N dimension, one token per column
-constexpr int kD2MaxLaunchT = 16;  // 9..16 tokens: two launches of up to kD2MaxT tokens (measured ~7% faster
-                                   // than the merged-code kernel; beyond 16 the merged-code kernel wins)
+constexpr int kD2MaxT = 16;       // tokens per launch: two groups of 8 (the m16n8k16 N dimension)
+constexpr int kD2MaxLaunchT = 32;  // larger decode batches: one launch per 16 tokens
 constexpr int kD2Acc = 3 * 2 * 4;  // per lane: y over the token's slices, A, B  ([2][4] each)
 
 struct D2Params {
@@ -98,15 +97,18 @@ __device__ __forceinline__ void cp_wait_dyn(int n) {
     else cp_wait<0>();
 }
 
-__global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2Params p) {
+// NG token groups of 8 per launch: 1 (T <= 8, capped at 80 registers so the router's CTAs stay
+// co-resident) or 2 (9..16 tokens: the A fragments of every item serve both groups)
+template <int NG>
+__global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __grid_constant__ D2Params p) {
     extern __shared__ __align__(16) uint8_t smem[];
-    __half* x16 = reinterpret_cast<__half*>(smem);                                   // [kD2MaxT + 1][xs_stride]
+    __half* x16 = reinterpret_cast<__half*>(smem);                                   // [T + 1][xs_stride]
     // [T][kblocks] {sum of the k-step-scaled fp16 X (offset cancellation), unscaled sum (A, B)}
     float2* xsum = reinterpret_cast<float2*>(smem + (size_t)(p.T + 1) * p.xs_stride * 2);  // rows 0..T-1 + zeros
     float* red = reinterpret_cast<float*>(smem);  // [warps][kD2Acc][32], aliases x16 after the passes
-    __shared__ float es_s[kD2Warps][kD2MaxT];
-    __shared__ float s_score[kD2MaxT][MOBI_MAX_SLICES - 1];
-    __shared__ int s_mask[kD2MaxT];
+    __shared__ float es_s[kD2Warps][8 * NG];
+    __shared__ float s_score[8 * NG][MOBI_MAX_SLICES - 1];
+    __shared__ int s_mask[8 * NG];
     const int tid = threadIdx.x, warp = warp_idx_uniform(), lane = tid & 31;
     float2* gcs = reinterpret_cast<float2*>(smem + p.gcs_off) + (size_t)warp * p.gpw * 32;  // [groups][32 rows]
     uint4* ring = reinterpret_cast<uint4*>(smem + p.ring_off) + (size_t)warp * kD2Ring * 32;   // [slots][32 lanes]
@@ -167,8 +169,6 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
         default: cp_wait<5>(); break;
     }
     __syncwarp();
-    float xg0 = 0.f, xg1 = 0.f, xu0 = 0.f, xu1 = 0.f;
-    int grp = 0, gleft = 0;
 
     // (1) X in place: bf16 -> per-token 2^-e scale (max over the warp's range) x 4^-ss per k-step ->
     //     fp16, and per-(token, k-block) sums of the fp16 values (scaled, and rescaled by 4^ss)
@@ -251,26 +251,43 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
         *reinterpret_cast<uint4*>(x16 + (size_t)T * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
     __syncwarp();
 
-    // yt: this lane's outputs (rows g/g+8 of both row groups, tokens 2c/2c+1) over the slices each
-    // token uses; ys: the current slice's partials
-    float yt[2][4], ys[2][4], A[2][4], B[2][4], D[2][4];
+    // yt: this lane's outputs (rows g/g+8 of both row groups, tokens 8gi+2c / 8gi+2c+1 of token group
+    // gi) over the slices each token uses; ys: the current slice's partials
+    float yt[NG][2][4], ys[NG][2][4], A[NG][2][4], B[NG][2][4], D[NG][2][4];
 #pragma unroll
-    for (int rg = 0; rg < 2; ++rg)
+    for (int gi = 0; gi < NG; ++gi)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) yt[rg][j] = ys[rg][j] = A[rg][j] = B[rg][j] = D[rg][j] = 0.f;
+        for (int rg = 0; rg < 2; ++rg)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) yt[gi][rg][j] = ys[gi][rg][j] = A[gi][rg][j] = B[gi][rg][j] = D[gi][rg][j] = 0.f;
     TRM(1);
     const int g = lane >> 2, c = lane & 3;
-    const int tg = g < T ? g : T;  // B-fragment token row (row T is zeros)
-    const int t0 = 2 * c, t1 = 2 * c + 1;  // this lane's D columns (tokens)
-    const float es0 = t0 < T ? es_s[warp][t0] : 0.f, es1 = t1 < T ? es_s[warp][t1] : 0.f;
-    const __half* xr = x16 + (size_t)tg * p.xs_stride + 2 * c;
+    const __half* xr[NG];  // B-fragment token rows (row T is zeros)
+    int tk0[NG], tk1[NG];  // this lane's D columns (tokens) per token group
+    float es0[NG], es1[NG];
+#pragma unroll
+    for (int gi = 0; gi < NG; ++gi) {
+        const int tg = 8 * gi + g < T ? 8 * gi + g : T;
+        xr[gi] = x16 + (size_t)tg * p.xs_stride + 2 * c;
+        tk0[gi] = 8 * gi + 2 * c;
+        tk1[gi] = 8 * gi + 2 * c + 1;
+        es0[gi] = tk0[gi] < T ? es_s[warp][tk0[gi]] : 0.f;
+        es1[gi] = tk1[gi] < T ? es_s[warp][tk1[gi]] : 0.f;
+    }
+    float xg0[NG], xg1[NG], xu0[NG], xu1[NG];
+#pragma unroll
+    for (int gi = 0; gi < NG; ++gi) xg0[gi] = xg1[gi] = xu0[gi] = xu1[gi] = 0.f;
+    int grp = 0, gleft = 0;
     const int kpg = p.single_group ? (1 << 30) : (int)(p.gs / kKBlock);  // k-blocks per group
     // (2)-(4) one stream of (slice, k-block) items: slice 1's k-blocks (already in flight since the
     // prologue), then -- once the masks are known -- those of every other slice in the batch's union
     const int nk = kw1 - kw0;
     const int gleft0 = p.single_group ? (1 << 30) : kpg - (kw0 % kpg);  // k-blocks left in the first group
     const uint32_t magic = 0x64006400u;  // fp16 1024: (1024 + c) halves
-    int n_items = nk, uni = 1, mt0 = 0, mt1 = 0;
+    int n_items = nk, uni = 1;
+    int mt0[NG], mt1[NG];
+#pragma unroll
+    for (int gi = 0; gi < NG; ++gi) mt0[gi] = mt1[gi] = 0;
     int csi = 0, ckb = kw0;  // consume cursor
     for (int ci = 0;; ++ci) {
         if (ci == nk) {
@@ -306,8 +323,11 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
             }
             __syncthreads();
             for (int t = 0; t < T; ++t) uni |= s_mask[t];
-            mt0 = t0 < T ? s_mask[t0] : 0;
-            mt1 = t1 < T ? s_mask[t1] : 0;
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {
+                mt0[gi] = tk0[gi] < T ? s_mask[tk0[gi]] : 0;
+                mt1[gi] = tk1[gi] < T ? s_mask[tk1[gi]] : 0;
+            }
             int ns = 1;
             for (int e0 = 1; e0 < p.E; ++e0)
                 if (uni >> e0 & 1) slist |= (uint32_t)e0 << (2 * ns++);
@@ -326,13 +346,18 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
         const uint32_t w1[4] = {q.x >> 8, q.y >> 8, q.z >> 8, q.w >> 8};  // row group 1's fields
         auto kstep = [&](auto SSc) {
             constexpr int SS = decltype(SSc)::value;
-            const __half* xk = xr + (size_t)kb * kKBlock + 16 * SS;
-            const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xk);
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xk + 8);
-            mma_f16_acc(D[0], frag<SS>(w0[0], magic), frag<SS>(w0[1], magic), frag<SS>(w0[2], magic),
-                        frag<SS>(w0[3], magic), b0, b1);
-            mma_f16_acc(D[1], frag<SS>(w1[0], magic), frag<SS>(w1[1], magic), frag<SS>(w1[2], magic),
-                        frag<SS>(w1[3], magic), b0, b1);
+            const uint32_t a00 = frag<SS>(w0[0], magic), a01 = frag<SS>(w0[1], magic), a02 = frag<SS>(w0[2], magic),
+                           a03 = frag<SS>(w0[3], magic);
+            const uint32_t a10 = frag<SS>(w1[0], magic), a11 = frag<SS>(w1[1], magic), a12 = frag<SS>(w1[2], magic),
+                           a13 = frag<SS>(w1[3], magic);
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {  // the A fragments serve every token group
+                const __half* xk = xr[gi] + (size_t)kb * kKBlock + 16 * SS;
+                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xk);
+                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xk + 8);
+                mma_f16_acc(D[gi][0], a00, a01, a02, a03, b0, b1);
+                mma_f16_acc(D[gi][1], a10, a11, a12, a13, b0, b1);
+            }
         };
         kstep(std::integral_constant<int, 0>{});
         kstep(std::integral_constant<int, 1>{});
@@ -340,11 +365,12 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
         kstep(std::integral_constant<int, 3>{});
         // refill: item ci + R - 1 goes into the slot just consumed (its data is in registers)
         if (pi < n_items && pi <= ci + kD2Ring - 1) issue(pi++);
-        {
-            const float2 s0 = t0 < T ? xsum[t0 * p.kblocks + kb] : make_float2(0.f, 0.f);
-            const float2 s1 = t1 < T ? xsum[t1 * p.kblocks + kb] : make_float2(0.f, 0.f);
-            xg0 += s0.x, xu0 += s0.y;
-            xg1 += s1.x, xu1 += s1.y;
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+            const float2 s0 = tk0[gi] < T ? xsum[tk0[gi] * p.kblocks + kb] : make_float2(0.f, 0.f);
+            const float2 s1 = tk1[gi] < T ? xsum[tk1[gi] * p.kblocks + kb] : make_float2(0.f, 0.f);
+            xg0[gi] += s0.x, xu0[gi] += s0.y;
+            xg1[gi] += s1.x, xu1[gi] += s1.y;
         }
         if (kb == kw0) {  // a slice starts: its group cursor
             grp = 0;
@@ -357,30 +383,40 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {  // rows g and g+8 of the row group
                     const float2 sc = gcs[grp * 32 + 16 * rg + g + 8 * h];
-                    ys[rg][2 * h] = fmaf(D[rg][2 * h] - 1024.f * xg0, sc.x, ys[rg][2 * h]);
-                    ys[rg][2 * h + 1] = fmaf(D[rg][2 * h + 1] - 1024.f * xg1, sc.x, ys[rg][2 * h + 1]);
-                    if (si == 0) {
-                        A[rg][2 * h] = fmaf(sc.x, xu0 * es0, A[rg][2 * h]);
-                        A[rg][2 * h + 1] = fmaf(sc.x, xu1 * es1, A[rg][2 * h + 1]);
-                        B[rg][2 * h] = fmaf(sc.y, xu0 * es0, B[rg][2 * h]);
-                        B[rg][2 * h + 1] = fmaf(sc.y, xu1 * es1, B[rg][2 * h + 1]);
+#pragma unroll
+                    for (int gi = 0; gi < NG; ++gi) {
+                        ys[gi][rg][2 * h] = fmaf(D[gi][rg][2 * h] - 1024.f * xg0[gi], sc.x, ys[gi][rg][2 * h]);
+                        ys[gi][rg][2 * h + 1] = fmaf(D[gi][rg][2 * h + 1] - 1024.f * xg1[gi], sc.x, ys[gi][rg][2 * h + 1]);
+                        if (si == 0) {
+                            A[gi][rg][2 * h] = fmaf(sc.x, xu0[gi] * es0[gi], A[gi][rg][2 * h]);
+                            A[gi][rg][2 * h + 1] = fmaf(sc.x, xu1[gi] * es1[gi], A[gi][rg][2 * h + 1]);
+                            B[gi][rg][2 * h] = fmaf(sc.y, xu0[gi] * es0[gi], B[gi][rg][2 * h]);
+                            B[gi][rg][2 * h + 1] = fmaf(sc.y, xu1[gi] * es1[gi], B[gi][rg][2 * h + 1]);
+                        }
                     }
                 }
-                D[rg][0] = D[rg][1] = D[rg][2] = D[rg][3] = 0.f;
+#pragma unroll
+                for (int gi = 0; gi < NG; ++gi) D[gi][rg][0] = D[gi][rg][1] = D[gi][rg][2] = D[gi][rg][3] = 0.f;
             }
-            xg0 = xg1 = xu0 = xu1 = 0.f;
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) xg0[gi] = xg1[gi] = xu0[gi] = xu1[gi] = 0.f;
             ++grp;
             gleft = kpg;
         }
         if (slice_end) {  // the slice's partials go to the tokens that use it (slice 1: every token)
-            const bool u0 = si == 0 || (mt0 >> e0 & 1), u1 = si == 0 || (mt1 >> e0 & 1);
             const float fs = __int_as_float((127 - 2 * e0) << 23);  // 4^-e0: S 4^(4-e), S = s / 2^6, e = e0 + 1
-            const float f0 = u0 ? fs * es0 : 0.f, f1 = u1 ? fs * es1 : 0.f;
 #pragma unroll
-            for (int rg = 0; rg < 2; ++rg) {
-                yt[rg][0] = fmaf(ys[rg][0], f0, yt[rg][0]), yt[rg][2] = fmaf(ys[rg][2], f0, yt[rg][2]);
-                yt[rg][1] = fmaf(ys[rg][1], f1, yt[rg][1]), yt[rg][3] = fmaf(ys[rg][3], f1, yt[rg][3]);
-                ys[rg][0] = ys[rg][1] = ys[rg][2] = ys[rg][3] = 0.f;
+            for (int gi = 0; gi < NG; ++gi) {
+                const bool u0 = si == 0 || (mt0[gi] >> e0 & 1), u1 = si == 0 || (mt1[gi] >> e0 & 1);
+                const float f0 = u0 ? fs * es0[gi] : 0.f, f1 = u1 ? fs * es1[gi] : 0.f;
+#pragma unroll
+                for (int rg = 0; rg < 2; ++rg) {
+                    yt[gi][rg][0] = fmaf(ys[gi][rg][0], f0, yt[gi][rg][0]);
+                    yt[gi][rg][2] = fmaf(ys[gi][rg][2], f0, yt[gi][rg][2]);
+                    yt[gi][rg][1] = fmaf(ys[gi][rg][1], f1, yt[gi][rg][1]);
+                    yt[gi][rg][3] = fmaf(ys[gi][rg][3], f1, yt[gi][rg][3]);
+                    ys[gi][rg][0] = ys[gi][rg][1] = ys[gi][rg][2] = ys[gi][rg][3] = 0.f;
+                }
             }
         }
     }
@@ -390,29 +426,32 @@ __global__ void __maxnreg__(80) decode_planes_kernel(const __grid_constant__ D2P
 
     // (5) warps' partials -> smem, then each (row, token) combines its slices in warp order
     {
-        float* r = red + (size_t)warp * kD2Acc * 32 + lane;
+        float* r = red + (size_t)warp * (NG * kD2Acc) * 32 + lane;
         int i = 0;
 #pragma unroll
-        for (int rg = 0; rg < 2; ++rg)
+        for (int gi = 0; gi < NG; ++gi)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                r[(i++) * 32] = yt[rg][j];
-                r[(i++) * 32] = A[rg][j];
-                r[(i++) * 32] = B[rg][j];
-            }
+            for (int rg = 0; rg < 2; ++rg)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    r[(i++) * 32] = yt[gi][rg][j];
+                    r[(i++) * 32] = A[gi][rg][j];
+                    r[(i++) * 32] = B[gi][rg][j];
+                }
     }
     __syncthreads();
-    if (tid < 32 * kD2MaxT) {
+    if (tid < 32 * 8 * NG) {
         const int rl = tid % 32, t = tid / 32;
         const int64_t row = (int64_t)rt * 32 + rl;
         if (t < T && row < p.out) {
+            const int gi = t / 8, tl = t % 8;
             const int rg = rl / 16, rr = rl % 16, g = rr % 8, hi = rr / 8;
-            const int ln = g * 4 + t / 2, j = hi * 2 + (t & 1);
-            const int base = (rg * 4 + j) * 3;
+            const int ln = g * 4 + tl / 2, j = hi * 2 + (tl & 1);
+            const int base = ((gi * 2 + rg) * 4 + j) * 3;
             const float kc = p.mt.kc[s_mask[t]];
             float acc = 0.f;
             for (int w = 0; w < kD2Warps; ++w) {
-                const float* r = red + (size_t)w * kD2Acc * 32 + ln;
+                const float* r = red + (size_t)w * (NG * kD2Acc) * 32 + ln;
                 acc += r[(base + 0) * 32] + (kc * r[(base + 1) * 32] - r[(base + 2) * 32]);
             }
             p.y[(int64_t)t * p.out + row] = __float2bfloat16_rn(acc);
@@ -435,38 +474,45 @@ struct D2Smem {
     size_t gcs_off, ring_off, total;
 };
 static D2Smem d2_smem(const mobi_layer* L, int64_t T) {
+    const int ng = T > 8 ? 2 : 1;
     const size_t xs = (size_t)(T + 1) * (L->in_pad + 8) * 2 + (size_t)T * L->kblocks * 8;
     D2Smem m;
-    m.gcs_off = (std::max(xs, (size_t)kD2Warps * kD2Acc * 32 * 4) + 15) / 16 * 16;
+    m.gcs_off = (std::max(xs, (size_t)kD2Warps * ng * kD2Acc * 32 * 4) + 15) / 16 * 16;
     m.ring_off = m.gcs_off + (size_t)kD2Warps * d2_groups_per_warp(L) * 32 * 8;
     m.total = m.ring_off + (size_t)kD2Warps * kD2Ring * 32 * 16;
     return m;
 }
+// up to 8 tokens the kernel must leave room for the router's CTAs (co-residency under PDL)
+constexpr size_t kD2SmemCoRes = 200 * 1024, kD2SmemMax = 225 * 1024;  // + static smem <= 227 KiB
 
 bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
     if (T < 1 || T > kD2MaxLaunchT || !L->dplanes || L->E > 4) return false;
-    // several launches only pay while each is a single wave of row tiles (gate/up: 448 tiles, not)
+    if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
+    if (!L->single_group && L->gs % kKBlock != 0) return false;
     static const int n_sm = [] {
         int dev = 0, n = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         return n;
     }();
+    // several launches only pay while each is a single wave of row tiles (gate/up: 448 tiles, not)
     if (T > kD2MaxT && cdiv(L->out, (int64_t)32) > n_sm) return false;
-    if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
-    if (!L->single_group && L->gs % kKBlock != 0) return false;
-    return d2_smem(L, std::min<int64_t>(T, kD2MaxT)).total <= 200 * 1024;
+    const int64_t Tg = std::min<int64_t>(T, kD2MaxT);
+    return d2_smem(L, Tg).total <= (Tg > 8 ? kD2SmemMax : kD2SmemCoRes);
 }
 
 int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
                          uint8_t* masks_out, float* scores_out, __nv_bfloat16* y, bool pdl, cudaStream_t st,
                          unsigned long long* trace) {
-    // one launch per group of <= kD2MaxT tokens (the m16n8k16 N width); each decides its tokens' masks
+    // one launch per <= kD2MaxT tokens (one or two m16n8k16 N groups); each decides its tokens' masks
     // from the router partials and streams only its own union of slices.  Under PDL the later groups'
     // prologue (activation staging, slice 1) overlaps the previous group's tail.
     static bool attr = false;
     if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kD2SmemMax));
+        MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kD2SmemMax));
         attr = true;
     }
     for (int64_t t0 = 0; t0 < T; t0 += kD2MaxT) {
@@ -515,7 +561,10 @@ int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = pdl ? 1 : 0;
-        MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_planes_kernel, p));
+        if (Tg > 8)
+            MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_planes_kernel<2>, p));
+        else
+            MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_planes_kernel<1>, p));
         ++L->last_launches;
     }
     return MOBI_OK;
