@@ -249,3 +249,27 @@ def test_forward_host_chunked_pipeline_equals_device_forward(T):
     assert torch.equal(yh, y.cpu()) and torch.equal(mh, m.cpu())
     y2 = layer.forward_host(xb.cpu(), delta)  # pageable buffers take the staging path
     assert torch.equal(y2, y.cpu())
+
+
+# router kernel variants (router_tc.cu): CTA-pair tiles with N = 128 and N = 256 hidden units, and the
+# 1-CTA tiles with K split over a cluster of 3 (DSMEM reduction into rank 0); shapes chosen so each
+# variant's selection rule fires on a 148-SM B200 (launch_router_tc)
+@pytest.mark.parametrize("out,inn,h,T", [(256, 512, 2048, 1024),   # pair, N = 128
+                                         (256, 256, 4096, 1280),   # pair, N = 256
+                                         (256, 1024, 256, 512),    # 1-CTA, cluster K-split x3
+                                         (256, 4096, 1024, 300)])  # 1-CTA, cluster K-split x3, ragged T
+def test_router_variants_match_oracle(orc, out, inn, h, T):
+    L, layer = make_layer(out, inn, gs=128, hidden=h, seed=h + T)
+    xb, x64 = make_x(T, inn, seed=T + 5)
+    s_gpu = layer.score(xb).cpu().numpy().astype(np.float64)
+    s_ref = oracle_scores(orc, layer, x64)
+    err = np.abs(s_gpu - s_ref)
+    assert np.all(err <= SCORE_ATOL + SCORE_RTOL * np.abs(s_ref)), f"max score err {err.max():.3e}"
+    delta = orc.calibrate_threshold(s_ref, 1 / 6)
+    y, m = layer.forward(xb, delta, return_masks=True)
+    near = np.any(np.abs(s_ref - delta) <= MASK_MARGIN, axis=1)
+    m_ref = O.masks_from_gates(orc.gate_hard(s_ref, delta))
+    assert np.array_equal(m.cpu().numpy()[~near], m_ref[~near])
+    y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 128,
+                                gates_from_masks(m.cpu().numpy(), 3))
+    assert_y_close(y, y_ref)
