@@ -234,20 +234,7 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
             rv[j] = k < in ? __ldg(reinterpret_cast<const uint4*>(row + k)) : make_uint4(0, 0, 0, 0);
         }
     }
-    sm100::pdl_wait();  // the router's masks / histogram (PDL launch; a no-op otherwise)
-    if (hist) {
-        // fused bucketing (the router decided the masks and counted the buckets): claim the next slot
-        // of this token's bucket.  The slot order inside a bucket is arbitrary, which cannot change
-        // any output: a token's result depends only on its own row and its bucket's effective weight.
-        if (threadIdx.x == 0) {
-            if (src == 0) build_tiles(hist, tiles, meta);
-            const int mk = masks[src];
-            const int i = bucket_start(hist, mk) + atomicAdd(&fill[mk], 1);
-            perm[i] = (int32_t)src;
-            pinv[src] = i;
-            s_row = i;
-        }
-    }
+    // the row's max (and so its 2^-e scale) does not depend on the router either
     float m = 0.f;
     auto vmax = [&](const uint4& q) {
         const __nv_bfloat162* pp = reinterpret_cast<const __nv_bfloat162*>(&q);
@@ -268,8 +255,23 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();  // also publishes s_row
+    __syncthreads();
     m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    sm100::pdl_wait();  // the router's masks / histogram (PDL launch; a no-op otherwise)
+    if (hist) {
+        // fused bucketing (the router decided the masks and counted the buckets): claim the next slot
+        // of this token's bucket.  The slot order inside a bucket is arbitrary, which cannot change
+        // any output: a token's result depends only on its own row and its bucket's effective weight.
+        if (threadIdx.x == 0) {
+            if (src == 0) build_tiles(hist, tiles, meta);
+            const int mk = masks[src];
+            const int i = bucket_start(hist, mk) + atomicAdd(&fill[mk], 1);
+            perm[i] = (int32_t)src;
+            pinv[src] = i;
+            s_row = i;
+        }
+    }
+    __syncthreads();  // publishes s_row
     const int64_t i = hist ? s_row : pinv[src];
     // k-block slab layout [in_pad/64][tpad][64]: element k of permuted row i at (k/64*tpad + i)*64 + k%64
     __half* dst = xperm + i * kKBlock;

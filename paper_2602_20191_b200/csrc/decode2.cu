@@ -495,8 +495,9 @@ bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         return n;
     }();
-    // several launches only pay while each is a single wave of row tiles (gate/up: 448 tiles, not)
-    if (T > kD2MaxT && cdiv(L->out, (int64_t)32) > n_sm) return false;
+    // one CTA per 32-row tile pays only while the tiles fit one wave: the latency chain of every
+    // wave is serial (gate/up, 448 tiles, is faster on the stream-K merged-code kernels)
+    if (cdiv(L->out, (int64_t)32) > n_sm) return false;
     const int64_t Tg = std::min<int64_t>(T, kD2MaxT);
     return d2_smem(L, Tg).total <= (Tg > 8 ? kD2SmemMax : kD2SmemCoRes);
 }
