@@ -351,8 +351,10 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
 // + PN/4 KiB of w1 for 128 x PN outputs, against 32 KiB for 128 x 128 in the 1-CTA kernel, whose
 // tiles sit at the measured ~71 B/cycle/SM L2->SMEM limit.  The leader's MMA thread issues for the
 // pair; both CTAs run the same fused SiLU.w2 / gate / histogram epilogue on their own tokens.
+// 8 epilogue warps (two per TMEM lane quarter, each taking half of the tile's hidden units), TMA, MMA
+constexpr int k2WarpTma = 8, k2WarpMma = 9, k2Threads = 320;
 template <int PN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
     router_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                       const RParams p) {
     constexpr int kBB = PN / 2 * kKBlock * 2;  // w1 half per stage
@@ -370,6 +372,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
     const uint32_t rank = cluster_ctarank();
     __shared__ int s_last;
+    __shared__ float s_pp[RM][3];  // the second column half's partial scores per token
+    unsigned long long g_start = 0, c_start = clock64();
+    if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_start));
+    auto MARK = [&](int i) {  // debug: per-CTA cycle marks [4096 + 8*cta + i]
+        if (p.trace && (threadIdx.x % 32) == 0 && blockIdx.x < 148)
+            p.trace[4096 + 8 * blockIdx.x + i] = (unsigned long long)(clock64() - c_start);
+    };
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
@@ -377,19 +386,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 8);
+            mbar_init(&acc_empty[b], 16);
         }
         fence_barrier_init();
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
     pdl_trigger();  // the gather may launch and start loading its rows
-    if (warp == kRWarpMma) tmem_alloc_2sm(tmem_slot, 512);
+    if (warp == k2WarpMma) tmem_alloc_2sm(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     cluster_sync();
     tc_fence_after();
     if (*tmem_slot != 0) __trap();
+    if (warp == 0) MARK(1);  // prologue done
     constexpr uint32_t tmem = 0;
     const int n_mp = (p.n_mt + 1) / 2;
     const int total = n_mp * p.n_nt;
@@ -398,7 +408,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         mp = pair % n_mp;
         nt = pair / n_mp;
     };
-    if (warp == kRWarpTma) {
+    if (warp == k2WarpTma) {
         const uint32_t full_leader = mapa_shared(smem_u32(full), 0);
         uint32_t it = 0;
         for (int pair = cid; pair < total; pair += ncl) {
@@ -417,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                 __syncwarp();
             }
         }
-    } else if (warp == kRWarpMma) {
+    } else if (warp == k2WarpMma) {
         if (rank == 0) {
             uint32_t it = 0, tc = 0;
             constexpr uint32_t idesc = idesc_f16(2 * RM, PN, 1);
@@ -444,7 +454,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             }
         }
     } else {
-        const int q = warp % 4;
+        const int q = warp % 4, half = warp / 4;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         const uint32_t acc_empty_leader = mapa_shared(smem_u32(acc_empty), 0);
         uint32_t tc = 0;
@@ -455,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             const int buf = tc & 1;
             const int64_t t = (int64_t)mt * RM + 32 * q + lane;
             const int64_t h0 = (int64_t)nt * PN;
-            for (int et = 32 * q + lane; et < PN; et += 128) {
+            for (int et = threadIdx.x; et < PN; et += 256) {
                 float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
                 const int64_t hj = h0 + et;
                 c.x = __ldg(p.b1 + hj);
@@ -464,11 +474,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                 if (p.nr > 2) c.w = __ldg(p.w2 + hj * p.nr + 2);
                 cst[buf * PN + et] = c;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, 256;" ::: "memory");
             mbar_wait(&acc_full[buf], (tc >> 1) & 1);
+            if (warp == 0 && tc == 0) MARK(2);  // first tile's accumulator complete
             tc_fence_after();
             float part0 = 0.f, part1 = 0.f, part2 = 0.f;
-            for (int c0 = 0; c0 < PN; c0 += 32) {
+            for (int c0 = half * (PN / 2); c0 < (half + 1) * (PN / 2); c0 += 32) {
                 uint32_t v[32];
                 tmem_ld32(tmem + lane_base + buf * PN + c0, v);
                 tmem_ld_wait();
@@ -482,7 +493,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                     part2 = fmaf(sv, c.w, part2);
                 }
             }
-            const float part[3] = {part0, part1, part2};
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -491,6 +501,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
                 else
                     mbar_arrive_cluster(acc_empty_leader + buf * 8);
             }
+            // the two column halves' partial scores, summed in a fixed order by the first half
+            if (half == 1) {
+                s_pp[32 * q + lane][0] = part0;
+                s_pp[32 * q + lane][1] = part1;
+                s_pp[32 * q + lane][2] = part2;
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            if (half == 1) continue;
+            const float part[3] = {part0 + s_pp[32 * q + lane][0], part1 + s_pp[32 * q + lane][1],
+                                   part2 + s_pp[32 * q + lane][2]};
             if (t < p.T) {
 #pragma unroll
                 for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
@@ -498,9 +518,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             }
             // last hidden tile of token tile mt: scores and slice masks for its tokens
             __threadfence();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 2, 128;" ::: "memory");
             if (q == 0 && lane == 0) s_last = (int64_t)mt * RM < p.T && atomicAdd(&p.cnt[mt], 1) == p.n_nt - 1;
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 2, 128;" ::: "memory");
             if (s_last) {
                 __threadfence();
                 int mk = 2 * kMaxBuckets;  // no token
@@ -525,10 +545,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             }
         }
     }
+    if (warp == 0) MARK(3);  // epilogue done
     tc_fence_before();
     __syncthreads();
     cluster_sync();  // the peer's remote arrivals and TMEM use are over before either CTA releases it
-    if (warp == kRWarpMma) tmem_dealloc_2sm(tmem, 512);
+    if (warp == k2WarpMma) tmem_dealloc_2sm(tmem, 512);
+    if (p.trace && threadIdx.x == 0 && blockIdx.x < 148) {
+        unsigned long long g_end;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_end));
+        p.trace[4096 + 8 * blockIdx.x + 4] = g_start;
+        p.trace[4096 + 8 * blockIdx.x + 5] = g_end;
+        p.trace[4096 + 8 * blockIdx.x + 6] = (unsigned long long)(clock64() - c_start);
+    }
 }
 
 // split-K finish: H = sum_ks hpart (fixed order) -> silu(H + b1) . w2 -> s_part[nt][t][k]
@@ -659,7 +687,7 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
                                                r2_smem(256)));
                 a256 = true;
             }
-            router_tc2_kernel<256><<<grid, 192, r2_smem(256), st>>>(tmap_x, *L->tmap_w1, p);
+            router_tc2_kernel<256><<<grid, k2Threads, r2_smem(256), st>>>(tmap_x, *L->tmap_w1, p);
         } else {
             static bool a128 = false;
             if (!a128) {
@@ -667,7 +695,7 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
                                                r2_smem(128)));
                 a128 = true;
             }
-            router_tc2_kernel<128><<<grid, 192, r2_smem(128), st>>>(tmap_x, *L->tmap_w1_64, p);
+            router_tc2_kernel<128><<<grid, k2Threads, r2_smem(128), st>>>(tmap_x, *L->tmap_w1_64, p);
         }
         MOBI_LAUNCH_CHECK();
         ++L->last_launches;
