@@ -143,6 +143,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t full_b_leader = mapa_shared(smem_u32(full_b), 0);
         uint32_t it = 0;
         for (int pair = cid; pair < total; pair += ncl) {
+            // this CTA's last unit: the next kernel (the next layer's router, PDL) may launch its CTAs
+            // onto SMs as this grid drains (it waits for this grid before touching anything we write)
+            if (pair + ncl >= total && elect_one_sync()) pdl_trigger();
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);

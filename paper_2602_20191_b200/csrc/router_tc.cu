@@ -8,6 +8,7 @@
 // E-1 partial scores, written to s_part[hidden tile][token][j] and summed in a fixed order by the
 // bucket kernel (deterministic, no atomics).
 #include <algorithm>
+#include <utility>
 #include <cstdlib>
 
 #include "mobi_internal.cuh"
@@ -96,7 +97,6 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
-    pdl_trigger();  // the gather may launch and start loading its rows
     const long long t_start = clock64();
     unsigned long long g_start = 0;
     if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(g_start));
@@ -110,6 +110,10 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
     tc_fence_after();
     if (p.csplit > 1) cluster_sync();  // peers' barriers initialised before any remote arrive
     if (*tmem_slot != 0) __trap();
+    // PDL: the prologue above overlapped the previous kernel; X (possibly its output) and every write
+    // wait for it.  Only then may the gather launch: it reads X before its own wait.
+    pdl_wait();
+    pdl_trigger();
     constexpr uint32_t tmem = 0;
     const int total = p.n_mt * p.n_nt * p.nsplit;
     // tile -> (token tile mt, hidden tile nt, k-split ks)
@@ -392,13 +396,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
         prefetch_tmap(&tmap_a);
         prefetch_tmap(&tmap_b);
     }
-    pdl_trigger();  // the gather may launch and start loading its rows
     if (warp == k2WarpMma) tmem_alloc_2sm(tmem_slot, 512);
     tc_fence_before();
     __syncthreads();
     cluster_sync();
     tc_fence_after();
     if (*tmem_slot != 0) __trap();
+    pdl_wait();     // PDL: X (possibly the previous kernel's output) and every write wait for it
+    pdl_trigger();  // the gather may launch and start loading its rows
     if (warp == 0) MARK(1);  // prologue done
     constexpr uint32_t tmem = 0;
     const int n_mp = (p.n_mt + 1) / 2;
@@ -602,6 +607,30 @@ bool router_tc_supported(const mobi_layer* L, const void* x) {
     return (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 }
 
+// Launch with programmatic stream serialization (PDL) and, when cluster > 0, a runtime cluster size.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              int cluster, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int n = 0;
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n++].val.programmaticStreamSerializationAllowed = 1;
+    if (cluster > 0) {
+        at[n].id = cudaLaunchAttributeClusterDimension;
+        at[n].val.clusterDim.x = (unsigned)cluster;
+        at[n].val.clusterDim.y = 1;
+        at[n++].val.clusterDim.z = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // development switch (MOBI_ROUTER_PAIR): 0 = never use the CTA-pair router
 int g_router_pair = [] {
     const char* e = std::getenv("MOBI_ROUTER_PAIR");
@@ -687,7 +716,8 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
                                                r2_smem(256)));
                 a256 = true;
             }
-            router_tc2_kernel<256><<<grid, k2Threads, r2_smem(256), st>>>(tmap_x, *L->tmap_w1, p);
+            MOBI_CUDA(launch_pdl(router_tc2_kernel<256>, dim3(grid), dim3(k2Threads), r2_smem(256), st, 0, tmap_x,
+                                 *L->tmap_w1, p));
         } else {
             static bool a128 = false;
             if (!a128) {
@@ -695,7 +725,8 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
                                                r2_smem(128)));
                 a128 = true;
             }
-            router_tc2_kernel<128><<<grid, k2Threads, r2_smem(128), st>>>(tmap_x, *L->tmap_w1_64, p);
+            MOBI_CUDA(launch_pdl(router_tc2_kernel<128>, dim3(grid), dim3(k2Threads), r2_smem(128), st, 0, tmap_x,
+                                 *L->tmap_w1_64, p));
         }
         MOBI_LAUNCH_CHECK();
         ++L->last_launches;
@@ -722,25 +753,13 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
     if (masks_ready) *masks_ready = p.nsplit == 1 || clus;
     if (p.nsplit != 1 && !clus) p.hist = nullptr;
     if (clus) {
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)total);
-        cfg.blockDim = dim3(kRThreads);
-        cfg.dynamicSmemBytes = kRSmem;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = (unsigned)p.csplit;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_tc_kernel, tmap_x, *L->tmap_w1, p));
+        MOBI_CUDA(launch_pdl(router_tc_kernel, dim3((unsigned)total), dim3(kRThreads), (size_t)kRSmem, st, p.csplit,
+                             tmap_x, *L->tmap_w1, p));
         ++L->last_launches;
         return MOBI_OK;
     }
     const int grid = std::min(total, sm_count());
-    router_tc_kernel<<<grid, kRThreads, kRSmem, st>>>(tmap_x, *L->tmap_w1, p);
-    MOBI_LAUNCH_CHECK();
+    MOBI_CUDA(launch_pdl(router_tc_kernel, dim3(grid), dim3(kRThreads), (size_t)kRSmem, st, 0, tmap_x, *L->tmap_w1, p));
     ++L->last_launches;
     if (p.nsplit > 1) {
         router_reduce_kernel<<<dim3((unsigned)T, (unsigned)p.n_nt), RN, 0, st>>>(L->hpart, p.nsplit, T, L->h, L->h_pad,
