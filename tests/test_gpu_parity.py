@@ -273,3 +273,25 @@ def test_router_variants_match_oracle(orc, out, inn, h, T):
     y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 128,
                                 gates_from_masks(m.cpu().numpy(), 3))
     assert_y_close(y, y_ref)
+
+
+@pytest.mark.parametrize("T", [1, 8, 300, 2048])
+def test_chained_layers_under_pdl_equal_synchronized(orc, T):
+    """Layer 2 consumes layer 1's output directly (no op in between), so its PDL-launched router may
+    be scheduled while layer 1's GEMM drains; it must still read the finished output.  Compared
+    bit-for-bit with the same two forwards separated by a device synchronisation."""
+    from paper_2602_20191_b200 import calibrate_threshold
+    _, l1 = make_layer(1024, 512, gs=128, seed=21)
+    _, l2 = make_layer(512, 1024, gs=128, seed=22)
+    xb, _ = make_x(T, 512, seed=T + 2)
+    d1 = calibrate_threshold(l1.score(xb), 1 / 6)
+    y1 = l1.forward(xb, d1)
+    d2 = calibrate_threshold(l2.score(y1), 1 / 6)
+    torch.cuda.synchronize()
+    ref2 = l2.forward(y1.clone(), d2)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        a = l1.forward(xb, d1)
+        b = l2.forward(a, d2)  # back to back on one stream
+    torch.cuda.synchronize()
+    assert torch.equal(a, y1) and torch.equal(b, ref2)
