@@ -733,9 +733,7 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
         return MOBI_OK;
     }
     const int tiles = p.n_mt * p.n_nt;
-    if (T <= 64 && L->hpart) {
-        p.nsplit = std::max(1, std::min(16, sm_count() / tiles));
-    } else if (g_router_csplit == 2 && p.kblocks >= 8) {  // experiment: fixed 2-way split at every T
+    if (g_router_csplit == 2 && p.kblocks >= 8) {  // experiment: fixed 2-way split at every T
         p.csplit = 2;
         p.nsplit = 2;
     } else if (g_router_csplit == 1 && 2 * tiles <= sm_count() && p.kblocks >= 8) {
@@ -744,6 +742,8 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
         // count only, so outputs are identical for every T of the same regime.
         p.csplit = std::min(kMaxCsplit, std::min(3, sm_count() / tiles));
         p.nsplit = p.csplit;
+    } else if (T <= 64 && L->hpart) {  // small K: global split-K partials + a reduce kernel
+        p.nsplit = std::max(1, std::min(16, sm_count() / tiles));
     }
     p.kb_per = (p.kblocks + p.nsplit - 1) / p.nsplit;
     p.nsplit = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty splits
