@@ -257,7 +257,9 @@ def test_forward_host_chunked_pipeline_equals_device_forward(T):
 @pytest.mark.parametrize("out,inn,h,T", [(256, 512, 2048, 1024),   # pair, N = 128
                                          (256, 256, 4096, 1280),   # pair, N = 256
                                          (256, 1024, 256, 512),    # 1-CTA, cluster K-split x3
-                                         (256, 4096, 1024, 300)])  # 1-CTA, cluster K-split x3, ragged T
+                                         (256, 4096, 1024, 300),   # 1-CTA, cluster K-split x3, ragged T
+                                         (256, 512, 2048, 1300),   # pair, ragged: the last pair's peer is empty
+                                         (256, 1024, 200, 400)])   # cluster K-split, partial hidden tile
 def test_router_variants_match_oracle(orc, out, inn, h, T):
     L, layer = make_layer(out, inn, gs=128, hidden=h, seed=h + T)
     xb, x64 = make_x(T, inn, seed=T + 5)
