@@ -86,8 +86,38 @@ class ClockSampler:
     def __init__(self, dev: int):
         self.dev = dev
         self.proc = None
+        self.nvml = None
+        self.samples = []
+
+    # NVML (pynvml) when the driver library loads: samples are taken on the host while the GPU runs
+    # the timed region (poll_until), so even a ~20 ms region yields many; nvidia-smi -lms otherwise
+    def _nvml_sample(self):
+        nv, h = self.nvml
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                nv.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.samples.append((sm, smax, fn(h)))
+        except Exception:
+            pass
+
+    def poll_until(self, event):
+        if not self.nvml:
+            return
+        self._nvml_sample()
+        while not event.query():
+            self._nvml_sample()
+            time.sleep(0.0005)
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.dev))
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -96,6 +126,16 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if self.nvml:
+            nv = self.nvml[0]
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
+            reasons = sorted({n for _, _, r in self.samples for n, b in bits.items() if r & b})
+            if not self.samples:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": reasons, "samples": 0, "source": "nvml"}
+            return {"sm_mhz": statistics.median([a for a, _, _ in self.samples]),
+                    "sm_max_mhz": max(b for _, b, _ in self.samples), "reasons": reasons,
+                    "samples": len(self.samples), "source": "nvml, polled while the timed region ran"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
         self.proc.terminate()
@@ -280,7 +320,8 @@ def main():
                             f"times) + per-slot graphs for the remainder")
     clk = ClockSampler(local)
     clk.start()
-    time.sleep(0.05)
+    if not clk.nvml:
+        time.sleep(0.05)
     if dist:
         tdist.barrier()
     torch.cuda.synchronize()
@@ -300,6 +341,7 @@ def main():
             step(i)
             launches += ring[i % R]["layer"].last_launches()
     e1.record(st)
+    clk.poll_until(e1)
     torch.cuda.synchronize()
     if dist:
         tdist.barrier()
