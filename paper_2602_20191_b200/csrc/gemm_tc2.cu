@@ -23,6 +23,25 @@
 #ifndef MOBI_RELAXED
 #define MOBI_RELAXED 1
 #endif
+// bottleneck experiments (development only; all 0 in the product): drop one producer's real work
+#ifndef MOBI_X_NOLOAD
+#define MOBI_X_NOLOAD 0  // dequantizers skip the code / constant loads
+#endif
+#ifndef MOBI_X_NOTMA
+#define MOBI_X_NOTMA 0   // the TMA warp arrives without loading B
+#endif
+#ifndef MOBI_X_NODQ
+#define MOBI_X_NODQ 0    // dequantizers store the raw code words (no ALU work)
+#endif
+#ifndef MOBI_TRACE_UNIT
+#define MOBI_TRACE_UNIT 0  // which of cluster 0's units the per-k-block trace records
+#endif
+#ifndef MOBI_X_NOWAIT
+#define MOBI_X_NOWAIT 0  // the MMA thread issues without waiting for the stage (timing only: garbage output)
+#endif
+#ifndef MOBI_X_NOEPI
+#define MOBI_X_NOEPI 0   // the epilogue releases TMEM without draining or storing
+#endif
 namespace mobi {
 int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int64_t rows, int64_t cols,
                  int box_rows);
@@ -30,22 +49,21 @@ namespace {
 
 using namespace sm100;
 
-#ifndef MOBI_TMA_CODES
-#define MOBI_TMA_CODES 0  // 1: a codes warp stages each k-block's codes + group constants in smem
-#endif
-constexpr int NSTAGE = MOBI_TMA_CODES ? 6 : 8;
+constexpr int NSTAGE = 8;
 constexpr int kDqWarps = 16;
-constexpr int kThreads = 32 * (2 + kDqWarps + 4 + (MOBI_TMA_CODES ? 1 : 0));
+constexpr int kThreads = 32 * (2 + kDqWarps + 4);
 constexpr int kWarpDq0 = 0, kWarpEpi0 = kDqWarps, kWarpTma = kDqWarps + 4, kWarpMma = kDqWarps + 5;
-constexpr int kWarpCodes = kDqWarps + 6;  // MOBI_TMA_CODES: streams the codes + constants of each stage
+// dynamic unit schedule: the leader's TMA warp claims units (atomic counter, units in decreasing
+// size order) and publishes them through a small ring to every role of both CTAs
+constexpr int kURing = 4;
+constexpr int kUnitConsumers = 1 + kDqWarps + 4;  // per CTA: MMA (leader) or TMA (peer) + dequant + epilogue
 constexpr int kHalfRows = kTokTile / 2;                  // token rows per CTA per stage
 constexpr int kStageBytes = kHalfRows * kKBlock * 2;     // 16 KiB
 constexpr int kBoxRows = 16;
 constexpr int kBoxBytes = kBoxRows * kKBlock * 2;        // 2 KiB
 constexpr int kACol0 = 256;
 constexpr int kYStageBytes = kTokTile * kRowTile * 2;    // 64 KiB
-constexpr int kCodeStage = MOBI_TMA_CODES ? kBlockBytes + 2 * kRowTile * 8 : 0;  // codes + 2 groups' (s, s*z)
-constexpr int kSmemBytes = NSTAGE * (kStageBytes + kCodeStage) + 1024 + 512 + kYStageBytes + kTokTile * 4;
+constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 + 512 + kYStageBytes + kTokTile * 4;
 constexpr int kBigBoxRows = kHalfRows;  // one TMA box per full half-tile
 
 struct Params {
@@ -64,17 +82,9 @@ struct Params {
     __nv_bfloat16* y;
     int vec_y;
     int* bk_hist;  // fused-bucketing histogram + slot counters: zeroed here for the next forward
+    int* unit_ctr;  // dynamic unit counter (meta[32]), zeroed by the kernel that builds the tile list
     unsigned long long* trace;
 };
-
-// one 64-k block on the pair: four K=16 cta_group::2 MMAs, M=256, N compile-time
-template <uint32_t N>
-__device__ __forceinline__ void issue_kblock_2sm(uint32_t acol, uint64_t bdesc, bool first) {
-    constexpr uint32_t idesc = idesc_f16(256, N, 0);
-#pragma unroll
-    for (int j = 0; j < kKBlock / 16; ++j)
-        mma_ts_f16_2sm(0u, acol + j * 8, bdesc + (uint64_t)(j * 2), idesc, (!first || j != 0) ? 1u : 0u);
-}
 
 template <bool TRACE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -82,24 +92,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                          const Params p) {
     // per-k-block event timeline (cluster 0, first tile): trace[20480 + (rank*8+ev)*64 + kb]
     auto EV = [&](int ev, int kb, uint32_t tile_idx) {
-        if (TRACE && blockIdx.x < 2 && tile_idx == 0 && kb < 64 && (threadIdx.x % 32) == 0)
+        if (TRACE && blockIdx.x < 2 && tile_idx == MOBI_TRACE_UNIT && kb < 64 && (threadIdx.x % 32) == 0)
             p.trace[20480 + (cluster_ctarank() * 8 + ev) * 64 + kb] = (unsigned long long)clock64();
+    };
+    // per-unit events (cluster 0, first 16 units, globaltimer ns): trace[24576 + (rank*8+ev)*16 + u]
+    auto EVU = [&](int ev, uint32_t u) {
+        if (TRACE && blockIdx.x < 2 && u < 16 && (threadIdx.x % 32) == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.trace[24576 + (cluster_ctarank() * 8 + ev) * 16 + u] = t;
+        }
     };
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stage_b = smem;
-    uint8_t* stage_c = smem + NSTAGE * kStageBytes;  // [NSTAGE][codes 8 KiB | (s, s*z) of 2 groups x 128 rows]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * (kStageBytes + kCodeStage));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * kStageBytes);
     // one full barrier per stage, in the leader: both halves' TMA bytes (one expect_tx arrival) and the
     // 8 + 8 dequant warps of the pair (the peer's arrive remotely)
     uint64_t* full_b = bars;                 // [NSTAGE] leader: stage complete (A in both TMEMs, B in both smems)
-    uint64_t* empty = bars + 2 * NSTAGE;     // [NSTAGE] each CTA: pair MMAs done with the stage
-    uint64_t* acc_full = bars + 3 * NSTAGE;  // each CTA
+    uint64_t* empty = bars + NSTAGE;         // [NSTAGE] each CTA: pair MMAs done with the stage
+    uint64_t* acc_full = bars + 2 * NSTAGE;  // each CTA
     uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1 + NSTAGE);
-    uint64_t* codes_full = bars + NSTAGE;    // [NSTAGE] each CTA: its codes + constants of the stage landed
-    __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * (kStageBytes + kCodeStage) + 512);
-    int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * (kStageBytes + kCodeStage) + 512 + kYStageBytes);
+    uint64_t* u_full = acc_empty + 1;        // [kURing] each CTA: unit slot published
+    uint64_t* u_empty = u_full + kURing;     // [kURing] leader: every consumer of both CTAs read the slot
+    int32_t* uring = reinterpret_cast<int32_t*>(u_empty + kURing);  // [kURing] unit index (-1 = done)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kURing);
+    __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 512);
+    int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
 
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
@@ -108,10 +127,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int s = 0; s < NSTAGE; ++s) {
             mbar_init(&full_b[s], 1 + kDqWarps);  // TMA expect_tx + 8 dequant warps per CTA x 2
             mbar_init(&empty[s], 1);
-            mbar_init(&codes_full[s], 1);
         }
         mbar_init(acc_full, 1);
         mbar_init(acc_empty, 8);  // 4 epilogue warps x 2 CTAs
+        for (int s = 0; s < kURing; ++s) {
+            mbar_init(&u_full[s], 1);
+            mbar_init(&u_empty[s], 2 * kUnitConsumers);
+        }
         fence_barrier_init();
         prefetch_tmap(&tmap_x);
         prefetch_tmap(&tmap_big);
@@ -137,15 +159,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         rt = (pair % n_pairs_row) * 2 + (int)rank;
         nc = max(32, (int)round_up(tt.n, 32));
     };
+    // unit ring: consumers read slot ui % kURing, then release it on the leader's u_empty
+    auto unit_get = [&](uint32_t ui) -> int {
+        const int s = (int)(ui % kURing);
+        const uint32_t ph = (ui / kURing) & 1;
+        if (rank == 0)
+            mbar_wait(&u_full[s], ph);
+        else
+            mbar_wait_cluster(&u_full[s], ph);  // published by the leader's thread (remote store + release)
+        const int u = *reinterpret_cast<volatile int32_t*>(&uring[s]);
+        __syncwarp();
+        if (lane == 0) {
+            if (rank == 0)
+                mbar_arrive(&u_empty[s]);
+            else
+                mbar_arrive_cluster(mapa_shared(smem_u32(&u_empty[s]), 0));
+        }
+        return u;
+    };
+    // producer (the leader's TMA warp): the first unit of cluster c is c, later ones come from the
+    // counter (claimed when this pair's TMA runs out of work, i.e. ~NSTAGE k-blocks ahead of its MMAs)
+    auto unit_put = [&](uint32_t ui) -> int {
+        const int s = (int)(ui % kURing);
+        mbar_wait_cluster(&u_empty[s], ((ui / kURing) & 1) ^ 1);
+        int u = 0;
+        if (lane == 0) {
+            u = ui == 0 ? cid : atomicAdd(p.unit_ctr, 1) + ncl;
+            if (u >= total) u = -1;
+            *reinterpret_cast<volatile int32_t*>(&uring[s]) = u;
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(mapa_shared(smem_u32(&uring[s]), 1)), "r"(u)
+                         : "memory");
+            mbar_arrive(&u_full[s]);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&u_full[s]), 1));
+        }
+        return __shfl_sync(0xffffffffu, u, 0);
+    };
 
     if (warp == kWarpTma) {
         // ---------------- TMA producer (both CTAs: own half of the token tile) ----------------
         const uint32_t full_b_leader = mapa_shared(smem_u32(full_b), 0);
         uint32_t it = 0;
-        for (int pair = cid; pair < total; pair += ncl) {
-            // this CTA's last unit: the next kernel (the next layer's router, PDL) may launch its CTAs
+        bool trig = false;
+        for (uint32_t ui = 0;; ++ui) {
+            const int pair = rank == 0 ? unit_put(ui) : unit_get(ui);
+            // the last wave of units: the next kernel (the next layer's router, PDL) may launch its CTAs
             // onto SMs as this grid drains (it waits for this grid before touching anything we write)
-            if (pair + ncl >= total && elect_one_sync()) pdl_trigger();
+            if (!trig && (pair < 0 || pair + ncl >= total)) {
+                trig = true;
+                if (elect_one_sync()) pdl_trigger();
+                __syncwarp();
+            }
+            if (pair < 0) break;
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
@@ -156,8 +220,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
-                EV(0, kb, (uint32_t)(pair != cid));
-                if (elect_one_sync()) {
+                EV(0, kb, ui);
+                if (MOBI_X_NOTMA) {
+                    if (elect_one_sync() && rank == 0) mbar_arrive_expect_tx(&full_b[s], 0);
+                } else if (elect_one_sync()) {
                     if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * (big ? kStageBytes : nbox * kBoxBytes));
                     if (big)
                         tma_load_2d_2sm(stage_b + s * kStageBytes, &tmap_big, full_b_leader + s * 8, 0,
@@ -170,74 +236,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 __syncwarp();
             }
         }
-    } else if (MOBI_TMA_CODES && warp == kWarpCodes) {
-        // ---------------- codes producer: this CTA's code block + group constants per stage ----------------
-        uint32_t it = 0;
-        for (int pair = cid; pair < total; pair += ncl) {
-            TokTile tt;
-            int rt, nc;
-            tile_of(pair, tt, rt, nc);
-            for (int kb = 0; kb < kb_n; ++kb, ++it) {
-                const int s = it % NSTAGE;
-                mbar_wait(&empty[s], ((it / NSTAGE) & 1) ^ 1);
-                if (elect_one_sync()) {
-                    uint8_t* dc = stage_c + s * kCodeStage;
-                    const int64_t g0 = p.single_group ? 0 : ((int64_t)kb * kKBlock) / p.gs;
-                    const int64_t g1 = p.single_group ? 0 : ((int64_t)kb * kKBlock + 32) / p.gs;
-                    mbar_arrive_expect_tx(&codes_full[s], kCodeStage);
-                    bulk_g2s(dc, p.codes8 + ((int64_t)rt * p.kblocks + kb) * kBlockBytes, kBlockBytes, &codes_full[s]);
-                    bulk_g2s(dc + kBlockBytes, p.gconst + g0 * p.out_pad + (int64_t)rt * kRowTile, kRowTile * 8,
-                             &codes_full[s]);
-                    bulk_g2s(dc + kBlockBytes + kRowTile * 8, p.gconst + g1 * p.out_pad + (int64_t)rt * kRowTile,
-                             kRowTile * 8, &codes_full[s]);
-                }
-                __syncwarp();
-            }
-        }
     } else if (warp == kWarpMma) {
-        // ---------------- MMA issuer (leader) ----------------
-        if (rank == 0) {
-            uint32_t it = 0, tc = 0;
-            for (int pair = cid; pair < total; pair += ncl, ++tc) {
-                TokTile tt;
-                int rt, nc;
-                tile_of(pair, tt, rt, nc);
-                mbar_wait_cluster(acc_empty, (tc & 1) ^ 1);
+        // ---------------- MMA issuer (leader, one thread) ----------------
+        // A tight single-thread loop: per k-block one CTA-scope wait, four MMAs and a commit with every
+        // operand in uniform registers (the per-unit N goes into a runtime instruction descriptor).  The
+        // peer's dequantizers and TMA signal the leader's full barrier; TMEM ordering comes from their
+        // tcgen05 fences, so no cluster-scope acquire (and its L1 invalidation) is needed per k-block.
+        if (rank == 0 && elect_one_sync()) {
+            const uint64_t bdesc0 = sdesc_sw128(smem_u32(stage_b));
+            uint32_t it = 0;
+            for (uint32_t tc = 0;; ++tc) {
+                const int s0 = (int)(tc % kURing);
+                mbar_wait(&u_full[s0], (tc / kURing) & 1);
+                const int pair = *reinterpret_cast<volatile int32_t*>(&uring[s0]);
+                mbar_arrive(&u_empty[s0]);
+                if (pair < 0) break;
+                const int tn = __ldg(&p.tiles[pair / n_pairs_row].n);
+                const uint32_t nc = (uint32_t)max(32, (int)round_up(tn, 32));
+                const uint32_t idesc = idesc_f16(256, nc, 0);
+                mbar_wait_cluster(acc_empty, (tc & 1) ^ 1);  // both CTAs' epilogues drained the accumulator
+                EVU(0, tc);
+                if (TRACE && blockIdx.x < 2 && tc < 16) p.trace[24576 + 6 * 16 + tc] = nc;
                 tc_fence_after();
                 for (int kb = 0; kb < kb_n; ++kb, ++it) {
-                    const int s = it % NSTAGE;
-                    const uint32_t ph = (it / NSTAGE) & 1;
-#if MOBI_MMA_WAIT == 0
-                    mbar_wait_cluster(&full_b[s], ph);
-#elif MOBI_MMA_WAIT == 1
-                    mbar_wait(&full_b[s], ph);
-#else
-                    mbar_wait_relaxed(&full_b[s], ph);
-#endif
-                    EV(1, kb, tc);
+                    const uint32_t s = it % NSTAGE;
+                    mbar_wait(&full_b[s], (it / NSTAGE) & 1);
                     tc_fence_after();
-                    if (elect_one_sync()) {
-                        const uint64_t bdesc = sdesc_sw128(smem_u32(stage_b + s * kStageBytes));
-                        const uint32_t acol = tmem + kACol0 + s * 32;
-                        const bool first = kb == 0;
-                        switch (nc) {
-                            case 32: issue_kblock_2sm<32>(acol, bdesc, first); break;
-                            case 64: issue_kblock_2sm<64>(acol, bdesc, first); break;
-                            case 96: issue_kblock_2sm<96>(acol, bdesc, first); break;
-                            case 128: issue_kblock_2sm<128>(acol, bdesc, first); break;
-                            case 160: issue_kblock_2sm<160>(acol, bdesc, first); break;
-                            case 192: issue_kblock_2sm<192>(acol, bdesc, first); break;
-                            case 224: issue_kblock_2sm<224>(acol, bdesc, first); break;
-                            default: issue_kblock_2sm<256>(acol, bdesc, first); break;
-                        }
-                        mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
-                        if (kb == kb_n - 1) mma_commit_2sm_mc(acc_full, (uint16_t)0x3);
-                    }
-                    __syncwarp();
-                    EV(3, kb, tc);
+                    const uint32_t acol = kACol0 + s * 32;
+                    const uint64_t bdesc = bdesc0 + (uint64_t)(s * (kStageBytes >> 4));
+#pragma unroll
+                    for (int j = 0; j < kKBlock / 16; ++j)
+                        mma_ts_f16_2sm(0u, acol + j * 8, bdesc + (uint64_t)(j * 2), idesc, (kb | j) != 0 ? 1u : 0u);
+                    mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
                 }
+                mma_commit_2sm_mc(acc_full, (uint16_t)0x3);
+                EVU(1, tc);
             }
         }
+        __syncwarp();
     } else if (warp < kWarpEpi0) {
         // ---------------- dequantizers ----------------
         // 16 warps = 4 TMEM lane quarters x 2 k-halves x 2 k-block parities: a warp dequantizes
@@ -249,7 +285,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
         const uint32_t full_leader = mapa_shared(smem_u32(full_b), 0);
         uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
-        for (int pair = cid; pair < total; pair += ncl, base += kb_n) {
+        for (uint32_t ui = 0;; ++ui, base += kb_n) {
+            const int pair = unit_get(ui);
+            if (pair < 0) break;
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
@@ -260,8 +298,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint8_t* cbase =
                 p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes + ((hh * 2) * kRowTile + 32 * q + lane) * 16;
             const float2* gcol = p.gconst + (rv ? R : 0);
-            auto ldc = [&](int gg) { return rv ? __ldg(gcol + (int64_t)gg * p.out_pad) : make_float2(0.f, 0.f); };
+            auto ldc = [&](int gg) {
+                if (MOBI_X_NOLOAD) return make_float2(0.01f * gg, 0.02f);
+                return rv ? __ldg(gcol + (int64_t)gg * p.out_pad) : make_float2(0.f, 0.f);
+            };
             auto ld = [&](int kb, uint4& c0, uint4& c1) {
+                if (MOBI_X_NOLOAD) {
+                    c0 = make_uint4(kb, kb * 3, kb * 5, kb * 7);
+                    c1 = make_uint4(kb * 11, kb, kb * 13, kb);
+                    return;
+                }
                 const uint8_t* b0 = cbase + (int64_t)kb * kBlockBytes;
                 c0 = *reinterpret_cast<const uint4*>(b0);
                 c1 = *reinterpret_cast<const uint4*>(b0 + kRowTile * 16);
@@ -272,42 +318,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const __half2 C2 = __float2half2_rn(fmaf(gcst.x, kc, -gcst.y));
                 const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&c0);
                 const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&c1);
+                if (MOBI_X_NODQ) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[2 * u] = v[2 * u + 1] = w0[u];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[8 + 2 * u] = v[8 + 2 * u + 1] = w1[u];
+                    return;
+                }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) dequant4(w0[u], mw, S2, C2, v[2 * u], v[2 * u + 1]);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) dequant4(w1[u], mw, S2, C2, v[8 + 2 * u], v[8 + 2 * u + 1]);
             };
-#if MOBI_TMA_CODES
-            // codes and constants arrive in the stage's smem with the B tile: no register prefetch ring
-            uint32_t v[16];
-            for (int kb = par; kb < kb_n; kb += 2) {
-                const uint32_t itk = base + kb;
-                const int s = itk % NSTAGE;
-                const uint32_t ph = (itk / NSTAGE) & 1;
-                mbar_wait(&codes_full[s], ph);  // (issued after empty[s]: the A stage is free too)
-                if (warp == 0 || warp == 4) EV(4, kb, base);
-                const uint8_t* dc = stage_c + s * kCodeStage;
-                const uint4 c0 = *reinterpret_cast<const uint4*>(dc + ((hh * 2) * kRowTile + 32 * q + lane) * 16);
-                const uint4 c1 = *reinterpret_cast<const uint4*>(dc + ((hh * 2 + 1) * kRowTile + 32 * q + lane) * 16);
-                const float2 gc = reinterpret_cast<const float2*>(dc + kBlockBytes)[hh * kRowTile + 32 * q + lane];
-                dq(c0, c1, gc, v);
-                tc_fence_after();
-                tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (warp == 0 || warp == 4) EV(5, kb, base);
-                if (lane == 0) {
-                    if (rank == 0)
-                        mbar_arrive_relaxed(&full_b[s]);
-                    else
-                        mbar_arrive_relaxed_cluster(full_leader + s * 8);
-                }
-            }
-            (void)ld;
-            (void)ldc;
-            (void)rv;
-#else
             // Ring of three static slots (codes + group constants), unrolled so a slot is refilled
             // right after it was consumed and each load has two iterations of lead time; no
             // register moves touch a pending load.
@@ -339,15 +361,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int s = itk % NSTAGE;
                 const uint32_t ph = (itk / NSTAGE) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
-                if (warp == 0 || warp == 4) EV(4, kb, base);
+                if (warp == 0 || warp == 4) EV(4, kb, ui);
                 tc_fence_after();
                 tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
                 fetch(kb + 6, ca, cb, ga);  // refill the consumed slot three of this warp's k-blocks ahead
+                if (warp == 0 || warp == 4) EV(6, kb, ui);
                 if (kb + 2 < kb_n) dq(na, nb, gn, v);
+                if (warp == 0 || warp == 4) EV(7, kb, ui);
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (warp == 0 || warp == 4) EV(5, kb, base);
+                if (warp == 0 || warp == 4) EV(5, kb, ui);
                 if (lane == 0) {
 #if MOBI_RELAXED
                     if (rank == 0)
@@ -369,7 +393,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (!step(kb + 2, c10, c11, g1, c20, c21, g2)) break;
                 if (!step(kb + 4, c20, c21, g2, c00, c01, g0)) break;
             }
-#endif
         }
     } else {
         // ---------------- epilogue ----------------
@@ -378,8 +401,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int q = warp % 4;
         const int et = threadIdx.x - 32 * kWarpEpi0;  // 0..127
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        uint32_t tc = 0;
-        for (int pair = cid; pair < total; pair += ncl, ++tc) {
+        for (uint32_t tc = 0;; ++tc) {
+            const int pair = unit_get(tc);
+            if (pair < 0) break;
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
@@ -394,8 +418,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // CTA-scope wait: the arrival is the tensor core's commit and TMEM visibility comes from
             // tcgen05.fence (a cluster-scope acquire would invalidate L1 on every poll)
             mbar_wait(acc_full, tc & 1);
+            if (warp == kWarpEpi0) EVU(2, tc);
             tc_fence_after();
+            if (MOBI_X_NOEPI) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty), 0));
+                continue;
+            }
             epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
+            if (warp == kWarpEpi0) EVU(5, tc);
             uint32_t va[16], vb[16];
             tmem_ld16(tmem + lane_base, va);
 #pragma unroll
@@ -417,6 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty), 0));  // leader's barrier
+            if (warp == kWarpEpi0) EVU(3, tc);
             epi_bar_sync();  // staging tile complete
             const int64_t r0 = (int64_t)rt * kRowTile + 8 * (et % 16);
             for (int t = et / 16; t < tt.n; t += 8) {
@@ -430,6 +463,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int u = 0; u < 8 && r0 + u < p.out; ++u) dp[u] = sp[u];
                 }
             }
+            if (warp == kWarpEpi0) EVU(4, tc);
         }
     }
     tc_fence_before();
@@ -493,6 +527,7 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
     p.trace = trace;
     p.bk_hist = L->bk_hist;
+    p.unit_ctr = L->meta + 32;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);

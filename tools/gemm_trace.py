@@ -42,8 +42,13 @@ def main():
         print(f"{nm:22s} mean {col.mean():12.0f}  min {col.min():12.0f}  max {col.max():12.0f}")
     timeline(full)
     if impl == 4:
-        print("-- peer CTA")
-        timeline(full, 20480 + 512)
+        ev = full[20480 + 512:20480 + 512 + 4 * 64].reshape(4, 64).astype(np.int64)
+        e0 = full[20480:20480 + 64].astype(np.int64)
+        t0 = e0[e0 > 0].min()
+        print("leader MMA thread: elected / desc done / 4 MMAs issued / committed")
+        for kb in range(24):
+            print(f"{kb:2d} " + " ".join(f"{(ev[e][kb] - t0) if ev[e][kb] else -1:10d}" for e in range(4)))
+    units(full)
     per = full[16 * 1024:20480].reshape(-1, 2)
     per = per[per[:, 0] > 0]
     for N in sorted(set(per[:, 0].tolist())):
@@ -52,13 +57,26 @@ def main():
               f"   ideal MMA {64 * 4 * 137.5 * N / 256:9.0f}")
 
 
+def units(full):
+    ev = full[24576:24576 + 2 * 8 * 16].reshape(2, 8, 16).astype(np.int64)
+    t0 = ev[ev > 0].min() if (ev > 0).any() else 0
+    names = ["mma:acc_empty ok", "mma:last kb", "epi:acc_full", "epi:released", "epi:scatter done", "epi:drain start"]
+    print("unit events (ns from first): leader / peer")
+    print("u   " + " ".join(f"{n:>17s}" for n in names))
+    print("unit N:", full[24576 + 6 * 16:24576 + 7 * 16].tolist())
+    for u in range(16):
+        for r in range(2):
+            print(f"{u:2d}{'LP'[r]} " + " ".join(f"{(ev[r][e][u] - t0) if ev[r][e][u] else -1:17d}" for e in range(6)))
+
+
 def timeline(full, base=20480):
     ev = full[base:base + 8 * 64].reshape(8, 64).astype(np.int64)
     t0 = ev[0][ev[0] > 0].min() if (ev[0] > 0).any() else 0
-    names = ["tma:empty ok", "mma:full_b ok", "mma:full_a ok", "mma:issued", "dq:empty ok", "dq:dq done", "dq:arrive"]
+    names = ["tma:empty ok", "mma:full_b ok", "-", "mma:issued", "dq:empty ok", "dq:arrive-ready", "dq:st+fetch",
+             "dq:dq done"]
     print("kb  " + " ".join(f"{n:>14s}" for n in names))
     for kb in range(0, 24):
-        print(f"{kb:2d}  " + " ".join(f"{(ev[e][kb] - t0) if ev[e][kb] else -1:14d}" for e in range(7)))
+        print(f"{kb:2d}  " + " ".join(f"{(ev[e][kb] - t0) if ev[e][kb] else -1:14d}" for e in range(8)))
 
 
 if __name__ == "__main__":
