@@ -31,9 +31,10 @@
  * offending dim/index like the reference's) or MOBI_ERUNTIME (CUDA/NCCL failure,
  * std::runtime_error).  mobi_last_error() returns the thread-local message of the last failure.
  *
- * Threading: a layer handle is immutable after create except for its internal workspace;
- * concurrent calls on one handle must be serialised by the caller (or use one handle per
- * stream).  Handles on different devices are independent.
+ * Threading: a layer handle's weights are immutable after create.  Each stream a handle is called
+ * on gets its own workspace (created on first use), so calls on distinct streams may run
+ * concurrently from any threads; calls on one stream are serialised by the handle (one call's
+ * launch sequence is contiguous on the stream).  Handles on different devices are independent.
  */
 #ifndef MOBI_B200_H
 #define MOBI_B200_H
@@ -166,11 +167,32 @@ MOBI_API int mobi_layer_profile_read(mobi_layer_t layer, double* ms /*[MOBI_PROF
 /* Number of kernels the last forward on this layer launched (for launch accounting). */
 MOBI_API int mobi_layer_last_launches(mobi_layer_t layer, int32_t* launches);
 
+/* Kernel ids reported by mobi_layer_last_plan. */
+#define MOBI_K_NONE 0
+#define MOBI_K_ROUTER_DECODE 1      /* decode GEMV router (router_dec_kernel, T <= 32)               */
+#define MOBI_K_ROUTER_TC 2          /* 1-CTA tcgen05 router tiles (128 tokens x 128 hidden)          */
+#define MOBI_K_ROUTER_TC_CLUSTER 3  /* the same with K split over a 2-3 CTA cluster (DSMEM sum)     */
+#define MOBI_K_ROUTER_TC_SPLITK 4   /* the same with global split-K partials + a reduce kernel       */
+#define MOBI_K_ROUTER_PAIR128 5     /* CTA-pair tcgen05 router, 256 tokens x 128 hidden per pair    */
+#define MOBI_K_ROUTER_PAIR256 6     /* CTA-pair tcgen05 router, 256 tokens x 256 hidden per pair    */
+#define MOBI_K_ROUTER_SIMT 7        /* CUDA-core router (inputs the tcgen05 router cannot take)      */
+#define MOBI_K_GEMM_DECODE_PLANES 11 /* decode GEMV over the union's 2-bit slice planes              */
+#define MOBI_K_GEMM_DECODE_MERGED 12 /* decode stream-K GEMV over the merged 8-bit codes             */
+#define MOBI_K_GEMM_SPLITK 13       /* 1-CTA tcgen05 nested residual GEMM with split-K (T <= 64)     */
+#define MOBI_K_GEMM_PAIR 14         /* CTA-pair tcgen05 nested residual GEMM (prefill)              */
+#define MOBI_K_GEMM_SIMT 15         /* CUDA-core reference GEMM (test hook only)                     */
+/* The last call's plan: plan[0] router kernel id, [1] GEMM kernel id, [2] GEMM grid (CTAs),
+ * [3] kernels launched, [4] token tiles of the bucketed GEMM (-1 for the decode kernels),
+ * [5] 256-row weight-tile pairs, [6] GEMM units = [4] x [5] (-1 for decode), [7] tokens.
+ * Synchronises the call's stream to read the device-side tile count. */
+MOBI_API int mobi_layer_last_plan(mobi_layer_t layer, int32_t* plan /*[8]*/);
+
 MOBI_API const char* mobi_last_error(void);
 
-/* Test hook (not part of the drop-in surface): impl 1 routes the GEMM through the CUDA-core
- * reference kernel (gemm_simt.cu) so the test-suite can cross-check the tcgen05 kernel. */
-MOBI_API int mobi_debug_set_impl(int impl);
+/* Test hook (not part of the drop-in surface), per layer: impl 1 routes the GEMM through the
+ * CUDA-core reference kernel (gemm_simt.cu) so the test-suite can cross-check the tcgen05 kernel;
+ * other values select traced / alternative kernels for development tools.  0 = production. */
+MOBI_API int mobi_layer_debug_impl(mobi_layer_t layer, int impl);
 MOBI_API const char* mobi_version(void);
 
 #ifdef __cplusplus

@@ -11,7 +11,7 @@ __all__ = ["MobiError", "MobiInvalidArgument", "build", "lib", "MobiLayer", "per
 
 def __getattr__(name):  # lazy: importing the package must not require torch/CUDA
     if name in ("MobiLayer", "permute_by_slice", "calibrate_threshold", "decompose", "ratio_from_target_bits",
-                "avg_bits_from_masks", "set_debug_impl"):
+                "avg_bits_from_masks"):
         from . import layer
         return getattr(layer, name)
     raise AttributeError(name)

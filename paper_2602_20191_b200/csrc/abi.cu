@@ -5,7 +5,10 @@
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
+#include <set>
 #include <sstream>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -14,13 +17,23 @@
 namespace mobi {
 
 static thread_local std::string g_err;
-static int g_impl_override = 0;  // test hook: 1 = CUDA-core reference GEMM, 2 = traced tcgen05,
-                                 // 5 = bucketed tcgen05 path at every T (no decode path), 6 = decode path without PDL
 static unsigned long long* g_trace_buf = nullptr;
 
 int set_error(int code, const std::string& msg) {
     g_err = msg;
     return code;
+}
+
+int func_attr_once_impl(const void* fn, cudaFuncAttribute attr, int value) {
+    static std::mutex mu;
+    static std::set<std::tuple<int, const void*, int>> done;
+    int dev = 0;
+    MOBI_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(std::make_tuple(dev, fn, (int)attr))) return MOBI_OK;
+    MOBI_CUDA(cudaFuncSetAttribute(fn, attr, value));
+    done.insert(std::make_tuple(dev, fn, (int)attr));
+    return MOBI_OK;
 }
 
 int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* cperm, int32_t* inverse,
@@ -91,7 +104,12 @@ void free_ws(mobi_layer* L) {
 
 int ensure_ws(mobi_layer* L, int64_t T) {
     if (T <= L->ws_T) return MOBI_OK;
-    cudaDeviceSynchronize();  // workspace may be in use by queued work
+    if (L->ws_T >= 0) {  // the old workspace may still be in use by work queued on this context's stream
+        if (L->ctx_bound)
+            MOBI_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(L->ctx_stream)));
+        else
+            MOBI_CUDA(cudaDeviceSynchronize());
+    }
     free_ws(L);
     const int64_t Tc = round_up(std::max<int64_t>(T, 1), 256);
     L->tpad_max = round_up(Tc + 2 * kMaxBuckets * (kBucketAlign - 1), kBucketAlign);
@@ -283,14 +301,14 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_device =
 int route_scores(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, float* scores_out, uint8_t* masks_out,
                  bool* masks_ready, cudaStream_t st, bool fuse_bucket = false) {
     *masks_ready = false;
-    if (g_impl_override == 7 && router_tc_supported(L, x)) {  // traced router (development hook)
+    if (L->impl == 7 && router_tc_supported(L, x)) {  // traced router (development hook)
         static unsigned long long* tbuf = nullptr;
         if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
         MOBI_CUDA(cudaMemsetAsync(tbuf, 0, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long), st));
         g_trace_buf = tbuf;
         return launch_router_tc(L, x, T, delta, scores_out, masks_out, masks_ready, st, tbuf);
     }
-    if (g_impl_override != 1 && router_tc_supported(L, x))
+    if (L->impl != 1 && router_tc_supported(L, x))
         return launch_router_tc(L, x, T, delta, scores_out, masks_out, masks_ready, st, nullptr, fuse_bucket);
     return launch_router(L, x, T, st);
 }
@@ -305,6 +323,67 @@ struct DeviceGuard {
         int cur = -1;
         cudaGetDevice(&cur);
         if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ---- per-stream contexts (re-entrancy, see mobi_layer in mobi_internal.cuh) ----
+mobi_layer* new_context(mobi_layer* H, void* stream) {
+    mobi_layer* c = new mobi_layer;
+    c->device = H->device;
+    c->n_sm = H->n_sm;
+    c->out = H->out, c->in = H->in, c->gs = H->gs, c->G = H->G;
+    c->E = H->E, c->b = H->b, c->nr = H->nr, c->h = H->h;
+    c->out_pad = H->out_pad, c->in_pad = H->in_pad, c->kblocks = H->kblocks, c->h_pad = H->h_pad;
+    c->group_shift = H->group_shift;
+    c->single_group = H->single_group;
+    c->codes8 = H->codes8, c->dplanes = H->dplanes, c->gconst = H->gconst;
+    c->w1t = H->w1t, c->b1 = H->b1, c->w2 = H->w2, c->b2 = H->b2;
+    c->mtab = H->mtab;
+    c->owner = H;
+    c->ctx_stream = stream;
+    c->ctx_bound = true;
+    c->call_mu = new std::mutex;
+    return c;
+}
+
+// the context serving `stream` (created on first use); call with the handle
+mobi_layer* context_for(mobi_layer* H, void* stream, int* rc) {
+    *rc = MOBI_OK;
+    std::lock_guard<std::mutex> g(*H->ctx_mu);
+    if (!H->ctx_bound) {
+        H->ctx_bound = true;
+        H->ctx_stream = stream;
+    }
+    if (H->ctx_stream == stream) return H;
+    for (mobi_layer* c : H->ctxs)
+        if (c->ctx_stream == stream) return c;
+    // a stream being captured into a CUDA graph cannot allocate a workspace: it records the handle's
+    // own (reserved) workspace, which the graph then uses wherever it is replayed
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(reinterpret_cast<cudaStream_t>(stream), &cap) != cudaSuccess) cudaGetLastError();
+    if (cap != cudaStreamCaptureStatusNone) return H;
+    mobi_layer* c = new_context(H, stream);
+    if (H->reserved_T > 0) *rc = ensure_ws(c, H->reserved_T);
+    H->ctxs.push_back(c);
+    return c;
+}
+
+// entry-point prologue: device guard + the stream's context, locked for the whole launch sequence
+struct CallScope {
+    DeviceGuard dg;
+    mobi_layer* C = nullptr;
+    std::unique_lock<std::mutex> lk;
+    int rc = MOBI_OK;
+    CallScope(mobi_layer* H, void* stream) : dg(H->device) {
+        C = context_for(H, stream, &rc);
+        lk = std::unique_lock<std::mutex>(*C->call_mu);
+        C->impl = H->impl;
+    }
+    // the handle reports the last call's launch accounting whichever context ran it
+    void publish(mobi_layer* H) {
+        H->last_launches = C->last_launches;
+        for (int i = 0; i < 8; ++i) H->plan[i] = C->plan[i];
+        H->plan_ctx = C;
     }
 };
 
@@ -354,14 +433,18 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
               uint8_t* masks_out, cudaStream_t st) {
     CHECK_ARG(T >= 0, "forward_elastic: negative token count " << T);
     L->last_launches = 0;
+    for (int i = 0; i < 8; ++i) L->plan[i] = 0;
+    L->plan[7] = (int32_t)T;
     if (T == 0) return MOBI_OK;
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
-    if ((g_impl_override == 0 || g_impl_override == 6 || g_impl_override == 9) && decode_supported(L, x, T)) {
+    // kernel choices follow the plan size (the whole batch when mobi_forward_host runs it in chunks)
+    const int64_t Tp = std::max(T, L->plan_T);
+    if ((L->impl == 0 || L->impl == 6 || L->impl == 9) && decode_supported(L, x, Tp)) {
         // decode-size batch: router GEMV -> (PDL) stream-K decode GEMM, no bucketing
         unsigned long long* tbuf = nullptr;
-        if (g_impl_override == 9) {  // traced (development hook): per-CTA globaltimer marks
+        if (L->impl == 9) {  // traced (development hook): per-CTA globaltimer marks
             static unsigned long long* buf = nullptr;
             if (!buf) MOBI_CUDA(cudaMalloc(&buf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
             MOBI_CUDA(cudaMemsetAsync(buf, 0, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long), st));
@@ -372,7 +455,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
             if ((rc = launch_router_dec(L, xb, T, delta, masks_out, nullptr, st, tbuf))) return rc;
         }
         ProfScope p(L, 3, st);
-        const bool pdl = !given_masks && g_impl_override != 6 && !L->prof;
+        const bool pdl = !given_masks && L->impl != 6 && !L->prof;
         if (decode_planes_supported(L, x, T))  // slice planes: stream only the slices the batch uses
             return launch_decode_planes(L, xb, T, given_masks, delta, masks_out, nullptr,
                                         reinterpret_cast<__nv_bfloat16*>(y), pdl, st, tbuf);
@@ -382,11 +465,11 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
     bool ready = false;
     if (!given_masks) {
         ProfScope p(L, 0, st);
-        if ((rc = route_scores(L, xb, T, delta, nullptr, masks_out, &ready, st, g_impl_override != 8))) return rc;
+        if ((rc = route_scores(L, xb, T, delta, nullptr, masks_out, &ready, st, L->impl != 8))) return rc;
     }
     // the tcgen05 router (prefill sizes) has already decided the masks and laid out the buckets;
     // otherwise (given masks, fallback router) the bucket kernel does it
-    const bool fused = ready && g_impl_override != 8;
+    const bool fused = ready && L->impl != 8;
     if (!fused) {
         ProfScope p(L, 1, st);
         if ((rc = launch_bucket(L, T, delta, ready ? L->masks : given_masks, nullptr, ready ? nullptr : masks_out,
@@ -398,23 +481,23 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
         if ((rc = launch_gather(L, xb, T, st, fused, fused && !L->prof))) return rc;
     }
     __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
-    if (fused && g_impl_override != 0 && g_impl_override != 3 && g_impl_override != 5)  // the tcgen05 GEMMs clear them
+    if (fused && L->impl != 0 && L->impl != 3 && L->impl != 5)  // the tcgen05 GEMMs clear them
         MOBI_CUDA(cudaMemsetAsync(L->bk_hist, 0, 48 * sizeof(int32_t), st));
     ProfScope p(L, 3, st);
-    if (g_impl_override == 1) return launch_gemm_simt(L, yb, T, st);
-    if (g_impl_override == 2 || g_impl_override == 4) {  // traced tcgen05 kernels (development hook)
+    if (L->impl == 1) return launch_gemm_simt(L, yb, T, st);
+    if (L->impl == 2 || L->impl == 4) {  // traced tcgen05 kernels (development hook)
         static unsigned long long* tbuf = nullptr;
         if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
         MOBI_CUDA(cudaMemsetAsync(tbuf, 0, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long), st));
         g_trace_buf = tbuf;
-        if (g_impl_override == 4) return launch_gemm_tc2(L, yb, T, st, tbuf);
+        if (L->impl == 4) return launch_gemm_tc2(L, yb, T, st, tbuf);
         return launch_gemm_tc(L, yb, T, st, tbuf);
     }
-    if (g_impl_override == 3) return launch_gemm_tc2(L, yb, T, st);  // CTA-pair kernel
-    if (g_impl_override == 5) return launch_gemm_tc(L, yb, T, st);   // 1-CTA kernel (comparison)
+    if (L->impl == 3) return launch_gemm_tc2(L, yb, T, st);  // CTA-pair kernel
+    if (L->impl == 5) return launch_gemm_tc(L, yb, T, st);   // 1-CTA kernel (comparison)
     // production: the CTA-pair kernel (B split across the pair: half the smem operand traffic per SM);
     // the 1-CTA kernel for batches small enough to need split-K
-    if (T <= 64) return launch_gemm_tc(L, yb, T, st);
+    if (Tp <= 64) return launch_gemm_tc(L, yb, T, st);
     return launch_gemm_tc2(L, yb, T, st, nullptr, !L->prof);
 }
 
@@ -428,8 +511,9 @@ extern "C" {
 const char* mobi_last_error(void) { return g_err.c_str(); }
 const char* mobi_version(void) { return "mobi_b200 0.1 (sm_100a)"; }
 
-int mobi_debug_set_impl(int impl) {
-    g_impl_override = impl;
+int mobi_layer_debug_impl(mobi_layer_t L, int impl) {
+    CHECK_ARG(L, "null layer");
+    L->impl = impl;
     return MOBI_OK;
 }
 
@@ -450,8 +534,13 @@ static int create_impl(const mobi_layer_desc* desc, int device, mobi_layer_t* ou
     MOBI_CUDA(cudaGetDeviceCount(&ndev));
     CHECK_ARG(device >= 0 && device < ndev, "mobi_layer_create: device " << device << " out of [0," << ndev << ")");
     DeviceGuard g(device);
+    int n_sm = 0;
+    MOBI_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
     mobi_layer* L = new mobi_layer;
     L->device = device;
+    L->n_sm = n_sm;
+    L->ctx_mu = new std::mutex;
+    L->call_mu = new std::mutex;
     int rc = validate_and_fill(desc, L, codes_on_device);
     if (!rc && codes_on_device) {
         cudaPointerAttributes pa{};
@@ -518,10 +607,36 @@ int mobi_layer_create_device(const mobi_layer_desc* desc, int device, mobi_layer
     return create_impl(desc, device, out, true);
 }
 
+static void destroy_context(mobi_layer* c) {  // workspace + lazily built host objects; weights are the handle's
+    free_ws(c);
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    for (auto& e : c->ev_pipe)
+        if (e) cudaEventDestroy(e);
+    dfree(c->gpart);
+    dfree(c->hpart);
+    dfree(c->dec_part);
+    dfree(c->dec_spart);
+    dfree(c->dec_cnt);
+    if (c->tmap_w1) delete c->tmap_w1;
+    if (c->tmap_w1_64) delete c->tmap_w1_64;
+    if (c->x_dev) cudaFree(c->x_dev);
+    if (c->y_dev) cudaFree(c->y_dev);
+    if (c->h_x) cudaFreeHost(c->h_x);
+    if (c->h_y) cudaFreeHost(c->h_y);
+    for (auto& e : c->ev_pool) cudaEventDestroy(e);
+    delete c->call_mu;
+    delete c;
+}
+
 int mobi_layer_destroy(mobi_layer_t L) {
     if (!L) return MOBI_OK;
     DeviceGuard g(L->device);
     cudaDeviceSynchronize();
+    for (mobi_layer* c : L->ctxs) destroy_context(c);
+    L->ctxs.clear();
+    delete L->ctx_mu;
+    delete L->call_mu;
     free_ws(L);
     dfree(L->codes8);
     dfree(L->dplanes);
@@ -554,7 +669,12 @@ int mobi_layer_reserve(mobi_layer_t L, int64_t max_tokens) {
     CHECK_ARG(L, "null layer");
     CHECK_ARG(max_tokens >= 0, "mobi_layer_reserve: negative token count");
     DeviceGuard g(L->device);
-    return ensure_ws(L, max_tokens);
+    std::lock_guard<std::mutex> lk(*L->ctx_mu);
+    L->reserved_T = std::max(L->reserved_T, max_tokens);
+    int rc = ensure_ws(L, max_tokens);
+    for (mobi_layer* c : L->ctxs)
+        if (!rc) rc = ensure_ws(c, max_tokens);
+    return rc;
 }
 
 int mobi_layer_info(mobi_layer_t L, int64_t* out, int64_t* in, int32_t* n_slices, int64_t* router_hidden,
@@ -598,56 +718,71 @@ int mobi_layer_unpack_codes(mobi_layer_t L, uint8_t* codes_host) {
     return rc;
 }
 
-int mobi_score(mobi_layer_t L, const void* x, int64_t T, float* scores, void* stream) {
-    CHECK_ARG(L, "null layer");
+int mobi_score(mobi_layer_t H, const void* x, int64_t T, float* scores, void* stream) {
+    CHECK_ARG(H, "null layer");
     CHECK_ARG(T >= 0, "score: negative token count");
     if (T == 0) return MOBI_OK;
-    DeviceGuard g(L->device);
+    CallScope cs(H, stream);
+    if (cs.rc) return cs.rc;
+    mobi_layer* L = cs.C;
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     L->last_launches = 0;
     bool ready = false;
     if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, INFINITY, scores, nullptr, &ready, S(stream))))
         return rc;
-    if (ready) return MOBI_OK;
-    return launch_bucket(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream));
+    if (!ready) rc = launch_bucket(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream));
+    cs.publish(H);
+    return rc;
 }
 
-int mobi_route(mobi_layer_t L, const void* x, int64_t T, float delta, float* scores, uint8_t* masks, int32_t* perm,
+int mobi_route(mobi_layer_t H, const void* x, int64_t T, float delta, float* scores, uint8_t* masks, int32_t* perm,
                int32_t* inverse, int32_t* bucket_count, void* stream) {
-    CHECK_ARG(L, "null layer");
+    CHECK_ARG(H, "null layer");
     CHECK_ARG(T >= 0, "score: negative token count");
     if (T == 0) return MOBI_OK;
-    DeviceGuard g(L->device);
+    CallScope cs(H, stream);
+    if (cs.rc) return cs.rc;
+    mobi_layer* L = cs.C;
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     L->last_launches = 0;
     bool ready = false;
     if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, delta, scores, masks, &ready, S(stream))))
         return rc;
-    return launch_bucket(L, T, delta, ready ? L->masks : nullptr, ready ? nullptr : scores, ready ? nullptr : masks,
-                         perm, inverse, bucket_count, S(stream), !ready);
+    rc = launch_bucket(L, T, delta, ready ? L->masks : nullptr, ready ? nullptr : scores, ready ? nullptr : masks, perm,
+                       inverse, bucket_count, S(stream), !ready);
+    cs.publish(H);
+    return rc;
 }
 
-int mobi_forward(mobi_layer_t L, const void* x, int64_t T, float delta, void* y, uint8_t* masks, void* stream) {
-    CHECK_ARG(L, "null layer");
-    DeviceGuard g(L->device);
-    return run_layer(L, x, T, delta, nullptr, y, masks, S(stream));
+int mobi_forward(mobi_layer_t H, const void* x, int64_t T, float delta, void* y, uint8_t* masks, void* stream) {
+    CHECK_ARG(H, "null layer");
+    CallScope cs(H, stream);
+    if (cs.rc) return cs.rc;
+    const int rc = run_layer(cs.C, x, T, delta, nullptr, y, masks, S(stream));
+    cs.publish(H);
+    return rc;
 }
 
-int mobi_forward_masked(mobi_layer_t L, const void* x, int64_t T, const uint8_t* masks, void* y, void* stream) {
-    CHECK_ARG(L, "null layer");
+int mobi_forward_masked(mobi_layer_t H, const void* x, int64_t T, const uint8_t* masks, void* y, void* stream) {
+    CHECK_ARG(H, "null layer");
     CHECK_ARG(masks != nullptr || T == 0, "forward_elastic: null gate masks");
-    DeviceGuard g(L->device);
-    return run_layer(L, x, T, 0.f, masks, y, nullptr, S(stream));
+    CallScope cs(H, stream);
+    if (cs.rc) return cs.rc;
+    const int rc = run_layer(cs.C, x, T, 0.f, masks, y, nullptr, S(stream));
+    cs.publish(H);
+    return rc;
 }
 
-int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta, void* y_host, uint8_t* masks_host,
+int mobi_forward_host(mobi_layer_t H, const void* x_host, int64_t T, float delta, void* y_host, uint8_t* masks_host,
                       void* stream) {
-    CHECK_ARG(L && x_host && y_host, "mobi_forward_host: null argument");
+    CHECK_ARG(H && x_host && y_host, "mobi_forward_host: null argument");
     CHECK_ARG(T >= 0, "forward_elastic: negative token count " << T);
     if (T == 0) return MOBI_OK;
-    DeviceGuard g(L->device);
+    CallScope cs(H, stream);
+    if (cs.rc) return cs.rc;
+    mobi_layer* L = cs.C;
     cudaStream_t st = S(stream);
     const size_t xb = (size_t)(T * L->in * 2), yb = (size_t)(T * L->out * 2);
     if (T > L->h_cap) {
@@ -679,8 +814,10 @@ int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta
     uint8_t* mdev = masks_host ? reinterpret_cast<uint8_t*>(L->x_dev) + xb : nullptr;
     void* ydst = yp ? y_host : L->h_y;
     // token chunks pipelined over three streams: the host->device copy of chunk i+1 and the
-    // device->host copy of chunk i-1 overlap the forward of chunk i (tokens are independent, so the
-    // chunked result is identical to the whole-batch one)
+    // device->host copy of chunk i-1 overlap the forward of chunk i.  Tokens are independent and
+    // every chunk runs the kernels the whole batch would (plan_T = T: router variant, cluster K-split
+    // and GEMM path are chosen from the batch size; no chunk is shorter than 256 tokens), so the
+    // chunked result is bit-identical to one whole-batch mobi_forward.
     static const int nch_env = [] {  // development knob: MOBI_E2E_CHUNKS overrides the chunk count
         const char* e = std::getenv("MOBI_E2E_CHUNKS");
         return e ? std::max(1, std::min(8, std::atoi(e))) : 0;
@@ -703,18 +840,26 @@ int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta
         cudaEvent_t* ev = L->ev_pipe;  // [0..7] copied in, [8..15] computed, [16] prior work
         MOBI_CUDA(cudaEventRecord(ev[16], st));  // prior work on the caller's stream
         MOBI_CUDA(cudaStreamWaitEvent(L->s_h2d, ev[16], 0));
+        struct PlanScope {  // kernels chosen for the whole batch while the chunks run
+            mobi_layer* L;
+            ~PlanScope() { L->plan_T = 0; }
+        } ps{L};
+        L->plan_T = T;
+        int rc = ensure_ws(L, step + 256);  // the largest chunk (a folded tail adds < 256 tokens)
+        if (rc) return rc;
         int c = 0;
-        for (int64_t t0 = 0; t0 < T; t0 += step, ++c) {
-            const int64_t n = std::min(step, T - t0);
+        for (int64_t t0 = 0; t0 < T && !rc; ++c) {
+            int64_t n = std::min(step, T - t0);
+            if (T - (t0 + n) < 256) n = T - t0;  // fold a short tail into this chunk
             const size_t xo = (size_t)(t0 * L->in * 2), yo = (size_t)(t0 * L->out * 2);
             MOBI_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(L->x_dev) + xo,
                                       reinterpret_cast<const uint8_t*>(xsrc) + xo, (size_t)(n * L->in * 2),
                                       cudaMemcpyHostToDevice, L->s_h2d));
             MOBI_CUDA(cudaEventRecord(ev[c], L->s_h2d));
             MOBI_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
-            int rc = run_layer(L, reinterpret_cast<uint8_t*>(L->x_dev) + xo, n, delta, nullptr,
-                               reinterpret_cast<uint8_t*>(L->y_dev) + yo, mdev ? mdev + t0 : nullptr, st);
-            if (rc) return rc;
+            rc = run_layer(L, reinterpret_cast<uint8_t*>(L->x_dev) + xo, n, delta, nullptr,
+                           reinterpret_cast<uint8_t*>(L->y_dev) + yo, mdev ? mdev + t0 : nullptr, st);
+            if (rc) break;
             MOBI_CUDA(cudaEventRecord(ev[8 + c], st));
             MOBI_CUDA(cudaStreamWaitEvent(L->s_d2h, ev[8 + c], 0));
             MOBI_CUDA(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(ydst) + yo,
@@ -722,7 +867,9 @@ int mobi_forward_host(mobi_layer_t L, const void* x_host, int64_t T, float delta
                                       cudaMemcpyDeviceToHost, L->s_d2h));
             if (masks_host)
                 MOBI_CUDA(cudaMemcpyAsync(masks_host + t0, mdev + t0, (size_t)n, cudaMemcpyDeviceToHost, L->s_d2h));
+            t0 += n;
         }
+        if (rc) return rc;
         MOBI_CUDA(cudaStreamSynchronize(L->s_d2h));
     }
     MOBI_CUDA(cudaStreamSynchronize(st));
@@ -820,6 +967,24 @@ int mobi_layer_profile_read(mobi_layer_t L, double* ms, int64_t* launches) {
 int mobi_layer_last_launches(mobi_layer_t L, int32_t* launches) {
     CHECK_ARG(L && launches, "null argument");
     *launches = L->last_launches;
+    return MOBI_OK;
+}
+
+int mobi_layer_last_plan(mobi_layer_t L, int32_t* plan) {
+    CHECK_ARG(L && plan, "null argument");
+    DeviceGuard g(L->device);
+    for (int i = 0; i < 8; ++i) plan[i] = L->plan[i];
+    plan[3] = L->last_launches;
+    plan[4] = plan[6] = -1;
+    plan[5] = (int32_t)(L->out_pad / (2 * kRowTile));
+    mobi_layer* c = L->plan_ctx ? L->plan_ctx : L;
+    if ((plan[1] == MOBI_K_GEMM_PAIR || plan[1] == MOBI_K_GEMM_SPLITK || plan[1] == MOBI_K_GEMM_SIMT) && c->meta) {
+        int32_t n = 0;
+        MOBI_CUDA(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(c->ctx_stream)));
+        MOBI_CUDA(cudaMemcpy(&n, c->meta, sizeof(n), cudaMemcpyDeviceToHost));
+        plan[4] = n;
+        plan[6] = n * plan[5];
+    }
     return MOBI_OK;
 }
 

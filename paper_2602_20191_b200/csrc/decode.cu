@@ -955,16 +955,6 @@ __global__ void __launch_bounds__(kFmaThreads, kFmaCps) decode_fma_kernel(const 
     }
 }
 
-int sm_count_dec() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
 
 struct DecPlan {
     int n_cta = 0, len_max = 0, xs_stride = 0;
@@ -976,7 +966,7 @@ DecPlan plan_decode(const mobi_layer* L, int64_t T) {
     DecPlan d;
     const int64_t n_rt = cdiv(L->out, kRowTile);
     d.U = n_rt * L->kblocks;
-    d.n_cta = (int)std::min<int64_t>(sm_count_dec(), d.U);
+    d.n_cta = (int)std::min<int64_t>(L->n_sm, d.U);
     d.len_max = (int)std::min<int64_t>(cdiv(d.U, d.n_cta), L->kblocks);
     d.xs_stride = d.len_max * kKBlock + 8;  // row stride = 16 mod 128 bytes: conflict-free B loads
     d.smem = dec_smem((int)T, d.len_max, d.xs_stride).total;
@@ -988,11 +978,9 @@ int g_dec_fma = 1;  // development switch: 0 = mma.sync decode kernel for every 
 
 template <int NT>
 int launch_decode_fma_t(mobi_layer* L, const DParams& p, size_t smem, bool pdl, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(decode_fma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+        MOBI_TRY(func_attr_once(decode_fma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kDecSmemMax));
-        attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)p.n_cta);
@@ -1006,16 +994,16 @@ int launch_decode_fma_t(mobi_layer* L, const DParams& p, size_t smem, bool pdl, 
     cfg.numAttrs = pdl ? 1 : 0;
     MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_fma_kernel<NT>, p));
     ++L->last_launches;
+    L->plan[1] = MOBI_K_GEMM_DECODE_MERGED;
+    L->plan[2] = p.n_cta;
     return MOBI_OK;
 }
 
 template <int MAXT>
 int launch_decode_gemm_t(mobi_layer* L, const DParams& p, size_t smem, bool pdl, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(decode_gemm_kernel<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+        MOBI_TRY(func_attr_once(decode_gemm_kernel<MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kDecSmemMax));
-        attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)p.n_cta);
@@ -1029,6 +1017,8 @@ int launch_decode_gemm_t(mobi_layer* L, const DParams& p, size_t smem, bool pdl,
     cfg.numAttrs = pdl ? 1 : 0;
     MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_gemm_kernel<MAXT>, p));
     ++L->last_launches;
+    L->plan[1] = MOBI_K_GEMM_DECODE_MERGED;
+    L->plan[2] = p.n_cta;
     return MOBI_OK;
 }
 
@@ -1065,20 +1055,18 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
     p.delta = delta;
     const int n_mt = (int)(L->h_pad / kRdRows);
     const dim3 grid((unsigned)(n_mt * kRdCluster));
-    static bool carve = false;
     auto smem_of = [](int nt) { return (size_t)kRdWarps * kRdRing * 32 * (2 + nt) * 16; };
-    if (!carve) {  // run with the SM configured for maximum shared memory, so the decode GEMM that
+    {  // run with the SM configured for maximum shared memory, so the decode GEMM that
                    // follows (PDL) can be co-resident while the router streams w1
-        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        MOBI_TRY(func_attr_once(router_dec_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                        (int)cudaSharedmemCarveoutMaxShared));
-        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        MOBI_TRY(func_attr_once(router_dec_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                        (int)cudaSharedmemCarveoutMaxShared));
-        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<4>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        MOBI_TRY(func_attr_once(router_dec_kernel<4>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                        (int)cudaSharedmemCarveoutMaxShared));
-        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(1)));
-        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(2)));
-        MOBI_CUDA(cudaFuncSetAttribute(router_dec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(4)));
-        carve = true;
+        MOBI_TRY(func_attr_once(router_dec_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(1)));
+        MOBI_TRY(func_attr_once(router_dec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(2)));
+        MOBI_TRY(func_attr_once(router_dec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(4)));
     }
     // PDL: the router's CTAs may launch while the previous kernel (e.g. the last layer's decode GEMM)
     // drains and prefetch their first w1 chunks; griddepcontrol.wait guards X and every write
@@ -1103,6 +1091,7 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
     }
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
+    L->plan[0] = MOBI_K_ROUTER_DECODE;
     return MOBI_OK;
 }
 
@@ -1141,7 +1130,7 @@ int launch_decode_gemm(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const u
     p.len_max = d.len_max;
     p.xs_stride = d.xs_stride;
     if (g_dec_fma && T <= kFmaMaxT) {
-        p.n_cta = (int)std::min<int64_t>((int64_t)kFmaCps * sm_count_dec(), d.U);
+        p.n_cta = (int)std::min<int64_t>((int64_t)kFmaCps * L->n_sm, d.U);
         p.len_max = (int)std::min<int64_t>(cdiv(d.U, p.n_cta), L->kblocks);
         const size_t sm = fma_smem(kFmaMaxT, p.len_max).total;
         if (T == 1) return launch_decode_fma_t<1>(L, p, fma_smem(1, p.len_max).total, pdl, st);

@@ -489,12 +489,7 @@ bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
     if (T < 1 || T > kD2MaxLaunchT || !L->dplanes || L->E > 4) return false;
     if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
     if (!L->single_group && L->gs % kKBlock != 0) return false;
-    static const int n_sm = [] {
-        int dev = 0, n = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        return n;
-    }();
+    const int n_sm = L->n_sm;
     // one CTA per 32-row tile pays only while the tiles fit one wave: the latency chain of every
     // wave is serial (gate/up, 448 tiles, is faster on the stream-K merged-code kernels)
     if (cdiv(L->out, (int64_t)32) > n_sm) return false;
@@ -508,13 +503,11 @@ int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const
     // one launch per <= kD2MaxT tokens (one or two m16n8k16 N groups); each decides its tokens' masks
     // from the router partials and streams only its own union of slices.  Under PDL the later groups'
     // prologue (activation staging, slice 1) overlaps the previous group's tail.
-    static bool attr = false;
-    if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+        MOBI_TRY(func_attr_once(decode_planes_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kD2SmemMax));
-        MOBI_CUDA(cudaFuncSetAttribute(decode_planes_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MOBI_TRY(func_attr_once(decode_planes_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kD2SmemMax));
-        attr = true;
     }
     for (int64_t t0 = 0; t0 < T; t0 += kD2MaxT) {
         const int64_t Tg = std::min<int64_t>(kD2MaxT, T - t0);
@@ -567,6 +560,8 @@ int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const
         else
             MOBI_CUDA(cudaLaunchKernelEx(&cfg, decode_planes_kernel<1>, p));
         ++L->last_launches;
+        L->plan[1] = MOBI_K_GEMM_DECODE_PLANES;
+        L->plan[2] = (int32_t)cfg.gridDim.x;
     }
     return MOBI_OK;
 }

@@ -99,6 +99,8 @@ int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st
                                            L->perm, L->tiles, L->meta, y);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
+    L->plan[1] = MOBI_K_GEMM_SIMT;
+    L->plan[2] = (int32_t)(grid.x * grid.y * grid.z);
     return MOBI_OK;
 }
 

@@ -527,15 +527,6 @@ PFN_encodeTiled get_encode() {
     return fn;
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
 
 }  // namespace
 
@@ -557,13 +548,11 @@ int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int
 }
 
 int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace) {
-    static bool attr = false;
-    if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+        MOBI_TRY(func_attr_once(mobi_gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBytes));
-        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MOBI_TRY(func_attr_once(mobi_gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBytes));
-        attr = true;
     }
     if (!L->tmap_x) {
         L->tmap_x = new CUtensorMap;
@@ -594,7 +583,7 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
     p.y = y;
     p.vec_y = (L->out % 8 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
     const int64_t max_pairs = (int64_t)(p.n_row_tiles / 2) * L->max_tiles;
-    const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
+    const int grid = 2 * (int)std::min<int64_t>(L->n_sm / 2, max_pairs);
     p.trace = trace;
     p.tile_counter = L->meta + 32;
     p.T = (int)T;
@@ -605,6 +594,8 @@ int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, 
         mobi_gemm_tc_kernel<true><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
     else
         mobi_gemm_tc_kernel<false><<<grid, kThreads, kSmemBytes, st>>>(*L->tmap_x, p);
+    L->plan[1] = MOBI_K_GEMM_SPLITK;
+    L->plan[2] = grid;
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     if (p.max_split > 1) {

@@ -261,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < kb_n; ++kb, ++it) {
                     const uint32_t s = it % NSTAGE;
                     mbar_wait(&full_b[s], (it / NSTAGE) & 1);
+                    EV(1, kb, tc);
                     tc_fence_after();
                     const uint32_t acol = kACol0 + s * 32;
                     const uint64_t bdesc = bdesc0 + (uint64_t)(s * (kStageBytes >> 4));
@@ -268,6 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < kKBlock / 16; ++j)
                         mma_ts_f16_2sm(0u, acol + j * 8, bdesc + (uint64_t)(j * 2), idesc, (kb | j) != 0 ? 1u : 0u);
                     mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
+                    EV(3, kb, tc);
                 }
                 mma_commit_2sm_mc(acc_full, (uint16_t)0x3);
                 EVU(1, tc);
@@ -472,27 +474,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == kWarpMma) tmem_dealloc_2sm(tmem, 512);
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
 
 }  // namespace
 
 int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace,
                     bool pdl) {
-    static bool attr = false;
-    if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+        MOBI_TRY(func_attr_once(mobi_gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBytes));
-        MOBI_CUDA(cudaFuncSetAttribute(mobi_gemm_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MOBI_TRY(func_attr_once(mobi_gemm_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kSmemBytes));
-        attr = true;
     }
     if (!L->tmap_x2) {
         L->tmap_x2 = new CUtensorMap[2];
@@ -524,7 +515,7 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     p.y = y;
     p.vec_y = (L->out % 8 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
     const int64_t max_pairs = (int64_t)(p.n_row_tiles / 2) * L->max_tiles;
-    const int grid = 2 * (int)std::min<int64_t>(sm_count() / 2, max_pairs);
+    const int grid = 2 * (int)std::min<int64_t>(L->n_sm / 2, max_pairs);
     p.trace = trace;
     p.bk_hist = L->bk_hist;
     p.unit_ctr = L->meta + 32;
@@ -544,6 +535,8 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
         MOBI_CUDA(cudaLaunchKernelEx(&cfg, mobi_gemm_tc2_kernel<false>, *(&L->tmap_x2[0]), *(&L->tmap_x2[1]), p));
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
+    L->plan[1] = MOBI_K_GEMM_PAIR;
+    L->plan[2] = grid;
     return MOBI_OK;
 }
 

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -75,6 +76,7 @@ struct MaskTable {
 
 struct mobi_layer {
     int device = 0;
+    int n_sm = 148;                          // SMs of `device` (grid sizing)
     int64_t out = 0, in = 0, gs = 0, G = 0;  // G = groups per row
     int32_t E = 0, b = 0;                    // slices, bits per slice
     int32_t nr = 0;                          // routed slices = E-1
@@ -135,6 +137,23 @@ struct mobi_layer {
     size_t ev_next = 0;
     double prof_ms[4] = {0, 0, 0, 0};
     int64_t prof_n[4] = {0, 0, 0, 0};
+
+    // Per-call state.  The handle's own workspace serves the first stream it is called on; every
+    // other stream gets a context -- a mobi_layer that shares the handle's weights and owns its own
+    // workspace -- so concurrent forwards on distinct streams never share scratch memory.  A
+    // context's call_mu keeps one forward's launch sequence contiguous on its stream when several
+    // host threads use the same stream.
+    mobi_layer* owner = nullptr;         // set on per-stream contexts
+    void* ctx_stream = nullptr;          // the stream this workspace serves
+    bool ctx_bound = false;
+    std::vector<mobi_layer*> ctxs;       // handle: contexts of the other streams
+    std::mutex* ctx_mu = nullptr;        // handle: guards ctxs
+    std::mutex* call_mu = nullptr;       // every context
+    int64_t reserved_T = 0;              // handle: mobi_layer_reserve (applied to new contexts)
+    int64_t plan_T = 0;                  // > T: choose kernels as for a batch of plan_T tokens (chunked calls)
+    int32_t impl = 0;                    // development hook (mobi_layer_debug_impl): kernel override
+    int32_t plan[8] = {};                // the last call's kernels (mobi_layer_last_plan)
+    mobi_layer* plan_ctx = nullptr;      // handle: the context that ran the last call
 };
 
 namespace mobi {
@@ -148,6 +167,18 @@ int set_error(int code, const std::string& msg);
             return ::mobi::set_error(MOBI_ERUNTIME, std::string(#call) + ": " +              \
                                                          cudaGetErrorString(e_));              \
     } while (0)
+#define MOBI_TRY(call)              \
+    do {                            \
+        const int rc_ = (call);     \
+        if (rc_) return rc_;        \
+    } while (0)
+// cudaFuncSetAttribute once per (current device, kernel, attribute): function attributes are
+// per-device state, so a process driving several GPUs sets them on each (abi.cu)
+int func_attr_once_impl(const void* fn, cudaFuncAttribute attr, int value);
+template <class F>
+inline int func_attr_once(F* fn, cudaFuncAttribute attr, int value) {
+    return func_attr_once_impl(reinterpret_cast<const void*>(fn), attr, value);
+}
 #define MOBI_LAUNCH_CHECK()                                                                   \
     do {                                                                                      \
         cudaError_t e_ = cudaGetLastError();                                                  \

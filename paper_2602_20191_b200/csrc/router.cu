@@ -76,6 +76,7 @@ int launch_router(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t
                                              L->nr, L->s_part);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
+    L->plan[0] = MOBI_K_ROUTER_SIMT;
     return MOBI_OK;
 }
 

@@ -147,40 +147,34 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             }
         }
     } else if (warp == kRWarpMma) {
-        uint32_t it = 0, tc = 0;
-        for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
-            int mt, nt, ks, kb0, kb1;
-            tile_of(tile, mt, nt, ks, kb0, kb1);
-            const uint32_t n_mma = (uint32_t)std::min<int64_t>(RN, round_up(p.h - (int64_t)nt * RN, 16));
-            const int buf = tc & 1;
-            mbar_wait(&acc_empty[buf], ((tc >> 1) & 1) ^ 1);
-            tc_fence_after();
-            for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                const int s = it % RS;
-                mbar_wait(&full[s], (it / RS) & 1);
-                if (kb < 64) TR(kb);
+        if (elect_one_sync()) {  // one thread, operands in uniform registers (see router_tc2_kernel)
+            uint32_t it = 0, tc = 0;
+            const uint64_t desc0 = sdesc_sw128(smem_u32(smem));
+            for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++tc) {
+                int mt, nt, ks, kb0, kb1;
+                tile_of(tile, mt, nt, ks, kb0, kb1);
+                const uint32_t n_mma = (uint32_t)std::min<int64_t>(RN, round_up(p.h - (int64_t)nt * RN, 16));
+                const uint32_t idesc = idesc_f16(RM, n_mma, 1);
+                const int buf = tc & 1;
+                mbar_wait(&acc_empty[buf], ((tc >> 1) & 1) ^ 1);
                 tc_fence_after();
-                if (elect_one_sync()) {
-                    const uint32_t a = smem_u32(smem + s * 2 * kAB);
-                    const uint64_t adesc = sdesc_sw128(a), bdesc = sdesc_sw128(a + kAB);
-                    const uint32_t d = tmem + buf * RN;
-                    if (n_mma == RN) {
-                        constexpr uint32_t idesc = idesc_f16(RM, RN, 1);
+                const uint32_t d = tmem + buf * RN;
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const uint32_t s = it % RS;
+                    mbar_wait(&full[s], (it / RS) & 1);
+                    if (kb < 64) TR(kb);
+                    tc_fence_after();
+                    const uint64_t adesc = desc0 + (uint64_t)((s * 2 * kAB) >> 4), bdesc = adesc + (uint64_t)(kAB >> 4);
 #pragma unroll
-                        for (int j = 0; j < kKBlock / 16; ++j)
-                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb != kb0) || (j != 0));
-                    } else {  // partial hidden tile (h % 128 != 0): runtime descriptor
-                        const uint32_t idesc = idesc_f16(RM, n_mma, 1);
-#pragma unroll
-                        for (int j = 0; j < kKBlock / 16; ++j)
-                            mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc, (kb != kb0) || (j != 0));
-                    }
+                    for (int j = 0; j < kKBlock / 16; ++j)
+                        mma_ss_f16(d, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc,
+                                   (kb != kb0 || j != 0) ? 1u : 0u);
                     mma_commit(&empty[s]);
-                    if (kb == kb1 - 1) mma_commit(&acc_full[buf]);
                 }
-                __syncwarp();
+                mma_commit(&acc_full[buf]);
             }
         }
+        __syncwarp();
     } else {
         const int q = warp % 4;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
@@ -433,31 +427,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
             }
         }
     } else if (warp == k2WarpMma) {
-        if (rank == 0) {
+        // one thread, CTA-scope stage waits, operands in uniform registers (a whole-warp loop with a
+        // cluster-scope acquire per k-block cost ~700 cycles per k-block, 2.7x the N = 128 MMAs)
+        if (rank == 0 && elect_one_sync()) {
             uint32_t it = 0, tc = 0;
             constexpr uint32_t idesc = idesc_f16(2 * RM, PN, 1);
+            const uint64_t desc0 = sdesc_sw128(smem_u32(smem));
             for (int pair = cid; pair < total; pair += ncl, ++tc) {
                 const int buf = tc & 1;
                 mbar_wait_cluster(&acc_empty[buf], ((tc >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
-                    const int s = it % NS;
-                    mbar_wait_cluster(&full[s], (it / NS) & 1);
+                    const uint32_t s = it % NS;
+                    mbar_wait(&full[s], (it / NS) & 1);
+                    if (p.trace && blockIdx.x == 0 && tc == 0 && kb < 64)
+                        p.trace[8192 + kb] = (unsigned long long)(clock64() - c_start);
                     tc_fence_after();
-                    if (elect_one_sync()) {
-                        const uint32_t a = smem_u32(smem + s * kStg);
-                        const uint64_t adesc = sdesc_sw128(a), bdesc = sdesc_sw128(a + kAB);
+                    const uint64_t adesc = desc0 + (uint64_t)((s * kStg) >> 4), bdesc = adesc + (uint64_t)(kAB >> 4);
 #pragma unroll
-                        for (int j = 0; j < kKBlock / 16; ++j)
-                            mma_ss_f16_2sm(tmem + buf * PN, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc,
-                                           (kb != 0) || (j != 0));
-                        mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
-                        if (kb == p.kblocks - 1) mma_commit_2sm_mc(&acc_full[buf], (uint16_t)0x3);
-                    }
-                    __syncwarp();
+                    for (int j = 0; j < kKBlock / 16; ++j)
+                        mma_ss_f16_2sm(tmem + buf * PN, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), idesc,
+                                       (kb | j) != 0 ? 1u : 0u);
+                    mma_commit_2sm_mc(&empty[s], (uint16_t)0x3);
                 }
+                mma_commit_2sm_mc(&acc_full[buf], (uint16_t)0x3);
             }
         }
+        __syncwarp();
     } else {
         const int q = warp % 4, half = warp / 4;
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
@@ -591,15 +587,6 @@ __global__ void __launch_bounds__(RN) router_reduce_kernel(const float* __restri
         for (int k = 0; k < nr; ++k) s_part[((int64_t)nt * T + t) * nr + k] = red[k][0];
 }
 
-int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return n;
-}
 
 }  // namespace
 
@@ -647,10 +634,8 @@ int g_router_csplit = [] {
 int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, float* scores_out,
                      uint8_t* masks_out, bool* masks_ready, cudaStream_t st, unsigned long long* trace,
                      bool fuse_bucket) {
-    static bool attr = false;
-    if (!attr) {
-        MOBI_CUDA(cudaFuncSetAttribute(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem));
-        attr = true;
+    {
+        MOBI_TRY(func_attr_once(router_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRSmem));
     }
     if (!L->tmap_w1) {
         L->tmap_w1 = new CUtensorMap;
@@ -688,12 +673,17 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
     // split K when the tile grid cannot fill the SMs (decode-size T)
     p.nsplit = 1;
     p.csplit = 1;
-    // CTA-pair tiles when they alone fill the SMs (fewer w1 bytes per SM per flop, see the kernel)
+    // CTA-pair tiles when they alone fill the SMs (fewer w1 bytes per SM per flop, see the kernel).
+    // The variant (and the cluster K-split below) is chosen from the plan size Tp -- the whole batch
+    // when mobi_forward_host runs it in chunks -- so every chunk sums each token's score in the same
+    // order as the whole-batch call.
+    const int64_t Tp = std::max(T, L->plan_T);
     const int n_mp = (int)cdiv(T, 2 * RM);
+    const int n_mp_plan = (int)cdiv(Tp, 2 * RM);
     int pn = 0;
-    if (g_router_pair && T > 64 && L->h % 256 == 0 && n_mp * (int)(L->h / 256) * 2 >= sm_count())
+    if (g_router_pair && Tp > 64 && L->h % 256 == 0 && n_mp_plan * (int)(L->h / 256) * 2 >= L->n_sm)
         pn = 256;
-    else if (g_router_pair && T > 64 && L->h % 128 == 0 && n_mp * (int)(L->h / 128) * 2 >= sm_count() * 3 / 4)
+    else if (g_router_pair && Tp > 64 && L->h % 128 == 0 && n_mp_plan * (int)(L->h / 128) * 2 >= L->n_sm * 3 / 4)
         pn = 128;
     if (pn == 128 && !L->tmap_w1_64) {
         L->tmap_w1_64 = new CUtensorMap;
@@ -705,25 +695,22 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
         }
     }
     if (pn) {
+        L->plan[0] = pn == 256 ? MOBI_K_ROUTER_PAIR256 : MOBI_K_ROUTER_PAIR128;
         p.n_nt = (int)(L->h / pn);
         L->htiles = p.n_nt;
         if (masks_ready) *masks_ready = true;
-        const int grid = 2 * std::min(n_mp * p.n_nt, sm_count() / 2);
+        const int grid = 2 * std::min(n_mp * p.n_nt, L->n_sm / 2);
         if (pn == 256) {
-            static bool a256 = false;
-            if (!a256) {
-                MOBI_CUDA(cudaFuncSetAttribute(router_tc2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            {
+                MOBI_TRY(func_attr_once(router_tc2_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                r2_smem(256)));
-                a256 = true;
             }
             MOBI_CUDA(launch_pdl(router_tc2_kernel<256>, dim3(grid), dim3(k2Threads), r2_smem(256), st, 0, tmap_x,
                                  *L->tmap_w1, p));
         } else {
-            static bool a128 = false;
-            if (!a128) {
-                MOBI_CUDA(cudaFuncSetAttribute(router_tc2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            {
+                MOBI_TRY(func_attr_once(router_tc2_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                r2_smem(128)));
-                a128 = true;
             }
             MOBI_CUDA(launch_pdl(router_tc2_kernel<128>, dim3(grid), dim3(k2Threads), r2_smem(128), st, 0, tmap_x,
                                  *L->tmap_w1_64, p));
@@ -733,17 +720,18 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
         return MOBI_OK;
     }
     const int tiles = p.n_mt * p.n_nt;
+    const int tiles_plan = (int)cdiv(Tp, RM) * p.n_nt;
     if (g_router_csplit == 2 && p.kblocks >= 8) {  // experiment: fixed 2-way split at every T
         p.csplit = 2;
         p.nsplit = 2;
-    } else if (g_router_csplit == 1 && 2 * tiles <= sm_count() && p.kblocks >= 8) {
+    } else if (g_router_csplit == 1 && 2 * tiles_plan <= L->n_sm && p.kblocks >= 8) {
         // too few tiles to fill the SMs: split K over a cluster of 2-3 CTAs per tile (DSMEM reduction
         // into rank 0, which keeps the fused gate/histogram epilogue).  The split depends on the tile
         // count only, so outputs are identical for every T of the same regime.
-        p.csplit = std::min(kMaxCsplit, std::min(3, sm_count() / tiles));
+        p.csplit = std::min(kMaxCsplit, std::min(3, L->n_sm / tiles_plan));
         p.nsplit = p.csplit;
-    } else if (T <= 64 && L->hpart) {  // small K: global split-K partials + a reduce kernel
-        p.nsplit = std::max(1, std::min(16, sm_count() / tiles));
+    } else if (Tp <= 64 && L->hpart) {  // small K: global split-K partials + a reduce kernel
+        p.nsplit = std::max(1, std::min(16, L->n_sm / tiles));
     }
     p.kb_per = (p.kblocks + p.nsplit - 1) / p.nsplit;
     p.nsplit = (p.kblocks + p.kb_per - 1) / p.kb_per;  // no empty splits
@@ -752,13 +740,14 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
     const bool clus = p.csplit > 1;
     if (masks_ready) *masks_ready = p.nsplit == 1 || clus;
     if (p.nsplit != 1 && !clus) p.hist = nullptr;
+    L->plan[0] = clus ? MOBI_K_ROUTER_TC_CLUSTER : (p.nsplit > 1 ? MOBI_K_ROUTER_TC_SPLITK : MOBI_K_ROUTER_TC);
     if (clus) {
         MOBI_CUDA(launch_pdl(router_tc_kernel, dim3((unsigned)total), dim3(kRThreads), (size_t)kRSmem, st, p.csplit,
                              tmap_x, *L->tmap_w1, p));
         ++L->last_launches;
         return MOBI_OK;
     }
-    const int grid = std::min(total, sm_count());
+    const int grid = std::min(total, L->n_sm);
     MOBI_CUDA(launch_pdl(router_tc_kernel, dim3(grid), dim3(kRThreads), (size_t)kRSmem, st, 0, tmap_x, *L->tmap_w1, p));
     ++L->last_launches;
     if (p.nsplit > 1) {

@@ -149,6 +149,23 @@ class MobiLayer:
         check(lib().mobi_layer_last_launches(self._h, C.byref(n)))
         return n.value
 
+    KERNEL_IDS = {0: None, 1: "router_dec", 2: "router_tc", 3: "router_tc_cluster", 4: "router_tc_splitk",
+                  5: "router_pair128", 6: "router_pair256", 7: "router_simt", 11: "decode_planes",
+                  12: "decode_merged", 13: "gemm_splitk", 14: "gemm_pair", 15: "gemm_simt"}
+
+    def last_plan(self) -> dict:
+        """Kernels the last call on this layer ran (mobi_layer_last_plan): router / GEMM kernel names,
+        GEMM grid, launches, token tiles, 256-row weight-tile pairs and GEMM units (tiles x pairs)."""
+        a = (_i32 * 8)()
+        check(lib().mobi_layer_last_plan(self._h, a))
+        return {"router": self.KERNEL_IDS.get(a[0], a[0]), "gemm": self.KERNEL_IDS.get(a[1], a[1]),
+                "gemm_ctas": a[2], "launches": a[3], "token_tiles": a[4], "row_pairs": a[5], "units": a[6],
+                "tokens": a[7]}
+
+    def set_debug_impl(self, impl: int) -> None:
+        """Test hook (per layer): 1 = CUDA-core reference GEMM/router, 0 = production kernels."""
+        check(lib().mobi_layer_debug_impl(self._h, impl))
+
     KERNELS = ("router", "bucket", "gather", "gemm")
 
     def profile(self, enable: bool = True):
@@ -299,7 +316,3 @@ def decompose(w: torch.Tensor, group_size: int, slice_bits: Sequence[int], gamma
                                _stream_ptr(stream)))
     return codes, scale, zero, cc
 
-
-def set_debug_impl(impl: int) -> None:
-    """Test hook: 1 = CUDA-core reference GEMM, 0 = tcgen05 (default)."""
-    check(lib().mobi_debug_set_impl(impl))

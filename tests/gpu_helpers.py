@@ -20,8 +20,8 @@ from oracle import oracle as O
 SCORE_ATOL = 2e-3
 SCORE_RTOL = 1e-4
 MASK_MARGIN = 1e-2
-Y_REL_L2 = 1e-2
-Y_MAX_ABS = 3e-2
+Y_REL_L2 = 4e-3   # ~2.5x the measured noise (1.6-1.8e-3); a 5% error in slice 3's scale gives 7e-3
+Y_MAX_ABS = 3e-2    # outlier guard; bf16 rounding of the largest |y| alone reaches ~1e-2, measured <= 2.4e-2 (toy)
 
 
 def bf16_round(a: np.ndarray) -> np.ndarray:

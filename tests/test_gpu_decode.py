@@ -24,9 +24,8 @@ def _cuda():
     _lib.lib()
 
 
-def _impl(n):
-    from paper_2602_20191_b200 import set_debug_impl
-    set_debug_impl(n)
+def _impl(layer, n):
+    layer.set_debug_impl(n)
 
 
 def _masks(T, seed):
@@ -63,11 +62,11 @@ def test_decode_masked_matches_oracle_and_bucketed(orc, out, inn, gs, h, T):
     y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], gs,
                                 gates_from_masks(masks, 3))
     assert_y_close(y, y_ref, f"decode {out}x{inn} T={T}")
-    _impl(5)
+    _impl(layer, 5)
     try:
         y_b = layer.forward_masked(xb, md)
     finally:
-        _impl(0)
+        _impl(layer, 0)
     assert_y_close(y_b, y_ref, f"bucketed {out}x{inn} T={T}")
 
 
@@ -101,11 +100,11 @@ def test_decode_deterministic_repeat_pdl_and_graph():
         y0 = layer.forward(xb, delta).clone()
         for _ in range(4):  # arrival counters must be reset by every launch
             assert torch.equal(layer.forward(xb, delta), y0)
-        _impl(6)  # same kernels without the programmatic (PDL) edge
+        _impl(layer, 6)  # same kernels without the programmatic (PDL) edge
         try:
             assert torch.equal(layer.forward(xb, delta), y0)
         finally:
-            _impl(0)
+            _impl(layer, 0)
         # CUDA-graph capture of the whole forward (router + decode GEMM), replayed on new inputs
         xg = xb.clone()
         yg = torch.empty_like(y0)

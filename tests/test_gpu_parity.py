@@ -98,16 +98,15 @@ def test_forward_full_matches_oracle(orc, out, inn, gs, h, T):
 
 
 def test_tcgen05_matches_cuda_core_reference_kernel():
-    from paper_2602_20191_b200 import set_debug_impl
     L, layer = make_layer(384, 512, gs=128, hidden=64, seed=9)
     xb, _ = make_x(700, 512, seed=2)
     masks = torch.from_numpy((np.arange(700) % 8 * 2 + 1).astype(np.uint8)).cuda()
     y_tc = layer.forward_masked(xb, masks)
-    set_debug_impl(1)
+    layer.set_debug_impl(1)
     try:
         y_ref = layer.forward_masked(xb, masks)
     finally:
-        set_debug_impl(0)
+        layer.set_debug_impl(0)
     d = (y_tc.float() - y_ref.float()).abs().max().item()
     assert d <= 2e-2 * y_ref.float().pow(2).mean().sqrt().item()
 
@@ -219,15 +218,14 @@ def test_llama_shapes(orc, out, inn, T):
 
 @pytest.mark.parametrize("inn,h,T", [(512, 128, 300), (4096, 1024, 130), (96, 16, 1)])
 def test_router_tcgen05_matches_cuda_core_router(orc, inn, h, T):
-    from paper_2602_20191_b200 import set_debug_impl
     L, layer = make_layer(64, inn, gs=32 if inn < 128 else 128, hidden=h, seed=inn)
     xb, x64 = make_x(T, inn, seed=T)
     s_tc = layer.score(xb).cpu().numpy()
-    set_debug_impl(1)
+    layer.set_debug_impl(1)
     try:
         s_cc = layer.score(xb).cpu().numpy()
     finally:
-        set_debug_impl(0)
+        layer.set_debug_impl(0)
     s_ref = oracle_scores(orc, layer, x64)
     for s in (s_tc, s_cc):
         assert np.all(np.abs(s - s_ref) <= SCORE_ATOL + SCORE_RTOL * np.abs(s_ref))

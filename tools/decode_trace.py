@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
-from paper_2602_20191_b200 import _lib, calibrate_threshold, set_debug_impl  # noqa: E402
+from paper_2602_20191_b200 import _lib, calibrate_threshold  # noqa: E402
 
 
 def main():
@@ -19,7 +19,7 @@ def main():
     delta = calibrate_threshold(layer.score(x), (args.target_bits - 2) / 6)
     for _ in range(5):
         layer.forward(x, delta)
-    set_debug_impl(9)
+    layer.set_debug_impl(9)
     # replay from a CUDA graph, as bench.py does at decode sizes: the PDL edge only overlaps the two
     # kernels when the dependent launch is already queued on the device
     y = torch.empty((x.shape[0], layer.out), dtype=torch.bfloat16, device=dev)
@@ -34,7 +34,7 @@ def main():
     torch.cuda.synchronize()
     g.replay()
     torch.cuda.synchronize()
-    set_debug_impl(0)
+    layer.set_debug_impl(0)
     full = np.zeros(32 * 1024, np.uint64)
     lib = _lib.lib()
     lib.mobi_debug_read_trace.argtypes = [C.c_void_p, C.c_int]

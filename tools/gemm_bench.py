@@ -24,11 +24,9 @@ def run(layer, x, masks, reps=20):
 def main():
     args = bench.parse()
     import os
-    from paper_2602_20191_b200 import set_debug_impl
-    set_debug_impl(int(os.environ.get("MOBI_IMPL", "0")))
     dev = torch.device("cuda", 0)
     layer, _ = bench.make_layer(args, dev, 1)
-    import os
+    layer.set_debug_impl(int(os.environ.get("MOBI_IMPL", "0")))
     quick = os.environ.get('GB_QUICK')
     for T in ((2048, 8192) if quick else (256, 2048, 8192)):
         args.tokens = T

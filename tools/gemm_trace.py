@@ -9,7 +9,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
-from paper_2602_20191_b200 import _lib, calibrate_threshold, set_debug_impl  # noqa: E402
+from paper_2602_20191_b200 import _lib, calibrate_threshold  # noqa: E402
 
 
 def main():
@@ -24,10 +24,10 @@ def main():
         layer.forward(x, delta)
     import os
     impl = int(os.environ.get("MOBI_TRACE_IMPL", "2"))
-    set_debug_impl(impl)
+    layer.set_debug_impl(impl)
     layer.forward(x, delta)
     torch.cuda.synchronize()
-    set_debug_impl(0)
+    layer.set_debug_impl(0)
     n = torch.cuda.get_device_properties(0).multi_processor_count
     full = np.zeros(32 * 1024, np.uint64)
     buf = full[: 16 * 1024].reshape(1024, 16)[:n]

@@ -4,7 +4,7 @@ from pathlib import Path
 import numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import bench
-from paper_2602_20191_b200 import _lib, set_debug_impl
+from paper_2602_20191_b200 import _lib
 args = bench.parse()
 dev = torch.device("cuda", 0)
 layer, _ = bench.make_layer(args, dev, 1)
@@ -16,10 +16,10 @@ e0.record()
 for _ in range(20): layer.score(x)
 e1.record(); torch.cuda.synchronize()
 print("score() avg us", e0.elapsed_time(e1) / 20 * 1e3)
-set_debug_impl(7)
+layer.set_debug_impl(7)
 layer.score(x)
 torch.cuda.synchronize()
-set_debug_impl(0)
+layer.set_debug_impl(0)
 full = np.zeros(32 * 1024, np.uint64)
 lib = _lib.lib(); lib.mobi_debug_read_trace.argtypes = [C.c_void_p, C.c_int]
 _lib.check(lib.mobi_debug_read_trace(full.ctypes.data, 1))
@@ -29,3 +29,6 @@ g0 = t[:, 4].min()
 print("CTAs", len(t), "start spread us", (t[:, 4].max() - g0) / 1e3, "end min/med/max us", (t[:, 5].min() - g0) / 1e3, np.median(t[:, 5] - g0) / 1e3, (t[:, 5].max() - g0) / 1e3)
 print("cycles: prologue med", np.median(t[:, 1]), "acc_full med", np.median(t[:, 2]), "epi done med", np.median(t[:, 3]), "total med/max", np.median(t[:, 6]), t[:, 6].max())
 print("clock GHz", np.median(t[:, 6] / (t[:, 5] - t[:, 4])))
+kbt = full.astype(np.int64)[8192:8192 + 64]
+print("CTA0 tile0 per-k-block full-ok cycles:", kbt[:24].tolist())
+print("cadence (median diff)", np.median(np.diff(kbt[kbt > 0])))
