@@ -911,19 +911,13 @@ int mobi_permute_by_slice(const uint8_t* masks, int64_t T, int32_t* perm, int32_
 int mobi_calibrate_threshold(const float* scores, int64_t n, double rho, double* delta, void* stream) {
     CHECK_ARG(n > 0, "calibrate_threshold: empty score sample");
     CHECK_ARG(rho >= 0.0 && rho <= 1.0, "calibrate_threshold: rho " << rho << " outside [0,1]");
-    CHECK_ARG(delta, "calibrate_threshold: null output");
-    std::vector<float> h((size_t)n);
-    MOBI_CUDA(cudaMemcpyAsync(h.data(), scores, n * 4, cudaMemcpyDeviceToHost, S(stream)));
-    MOBI_CUDA(cudaStreamSynchronize(S(stream)));
-    std::vector<double> s(h.begin(), h.end());
-    // router.hpp:167-174: sort descending, delta = s[floor(rho*N + 1e-9)] (min-1 past the end)
+    CHECK_ARG(delta && scores, "calibrate_threshold: null argument");
+    // router.hpp:167-174: sort descending, delta = s[floor(rho*N + 1e-9)], or min - 1 past the end;
+    // the rank is selected on the device (radix select, select.cu), bit-identical to sorting
     const int64_t k = (int64_t)std::floor(rho * (double)n + 1e-9);
-    if (k >= n) {
-        *delta = *std::min_element(s.begin(), s.end()) - 1.0;
-    } else {
-        std::nth_element(s.begin(), s.begin() + k, s.end(), std::greater<double>());
-        *delta = s[(size_t)k];
-    }
+    float v = 0.f;
+    MOBI_TRY(launch_select_desc(scores, n, std::min(k, n - 1), &v, S(stream)));
+    *delta = k >= n ? (double)v - 1.0 : (double)v;
     return MOBI_OK;
 }
 

@@ -226,6 +226,8 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
 int launch_decode_gemm(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
                        uint8_t* masks_out, float* scores_out, __nv_bfloat16* y, bool pdl, cudaStream_t st,
                        unsigned long long* trace = nullptr);
+// select.cu: the score of descending rank k (exact fp32) -> host (synchronous on `st`)
+int launch_select_desc(const float* scores, int64_t n, int64_t k, float* out_host, cudaStream_t st);
 // decompose.cu
 int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,
                      int32_t E, double gamma, uint8_t* codes, double* scale, double* zero,

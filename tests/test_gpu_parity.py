@@ -194,11 +194,18 @@ def test_permute_by_slice_generic_keys(orc):
 
 
 def test_calibrate_threshold_matches_reference_on_device_scores(orc):
+    """router.hpp:167-174 on the device (radix select, select.cu): bit-identical to the oracle's sort,
+    on 1.5e6 pooled scores (the toy calibration pool is 49152), with ties and negative zeros."""
     from paper_2602_20191_b200 import calibrate_threshold
-    s = torch.randn(4096 * 3, device="cuda")
-    s64 = s.double().cpu().numpy()
-    for rho in (0.0, 0.1, 1 / 6, 1 / 3, 0.9, 1.0):
-        assert calibrate_threshold(s, rho) == orc.calibrate_threshold(s64, rho)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    pools = [torch.randn(4096 * 3, device="cuda", generator=g),
+             14.0 * torch.randn(500_000 * 3, device="cuda", generator=g),
+             torch.round(torch.randn(300_000, device="cuda", generator=g) * 4) / 4,  # heavy ties
+             torch.tensor([0.0, -0.0, 1.0, -1.0, 0.0, 2.5, -0.0], device="cuda")]
+    for s in pools:
+        s64 = s.double().cpu().numpy()
+        for rho in (0.0, 1e-6, 0.1, 1 / 6, 1 / 3, 0.5, 0.9, 1.0 - 1e-7, 1.0):
+            assert calibrate_threshold(s, rho) == orc.calibrate_threshold(s64, rho), (s.numel(), rho)
 
 
 @pytest.mark.parametrize("out,inn,T", [(4096, 4096, 16), (1024, 4096, 4)])
