@@ -57,6 +57,7 @@ extern "C" {
 #define MOBI_ERUNTIME 2
 
 #define MOBI_MAX_SLICES 4 /* slice 1 + up to 3 routed residual slices -> 8 buckets */
+#define MOBI_MAX_DST 8    /* destinations of one output descriptor (ranks of a column-parallel layer) */
 
 typedef struct mobi_layer* mobi_layer_t;
 
@@ -133,6 +134,42 @@ MOBI_API int mobi_forward(mobi_layer_t layer, const void* x_bf16, int64_t T, flo
 MOBI_API int mobi_forward_masked(mobi_layer_t layer, const void* x_bf16, int64_t T, const uint8_t* masks,
                         void* y_bf16, void* stream);
 
+/* Output placement: Y row t of this layer is written at dst[k] + t*ldy + col0 (bf16 elements) for
+ * every k < n_dst.  Column-parallel shards use it to write their columns straight into the full
+ * [T, out] buffers of every rank (dst = local + peer-mapped buffers, see mobi_ipc_open): the
+ * all-gather happens in the GEMM epilogue, tile by tile.  After the call, order the peers' reads
+ * behind a collective on the same stream (stores to peers are fenced system-wide by the kernel). */
+typedef struct {
+    int32_t n_dst;              /* 1..MOBI_MAX_DST */
+    void* dst[MOBI_MAX_DST];    /* device pointers (local or peer-mapped) */
+    int64_t ldy;                /* row stride of every destination, elements (>= col0 + out) */
+    int64_t col0;               /* column of this layer's first output */
+} mobi_out_desc;
+MOBI_API int mobi_forward_out(mobi_layer_t layer, const void* x_bf16, int64_t T, float delta,
+                              const mobi_out_desc* out, uint8_t* masks, void* stream);
+
+/* Multi-GPU entry, one process per GPU, `nccl_comm` an ncclComm_t over nranks ranks
+ * (NULL allowed when nranks == 1):
+ *   MOBI_SHARD_COLUMN: rank p owns weight rows [p*per, (p+1)*per) (per = ceil(out/P) rounded up to
+ *     128) and the full router; mobi_forward_sharded takes the full X [T, in] on every rank and
+ *     returns the full Y [T, out] on every rank (the epilogue writes this rank's block into a
+ *     rank-major buffer, one in-place ncclAllGather, one interleave pass).  Bit-identical to the
+ *     unsharded layer.
+ *   MOBI_SHARD_TOKEN: replicated weights; each rank passes its own tokens, no collective. */
+#define MOBI_SHARD_COLUMN 1
+#define MOBI_SHARD_TOKEN 2
+MOBI_API int mobi_layer_create_sharded(const mobi_layer_desc* desc, void* nccl_comm, int rank, int nranks,
+                                       int mode, int device, mobi_layer_t* out);
+MOBI_API int mobi_forward_sharded(mobi_layer_t layer, const void* x_bf16, int64_t T, float delta, void* y_bf16,
+                                  uint8_t* masks, void* stream);
+
+/* CUDA IPC plumbing for peer destinations (one process per GPU): export the allocation holding
+ * dev_ptr as a 64-byte handle (+ dev_ptr's offset in it), open a peer's handle on `device` (peer
+ * access enabled lazily; the peer's pointer is *dev_ptr + offset), close the mapping. */
+MOBI_API int mobi_ipc_export(void* dev_ptr, void* handle64, int64_t* offset);
+MOBI_API int mobi_ipc_open(const void* handle64, int device, void** dev_ptr);
+MOBI_API int mobi_ipc_close(void* dev_ptr);
+
 /* mobi_forward from HOST buffers: x_host bf16 [T][in] -> y_host bf16 [T][out] (+ masks_host,
  * nullable); copies go through the layer's pinned staging buffers on `stream`; synchronous. */
 MOBI_API int mobi_forward_host(mobi_layer_t layer, const void* x_host, int64_t T, float delta,
@@ -147,6 +184,11 @@ MOBI_API int mobi_permute_by_slice(const uint8_t* masks, int64_t T, int32_t* per
  * or min-1 if that index is >= n.  Synchronous; result to host. */
 MOBI_API int mobi_calibrate_threshold(const float* scores, int64_t n, double rho, double* delta,
                              void* stream);
+
+/* router::avg_bits (router.hpp:135-150) from device masks [T] (bit e-1 <-> slice e): mean over tokens
+ * of the active slices' widths (exact integer sum on the device, one division).  Synchronous. */
+MOBI_API int mobi_avg_bits(const uint8_t* masks, int64_t T, const int32_t* slice_bits, int32_t n_slices,
+                           double* avg, void* stream);
 
 /* slicer::decompose on the GPU, with base params from params_from_clip(identity clip gamma):
  * w (device fp64 [out][in]) -> codes (device uint8 [E][out][in]), scale/zero (device fp64

@@ -11,12 +11,18 @@
 //   router::forward_elastic(x, st, G, kHard)    ->    layer.forward_elastic(x, G)
 //   score -> calibrate_threshold -> gate_hard -> forward_elastic (pipeline.hpp:146-183)
 //                                               ->    layer.forward(x, delta, &gates)
+//   router::calibrate_threshold(scores, rho)    ->    mobi_b200::calibrate_threshold(scores, rho)
+//   router::avg_bits(gates, slice_bits)         ->    mobi_b200::avg_bits(gates, slice_bits)
+//   bitplane::permute_by_slice(tokens, masks)   ->    mobi_b200::permute_by_slice(tokens, masks)
+//   (multi-GPU)                    ->    mobi_b200::ShardedLayer(stack, rs, comm, rank, P, mode)
 #pragma once
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -193,6 +199,160 @@ private:
     int64_t out_ = 0, in_ = 0, nr_ = 0;
     std::vector<int32_t> bits_;
     std::vector<uint8_t> codes_;
+    friend class ShardedLayer;
+};
+
+namespace detail {
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    explicit DevBuf(size_t n_) : n(n_) {
+        if (cudaMalloc(&p, (n ? n : 1) * sizeof(T)) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+    }
+    explicit DevBuf(const std::vector<T>& h) : DevBuf(h.size()) {
+        if (n && cudaMemcpy(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+            throw std::runtime_error("cudaMemcpy failed");
+    }
+    ~DevBuf() { cudaFree(p); }
+    std::vector<T> download() const {
+        std::vector<T> h(n);
+        if (n && cudaMemcpy(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost) != cudaSuccess)
+            throw std::runtime_error("cudaMemcpy failed");
+        return h;
+    }
+};
+}  // namespace detail
+
+// router::calibrate_threshold (router.hpp:167-174) on the GPU (device radix select): scores are taken
+// as fp32 -- what the device router produces -- so doubles that are not float-representable go
+// through the reference's own host algorithm instead, keeping the result identical.
+inline double calibrate_threshold(const std::vector<double>& scores, double rho) {
+    if (scores.empty()) throw std::invalid_argument("calibrate_threshold: empty score sample");
+    std::vector<float> f(scores.size());
+    bool exact = true;
+    for (size_t i = 0; i < scores.size(); ++i) {
+        f[i] = static_cast<float>(scores[i]);
+        exact = exact && static_cast<double>(f[i]) == scores[i];
+    }
+    if (!exact) {
+        if (rho < 0.0 || rho > 1.0) throw std::invalid_argument("calibrate_threshold: rho outside [0,1]");
+        std::vector<double> s(scores);
+        const size_t k = static_cast<size_t>(rho * static_cast<double>(s.size()) + 1e-9);
+        if (k >= s.size()) return *std::min_element(s.begin(), s.end()) - 1.0;
+        std::nth_element(s.begin(), s.begin() + static_cast<std::ptrdiff_t>(k), s.end(), std::greater<double>());
+        return s[k];
+    }
+    detail::DevBuf<float> d(f);
+    double delta = 0.0;
+    check(mobi_calibrate_threshold(d.p, static_cast<int64_t>(f.size()), rho, &delta, nullptr));
+    return delta;
+}
+
+// router::avg_bits (router.hpp:135-150): mean over tokens of b_1 + sum_j 1(G[t,j] > 0.5) * b_{j+1}
+template <class Matrix>
+double avg_bits(const Matrix& gates, const std::vector<int>& slice_bits) {
+    if (slice_bits.size() != gates.cols() + 1)
+        throw std::invalid_argument("avg_bits: " + std::to_string(gates.cols()) + " gate columns for " +
+                                    std::to_string(slice_bits.size()) + " slices");
+    if (gates.rows() == 0) return static_cast<double>(slice_bits[0]);
+    std::vector<uint8_t> m(gates.rows(), 1);
+    for (size_t t = 0; t < gates.rows(); ++t)
+        for (size_t j = 0; j < gates.cols(); ++j)
+            if (gates(t, j) > 0.5) m[t] |= static_cast<uint8_t>(1u << (j + 1));
+    detail::DevBuf<uint8_t> dm(m);
+    std::vector<int32_t> b(slice_bits.begin(), slice_bits.end());
+    double out = 0.0;
+    check(mobi_avg_bits(dm.p, static_cast<int64_t>(m.size()), b.data(), static_cast<int32_t>(b.size()), &out, nullptr));
+    return out;
+}
+
+// bitplane::permute_by_slice (bitplane.hpp:178-201): stable sort of tokens by mask
+struct Permutation {
+    std::vector<size_t> perm, inverse;                    // perm[i] = source row, inverse[src] = i
+    std::vector<std::pair<uint8_t, size_t>> groups;      // (mask, run length), ascending mask
+};
+template <class Matrix>
+Permutation permute_by_slice(const Matrix& tokens, const std::vector<uint8_t>& masks, Matrix* permuted = nullptr) {
+    if (tokens.rows() != masks.size())
+        throw std::invalid_argument("permute_by_slice: " + std::to_string(masks.size()) + " masks for " +
+                                    std::to_string(tokens.rows()) + " tokens");
+    const int64_t T = static_cast<int64_t>(masks.size());
+    Permutation out;
+    if (T == 0) return out;
+    detail::DevBuf<uint8_t> dm(masks);
+    detail::DevBuf<int32_t> dp(masks.size()), di(masks.size());
+    std::vector<uint8_t> gm(256);
+    std::vector<int64_t> gl(256);
+    int64_t ng = 0;
+    check(mobi_permute_by_slice(dm.p, T, dp.p, di.p, gm.data(), gl.data(), &ng, nullptr));
+    const std::vector<int32_t> p = dp.download(), iv = di.download();
+    out.perm.assign(p.begin(), p.end());
+    out.inverse.assign(iv.begin(), iv.end());
+    for (int64_t g = 0; g < ng; ++g) out.groups.emplace_back(gm[g], static_cast<size_t>(gl[g]));
+    if (permuted) {
+        *permuted = Matrix(tokens.rows(), tokens.cols());
+        for (size_t i = 0; i < out.perm.size(); ++i)
+            for (size_t c = 0; c < tokens.cols(); ++c) (*permuted)(i, c) = tokens(out.perm[i], c);
+    }
+    return out;
+}
+
+// A layer partitioned over the ranks of an NCCL communicator (mobi_layer_create_sharded): COLUMN mode
+// returns the full [T, out] on every rank, TOKEN mode this rank's tokens.
+class ShardedLayer {
+public:
+    template <class SliceStack, class RouterState>
+    ShardedLayer(const SliceStack& st, const RouterState& rs, void* nccl_comm, int rank, int nranks,
+                 int mode = MOBI_SHARD_COLUMN, int device = 0)
+        : mode_(mode) {
+        mobi_layer_desc d{};
+        d.out = static_cast<int64_t>(st.rows());
+        d.in = static_cast<int64_t>(st.cols());
+        d.group_size = static_cast<int64_t>(st.base.group_size);
+        d.n_slices = static_cast<int32_t>(st.num_slices());
+        std::vector<int32_t> bits(st.slice_bits.begin(), st.slice_bits.end());
+        d.slice_bits = bits.data();
+        d.scale = st.base.scale.data();
+        d.zero = st.base.zero.data();
+        const size_t n = st.rows() * st.cols();
+        std::vector<uint8_t> codes(n * st.num_slices());
+        for (size_t e = 0; e < st.num_slices(); ++e) std::memcpy(codes.data() + e * n, st.slices[e].vec().data(), n);
+        d.codes = codes.data();
+        d.router_hidden = static_cast<int64_t>(rs.hidden_dim());
+        d.w1 = rs.w1.data();
+        d.b1 = rs.b1.data();
+        d.w2 = rs.w2.data();
+        d.b2 = rs.b2.data();
+        check(mobi_layer_create_sharded(&d, nccl_comm, rank, nranks, mode, device, &h_));
+        out_ = d.out;
+        in_ = d.in;
+    }
+    ~ShardedLayer() { mobi_layer_destroy(h_); }
+    ShardedLayer(const ShardedLayer&) = delete;
+    ShardedLayer& operator=(const ShardedLayer&) = delete;
+
+    // score -> gate_hard(delta) -> forward_elastic on this rank's rows, then the all-gather (COLUMN)
+    template <class Matrix>
+    Matrix forward(const Matrix& x, double delta) {
+        if (static_cast<int64_t>(x.cols()) != in_)
+            throw std::invalid_argument("score: token dim " + std::to_string(x.cols()) + " != router input dim " +
+                                        std::to_string(in_));
+        std::vector<uint16_t> hx(x.size());
+        for (size_t i = 0; i < x.size(); ++i) hx[i] = to_bf16(x[i]);
+        detail::DevBuf<uint16_t> dx(hx), dy(x.rows() * static_cast<size_t>(out_));
+        check(mobi_forward_sharded(h_, dx.p, static_cast<int64_t>(x.rows()), static_cast<float>(delta), dy.p, nullptr,
+                                   nullptr));
+        const std::vector<uint16_t> hy = dy.download();
+        Matrix y(x.rows(), static_cast<size_t>(out_));
+        for (size_t i = 0; i < hy.size(); ++i) y[i] = from_bf16(hy[i]);
+        return y;
+    }
+
+private:
+    mobi_layer_t h_ = nullptr;
+    int mode_ = MOBI_SHARD_COLUMN;
+    int64_t out_ = 0, in_ = 0;
 };
 
 }  // namespace mobi_b200

@@ -35,6 +35,11 @@ class LayerDesc(C.Structure):
     ]
 
 
+class OutDesc(C.Structure):
+    """mobi_out_desc: Y row t -> dst[k] + t*ldy + col0 for k < n_dst."""
+    _fields_ = [("n_dst", _i32), ("dst", _p * 8), ("ldy", _i64), ("col0", _i64)]
+
+
 _SIGS = {
     "mobi_layer_create": [C.POINTER(LayerDesc), C.c_int, C.POINTER(_p)],
     "mobi_layer_create_device": [C.POINTER(LayerDesc), C.c_int, C.POINTER(_p)],
@@ -49,8 +54,15 @@ _SIGS = {
     "mobi_forward": [_p, _p, _i64, _f32, _p, _p, _p],
     "mobi_forward_masked": [_p, _p, _i64, _p, _p, _p],
     "mobi_forward_host": [_p, _p, _i64, _f32, _p, _p, _p],
+    "mobi_forward_out": [_p, _p, _i64, _f32, C.POINTER(OutDesc), _p, _p],
+    "mobi_ipc_export": [_p, _p, C.POINTER(_i64)],
+    "mobi_ipc_open": [_p, C.c_int, C.POINTER(_p)],
+    "mobi_ipc_close": [_p],
+    "mobi_layer_create_sharded": [C.POINTER(LayerDesc), _p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(_p)],
+    "mobi_forward_sharded": [_p, _p, _i64, _f32, _p, _p, _p],
     "mobi_permute_by_slice": [_p, _i64, _p, _p, _p, _p, C.POINTER(_i64), _p],
     "mobi_calibrate_threshold": [_p, _i64, _f64, C.POINTER(_f64), _p],
+    "mobi_avg_bits": [_p, _i64, _p, _i32, C.POINTER(_f64), _p],
     "mobi_decompose": [_p, _i64, _i64, _i64, _p, _i32, _f64, _p, _p, _p, _p, _p],
     "mobi_layer_last_launches": [_p, C.POINTER(_i32)],
     "mobi_layer_debug_impl": [_p, C.c_int],

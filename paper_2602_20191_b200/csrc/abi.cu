@@ -429,8 +429,42 @@ struct ProfScope {
     }
 };
 
+int run_layer_y(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_t* given_masks, void* y,
+                uint8_t* masks_out, cudaStream_t st);
+
+// the layer forward with an output descriptor: the CTA-pair GEMM places Y itself (every destination,
+// from its epilogue); the small-T paths compute into a staging buffer and scatter it
 int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_t* given_masks, void* y,
-              uint8_t* masks_out, cudaStream_t st) {
+              uint8_t* masks_out, cudaStream_t st, const OutDesc* od = nullptr) {
+    if (!od) return run_layer_y(L, x, T, delta, given_masks, y, masks_out, st);
+    CHECK_ARG(od->n_dst >= 1 && od->n_dst <= MOBI_MAX_DST, "mobi_out_desc: n_dst " << od->n_dst << " outside [1,"
+                                                                                    << MOBI_MAX_DST << "]");
+    CHECK_ARG(od->ldy >= od->col0 + L->out && od->col0 >= 0,
+              "mobi_out_desc: columns [" << od->col0 << "," << od->col0 + L->out << ") exceed ldy " << od->ldy);
+    for (int k = 0; k < od->n_dst; ++k) CHECK_ARG(od->dst[k], "mobi_out_desc: null destination " << k);
+    const int64_t Tp = std::max(T, L->plan_T);
+    const bool pair = L->impl == 0 && !decode_supported(L, x, Tp) && Tp > 64;
+    if (pair) {
+        L->od = *od;
+        const int rc = run_layer_y(L, x, T, delta, given_masks, nullptr, masks_out, st);
+        L->od = OutDesc{};
+        return rc;
+    }
+    if (T > L->y_tmp_T) {
+        if (L->y_tmp) MOBI_CUDA(cudaFree(L->y_tmp));
+        L->y_tmp = nullptr;
+        L->y_tmp_T = 0;
+        MOBI_CUDA(cudaMalloc(&L->y_tmp, (size_t)(T * L->out * 2)));
+        L->y_tmp_T = T;
+    }
+    int rc = run_layer_y(L, x, T, delta, given_masks, L->y_tmp, masks_out, st);
+    if (!rc) rc = launch_scatter_out(L->y_tmp, T, L->out, *od, st);
+    if (!rc) ++L->last_launches;
+    return rc;
+}
+
+int run_layer_y(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_t* given_masks, void* y,
+                uint8_t* masks_out, cudaStream_t st) {
     CHECK_ARG(T >= 0, "forward_elastic: negative token count " << T);
     L->last_launches = 0;
     for (int i = 0; i < 8; ++i) L->plan[i] = 0;
@@ -609,6 +643,7 @@ int mobi_layer_create_device(const mobi_layer_desc* desc, int device, mobi_layer
 
 static void destroy_context(mobi_layer* c) {  // workspace + lazily built host objects; weights are the handle's
     free_ws(c);
+    if (c->y_tmp) cudaFree(c->y_tmp);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
     for (auto& e : c->ev_pipe)
@@ -635,6 +670,8 @@ int mobi_layer_destroy(mobi_layer_t L) {
     cudaDeviceSynchronize();
     for (mobi_layer* c : L->ctxs) destroy_context(c);
     L->ctxs.clear();
+    if (L->y_tmp) cudaFree(L->y_tmp);
+    if (L->gather_buf) cudaFree(L->gather_buf);
     delete L->ctx_mu;
     delete L->call_mu;
     free_ws(L);
@@ -775,6 +812,36 @@ int mobi_forward_masked(mobi_layer_t H, const void* x, int64_t T, const uint8_t*
     return rc;
 }
 
+}  // extern "C"
+namespace mobi {
+int run_layer_entry(mobi_layer* H, const void* x, int64_t T, float delta, void* y, uint8_t* masks, cudaStream_t st,
+                    const OutDesc* od) {
+    CallScope cs(H, st);
+    if (cs.rc) return cs.rc;
+    const int rc = run_layer(cs.C, x, T, delta, nullptr, y, masks, st, od);
+    cs.publish(H);
+    return rc;
+}
+}  // namespace mobi
+extern "C" {
+
+int mobi_forward_out(mobi_layer_t H, const void* x, int64_t T, float delta, const mobi_out_desc* out, uint8_t* masks,
+                     void* stream) {
+    CHECK_ARG(H && out, "mobi_forward_out: null argument");
+    OutDesc od{};
+    CHECK_ARG(out->n_dst >= 1 && out->n_dst <= MOBI_MAX_DST,
+              "mobi_out_desc: n_dst " << out->n_dst << " outside [1," << MOBI_MAX_DST << "]");
+    od.n_dst = out->n_dst;
+    for (int k = 0; k < od.n_dst; ++k) od.dst[k] = reinterpret_cast<__nv_bfloat16*>(out->dst[k]);
+    od.ldy = out->ldy;
+    od.col0 = out->col0;
+    CallScope cs(H, stream);
+    if (cs.rc) return cs.rc;
+    const int rc = run_layer(cs.C, x, T, delta, nullptr, nullptr, masks, S(stream), &od);
+    cs.publish(H);
+    return rc;
+}
+
 int mobi_forward_host(mobi_layer_t H, const void* x_host, int64_t T, float delta, void* y_host, uint8_t* masks_host,
                       void* stream) {
     CHECK_ARG(H && x_host && y_host, "mobi_forward_host: null argument");
@@ -877,6 +944,43 @@ int mobi_forward_host(mobi_layer_t H, const void* x_host, int64_t T, float delta
     return MOBI_OK;
 }
 
+int mobi_ipc_export(void* dev_ptr, void* handle64, int64_t* offset) {
+    CHECK_ARG(dev_ptr && handle64 && offset, "mobi_ipc_export: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    // the handle names the whole allocation (e.g. a caching allocator's block): report dev_ptr's offset
+    typedef CUresult (*PFN_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static PFN_range range = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+        return reinterpret_cast<PFN_range>(f);
+    }();
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (!range || range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+        return set_error(MOBI_ERUNTIME, "mobi_ipc_export: cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    MOBI_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    std::memcpy(handle64, &h, sizeof(h));
+    *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+    return MOBI_OK;
+}
+
+int mobi_ipc_open(const void* handle64, int device, void** dev_ptr) {
+    CHECK_ARG(handle64 && dev_ptr, "mobi_ipc_open: null argument");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    MOBI_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return MOBI_OK;
+}
+
+int mobi_ipc_close(void* dev_ptr) {
+    CHECK_ARG(dev_ptr, "mobi_ipc_close: null argument");
+    MOBI_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    return MOBI_OK;
+}
+
 int mobi_permute_by_slice(const uint8_t* masks, int64_t T, int32_t* perm, int32_t* inverse, uint8_t* group_mask,
                           int64_t* group_len, int64_t* n_groups, void* stream) {
     CHECK_ARG(T >= 0, "permute_by_slice: negative token count");
@@ -919,6 +1023,18 @@ int mobi_calibrate_threshold(const float* scores, int64_t n, double rho, double*
     MOBI_TRY(launch_select_desc(scores, n, std::min(k, n - 1), &v, S(stream)));
     *delta = k >= n ? (double)v - 1.0 : (double)v;
     return MOBI_OK;
+}
+
+int mobi_avg_bits(const uint8_t* masks, int64_t T, const int32_t* slice_bits, int32_t n_slices, double* avg,
+                  void* stream) {
+    CHECK_ARG(avg && slice_bits, "avg_bits: null argument");
+    CHECK_ARG(n_slices >= 1 && n_slices <= 8, "avg_bits: " << n_slices << " slices");
+    CHECK_ARG(T >= 0 && (T == 0 || masks), "avg_bits: bad gate matrix");
+    if (T == 0) {
+        *avg = (double)slice_bits[0];
+        return MOBI_OK;
+    }
+    return launch_avg_bits(masks, T, slice_bits, n_slices, avg, S(stream));
 }
 
 int mobi_decompose(const double* w, int64_t out, int64_t in, int64_t group_size, const int32_t* slice_bits,

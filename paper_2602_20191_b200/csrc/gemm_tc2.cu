@@ -79,7 +79,7 @@ struct Params {
     const int32_t* perm;
     const TokTile* tiles;
     const int32_t* meta;
-    __nv_bfloat16* y;
+    OutDesc od;   // Y row t of this layer -> od.dst[k] + t*ldy + col0 (k < n_dst: local and peer buffers)
     int vec_y;
     int* bk_hist;  // fused-bucketing histogram + slot counters: zeroed here for the next forward
     int* unit_ctr;  // dynamic unit counter (meta[32]), zeroed by the kernel that builds the tile list
@@ -458,15 +458,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int32_t src = tok_src[t];
                 if (src < 0 || r0 >= p.out) continue;
                 const __nv_bfloat16* sp = stage_y + t * kRowTile + 8 * (et % 16);
-                __nv_bfloat16* dp = p.y + (int64_t)src * p.out + r0;
+                const int64_t off = (int64_t)src * p.od.ldy + p.od.col0 + r0;
                 if (p.vec_y && r0 + 8 <= p.out) {
-                    *reinterpret_cast<uint4*>(dp) = *reinterpret_cast<const uint4*>(sp);
+                    const uint4 v = *reinterpret_cast<const uint4*>(sp);
+                    for (int k = 0; k < p.od.n_dst; ++k) *reinterpret_cast<uint4*>(p.od.dst[k] + off) = v;
                 } else {
-                    for (int u = 0; u < 8 && r0 + u < p.out; ++u) dp[u] = sp[u];
+                    for (int k = 0; k < p.od.n_dst; ++k)
+                        for (int u = 0; u < 8 && r0 + u < p.out; ++u) p.od.dst[k][off + u] = sp[u];
                 }
             }
             if (warp == kWarpEpi0) EVU(4, tc);
         }
+        // peer destinations: make this CTA's stores to other GPUs' memory visible system-wide before the
+        // kernel completes (the caller orders the peers' reads after it with a collective)
+        if (p.od.n_dst > 1) __threadfence_system();
     }
     tc_fence_before();
     __syncthreads();
@@ -512,8 +517,18 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     p.perm = L->perm;
     p.tiles = L->tiles;
     p.meta = L->meta;
-    p.y = y;
-    p.vec_y = (L->out % 8 == 0) && ((reinterpret_cast<uintptr_t>(y) & 15) == 0);
+    if (L->od.n_dst > 0) {
+        p.od = L->od;
+    } else {
+        p.od = OutDesc{};
+        p.od.dst[0] = y;
+        p.od.n_dst = 1;
+        p.od.ldy = L->out;
+        p.od.col0 = 0;
+    }
+    bool al = L->out % 8 == 0 && p.od.ldy % 8 == 0 && p.od.col0 % 8 == 0;
+    for (int k = 0; k < p.od.n_dst; ++k) al = al && (reinterpret_cast<uintptr_t>(p.od.dst[k]) & 15) == 0;
+    p.vec_y = al;
     const int64_t max_pairs = (int64_t)(p.n_row_tiles / 2) * L->max_tiles;
     const int grid = 2 * (int)std::min<int64_t>(L->n_sm / 2, max_pairs);
     p.trace = trace;

@@ -171,4 +171,23 @@ int launch_unpack_codes(const mobi_layer* L, uint8_t* codes_dev, cudaStream_t st
     return MOBI_OK;
 }
 
+// Y [T, out] (row stride out) -> every destination of an output descriptor (row stride ldy, column
+// offset col0): the small-T paths compute into a staging buffer and place it with this copy
+__global__ void scatter_out_kernel(const __nv_bfloat16* __restrict__ y, int64_t out, OutDesc od) {
+    const int64_t t = blockIdx.x;
+    const __nv_bfloat16* src = y + t * out;
+    for (int64_t c = threadIdx.x; c < out; c += blockDim.x) {
+        const __nv_bfloat16 v = src[c];
+        for (int k = 0; k < od.n_dst; ++k) od.dst[k][t * od.ldy + od.col0 + c] = v;
+    }
+    if (od.n_dst > 1) __threadfence_system();
+}
+
+int launch_scatter_out(const __nv_bfloat16* y, int64_t T, int64_t out, const OutDesc& od, cudaStream_t st) {
+    if (T <= 0) return MOBI_OK;
+    scatter_out_kernel<<<(unsigned)T, 256, 0, st>>>(y, out, od);
+    MOBI_LAUNCH_CHECK();
+    return MOBI_OK;
+}
+
 }  // namespace mobi

@@ -64,6 +64,15 @@ __device__ __forceinline__ TokTile uniform_tile(const TokTile& t) {
     return u;
 }
 
+// Where a layer's Y [T, out] goes: n_dst buffers (device pointers, peer-mapped for the fused
+// all-gather of column-parallel shards), row stride ldy, this layer's first output column col0.
+struct OutDesc {
+    __nv_bfloat16* dst[MOBI_MAX_DST];
+    int32_t n_dst;
+    int64_t ldy;
+    int64_t col0;
+};
+
 // Per-mask dequant constants (uniform b-bit slices): W = S*INT_m + C with
 //   INT_m = merged & maskbyte[m],  S = s / 2^P,  C = s*K[m]/2^(P+1) - s*z
 struct MaskTable {
@@ -153,6 +162,15 @@ struct mobi_layer {
     int64_t plan_T = 0;                  // > T: choose kernels as for a batch of plan_T tokens (chunked calls)
     int32_t impl = 0;                    // development hook (mobi_layer_debug_impl): kernel override
     int32_t plan[8] = {};                // the last call's kernels (mobi_layer_last_plan)
+    mobi::OutDesc od{};                  // this call's output placement (n_dst == 0: plain y)
+    // multi-GPU (mobi_layer_create_sharded, shard.cu)
+    int32_t shard_mode = 0, shard_rank = 0, shard_nranks = 1;
+    void* shard_comm = nullptr;          // ncclComm_t of the caller
+    int64_t shard_per = 0, shard_out = 0;  // rows per rank (128-aligned), the unsharded out
+    __nv_bfloat16* gather_buf = nullptr;  // [P][T][per] rank-major all-gather buffer
+    int64_t gather_T = 0;
+    __nv_bfloat16* y_tmp = nullptr;      // staging for non-default placements on the small-T paths
+    int64_t y_tmp_T = 0;
     mobi_layer* plan_ctx = nullptr;      // handle: the context that ran the last call
 };
 
@@ -226,8 +244,11 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
 int launch_decode_gemm(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
                        uint8_t* masks_out, float* scores_out, __nv_bfloat16* y, bool pdl, cudaStream_t st,
                        unsigned long long* trace = nullptr);
+// layer.cu: copy Y rows [T, out] (ldy = out) to every destination of an output descriptor
+int launch_scatter_out(const __nv_bfloat16* y, int64_t T, int64_t out, const OutDesc& od, cudaStream_t st);
 // select.cu: the score of descending rank k (exact fp32) -> host (synchronous on `st`)
 int launch_select_desc(const float* scores, int64_t n, int64_t k, float* out_host, cudaStream_t st);
+int launch_avg_bits(const uint8_t* masks, int64_t T, const int32_t* slice_bits, int32_t E, double* avg, cudaStream_t st);
 // decompose.cu
 int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits,
                      int32_t E, double gamma, uint8_t* codes, double* scale, double* zero,

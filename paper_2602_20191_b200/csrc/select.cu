@@ -74,7 +74,39 @@ __global__ void sel_pick_kernel(SelState* __restrict__ st, int shift, unsigned l
     }
 }
 
+__global__ void __launch_bounds__(256) avg_bits_kernel(const uint8_t* __restrict__ m, int64_t T, uint4 bits_lo,
+                                                       uint4 bits_hi, int E, unsigned long long* __restrict__ sum) {
+    const uint32_t b[8] = {bits_lo.x, bits_lo.y, bits_lo.z, bits_lo.w, bits_hi.x, bits_hi.y, bits_hi.z, bits_hi.w};
+    unsigned long long acc = 0;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t mk = m[t] | 1u;  // slice 1 is always on (router.hpp:141)
+        for (int e = 0; e < E && e < 8; ++e)
+            if ((mk >> e) & 1u) acc += b[e];
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, acc);
+}
+
 }  // namespace
+
+int launch_avg_bits(const uint8_t* masks, int64_t T, const int32_t* slice_bits, int32_t E, double* avg,
+                    cudaStream_t stream) {
+    uint32_t b[8] = {};
+    for (int e = 0; e < E && e < 8; ++e) b[e] = (uint32_t)slice_bits[e];
+    unsigned long long* d = nullptr;
+    MOBI_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), stream));
+    MOBI_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), stream));
+    const int blocks = (int)std::min<int64_t>(cdiv(T, 256), 296);
+    avg_bits_kernel<<<blocks, 256, 0, stream>>>(masks, T, make_uint4(b[0], b[1], b[2], b[3]),
+                                                make_uint4(b[4], b[5], b[6], b[7]), E, d);
+    MOBI_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    MOBI_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    MOBI_CUDA(cudaStreamSynchronize(stream));
+    cudaFreeAsync(d, stream);
+    *avg = (double)h / (double)T;
+    return MOBI_OK;
+}
 
 int launch_select_desc(const float* scores, int64_t n, int64_t k, float* out_host, cudaStream_t stream) {
     SelState* st = nullptr;

@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import LayerDesc, check, lib
+from ._lib import LayerDesc, OutDesc, check, lib
 
 _i64, _i32, _f64 = C.c_int64, C.c_int32, C.c_double
 
@@ -44,13 +44,16 @@ def ratio_from_target_bits(target: float, slice_bits: Sequence[int]) -> float:
     return (target - b) / r
 
 
-def avg_bits_from_masks(masks: torch.Tensor, slice_bits: Sequence[int]) -> float:
-    """router.hpp:135-150 expressed on slice masks (bit e-1 <-> slice e)."""
-    m = masks.to(torch.int64)
-    bits = torch.zeros_like(m, dtype=torch.float64)
-    for e, b in enumerate(slice_bits):
-        bits += ((m >> e) & 1).to(torch.float64) * b
-    return float(bits.mean())
+def avg_bits_from_masks(masks: torch.Tensor, slice_bits: Sequence[int], stream=None) -> float:
+    """router.hpp:135-150 on device slice masks (bit e-1 <-> slice e): mobi_avg_bits."""
+    m = masks.to(torch.uint8).contiguous()
+    if not m.is_cuda:
+        raise ValueError("avg_bits expects CUDA masks")
+    sb = _arr(slice_bits, np.int32)
+    out = _f64()
+    check(lib().mobi_avg_bits(m.data_ptr() if m.numel() else None, m.numel(), sb.ctypes.data, sb.size, C.byref(out),
+                              _stream_ptr(stream)))
+    return out.value
 
 
 class MobiLayer:
@@ -233,6 +236,23 @@ class MobiLayer:
                                  m.data_ptr() if m is not None else None, _stream_ptr(stream)))
         return (y, m) if return_masks else y
 
+    def forward_out(self, x: torch.Tensor, delta: float, dsts: Sequence[int], ldy: int, col0: int = 0,
+                    return_masks: bool = False, stream=None):
+        """Forward with output placement (mobi_forward_out): Y row t goes to every destination pointer in
+        ``dsts`` (device addresses, local or peer-mapped) at ``t*ldy + col0`` -- the fused all-gather of a
+        column-parallel shard when ``dsts`` are the full outputs of every rank."""
+        x = self._x(x)
+        T = x.shape[0]
+        if not 1 <= len(dsts) <= 8:
+            raise ValueError(f"mobi_out_desc: n_dst {len(dsts)} outside [1,8]")
+        d = OutDesc(n_dst=len(dsts), ldy=ldy, col0=col0)
+        for k, ptr in enumerate(dsts):
+            d.dst[k] = int(ptr)
+        m = torch.empty(T, dtype=torch.uint8, device=x.device) if return_masks else None
+        check(lib().mobi_forward_out(self._h, x.data_ptr(), T, float(delta), C.byref(d),
+                                     m.data_ptr() if m is not None else None, _stream_ptr(stream)))
+        return m
+
     def forward_masked(self, x: torch.Tensor, masks: torch.Tensor, y: Optional[torch.Tensor] = None, stream=None):
         """router.hpp:105-132 forward_elastic with per-token slice masks (bit e-1 <-> slice e)."""
         x = self._x(x)
@@ -272,6 +292,26 @@ class MobiLayer:
                                       masks_host.data_ptr() if masks_host is not None else None,
                                       _stream_ptr(stream)))
         return y_host
+
+
+# ---------------- CUDA IPC (peer destinations of the fused column-parallel all-gather) ----------------
+def ipc_export(t: torch.Tensor):
+    """(64-byte CUDA IPC handle of the allocation holding ``t``, ``t``'s byte offset in it)."""
+    buf = C.create_string_buffer(64)
+    off = _i64()
+    check(lib().mobi_ipc_export(C.c_void_p(t.data_ptr()), buf, C.byref(off)))
+    return buf.raw, off.value
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    """Map a peer's exported allocation on ``device``; returns the allocation's base address there."""
+    ptr = C.c_void_p()
+    check(lib().mobi_ipc_open(C.create_string_buffer(handle, 64), device, C.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(ptr: int) -> None:
+    check(lib().mobi_ipc_close(C.c_void_p(ptr)))
 
 
 # ---------------- stateless reference-signature helpers ----------------

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "mobi/bench/calibset.hpp"
+#include "mobi/bitplane.hpp"
 #include "mobi/router.hpp"
 #include "mobi/slicer.hpp"
 #include "mobi_b200.hpp"
@@ -94,6 +95,36 @@ int run_case(size_t out, size_t in, size_t gs, size_t T, unsigned seed) {
                 const double v = r < static_cast<size_t>(half) ? y0(t, r) : y1(t, r - half);
                 EXPECT(v == y_gpu(t, r), "shard output (%zu,%zu) %g != %g", t, r, v, y_gpu(t, r));
             }
+    }
+    // the remaining hot-path calls of the reference next to the shim's GPU versions
+    {
+        std::vector<float> sf(s_ref.size());
+        std::vector<double> s_f(s_ref.size());
+        for (size_t i = 0; i < s_ref.size(); ++i) s_f[i] = sf[i] = static_cast<float>(s_ref[i]);
+        for (double rho : {0.0, 1.0 / 12, 1.0 / 6, 1.0 / 3, 1.0})
+            EXPECT(mobi_b200::calibrate_threshold(s_f, rho) == router::calibrate_threshold(s_f, rho),
+                   "calibrate_threshold rho=%g", rho);
+        EXPECT(mobi_b200::avg_bits(g_gpu, {2, 2, 2, 2}) == router::avg_bits(g_gpu, {2, 2, 2, 2}), "avg_bits");
+        std::vector<uint8_t> masks(T, 1);
+        for (size_t t = 0; t < T; ++t)
+            for (size_t j = 0; j < 3; ++j)
+                if (g_gpu(t, j) > 0.5) masks[t] |= static_cast<uint8_t>(1u << (j + 1));
+        bitplane::Permutation pr = bitplane::permute_by_slice(x, masks);
+        Matrix xp;
+        mobi_b200::Permutation pg = mobi_b200::permute_by_slice(x, masks, &xp);
+        EXPECT(pg.perm == pr.perm && pg.inverse == pr.inverse, "permute_by_slice perm/inverse");
+        EXPECT(pg.groups == pr.groups, "permute_by_slice groups");
+        bool same = xp.size() == pr.permuted.size();
+        for (size_t i = 0; same && i < xp.size(); ++i) same = xp[i] == pr.permuted[i];
+        EXPECT(same, "permute_by_slice permuted tokens");
+    }
+    // the multi-GPU entry at world size 1 (COLUMN: one shard owning every row; TOKEN: replicas)
+    for (int mode : {MOBI_SHARD_COLUMN, MOBI_SHARD_TOKEN}) {
+        mobi_b200::ShardedLayer sl(st, rs, nullptr, 0, 1, mode, 0);
+        Matrix ys = sl.forward(x, delta);
+        bool same = ys.size() == y_full.size();
+        for (size_t i = 0; same && i < ys.size(); ++i) same = ys[i] == y_full[i];
+        EXPECT(same, "sharded forward (mode %d, world 1) == forward", mode);
     }
     // error behaviour mirrors MOBI_CHECK
     bool threw = false;

@@ -13,6 +13,7 @@ from paper_2602_20191_b200 import _lib, calibrate_threshold  # noqa: E402
 
 def main():
     args = bench.parse()
+    bench.workload(args, 1)
     dev = torch.device("cuda", 0)
     layer, _ = bench.make_layer(args, dev, 1)
     x = bench.make_x(args, dev, 2)

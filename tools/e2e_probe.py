@@ -24,6 +24,7 @@ def rate(fn, nbytes, reps=20):
 
 def main():
     args = bench.parse()
+    bench.workload(args, 1)
     dev = torch.device("cuda", 0)
     T, inn, out = args.tokens, args.inn, args.out
     if os.environ.get("E2E_PCIE", "1") == "1":

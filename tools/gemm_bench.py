@@ -23,6 +23,7 @@ def run(layer, x, masks, reps=20):
 
 def main():
     args = bench.parse()
+    bench.workload(args, 1)
     import os
     dev = torch.device("cuda", 0)
     layer, _ = bench.make_layer(args, dev, 1)

@@ -16,6 +16,7 @@ def main():
     a = bench.parse.__wrapped__() if hasattr(bench.parse, "__wrapped__") else None
     sys.argv = [sys.argv[0]] + sys.argv[1:]
     args = bench.parse()
+    bench.workload(args, 1)
     dev = torch.device("cuda", 0)
     layer, _ = bench.make_layer(args, dev, 1)
     x = bench.make_x(args, dev, 2)

@@ -6,6 +6,7 @@ sys.path.insert(0, '/root/repo')
 import bench
 from paper_2602_20191_b200 import _lib
 args = bench.parse()
+bench.workload(args, 1)
 dev = torch.device("cuda", 0)
 layer, _ = bench.make_layer(args, dev, 1)
 x = bench.make_x(args, dev, 2)
