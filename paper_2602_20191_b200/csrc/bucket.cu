@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(BK_THREADS) bucket_kernel(
             c += __shfl_sync(0xffffffffu, incl, 31);
             a += __shfl_sync(0xffffffffu, inclp, 31);
         }
+        __syncwarp();  // lane 0 reads every lane's pstart[] below (racecheck: intra-warp hazard)
         if (perm && lane == 0) {
             int n = 0;
             for (int v = 0; v < NKEY_MASK && v < NKEY; ++v)

@@ -11,7 +11,17 @@
 //   * barriers: the peer's TMA completes on the leader's full_b, the peer's dequantizers and
 //     epilogue arrive on the leader's full_a / acc_empty (mapa addresses, release.cluster); the
 //     leader's MMA commits are multicast to both CTAs' empty / acc_full.
-// With half-height B stages (16 KiB) the ring is 8 deep in both smem (B) and TMEM (A).
+// With half-height B stages (16 KiB) the ring is 6 deep in both smem (B) and TMEM (A).
+//
+// Codes reach the dequantizers through shared memory: a code warp per CTA bulk-copies each
+// k-block's 8 KiB code block and the 1 KiB (s, s*z) slices of its groups into a 6-deep ring that the
+// dequantizers release as soon as they have read it (not when the MMAs finish), so a copy is issued
+// up to 8 + 5 k-blocks ahead of the MMA that consumes it.  A stage is two k-blocks (16 KiB of codes, one
+// bulk copy) plus the constants of the groups they touch (one 1 KiB copy per group: one for gs >= 128):
+// a single producer thread pays ~200 cycles of issue latency per bulk/TMA instruction, so per-k-block
+// instruction counts, not bytes, bound the producers.  Likewise the B tile of a stage is ONE TMA box
+// (16/32/64/128 rows, the smallest >= N/2; rows past the tile are loaded and ignored).  (Per-lane LDG
+// prefetch rings of codes were bound by load issue and L2 latency: ~700 cycles per k-block whatever N.)
 #include <algorithm>
 
 #include "mobi_internal.cuh"
@@ -20,15 +30,15 @@
 #ifndef MOBI_MMA_WAIT
 #define MOBI_MMA_WAIT 0
 #endif
-#ifndef MOBI_RELAXED
-#define MOBI_RELAXED 1
-#endif
 // bottleneck experiments (development only; all 0 in the product): drop one producer's real work
-#ifndef MOBI_X_NOLOAD
-#define MOBI_X_NOLOAD 0  // dequantizers skip the code / constant loads
-#endif
 #ifndef MOBI_X_NOTMA
 #define MOBI_X_NOTMA 0   // the TMA warp arrives without loading B
+#endif
+#ifndef MOBI_X_NOCODE
+#define MOBI_X_NOCODE 0  // the code warp arrives without copying (codes/constants garbage)
+#endif
+#ifndef MOBI_X_NOST
+#define MOBI_X_NOST 0    // dequantizers skip the TMEM store (garbage A)
 #endif
 #ifndef MOBI_X_NODQ
 #define MOBI_X_NODQ 0    // dequantizers store the raw code words (no ALU work)
@@ -49,22 +59,27 @@ namespace {
 
 using namespace sm100;
 
-constexpr int NSTAGE = 8;
+constexpr int NSTAGE = 5;   // B (smem) / A (TMEM) stages
+constexpr int NCS = 4;      // code stages (smem, 2 k-blocks each), released by the dequantizers, not by the MMAs
+constexpr int kCodeKb = 2;  // k-blocks per code stage: one 16 KiB bulk copy (a row tile's k-blocks are contiguous)
 constexpr int kDqWarps = 16;
-constexpr int kThreads = 32 * (2 + kDqWarps + 4);
+constexpr int kThreads = 32 * (4 + kDqWarps + 4);
 constexpr int kWarpDq0 = 0, kWarpEpi0 = kDqWarps, kWarpTma = kDqWarps + 4, kWarpMma = kDqWarps + 5;
+constexpr int kWarpCode = kDqWarps + 6;  // 2 warps bulk-copy the code stages (alternating) into smem
+constexpr int kCodeWarps = 2;
 // dynamic unit schedule: the leader's TMA warp claims units (atomic counter, units in decreasing
 // size order) and publishes them through a small ring to every role of both CTAs
 constexpr int kURing = 4;
-constexpr int kUnitConsumers = 1 + kDqWarps + 4;  // per CTA: MMA (leader) or TMA (peer) + dequant + epilogue
+constexpr int kUnitConsumers = 1 + kCodeWarps + kDqWarps + 4;  // per CTA: MMA (leader) or TMA (peer) + code + dequant + epilogue
 constexpr int kHalfRows = kTokTile / 2;                  // token rows per CTA per stage
 constexpr int kStageBytes = kHalfRows * kKBlock * 2;     // 16 KiB
-constexpr int kBoxRows = 16;
-constexpr int kBoxBytes = kBoxRows * kKBlock * 2;        // 2 KiB
 constexpr int kACol0 = 256;
 constexpr int kYStageBytes = kTokTile * kRowTile * 2;    // 64 KiB
-constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 + 512 + kYStageBytes + kTokTile * 4;
-constexpr int kBigBoxRows = kHalfRows;  // one TMA box per full half-tile
+constexpr int kConstOff = kCodeKb * kBlockBytes;
+constexpr int kCodeStage = kConstOff + 2 * kCodeKb * kRowTile * 8;  // codes + (s, s*z) of up to 4 groups x 128 rows
+constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 + 512 + kYStageBytes + kTokTile * 4 + NCS * kCodeStage;
+static_assert(kSmemBytes <= 232448, "tc2 shared memory");
+static_assert(NCS % kCodeWarps == 0, "each code warp owns fixed ring slots");
 
 struct Params {
     const uint8_t* codes8;
@@ -74,6 +89,7 @@ struct Params {
     int64_t out, G, gs, kblocks;
     int64_t tpad;
     int single_group;
+    int g_uniform;  // every code stage (128 columns) lies in one group: single group or gs % 128 == 0
     int n_row_tiles;
     const float* escale;
     const int32_t* perm;
@@ -88,7 +104,8 @@ struct Params {
 
 template <bool TRACE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    mobi_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_big,
+    mobi_gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmap16, const __grid_constant__ CUtensorMap tmap32,
+                         const __grid_constant__ CUtensorMap tmap64, const __grid_constant__ CUtensorMap tmap128,
                          const Params p) {
     // per-k-block event timeline (cluster 0, first tile): trace[20480 + (rank*8+ev)*64 + kb]
     auto EV = [&](int ev, int kb, uint32_t tile_idx) {
@@ -115,17 +132,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
     uint64_t* u_full = acc_empty + 1;        // [kURing] each CTA: unit slot published
     uint64_t* u_empty = u_full + kURing;     // [kURing] leader: every consumer of both CTAs read the slot
-    int32_t* uring = reinterpret_cast<int32_t*>(u_empty + kURing);  // [kURing] unit index (-1 = done)
+    int32_t* uring = reinterpret_cast<int32_t*>(u_empty + kURing + 2 * NCS);  // [kURing] unit index (-1 = done)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kURing);
     __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 512);
     int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);
+    uint8_t* stage_c = smem + NSTAGE * kStageBytes + 512 + kYStageBytes + kTokTile * 4;  // [NCS][kCodeStage]
+    uint64_t* c_full = u_empty + kURing;   // [NCS] each CTA: the stage's codes + constants landed
+    uint64_t* c_empty = c_full + NCS;      // [NCS] each CTA: the 8 dequant warps of its two k-blocks read them
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
 
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
     const uint32_t rank = cluster_ctarank();
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full_b[s], 1 + kDqWarps);  // TMA expect_tx + 8 dequant warps per CTA x 2
+            mbar_init(&full_b[s], 1 + kDqWarps / 2);  // TMA expect_tx + 4 dequant warps per CTA x 2
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
@@ -134,9 +154,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_init(&u_full[s], 1);
             mbar_init(&u_empty[s], 2 * kUnitConsumers);
         }
+        for (int s = 0; s < NCS; ++s) {
+            mbar_init(&c_full[s], 1);
+            mbar_init(&c_empty[s], kDqWarps / 2);
+        }
         fence_barrier_init();
-        prefetch_tmap(&tmap_x);
-        prefetch_tmap(&tmap_big);
+        prefetch_tmap(&tmap16);
+        prefetch_tmap(&tmap32);
+        prefetch_tmap(&tmap64);
+        prefetch_tmap(&tmap128);
     }
     if (warp == kWarpMma) tmem_alloc_2sm(tmem_slot, 512);
     pdl_wait();  // PDL launch: everything above overlapped the gather; its outputs are visible from here
@@ -213,9 +239,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
-            const bool big = nc == kTokTile;  // full tile: one 128-row box per CTA
-            const int nbox = big ? 1 : nc / 2 / kBoxRows;
-            const int row_half = tt.row0 + (int)rank * (nc / 2);
+            // one box per CTA per stage: the smallest of 16/32/64/128 rows covering N/2
+            const int half = nc / 2;
+            const int bx = half <= 16 ? 16 : half <= 32 ? 32 : half <= 64 ? 64 : 128;
+            const CUtensorMap* tm = bx == 16 ? &tmap16 : bx == 32 ? &tmap32 : bx == 64 ? &tmap64 : &tmap128;
+            const int row_half = tt.row0 + (int)rank * half;
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
@@ -224,14 +252,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (MOBI_X_NOTMA) {
                     if (elect_one_sync() && rank == 0) mbar_arrive_expect_tx(&full_b[s], 0);
                 } else if (elect_one_sync()) {
-                    if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * (big ? kStageBytes : nbox * kBoxBytes));
-                    if (big)
-                        tma_load_2d_2sm(stage_b + s * kStageBytes, &tmap_big, full_b_leader + s * 8, 0,
-                                        (int)(kb * p.tpad) + row_half);
-                    else
-                        for (int j = 0; j < nbox; ++j)
-                            tma_load_2d_2sm(stage_b + s * kStageBytes + j * kBoxBytes, &tmap_x, full_b_leader + s * 8,
-                                            0, (int)(kb * p.tpad) + row_half + j * kBoxRows);
+                    if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * bx * kKBlock * 2);
+                    tma_load_2d_2sm(stage_b + s * kStageBytes, tm, full_b_leader + s * 8, 0,
+                                    (int)(kb * p.tpad) + row_half);
                 }
                 __syncwarp();
             }
@@ -276,125 +299,147 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
         __syncwarp();
-    } else if (warp < kWarpEpi0) {
-        // ---------------- dequantizers ----------------
-        // 16 warps = 4 TMEM lane quarters x 2 k-halves x 2 k-block parities: a warp dequantizes
-        // 32 codes of its row for every other k-block, so two k-blocks are in flight at once.
-        const int idx = warp - kWarpDq0;
-        const int q = warp % 4;
-        const int par = (idx / 4) & 1;
-        const int hh = idx / 8;
-        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        const uint32_t full_leader = mapa_shared(smem_u32(full_b), 0);
-        uint32_t base = 0;  // global k-block counter at the start of the tile (stage/phase)
-        for (uint32_t ui = 0;; ++ui, base += kb_n) {
+    } else if (warp >= kWarpCode) {
+        // ---------------- code producers (each CTA: its own 128-row tile) ----------------
+        // two warps alternate code stages (global stage parity): a single thread needs ~1000 cycles to
+        // issue one stage's expect_tx + bulk copies, longer than the MMAs of two k-blocks at N <= 128
+        // per k-block: the 8 KiB code block and, for each k-half, the 1 KiB (s, s*z) row slice of its
+        // group; the ring slot is released by the dequantizers as soon as they have read it
+        uint32_t it = 0;
+        for (uint32_t ui = 0;; ++ui) {
             const int pair = unit_get(ui);
             if (pair < 0) break;
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
-            const int64_t R = (int64_t)rt * kRowTile + 32 * q + lane;
-            const bool rv = R < p.out;
+            const uint8_t* csrc = p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes;
+            const float2* gsrc = p.gconst + (int64_t)rt * kRowTile;
+            for (int kb0 = 0; kb0 < kb_n; kb0 += kCodeKb, ++it) {
+                if ((int)(it % kCodeWarps) != warp - kWarpCode) continue;
+                const int s = (int)(it % NCS);
+                mbar_wait(&c_empty[s], ((it / NCS) & 1) ^ 1);
+                EV(6, kb0, ui);
+                if (MOBI_X_NOCODE) {
+                    if (elect_one_sync()) mbar_arrive_expect_tx(&c_full[s], 0);
+                } else if (elect_one_sync()) {
+                    uint8_t* dc = stage_c + s * kCodeStage;
+                    const int nkb = min(kCodeKb, kb_n - kb0);
+                    // groups of the stage's first and last 32-column chunks (gs is a multiple of 32 or >= in)
+                    const int g0 = p.single_group ? 0 : (int)((uint32_t)(kb0 * kKBlock) / (uint32_t)p.gs);
+                    const int g1 = p.single_group ? 0 : (int)((uint32_t)((kb0 + nkb) * kKBlock - 32) / (uint32_t)p.gs);
+                    mbar_arrive_expect_tx(&c_full[s], nkb * kBlockBytes + (uint32_t)(g1 - g0 + 1) * kRowTile * 8);
+                    bulk_g2s(dc, csrc + (int64_t)kb0 * kBlockBytes, nkb * kBlockBytes, &c_full[s]);
+                    for (int g = g0; g <= g1; ++g)
+                        bulk_g2s(dc + kConstOff + (g - g0) * kRowTile * 8, gsrc + (int64_t)g * p.out_pad, kRowTile * 8,
+                                 &c_full[s]);
+                }
+                __syncwarp();
+                EV(7, kb0, ui);
+            }
+        }
+    } else if (warp < kWarpEpi0) {
+        // ---------------- dequantizers ----------------
+        // 16 warps = 4 TMEM lane quarters x 4 k-block phases: a warp dequantizes the 64 codes of its
+        // row in every fourth k-block (one 32-column TMEM store), so each warp has four k-blocks of MMA
+        // time to cover its smem reads, ALU work and the TMEM store latency.  Code stage j (k-blocks 2j,
+        // 2j+1) is read by the 8 warps of phases 2(j%2), 2(j%2)+1.  Per k-block: dequantize (codes
+        // already in registers), release the code stage, read the next k-block's codes, then -- once
+        // the MMAs are done with the A stage -- store into TMEM and arrive on the stage's full barrier.
+        const int idx = warp - kWarpDq0;
+        const int q = idx % 4;
+        const int ph4 = idx / 4;            // (code-stage parity, k-block inside the stage)
+        const int jpar = ph4 >> 1;          // code stages j with j % 2 == jpar
+        const int sub = ph4 & 1;            // k-block inside the stage
+        const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        const uint32_t full_leader = mapa_shared(smem_u32(full_b), 0);
+        const int c_off = sub * kBlockBytes + (32 * q + lane) * 16;  // + (h*2 + c) * kRowTile * 16
+        uint32_t base = 0;   // global k-block counter at the start of the unit (A/B stage and phase)
+        uint32_t cbase = 0;  // global code-stage counter at the start of the unit
+        for (uint32_t ui = 0;; ++ui) {
+            const int pair = unit_get(ui);
+            if (pair < 0) break;
+            TokTile tt;
+            int rt, nc;
+            tile_of(pair, tt, rt, nc);
             const uint32_t mw = p.mt.maskword[tt.mask];
             const float kc = p.mt.kc[tt.mask];
-            const uint8_t* cbase =
-                p.codes8 + (int64_t)rt * p.kblocks * kBlockBytes + ((hh * 2) * kRowTile + 32 * q + lane) * 16;
-            const float2* gcol = p.gconst + (rv ? R : 0);
-            auto ldc = [&](int gg) {
-                if (MOBI_X_NOLOAD) return make_float2(0.01f * gg, 0.02f);
-                return rv ? __ldg(gcol + (int64_t)gg * p.out_pad) : make_float2(0.f, 0.f);
-            };
-            auto ld = [&](int kb, uint4& c0, uint4& c1) {
-                if (MOBI_X_NOLOAD) {
-                    c0 = make_uint4(kb, kb * 3, kb * 5, kb * 7);
-                    c1 = make_uint4(kb * 11, kb, kb * 13, kb);
-                    return;
-                }
-                const uint8_t* b0 = cbase + (int64_t)kb * kBlockBytes;
-                c0 = *reinterpret_cast<const uint4*>(b0);
-                c1 = *reinterpret_cast<const uint4*>(b0 + kRowTile * 16);
-            };
-            // group of k = kb*64 + 32*hh, tracked incrementally (k advances by 128 per step)
-            auto dq = [&](const uint4& c0, const uint4& c1, float2 gcst, uint32_t (&v)[16]) {
-                const __half2 S2 = __float2half2_rn(gcst.x * p.mt.inv_2p);
-                const __half2 C2 = __float2half2_rn(fmaf(gcst.x, kc, -gcst.y));
-                const uint32_t* w0 = reinterpret_cast<const uint32_t*>(&c0);
-                const uint32_t* w1 = reinterpret_cast<const uint32_t*>(&c1);
-                if (MOBI_X_NODQ) {
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) v[2 * u] = v[2 * u + 1] = w0[u];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) v[8 + 2 * u] = v[8 + 2 * u + 1] = w1[u];
-                    return;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) dequant4(w0[u], mw, S2, C2, v[2 * u], v[2 * u + 1]);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) dequant4(w1[u], mw, S2, C2, v[8 + 2 * u], v[8 + 2 * u + 1]);
-            };
-            // Ring of three static slots (codes + group constants), unrolled so a slot is refilled
-            // right after it was consumed and each load has two iterations of lead time; no
-            // register moves touch a pending load.
-            uint4 c00, c01, c10, c11, c20, c21;
-            float2 g0 = make_float2(0.f, 0.f), g1 = g0, g2 = g0;
-            int gp = 0, kinp = 0;  // group cursor at the next k-block to prefetch
-            if (!p.single_group) {
-                kinp = par * kKBlock + hh * 32;
-                while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
-            }
-            auto fetch = [&](int kb, uint4& c0, uint4& c1, float2& gc) {
+            const int ncs_u = (kb_n + kCodeKb - 1) / kCodeKb;
+            // this warp's code stages: j = j0, j0 + 2, ... (global stage parity, so both phases of a
+            // stage agree on which warps read it across units with an odd stage count)
+            const int j0 = (int)((jpar - (int)(cbase & 1) + 2) & 1);
+            uint4 c[4];
+            float2 g[2];
+            auto load = [&](int j) {
+                const uint32_t cit = cbase + j;
+                const int cs = (int)(cit % NCS);
+                mbar_wait(&c_full[cs], (cit / NCS) & 1);
+                const int kb = kCodeKb * j + sub;
+                if (warp == 0) EV(2, kb, ui);
                 if (kb < kb_n) {
-                    ld(kb, c0, c1);
-                    gc = ldc(gp);
-                }
-                if (!p.single_group) {
-                    kinp += 2 * kKBlock;
-                    while (kinp >= p.gs) kinp -= (int)p.gs, ++gp;
+                    const uint8_t* dc = stage_c + cs * kCodeStage + c_off;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) c[u] = *reinterpret_cast<const uint4*>(dc + u * kRowTile * 16);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        // group slot inside the stage: 0 whenever a stage's 128 columns are one group
+                        const int gslot = p.g_uniform ? 0
+                                                      : (int)((uint32_t)(kb * kKBlock + 32 * hh) / (uint32_t)p.gs -
+                                                              (uint32_t)(kCodeKb * j * kKBlock) / (uint32_t)p.gs);
+                        g[hh] = *reinterpret_cast<const float2*>(stage_c + cs * kCodeStage + kConstOff +
+                                                                  (gslot * kRowTile + 32 * q + lane) * 8);
+                    }
                 }
             };
-            fetch(par, c00, c01, g0);
-            fetch(par + 2, c10, c11, g1);
-            fetch(par + 4, c20, c21, g2);
-            uint32_t v[16];
-            auto step = [&](int kb, uint4& ca, uint4& cb, float2& ga, uint4& na, uint4& nb, float2& gn) -> bool {
-                // v holds k-block kb (dequantized from the slot (ca, cb)); (na, nb) holds kb+2
-                if (kb >= kb_n) return false;
+            uint32_t v[32];
+            if (j0 < ncs_u) load(j0);
+            for (int j = j0; j < ncs_u; j += 2) {
+                const int kb = kCodeKb * j + sub;
+                const bool valid = kb < kb_n;
+                if (valid) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const __half2 S2 = __float2half2_rn(g[hh].x * p.mt.inv_2p);
+                        const __half2 C2 = __float2half2_rn(fmaf(g[hh].x, kc, -g[hh].y));
+#pragma unroll
+                        for (int cc = 0; cc < 2; ++cc) {
+                            const uint32_t* w = reinterpret_cast<const uint32_t*>(&c[hh * 2 + cc]);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int o = hh * 16 + cc * 8 + 2 * u;
+                                if (MOBI_X_NODQ)
+                                    v[o] = v[o + 1] = w[u];
+                                else
+                                    dequant4(w[u], mw, S2, C2, v[o], v[o + 1]);
+                            }
+                        }
+                    }
+                }
+                // the stage's data is in registers (consumed above): release the slot to the code warp
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&c_empty[(cbase + j) % NCS]);
+                if (j + 2 < ncs_u) load(j + 2);  // smem latency overlaps the TMEM store below
+                if (!valid) continue;
                 const uint32_t itk = base + kb;
-                const int s = itk % NSTAGE;
-                const uint32_t ph = (itk / NSTAGE) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                if (warp == 0 || warp == 4) EV(4, kb, ui);
+                const int s = (int)(itk % NSTAGE);
+                mbar_wait(&empty[s], ((itk / NSTAGE) & 1) ^ 1);
+                if (warp == 0) EV(4, kb, ui);
                 tc_fence_after();
-                tmem_st16(tmem + lane_base + kACol0 + s * 32 + hh * 16, v);
-                fetch(kb + 6, ca, cb, ga);  // refill the consumed slot three of this warp's k-blocks ahead
-                if (warp == 0 || warp == 4) EV(6, kb, ui);
-                if (kb + 2 < kb_n) dq(na, nb, gn, v);
-                if (warp == 0 || warp == 4) EV(7, kb, ui);
-                tmem_st_wait();
+                if (!MOBI_X_NOST) {
+                    tmem_st32(tmem + lane_base + kACol0 + s * 32, v);
+                    tmem_st_wait();
+                }
                 tc_fence_before();
                 __syncwarp();
-                if (warp == 0 || warp == 4) EV(5, kb, ui);
+                if (warp == 0) EV(5, kb, ui);
                 if (lane == 0) {
-#if MOBI_RELAXED
                     if (rank == 0)
                         mbar_arrive_relaxed(&full_b[s]);
                     else
                         mbar_arrive_relaxed_cluster(full_leader + s * 8);
-#else
-                    if (rank == 0)
-                        mbar_arrive(&full_b[s]);
-                    else
-                        mbar_arrive_cluster(full_leader + s * 8);
-#endif
                 }
-                return true;
-            };
-            if (par < kb_n) dq(c00, c01, g0, v);
-            for (int kb = par; kb < kb_n; kb += 6) {
-                if (!step(kb, c00, c01, g0, c10, c11, g1)) break;
-                if (!step(kb + 2, c10, c11, g1, c20, c21, g2)) break;
-                if (!step(kb + 4, c20, c21, g2, c00, c01, g0)) break;
             }
+            base += kb_n;
+            cbase += ncs_u;
         }
     } else {
         // ---------------- epilogue ----------------
@@ -491,10 +536,11 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
                                        kSmemBytes));
     }
     if (!L->tmap_x2) {
-        L->tmap_x2 = new CUtensorMap[2];
+        L->tmap_x2 = new CUtensorMap[4];
         const int64_t rows = L->kblocks * L->tpad_max;
-        int rc = make_tmap_2d(&L->tmap_x2[0], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, kKBlock, kBoxRows);
-        if (!rc) rc = make_tmap_2d(&L->tmap_x2[1], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, kKBlock, kBigBoxRows);
+        int rc = 0;
+        for (int i = 0; i < 4 && !rc; ++i)
+            rc = make_tmap_2d(&L->tmap_x2[i], L->xperm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rows, kKBlock, 16 << i);
         if (rc) {
             delete[] L->tmap_x2;
             L->tmap_x2 = nullptr;
@@ -512,6 +558,7 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     p.kblocks = L->kblocks;
     p.tpad = L->tpad_max;
     p.single_group = L->single_group;
+    p.g_uniform = L->single_group || L->gs % (kCodeKb * kKBlock) == 0;
     p.n_row_tiles = (int)(L->out_pad / kRowTile);
     p.escale = L->escale;
     p.perm = L->perm;
@@ -545,9 +592,11 @@ int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
     if (trace)
-        MOBI_CUDA(cudaLaunchKernelEx(&cfg, mobi_gemm_tc2_kernel<true>, *(&L->tmap_x2[0]), *(&L->tmap_x2[1]), p));
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, mobi_gemm_tc2_kernel<true>, L->tmap_x2[0], L->tmap_x2[1], L->tmap_x2[2],
+                                     L->tmap_x2[3], p));
     else
-        MOBI_CUDA(cudaLaunchKernelEx(&cfg, mobi_gemm_tc2_kernel<false>, *(&L->tmap_x2[0]), *(&L->tmap_x2[1]), p));
+        MOBI_CUDA(cudaLaunchKernelEx(&cfg, mobi_gemm_tc2_kernel<false>, L->tmap_x2[0], L->tmap_x2[1], L->tmap_x2[2],
+                                     L->tmap_x2[3], p));
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     L->plan[1] = MOBI_K_GEMM_PAIR;

@@ -136,7 +136,7 @@ struct mobi_layer {
     CUtensorMap* tmap_x = nullptr;  // host copies, rebuilt when the workspace changes
     CUtensorMap* tmap_w1 = nullptr; // router w1t (fixed for the layer's lifetime), 128-row boxes
     CUtensorMap* tmap_w1_64 = nullptr;  // the same with 64-row boxes (CTA-pair router, N = 128)
-    CUtensorMap* tmap_x2 = nullptr; // xperm, 16-row boxes (CTA-pair GEMM)
+    CUtensorMap* tmap_x2 = nullptr; // xperm, 16/32/64/128-row boxes (CTA-pair GEMM)
     int32_t last_launches = 0;
     int64_t device_bytes = 0;
     // profiling: event pairs around each launch, resolved lazily

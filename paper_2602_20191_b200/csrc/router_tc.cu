@@ -364,7 +364,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
     uint64_t* full = bars;                 // [NS] leader: both CTAs' bytes of the stage
     uint64_t* empty = bars + NS;           // [NS] each CTA: the pair's MMAs are done with the stage
     uint64_t* acc_full = bars + 2 * NS;    // [2] each CTA
-    uint64_t* acc_empty = acc_full + 2;    // [2] leader: 4 epilogue warps x 2 CTAs drained the buffer
+    uint64_t* acc_empty = acc_full + 2;    // [2] leader: 8 epilogue warps x 2 CTAs drained the buffer
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
     float4* cst = reinterpret_cast<float4*>(smem + RS * 2 * kAB + 1024);  // [2][PN] {b1, w2[0..2]}
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;

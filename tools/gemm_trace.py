@@ -73,8 +73,8 @@ def units(full):
 def timeline(full, base=20480):
     ev = full[base:base + 8 * 64].reshape(8, 64).astype(np.int64)
     t0 = ev[0][ev[0] > 0].min() if (ev[0] > 0).any() else 0
-    names = ["tma:empty ok", "mma:full_b ok", "-", "mma:issued", "dq:empty ok", "dq:arrive-ready", "dq:st+fetch",
-             "dq:dq done"]
+    names = ["tma:empty ok", "mma:full_b ok", "dq:c_full ok", "mma:issued", "dq:empty ok", "dq:arrive-ready", "cw:c_empty ok",
+             "cw:issued"]
     print("kb  " + " ".join(f"{n:>14s}" for n in names))
     for kb in range(0, 24):
         print(f"{kb:2d}  " + " ".join(f"{(ev[e][kb] - t0) if ev[e][kb] else -1:14d}" for e in range(8)))

@@ -177,13 +177,12 @@ int main() {
     unsigned long long* d_out;
     cudaMalloc(&d_out, 8 * 2048);
     run<0, 16384, 8>("bulk distinct 148 SMs", buf, bytes, d_out, nsm);
-    run<0, 16384, 8>("bulk distinct 32 SMs", buf, bytes, d_out, 32);
-    run<0, 16384, 8>("bulk distinct 74 SMs", buf, bytes, d_out, 74);
+    run<0, 16384, 4>("bulk distinct 148 SMs", buf, bytes, d_out, nsm);
+    run<0, 8192, 8>("bulk distinct 148 SMs", buf, bytes, d_out, nsm);
     run<0, 16384, 8, 32, 2>("bulk distinct 2 producers 148", buf, bytes, d_out, nsm);
-    run<0, 16384, 8, 32, 2>("bulk distinct 2 producers 32", buf, bytes, d_out, 32);
-    run<2, 16384, 8>("bulk multicast pairs 148", buf, bytes, d_out, nsm);
+    run<1, 16384, 8>("bulk pairs-same 148", buf, bytes, d_out, nsm);
     run<3, 16384, 8>("bulk all-same 148", buf, bytes, d_out, nsm);
-    run<4, 32768, 6, 256>("tensor contiguous 148", buf, bytes, d_out, nsm);
-    run<4, 32768, 6, 256>("tensor contiguous 32", buf, bytes, d_out, 32);
+    run<4, 16384, 6, 128>("tensor contiguous 148 box128", buf, bytes, d_out, nsm);
+    run<4, 32768, 6, 256>("tensor contiguous 148 box256", buf, bytes, d_out, nsm);
     return 0;
 }
