@@ -52,32 +52,42 @@
 #ifndef MOBI_X_NOEPI
 #define MOBI_X_NOEPI 0   // the epilogue releases TMEM without draining or storing
 #endif
+#ifndef MOBI_WAIT_SLEEP
+#define MOBI_WAIT_SLEEP 1
+#endif
 namespace mobi {
 int make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int64_t rows, int64_t cols,
                  int box_rows);
 namespace {
 
 using namespace sm100;
+#if MOBI_WAIT_SLEEP
+#define WAITX mbar_wait_sleep
+#else
+#define WAITX mbar_wait
+#endif
 
 constexpr int NSTAGE = 5;   // B (smem) / A (TMEM) stages
 constexpr int NCS = 4;      // code stages (smem, 2 k-blocks each), released by the dequantizers, not by the MMAs
 constexpr int kCodeKb = 2;  // k-blocks per code stage: one 16 KiB bulk copy (a row tile's k-blocks are contiguous)
 constexpr int kDqWarps = 16;
-constexpr int kThreads = 32 * (4 + kDqWarps + 4);
-constexpr int kWarpDq0 = 0, kWarpEpi0 = kDqWarps, kWarpTma = kDqWarps + 4, kWarpMma = kDqWarps + 5;
-constexpr int kWarpCode = kDqWarps + 6;  // 2 warps bulk-copy the code stages (alternating) into smem
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter (alternate 16-column chunks)
+constexpr int kThreads = 32 * (4 + kDqWarps + kEpiWarps);
+constexpr int kWarpDq0 = 0, kWarpEpi0 = kDqWarps, kWarpTma = kDqWarps + kEpiWarps, kWarpMma = kWarpTma + 1;
+constexpr int kWarpCode = kWarpTma + 2;  // 2 warps bulk-copy the code stages (alternating) into smem
 constexpr int kCodeWarps = 2;
 // dynamic unit schedule: the leader's TMA warp claims units (atomic counter, units in decreasing
 // size order) and publishes them through a small ring to every role of both CTAs
 constexpr int kURing = 4;
-constexpr int kUnitConsumers = 1 + kCodeWarps + kDqWarps + 4;  // per CTA: MMA (leader) or TMA (peer) + code + dequant + epilogue
+constexpr int kUnitConsumers = 1 + kCodeWarps + kDqWarps + kEpiWarps;  // per CTA: MMA (leader) or TMA (peer) + code + dequant + epilogue
 constexpr int kHalfRows = kTokTile / 2;                  // token rows per CTA per stage
 constexpr int kStageBytes = kHalfRows * kKBlock * 2;     // 16 KiB
 constexpr int kACol0 = 256;
 constexpr int kYStageBytes = kTokTile * kRowTile * 2;    // 64 KiB
 constexpr int kConstOff = kCodeKb * kBlockBytes;
 constexpr int kCodeStage = kConstOff + 2 * kCodeKb * kRowTile * 8;  // codes + (s, s*z) of up to 4 groups x 128 rows
-constexpr int kSmemBytes = NSTAGE * kStageBytes + 1024 + 512 + kYStageBytes + kTokTile * 4 + NCS * kCodeStage;
+// (no alignment slack: the dynamic smem base is declared 1024-aligned; checked at run time)
+constexpr int kSmemBytes = NSTAGE * kStageBytes + 512 + kYStageBytes + 2 * kTokTile * 4 + NCS * kCodeStage;
 static_assert(kSmemBytes <= 232448, "tc2 shared memory");
 static_assert(NCS % kCodeWarps == 0, "each code warp owns fixed ring slots");
 
@@ -120,36 +130,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             p.trace[24576 + (cluster_ctarank() * 8 + ev) * 16 + u] = t;
         }
     };
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
     uint8_t* stage_b = smem;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * kStageBytes);
     // one full barrier per stage, in the leader: both halves' TMA bytes (one expect_tx arrival) and the
     // 8 + 8 dequant warps of the pair (the peer's arrive remotely)
-    uint64_t* full_b = bars;                 // [NSTAGE] leader: stage complete (A in both TMEMs, B in both smems)
+    uint64_t* full_b = bars;                 // [NSTAGE] leader: B of the stage landed in both CTAs' smem (TMA)
     uint64_t* empty = bars + NSTAGE;         // [NSTAGE] each CTA: pair MMAs done with the stage
     uint64_t* acc_full = bars + 2 * NSTAGE;  // each CTA
     uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
     uint64_t* u_full = acc_empty + 1;        // [kURing] each CTA: unit slot published
     uint64_t* u_empty = u_full + kURing;     // [kURing] leader: every consumer of both CTAs read the slot
-    int32_t* uring = reinterpret_cast<int32_t*>(u_empty + kURing + 2 * NCS);  // [kURing] unit index (-1 = done)
+    int32_t* uring = reinterpret_cast<int32_t*>(u_empty + kURing + 2 * NCS + NSTAGE);  // [kURing] unit (-1 = done)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + kURing);
-    __nv_bfloat16* stage_y = reinterpret_cast<__nv_bfloat16*>(smem + NSTAGE * kStageBytes + 512);
-    int32_t* tok_src = reinterpret_cast<int32_t*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);
-    uint8_t* stage_c = smem + NSTAGE * kStageBytes + 512 + kYStageBytes + kTokTile * 4;  // [NCS][kCodeStage]
+    uint8_t* stage_y = smem + NSTAGE * kStageBytes + 512;  // [128 rows][256 tokens] bf16, 16-byte chunks swizzled
+    float* tok_es = reinterpret_cast<float*>(smem + NSTAGE * kStageBytes + 512 + kYStageBytes);  // [kTokTile]
+    int32_t* tok_src = reinterpret_cast<int32_t*>(tok_es + kTokTile);                               // [kTokTile]
+    uint8_t* stage_c = smem + NSTAGE * kStageBytes + 512 + kYStageBytes + 2 * kTokTile * 4;  // [NCS][kCodeStage]
     uint64_t* c_full = u_empty + kURing;   // [NCS] each CTA: the stage's codes + constants landed
     uint64_t* c_empty = c_full + NCS;      // [NCS] each CTA: the 8 dequant warps of its two k-blocks read them
-    auto epi_bar_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    uint64_t* full_a = c_empty + NCS;      // [NSTAGE] leader: A of the stage stored in both CTAs' TMEM
+    auto epi_bar_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); };
 
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
     const uint32_t rank = cluster_ctarank();
     if (threadIdx.x == 0) {
+        if (smem_u32(smem_raw) & 1023) __trap();  // SW128 B stages need 1024-byte alignment
         for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full_b[s], 1 + kDqWarps / 2);  // TMA expect_tx + 4 dequant warps per CTA x 2
+            mbar_init(&full_b[s], 1);             // the leader's TMA expect_tx (both CTAs' bytes)
+            mbar_init(&full_a[s], kDqWarps / 2);  // 4 dequant warps per CTA x 2
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
-        mbar_init(acc_empty, 8);  // 4 epilogue warps x 2 CTAs
+        mbar_init(acc_empty, 2 * kEpiWarps);  // every epilogue warp of both CTAs
         for (int s = 0; s < kURing; ++s) {
             mbar_init(&u_full[s], 1);
             mbar_init(&u_empty[s], 2 * kUnitConsumers);
@@ -190,7 +204,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int s = (int)(ui % kURing);
         const uint32_t ph = (ui / kURing) & 1;
         if (rank == 0)
-            mbar_wait(&u_full[s], ph);
+            WAITX(&u_full[s], ph);
         else
             mbar_wait_cluster(&u_full[s], ph);  // published by the leader's thread (remote store + release)
         const int u = *reinterpret_cast<volatile int32_t*>(&uring[s]);
@@ -247,7 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < kb_n; ++kb, ++it) {
                 const int s = it % NSTAGE;
                 const uint32_t ph = (it / NSTAGE) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
+                WAITX(&empty[s], ph ^ 1);
                 EV(0, kb, ui);
                 if (MOBI_X_NOTMA) {
                     if (elect_one_sync() && rank == 0) mbar_arrive_expect_tx(&full_b[s], 0);
@@ -270,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t it = 0;
             for (uint32_t tc = 0;; ++tc) {
                 const int s0 = (int)(tc % kURing);
-                mbar_wait(&u_full[s0], (tc / kURing) & 1);
+                WAITX(&u_full[s0], (tc / kURing) & 1);
                 const int pair = *reinterpret_cast<volatile int32_t*>(&uring[s0]);
                 mbar_arrive(&u_empty[s0]);
                 if (pair < 0) break;
@@ -283,7 +297,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 for (int kb = 0; kb < kb_n; ++kb, ++it) {
                     const uint32_t s = it % NSTAGE;
-                    mbar_wait(&full_b[s], (it / NSTAGE) & 1);
+                    WAITX(&full_a[s], (it / NSTAGE) & 1);
+                    EV(7, kb, tc);
+                    WAITX(&full_b[s], (it / NSTAGE) & 1);
                     EV(1, kb, tc);
                     tc_fence_after();
                     const uint32_t acol = kACol0 + s * 32;
@@ -317,24 +333,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int kb0 = 0; kb0 < kb_n; kb0 += kCodeKb, ++it) {
                 if ((int)(it % kCodeWarps) != warp - kWarpCode) continue;
                 const int s = (int)(it % NCS);
-                mbar_wait(&c_empty[s], ((it / NCS) & 1) ^ 1);
+                WAITX(&c_empty[s], ((it / NCS) & 1) ^ 1);
                 EV(6, kb0, ui);
+#ifndef MOBI_LANE_ISSUE
+#define MOBI_LANE_ISSUE 1
+#endif
                 if (MOBI_X_NOCODE) {
                     if (elect_one_sync()) mbar_arrive_expect_tx(&c_full[s], 0);
-                } else if (elect_one_sync()) {
+                } else {
                     uint8_t* dc = stage_c + s * kCodeStage;
                     const int nkb = min(kCodeKb, kb_n - kb0);
                     // groups of the stage's first and last 32-column chunks (gs is a multiple of 32 or >= in)
                     const int g0 = p.single_group ? 0 : (int)((uint32_t)(kb0 * kKBlock) / (uint32_t)p.gs);
                     const int g1 = p.single_group ? 0 : (int)((uint32_t)((kb0 + nkb) * kKBlock - 32) / (uint32_t)p.gs);
-                    mbar_arrive_expect_tx(&c_full[s], nkb * kBlockBytes + (uint32_t)(g1 - g0 + 1) * kRowTile * 8);
-                    bulk_g2s(dc, csrc + (int64_t)kb0 * kBlockBytes, nkb * kBlockBytes, &c_full[s]);
-                    for (int g = g0; g <= g1; ++g)
-                        bulk_g2s(dc + kConstOff + (g - g0) * kRowTile * 8, gsrc + (int64_t)g * p.out_pad, kRowTile * 8,
-                                 &c_full[s]);
+                    if (lane == 0)
+                        mbar_arrive_expect_tx(&c_full[s], nkb * kBlockBytes + (uint32_t)(g1 - g0 + 1) * kRowTile * 8);
+                    __syncwarp();
+                    if (MOBI_LANE_ISSUE) {
+                        // one instruction, one copy per lane: lane 0 the codes, lane 1 + j group g0 + j
+                        if (lane <= g1 - g0 + 1) {
+                            const bool cl = lane == 0;
+                            const int g = g0 + lane - 1;
+                            bulk_g2s(cl ? dc : dc + kConstOff + (g - g0) * kRowTile * 8,
+                                     cl ? (const void*)(csrc + (int64_t)kb0 * kBlockBytes)
+                                        : (const void*)(gsrc + (int64_t)g * p.out_pad),
+                                     cl ? nkb * kBlockBytes : kRowTile * 8, &c_full[s]);
+                        }
+                    } else if (lane == 0) {
+                        bulk_g2s(dc, csrc + (int64_t)kb0 * kBlockBytes, nkb * kBlockBytes, &c_full[s]);
+                        for (int g = g0; g <= g1; ++g)
+                            bulk_g2s(dc + kConstOff + (g - g0) * kRowTile * 8, gsrc + (int64_t)g * p.out_pad,
+                                     kRowTile * 8, &c_full[s]);
+                    }
                 }
                 __syncwarp();
-                EV(7, kb0, ui);
             }
         }
     } else if (warp < kWarpEpi0) {
@@ -351,7 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int jpar = ph4 >> 1;          // code stages j with j % 2 == jpar
         const int sub = ph4 & 1;            // k-block inside the stage
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        const uint32_t full_leader = mapa_shared(smem_u32(full_b), 0);
+        const uint32_t full_leader = mapa_shared(smem_u32(full_a), 0);
         const int c_off = sub * kBlockBytes + (32 * q + lane) * 16;  // + (h*2 + c) * kRowTile * 16
         uint32_t base = 0;   // global k-block counter at the start of the unit (A/B stage and phase)
         uint32_t cbase = 0;  // global code-stage counter at the start of the unit
@@ -372,9 +404,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             auto load = [&](int j) {
                 const uint32_t cit = cbase + j;
                 const int cs = (int)(cit % NCS);
-                mbar_wait(&c_full[cs], (cit / NCS) & 1);
+                WAITX(&c_full[cs], (cit / NCS) & 1);
                 const int kb = kCodeKb * j + sub;
-                if (warp == 0) EV(2, kb, ui);
                 if (kb < kb_n) {
                     const uint8_t* dc = stage_c + cs * kCodeStage + c_off;
 #pragma unroll
@@ -421,7 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (!valid) continue;
                 const uint32_t itk = base + kb;
                 const int s = (int)(itk % NSTAGE);
-                mbar_wait(&empty[s], ((itk / NSTAGE) & 1) ^ 1);
+                WAITX(&empty[s], ((itk / NSTAGE) & 1) ^ 1);
                 if (warp == 0) EV(4, kb, ui);
                 tc_fence_after();
                 if (!MOBI_X_NOST) {
@@ -431,9 +462,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (warp == 0) EV(5, kb, ui);
+                if (warp == 3) EV(2, kb, ui);
                 if (lane == 0) {
                     if (rank == 0)
-                        mbar_arrive_relaxed(&full_b[s]);
+                        mbar_arrive_relaxed(&full_a[s]);
                     else
                         mbar_arrive_relaxed_cluster(full_leader + s * 8);
                 }
@@ -443,28 +475,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else {
         // ---------------- epilogue ----------------
-        // drain TMEM -> (x 2^e) -> bf16 -> smem tile [token][128 rows], release the accumulator,
-        // then scatter whole 256-byte token rows into Y[perm[i]] with 16-byte stores
-        const int q = warp % 4;
-        const int et = threadIdx.x - 32 * kWarpEpi0;  // 0..127
+        // The accumulator is released as soon as it is drained into a TRANSPOSED staging tile
+        // [row][token] (each thread: its TMEM lane = weight row, 16 tokens per load, two 16-byte smem
+        // stores); the un-permute scatter of whole 256-byte token rows into Y[perm[i]] reads that tile
+        // back transposed (8 rows x 2 tokens per thread) while the next unit's MMAs run.  16-byte chunks
+        // of a row are XOR-swizzled by g(r) so both the drain stores and the scatter reads spread over
+        // the banks.
+        const int q = warp % 4;                       // TMEM lane quarter (hardware: warp id % 4)
+        const int half = (warp - kWarpEpi0) / 4;      // 16-column chunks c with c % 2 == half
+        const int et = threadIdx.x - 32 * kWarpEpi0;  // 0 .. 32*kEpiWarps-1
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+        auto swz = [](int r) { return ((r >> 3) ^ ((r & 1) << 2)) & 7; };
+        const int my_r = 32 * q + lane;
+        uint8_t* my_row = stage_y + my_r * (kTokTile * 2);
+        const int my_g = swz(my_r);
         for (uint32_t tc = 0;; ++tc) {
             const int pair = unit_get(tc);
             if (pair < 0) break;
             TokTile tt;
             int rt, nc;
             tile_of(pair, tt, rt, nc);
-            int32_t src_r[kTokTile / 32];
-            float es_r[kTokTile / 32];
-#pragma unroll
-            for (int c = 0; c < kTokTile / 32; ++c) {
-                const bool ok = 32 * c + lane < tt.n;
-                src_r[c] = ok ? __ldg(p.perm + tt.row0 + 32 * c + lane) : -1;
-                es_r[c] = ok ? __ldg(p.escale + tt.row0 + 32 * c + lane) : 0.f;
+            epi_bar_sync();  // the previous unit's scatter has finished reading the staging tile
+            for (int t = et; t < nc; t += 32 * kEpiWarps) {
+                const bool ok = t < tt.n;
+                tok_es[t] = ok ? __ldg(p.escale + tt.row0 + t) : 0.f;
+                tok_src[t] = ok ? __ldg(p.perm + tt.row0 + t) : -1;
             }
+            epi_bar_sync();
             // CTA-scope wait: the arrival is the tensor core's commit and TMEM visibility comes from
             // tcgen05.fence (a cluster-scope acquire would invalidate L1 on every poll)
-            mbar_wait(acc_full, tc & 1);
+            WAITX(acc_full, tc & 1);
             if (warp == kWarpEpi0) EVU(2, tc);
             tc_fence_after();
             if (MOBI_X_NOEPI) {
@@ -473,43 +513,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty), 0));
                 continue;
             }
-            epi_bar_sync();  // the previous tile's scatter has finished reading the staging tile
             if (warp == kWarpEpi0) EVU(5, tc);
             uint32_t va[16], vb[16];
-            tmem_ld16(tmem + lane_base, va);
+            if (16 * half < tt.n) tmem_ld16(tmem + lane_base + 16 * half, va);
 #pragma unroll
-            for (int c = 0; c < kTokTile / 16; ++c) {
+            for (int i = 0; i < kTokTile / 32; ++i) {
+                const int c = 2 * i + half;
                 const int c0 = 16 * c;
                 if (c0 >= tt.n) break;
+                if (TRACE && warp == kWarpEpi0 && lane == 0 && blockIdx.x < 2 && tc == MOBI_TRACE_UNIT)
+                    p.trace[28672 + rank * 64 + 2 * i] = (unsigned long long)clock64();
                 tmem_ld_wait();
-                uint32_t(&cur)[16] = (c & 1) ? vb : va;
-                uint32_t(&nxt)[16] = (c & 1) ? va : vb;
-                if (c0 + 16 < tt.n) tmem_ld16(tmem + lane_base + c0 + 16, nxt);
-                const float my_es = es_r[c / 2];
-                if (q == 0 && (c & 1) == 0) tok_src[c0 + lane] = src_r[c / 2];
+                if (TRACE && warp == kWarpEpi0 && lane == 0 && blockIdx.x < 2 && tc == MOBI_TRACE_UNIT)
+                    p.trace[28672 + rank * 64 + 2 * i + 1] = (unsigned long long)clock64();
+                uint32_t(&cur)[16] = (i & 1) ? vb : va;
+                uint32_t(&nxt)[16] = (i & 1) ? va : vb;
+                if (c0 + 32 < tt.n) tmem_ld16(tmem + lane_base + c0 + 32, nxt);
+                uint32_t w[8];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const float es = __shfl_sync(0xffffffffu, my_es, (c & 1) * 16 + j);
-                    stage_y[(c0 + j) * kRowTile + 32 * q + lane] = __float2bfloat16_rn(__uint_as_float(cur[j]) * es);
+                for (int j4 = 0; j4 < 4; ++j4) {
+                    const float4 es = reinterpret_cast<const float4*>(tok_es + c0)[j4];  // broadcast
+                    const __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(cur[4 * j4]) * es.x,
+                                                                    __uint_as_float(cur[4 * j4 + 1]) * es.y);
+                    const __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(cur[4 * j4 + 2]) * es.z,
+                                                                    __uint_as_float(cur[4 * j4 + 3]) * es.w);
+                    w[2 * j4] = *reinterpret_cast<const uint32_t*>(&lo);
+                    w[2 * j4 + 1] = *reinterpret_cast<const uint32_t*>(&hi);
                 }
+                const int ch = 2 * c;  // 16-byte chunk (8 tokens) index
+                *reinterpret_cast<uint4*>(my_row + ((ch ^ my_g) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(my_row + (((ch + 1) ^ my_g) << 4)) = make_uint4(w[4], w[5], w[6], w[7]);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(acc_empty), 0));  // leader's barrier
             if (warp == kWarpEpi0) EVU(3, tc);
             epi_bar_sync();  // staging tile complete
-            const int64_t r0 = (int64_t)rt * kRowTile + 8 * (et % 16);
-            for (int t = et / 16; t < tt.n; t += 8) {
-                const int32_t src = tok_src[t];
-                if (src < 0 || r0 >= p.out) continue;
-                const __nv_bfloat16* sp = stage_y + t * kRowTile + 8 * (et % 16);
-                const int64_t off = (int64_t)src * p.od.ldy + p.od.col0 + r0;
-                if (p.vec_y && r0 + 8 <= p.out) {
-                    const uint4 v = *reinterpret_cast<const uint4*>(sp);
-                    for (int k = 0; k < p.od.n_dst; ++k) *reinterpret_cast<uint4*>(p.od.dst[k] + off) = v;
-                } else {
-                    for (int k = 0; k < p.od.n_dst; ++k)
-                        for (int u = 0; u < 8 && r0 + u < p.out; ++u) p.od.dst[k][off + u] = sp[u];
+            // scatter: thread = (8-row chunk et%16, token pair); 8 four-byte reads give 8 rows x 2 tokens
+            const int rc0 = 8 * (et % 16);
+            const int64_t r0 = (int64_t)rt * kRowTile + rc0;
+            for (int t = 2 * (et / 16); t < tt.n; t += 2 * (32 * kEpiWarps / 16)) {
+                uint32_t wv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int r = rc0 + u;
+                    wv[u] = *reinterpret_cast<const uint32_t*>(stage_y + r * (kTokTile * 2) +
+                                                              (((t >> 3) ^ swz(r)) << 4) + (t & 7) * 2);
+                }
+                const uint4 y0 = make_uint4(__byte_perm(wv[0], wv[1], 0x5410), __byte_perm(wv[2], wv[3], 0x5410),
+                                            __byte_perm(wv[4], wv[5], 0x5410), __byte_perm(wv[6], wv[7], 0x5410));
+                const uint4 y1 = make_uint4(__byte_perm(wv[0], wv[1], 0x7632), __byte_perm(wv[2], wv[3], 0x7632),
+                                            __byte_perm(wv[4], wv[5], 0x7632), __byte_perm(wv[6], wv[7], 0x7632));
+                if (r0 >= p.out) continue;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (t + h >= tt.n) break;
+                    const int32_t src = tok_src[t + h];
+                    const uint4 v = h ? y1 : y0;
+                    const int64_t off = (int64_t)src * p.od.ldy + p.od.col0 + r0;
+                    if (p.vec_y && r0 + 8 <= p.out) {
+                        for (int k = 0; k < p.od.n_dst; ++k) *reinterpret_cast<uint4*>(p.od.dst[k] + off) = v;
+                    } else {
+                        const __nv_bfloat16* e8 = reinterpret_cast<const __nv_bfloat16*>(&v);
+                        for (int k = 0; k < p.od.n_dst; ++k)
+                            for (int u = 0; u < 8 && r0 + u < p.out; ++u) p.od.dst[k][off + u] = e8[u];
+                    }
                 }
             }
             if (warp == kWarpEpi0) EVU(4, tc);

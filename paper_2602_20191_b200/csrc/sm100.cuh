@@ -48,6 +48,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// wait with a suspend-time hint: the thread sleeps in the barrier unit until the phase completes (or
+// the hint expires) instead of re-issuing try_wait, so many waiting warps do not flood the MIO pipe
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@P1 bra DONES_%=;\n\t"
+        "bra WAITS_%=;\n\t"
+        "DONES_%=:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

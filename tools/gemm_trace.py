@@ -50,6 +50,10 @@ def main():
         for kb in range(24):
             print(f"{kb:2d} " + " ".join(f"{(ev[e][kb] - t0) if ev[e][kb] else -1:10d}" for e in range(4)))
     units(full)
+    ch = full[28672:28672 + 64].astype(np.int64)
+    if ch[0]:
+        print("epilogue warp 0 drain (cycles from first chunk): before wait / after wait")
+        print(" ".join(f"{int(ch[2*i]-ch[0])}/{int(ch[2*i+1]-ch[0])}" for i in range(8) if ch[2*i]))
     per = full[16 * 1024:20480].reshape(-1, 2)
     per = per[per[:, 0] > 0]
     for N in sorted(set(per[:, 0].tolist())):
@@ -71,10 +75,16 @@ def units(full):
 
 
 def timeline(full, base=20480):
+    timeline1(full, base)
+    print("peer CTA (clock of the peer SM, offset unknown):")
+    timeline1(full, base + 8 * 64)
+
+
+def timeline1(full, base):
     ev = full[base:base + 8 * 64].reshape(8, 64).astype(np.int64)
     t0 = ev[0][ev[0] > 0].min() if (ev[0] > 0).any() else 0
-    names = ["tma:empty ok", "mma:full_b ok", "dq:c_full ok", "mma:issued", "dq:empty ok", "dq:arrive-ready", "cw:c_empty ok",
-             "cw:issued"]
+    names = ["tma:empty ok", "mma:full_b ok", "dq3:arrive", "mma:issued", "dq:empty ok", "dq:arrive-ready", "cw:c_empty ok",
+             "mma:full_a ok"]
     print("kb  " + " ".join(f"{n:>14s}" for n in names))
     for kb in range(0, 24):
         print(f"{kb:2d}  " + " ".join(f"{(ev[e][kb] - t0) if ev[e][kb] else -1:14d}" for e in range(8)))
