@@ -396,13 +396,19 @@ def main_mobi(args, rank, world, local, config):
     tokens_total = T * args.steps * (1 if column else world)
     value = tokens_total / (ms / 1e3)
 
-    # which kernels the step ran (mobi_layer_last_plan) and the realized bits of the last ring entry
-    _, m = step(0, masks=True)
+    # which kernels the step ran (mobi_layer_last_plan) and the realized bits over every ring entry's
+    # tokens (decode batches of 1..32 tokens realize 2/4/6/8 bits each: the budget shows over the ring)
+    ms_all = []
+    for i in range(R):
+        _, m = step(i, masks=True)
+        ms_all.append(m)
     plan = ring[0]["layer"].last_plan() if hasattr(ring[0]["layer"], "last_plan") else \
         ring[0]["layer"].local.last_plan()
+    m = torch.cat(ms_all)
     realized = avg_bits_from_masks(m, SLICE_BITS)
     counts = torch.bincount(m.to(torch.int64), minlength=16).cpu().tolist()
     config["realized_avg_bits"] = round(realized, 4)
+    config["realized_over_tokens"] = int(m.numel())
     config["buckets"] = {str(i): c for i, c in enumerate(counts) if c}
     config["kernels"] = {k: plan[k] for k in ("router", "gemm", "gemm_ctas", "token_tiles", "units")}
 
