@@ -56,7 +56,7 @@ extern "C" {
 #define MOBI_EINVAL 1
 #define MOBI_ERUNTIME 2
 
-#define MOBI_MAX_SLICES 4 /* slice 1 + up to 3 routed residual slices -> 8 buckets */
+#define MOBI_MAX_SLICES 8 /* slice 1 + up to 7 routed residual slices (sum of widths <= 8 bits) */
 #define MOBI_MAX_DST 8    /* destinations of one output descriptor (ranks of a column-parallel layer) */
 
 typedef struct mobi_layer* mobi_layer_t;
@@ -68,7 +68,9 @@ typedef struct {
     int64_t in;         /* input dim (QuantParams::cols)                                 */
     int64_t group_size; /* qcore::kDefaultGroupSize = 128; group = r*ceil(in/gs) + c/gs   */
     int32_t n_slices;   /* E (SliceStack::num_slices), 2..MOBI_MAX_SLICES                */
-    const int32_t* slice_bits; /* [E], uniform widths, sum <= 8 (slice.bits = 2 2 2 2)  */
+    const int32_t* slice_bits; /* [E] widths >= 1, sum <= 8 (slice.bits = 2 2 2 2); uniform widths
+                                  with E <= 4 run the tcgen05 / slice-plane kernels, any other
+                                  layout the generic per-slice CUDA-core kernels */
     const double* scale; /* [out*ceil(in/gs)] base (slice-1) scales, > 0               */
     const double* zero;  /* [out*ceil(in/gs)] base (slice-1) continuous zeros          */
     /* slice payload, exactly one of: */
@@ -119,7 +121,7 @@ MOBI_API int mobi_score(mobi_layer_t layer, const void* x_bf16, int64_t T, float
 
 /* score -> gate_hard(delta) -> mask_t = 1 | sum_j 1(S[t,j]-delta>0) << (j+1) -> stable bucket
  * permutation.  All outputs device, each nullable.  perm[i] = source token of permuted row i,
- * inverse[t] = permuted row of token t; bucket_count[m] = tokens with mask m (m < 2^(E-1)*2). */
+ * inverse[t] = permuted row of token t; bucket_count[m] = tokens with mask m (m < 2^E). */
 MOBI_API int mobi_route(mobi_layer_t layer, const void* x_bf16, int64_t T, float delta, float* scores,
                uint8_t* masks, int32_t* perm, int32_t* inverse, int32_t* bucket_count,
                void* stream);
@@ -223,6 +225,7 @@ MOBI_API int mobi_layer_last_launches(mobi_layer_t layer, int32_t* launches);
 #define MOBI_K_GEMM_SPLITK 13       /* 1-CTA tcgen05 nested residual GEMM with split-K (T <= 64)     */
 #define MOBI_K_GEMM_PAIR 14         /* CTA-pair tcgen05 nested residual GEMM (prefill)              */
 #define MOBI_K_GEMM_SIMT 15         /* CUDA-core reference GEMM (test hook only)                     */
+#define MOBI_K_GEMM_GENERIC 16      /* per-slice CUDA-core GEMM: non-uniform widths or > 4 slices    */
 /* The last call's plan: plan[0] router kernel id, [1] GEMM kernel id, [2] GEMM grid (CTAs),
  * [3] kernels launched, [4] token tiles of the bucketed GEMM (-1 for the decode kernels),
  * [5] 256-row weight-tile pairs, [6] GEMM units = [4] x [5] (-1 for decode), [7] tokens.

@@ -82,6 +82,8 @@ float bf2f(uint16_t b) {
 }
 
 void free_ws(mobi_layer* L) {
+    if (L->hist256) cudaFree(L->hist256);
+    L->hist256 = nullptr;
     dfree(L->s_part);
     dfree(L->scores);
     dfree(L->masks);
@@ -155,11 +157,11 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_dev
               "mobi_layer_create: " << d->n_slices << " slices; supported 2.." << MOBI_MAX_SLICES);
     CHECK_ARG(d->slice_bits != nullptr, "decompose: slice_bits is empty");
     int total = 0;
+    bool uniform = true;
     for (int e = 0; e < d->n_slices; ++e) {
         CHECK_ARG(d->slice_bits[e] >= 1 && d->slice_bits[e] <= 8,
                   "decompose: slice bit width " << d->slice_bits[e] << " out of [1,8]");
-        CHECK_ARG(d->slice_bits[e] == d->slice_bits[0],
-                  "merged_params: slice widths must be uniform for the merged code");
+        uniform = uniform && d->slice_bits[e] == d->slice_bits[0];
         total += d->slice_bits[e];
     }
     CHECK_ARG(total <= 8, "decompose: total bits " << total << " exceed the 8-bit code budget");
@@ -173,8 +175,17 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_dev
     L->G = cdiv(d->in, d->group_size);
     L->single_group = d->group_size >= d->in;
     L->E = d->n_slices;
-    L->b = d->slice_bits[0];
+    // uniform widths with E <= 4: the folded-weight kernels (W_m = S (INT & maskbyte(m)) + C_m needs
+    // equal widths, see mobi_internal.cuh); anything else: the generic per-slice kernels (gemm_generic.cu)
+    L->generic = !uniform || d->n_slices > kFastSlices;
+    L->b = uniform ? d->slice_bits[0] : 0;
     L->nr = d->n_slices - 1;
+    L->sl.E = L->E;
+    for (int e = L->E - 1, off = 0; e >= 0; --e) {  // INT = ((c1 << b2 | c2) << b3 | c3) ...
+        L->sl.b[e] = d->slice_bits[e];
+        L->sl.off[e] = off;
+        off += d->slice_bits[e];
+    }
     const int64_t ng = L->out * L->G;
     for (int64_t g = 0; g < ng; ++g) {
         CHECK_ARG(std::isfinite(d->scale[g]) && d->scale[g] > 0.0, "QuantParams: non-positive scale at group " << g);
@@ -183,15 +194,16 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_dev
     CHECK_ARG((d->codes != nullptr) != (d->planes != nullptr),
               "mobi_layer_create: give exactly one of codes (SliceStack) or planes (LayerRecord)");
     if (d->codes && !codes_on_device) {
-        const int qmax = (1 << L->b) - 1;
         const int64_t n = L->out * L->in;
-        for (int e = 0; e < L->E; ++e)
+        for (int e = 0; e < L->E; ++e) {
+            const int qmax = (1 << L->sl.b[e]) - 1;
             for (int64_t i = 0; i < n; ++i)
                 if (d->codes[(int64_t)e * n + i] > qmax)
                     return set_error(MOBI_EINVAL, "dequantize_centered: code " + std::to_string(d->codes[e * n + i]) +
                                                       " out of [0," + std::to_string(qmax) + "] at (" +
                                                       std::to_string(i / L->in) + "," + std::to_string(i % L->in) +
                                                       ")");
+        }
     } else if (!d->codes) {
         CHECK_ARG(d->plane_bits == total, "bitplane: planes carry " << d->plane_bits << " bits, slices need " << total);
         CHECK_ARG(d->words_per_row == cdiv(d->in, 64),
@@ -204,6 +216,7 @@ int validate_and_fill(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_dev
     L->in_pad = round_up(L->in, kKBlock);
     L->kblocks = L->in_pad / kKBlock;
     L->h_pad = round_up(L->h, 128);
+    if (L->generic) return MOBI_OK;
     // per-mask dequant constants (uniform b-bit slices, see mobi_internal.cuh)
     const int P = (L->E - 1) * L->b;
     const unsigned fm = (1u << L->b) - 1u;
@@ -228,13 +241,14 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_device =
     // weights: tiled merged codes (repacked on the device)
     if ((rc = dmalloc(&L->codes8, (size_t)(L->out_pad * L->in_pad), L))) return rc;
     if (d->codes && codes_on_device) {
-        int64_t bad = -1;
-        if ((rc = check_codes_device(d->codes, (int64_t)L->E * L->out * L->in, (1 << L->b) - 1, &bad))) return rc;
-        if (bad >= 0) {
-            const int64_t i = bad % (L->out * L->in);
-            return set_error(MOBI_EINVAL, "dequantize_centered: code out of [0," + std::to_string((1 << L->b) - 1) +
-                                              "] at (" + std::to_string(i / L->in) + "," + std::to_string(i % L->in) +
-                                              ")");
+        const int64_t n = L->out * L->in;
+        for (int e = 0; e < L->E; ++e) {
+            int64_t bad = -1;
+            const int qmax = (1 << L->sl.b[e]) - 1;
+            if ((rc = check_codes_device(d->codes + (int64_t)e * n, n, qmax, &bad))) return rc;
+            if (bad >= 0)
+                return set_error(MOBI_EINVAL, "dequantize_centered: code out of [0," + std::to_string(qmax) + "] at (" +
+                                                  std::to_string(bad / L->in) + "," + std::to_string(bad % L->in) + ")");
         }
         rc = launch_pack_codes(L, d->codes, 0);
         cudaDeviceSynchronize();
@@ -259,7 +273,7 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_device =
         if (rc) return rc;
     }
     // decode slice planes (2-bit slices only): the decode GEMV streams just the slices a batch uses
-    if (L->b == 2) {
+    if (L->b == 2 && !L->generic) {
         if ((rc = dmalloc(&L->dplanes, (size_t)(L->E * (L->out_pad / 32) * L->kblocks * 512), L))) return rc;
         if ((rc = launch_pack_dplanes(L, 0))) return rc;
         MOBI_CUDA(cudaDeviceSynchronize());
@@ -301,6 +315,7 @@ int upload_layer(const mobi_layer_desc* d, mobi_layer* L, bool codes_on_device =
 int route_scores(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float delta, float* scores_out, uint8_t* masks_out,
                  bool* masks_ready, cudaStream_t st, bool fuse_bucket = false) {
     *masks_ready = false;
+    if (L->generic) return launch_router(L, x, T, st);  // more than 3 routed scores: CUDA-core router
     if (L->impl == 7 && router_tc_supported(L, x)) {  // traced router (development hook)
         static unsigned long long* tbuf = nullptr;
         if (!tbuf) MOBI_CUDA(cudaMalloc(&tbuf, (16 * 1024 + 16 * 1024) * sizeof(unsigned long long)));
@@ -333,6 +348,7 @@ mobi_layer* new_context(mobi_layer* H, void* stream) {
     c->n_sm = H->n_sm;
     c->out = H->out, c->in = H->in, c->gs = H->gs, c->G = H->G;
     c->E = H->E, c->b = H->b, c->nr = H->nr, c->h = H->h;
+    c->generic = H->generic, c->sl = H->sl;
     c->out_pad = H->out_pad, c->in_pad = H->in_pad, c->kblocks = H->kblocks, c->h_pad = H->h_pad;
     c->group_shift = H->group_shift;
     c->single_group = H->single_group;
@@ -443,7 +459,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
               "mobi_out_desc: columns [" << od->col0 << "," << od->col0 + L->out << ") exceed ldy " << od->ldy);
     for (int k = 0; k < od->n_dst; ++k) CHECK_ARG(od->dst[k], "mobi_out_desc: null destination " << k);
     const int64_t Tp = std::max(T, L->plan_T);
-    const bool pair = L->impl == 0 && !decode_supported(L, x, Tp) && Tp > 64;
+    const bool pair = L->impl == 0 && !L->generic && !decode_supported(L, x, Tp) && Tp > 64;
     if (pair) {
         L->od = *od;
         const int rc = run_layer_y(L, x, T, delta, given_masks, nullptr, masks_out, st);
@@ -473,6 +489,20 @@ int run_layer_y(mobi_layer* L, const void* x, int64_t T, float delta, const uint
     int rc;
     if ((rc = ensure_ws(L, T))) return rc;
     const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+    if (L->generic) {  // non-uniform widths / more than 4 slices: router -> masks -> per-slice GEMM
+        if (!given_masks) {
+            ProfScope p(L, 0, st);
+            if ((rc = launch_router(L, xb, T, st))) return rc;
+        }
+        {
+            ProfScope p(L, 1, st);
+            if ((rc = launch_bucket_generic(L, T, delta, given_masks, nullptr, masks_out, nullptr, nullptr, nullptr, st,
+                                            given_masks != nullptr)))
+                return rc;
+        }
+        ProfScope p(L, 3, st);
+        return launch_gemm_generic(L, xb, T, L->masks, reinterpret_cast<__nv_bfloat16*>(y), st);
+    }
     // kernel choices follow the plan size (the whole batch when mobi_forward_host runs it in chunks)
     const int64_t Tp = std::max(T, L->plan_T);
     if ((L->impl == 0 || L->impl == 6 || L->impl == 9) && decode_supported(L, x, Tp)) {
@@ -768,7 +798,10 @@ int mobi_score(mobi_layer_t H, const void* x, int64_t T, float* scores, void* st
     bool ready = false;
     if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, INFINITY, scores, nullptr, &ready, S(stream))))
         return rc;
-    if (!ready) rc = launch_bucket(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream));
+    if (L->generic)
+        rc = launch_bucket_generic(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream), false);
+    else if (!ready)
+        rc = launch_bucket(L, T, INFINITY, nullptr, scores, nullptr, nullptr, nullptr, nullptr, S(stream));
     cs.publish(H);
     return rc;
 }
@@ -787,6 +820,11 @@ int mobi_route(mobi_layer_t H, const void* x, int64_t T, float delta, float* sco
     bool ready = false;
     if ((rc = route_scores(L, reinterpret_cast<const __nv_bfloat16*>(x), T, delta, scores, masks, &ready, S(stream))))
         return rc;
+    if (L->generic) {
+        rc = launch_bucket_generic(L, T, delta, nullptr, scores, masks, perm, inverse, bucket_count, S(stream), false);
+        cs.publish(H);
+        return rc;
+    }
     rc = launch_bucket(L, T, delta, ready ? L->masks : nullptr, ready ? nullptr : scores, ready ? nullptr : masks, perm,
                        inverse, bucket_count, S(stream), !ready);
     cs.publish(H);

@@ -325,6 +325,25 @@ int launch_bucket(mobi_layer* L, int64_t T, float delta, const uint8_t* given_ma
     return MOBI_OK;
 }
 
+int launch_bucket_generic(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks, float* scores_out,
+                          uint8_t* masks_out, int32_t* cperm_out, int32_t* inverse_out, int32_t* counts_out,
+                          cudaStream_t st, bool sanitize) {
+    // every mask value (up to 2^8) is a key; counts land in a 256-entry scratch, 2^E are returned
+    int32_t* counts = nullptr;
+    if (counts_out) {
+        if (!L->hist256) MOBI_CUDA(cudaMalloc(&L->hist256, 256 * sizeof(int32_t)));
+        counts = L->hist256;
+    }
+    bucket_kernel<NKEY_ALL><<<1, BK_THREADS, 0, st>>>(L->s_part, (int)L->htiles, T, L->nr, L->b2, delta, given_masks,
+                                                      sanitize ? 1 : 0, scores_out, L->masks, masks_out, nullptr, 0,
+                                                      cperm_out, inverse_out, counts, nullptr, nullptr, nullptr);
+    MOBI_LAUNCH_CHECK();
+    ++L->last_launches;
+    if (counts_out)
+        MOBI_CUDA(cudaMemcpyAsync(counts_out, counts, sizeof(int32_t) * ((size_t)1 << L->E), cudaMemcpyDeviceToDevice, st));
+    return MOBI_OK;
+}
+
 int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* cperm, int32_t* inverse,
                    int32_t* hist256, cudaStream_t st) {
     bucket_kernel<NKEY_ALL><<<1, BK_THREADS, 0, st>>>(nullptr, 0, T, 0, nullptr, 0.f, masks, 0, nullptr, keys_tmp,

@@ -133,7 +133,7 @@ __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWar
     __shared__ float red[kRdWarps][kRdRows][8 * NT + 1];
     __shared__ float hsum[8 * NT][kRdRows];
     __shared__ float act[8 * NT][kRdRows];
-    __shared__ float sb1[kRdRows], sw2[kRdRows * (MOBI_MAX_SLICES - 1)];
+    __shared__ float sb1[kRdRows], sw2[kRdRows * (kFastSlices - 1)];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, c = lane & 3;
     const uint32_t rank = cluster_ctarank();
     const int mt = blockIdx.x / kRdCluster;
@@ -311,7 +311,7 @@ template <int MAXT>
 __global__ void __launch_bounds__(kDecThreads, 1) decode_gemm_kernel(const __grid_constant__ DParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ float s_escale[kDecMaxT + 1];
-    __shared__ float s_score[kDecMaxT][MOBI_MAX_SLICES - 1];
+    __shared__ float s_score[kDecMaxT][kFastSlices - 1];
     __shared__ int s_mask[kDecMaxT];
     __shared__ int s_tmask[MAXT], s_ttok[MAXT][8];
     __shared__ int s_ntiles, s_flag;
@@ -699,7 +699,7 @@ __host__ __device__ inline FmaSmem fma_smem(int T, int len_max) {
 template <int NT>
 __global__ void __launch_bounds__(kFmaThreads, kFmaCps) decode_fma_kernel(const __grid_constant__ DParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ float s_score[kDecMaxT][MOBI_MAX_SLICES - 1];
+    __shared__ float s_score[kDecMaxT][kFastSlices - 1];
     __shared__ int s_mask[kDecMaxT];
     __shared__ float red[kFmaParts - 1][NT][kRowTile];
     __shared__ int s_flag;
@@ -1025,7 +1025,7 @@ int launch_decode_gemm_t(mobi_layer* L, const DParams& p, size_t smem, bool pdl,
 }  // namespace
 
 bool decode_supported(const mobi_layer* L, const void* x, int64_t T) {
-    if (T < 1 || T > kDecMaxT) return false;
+    if (L->generic || T < 1 || T > kDecMaxT) return false;
     if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
     if (!L->single_group && L->gs % kKBlock != 0) return false;
     return plan_decode(L, T).smem <= kDecSmemMax;

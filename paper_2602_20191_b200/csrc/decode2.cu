@@ -107,7 +107,7 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
     float2* xsum = reinterpret_cast<float2*>(smem + (size_t)(p.T + 1) * p.xs_stride * 2);  // rows 0..T-1 + zeros
     float* red = reinterpret_cast<float*>(smem);  // [warps][kD2Acc][32], aliases x16 after the passes
     __shared__ float es_s[kD2Warps][8 * NG];
-    __shared__ float s_score[8 * NG][MOBI_MAX_SLICES - 1];
+    __shared__ float s_score[8 * NG][kFastSlices - 1];
     __shared__ int s_mask[8 * NG];
     const int tid = threadIdx.x, warp = warp_idx_uniform(), lane = tid & 31;
     float2* gcs = reinterpret_cast<float2*>(smem + p.gcs_off) + (size_t)warp * p.gpw * 32;  // [groups][32 rows]

@@ -40,7 +40,7 @@ __global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int6
     const double z1 = __ddiv_rn(-lo, s);
     scale[gi] = s;
     zero[gi] = z1;
-    unsigned long long cl[MOBI_MAX_SLICES] = {0, 0, 0, 0};
+    unsigned long long cl[MOBI_MAX_SLICES] = {};
     for (int64_t c = c0; c < c1; ++c) {
         double v = row[c];
         int bb = 0;

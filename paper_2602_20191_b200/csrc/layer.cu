@@ -13,7 +13,7 @@ namespace {
 
 // one thread = one (row, 16-column chunk): merge E slice codes, store 16 bytes
 __global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, int64_t out, int64_t in,
-                                  int64_t out_pad, int64_t kblocks, int E, int b,
+                                  int64_t out_pad, int64_t kblocks, SliceLayout sl,
                                   uint8_t* __restrict__ dst) {
     const int64_t nchunks = kblocks * (kKBlock / 16);
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -26,7 +26,7 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ codes, int64_t out
         const int64_t k = k0 + j;
         unsigned m = 0;
         if (R < out && k < in) {
-            for (int e = 0; e < E; ++e) m = (m << b) | codes[(int64_t)e * out * in + R * in + k];
+            for (int e = 0; e < sl.E; ++e) m |= (unsigned)codes[(int64_t)e * out * in + R * in + k] << sl.off[e];
         }
         v[j] = (uint8_t)m;
     }
@@ -64,7 +64,7 @@ __global__ void pack_planes_kernel(const uint64_t* __restrict__ planes, int bits
 
 // K6: tiled merged codes -> slice codes [E][out][in]  (LayerRecord::stack() split)
 __global__ void unpack_codes_kernel(const uint8_t* __restrict__ src, int64_t out, int64_t in,
-                                    int64_t kblocks, int E, int b, uint8_t* __restrict__ codes) {
+                                    int64_t kblocks, SliceLayout sl, uint8_t* __restrict__ codes) {
     const int64_t nchunks = kblocks * (kKBlock / 16);
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= out * nchunks) return;
@@ -72,12 +72,11 @@ __global__ void unpack_codes_kernel(const uint8_t* __restrict__ src, int64_t out
     uint4 q = *reinterpret_cast<const uint4*>(src + code_offset(R, k0, kblocks));
     uint8_t v[16];
     memcpy(v, &q, 16);
-    const unsigned fm = (1u << b) - 1u;
     for (int j = 0; j < 16; ++j) {
         const int64_t k = k0 + j;
         if (k >= in) break;
-        for (int e = 0; e < E; ++e)
-            codes[(int64_t)e * out * in + R * in + k] = (uint8_t)((v[j] >> ((E - 1 - e) * b)) & fm);
+        for (int e = 0; e < sl.E; ++e)
+            codes[(int64_t)e * out * in + R * in + k] = (uint8_t)((v[j] >> sl.off[e]) & ((1u << sl.b[e]) - 1u));
     }
 }
 
@@ -149,7 +148,7 @@ int launch_pack_dplanes(mobi_layer* L, cudaStream_t st) {
 int launch_pack_codes(mobi_layer* L, const uint8_t* codes_dev, cudaStream_t st) {
     const int64_t n = L->out_pad * L->kblocks * (kKBlock / 16);
     pack_codes_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(codes_dev, L->out, L->in, L->out_pad,
-                                                             L->kblocks, L->E, L->b, L->codes8);
+                                                             L->kblocks, L->sl, L->codes8);
     MOBI_LAUNCH_CHECK();
     return MOBI_OK;
 }
@@ -166,7 +165,7 @@ int launch_pack_planes(mobi_layer* L, const uint64_t* planes_dev, int bits, int6
 int launch_unpack_codes(const mobi_layer* L, uint8_t* codes_dev, cudaStream_t st) {
     const int64_t n = L->out * L->kblocks * (kKBlock / 16);
     unpack_codes_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(L->codes8, L->out, L->in, L->kblocks,
-                                                               L->E, L->b, codes_dev);
+                                                               L->sl, codes_dev);
     MOBI_LAUNCH_CHECK();
     return MOBI_OK;
 }

@@ -31,7 +31,8 @@ constexpr int kKBlock = 64;
 constexpr int kBlockBytes = kRowTile * kKBlock;  // 8192
 constexpr int kBucketAlign = 16;                 // bucket starts in the permuted token order
 constexpr int kTokTile = 256;                    // tokens per GEMM tile (MMA N <= 256)
-constexpr int kMaxBuckets = 1 << (MOBI_MAX_SLICES - 1);  // 8 masks (slice-1 bit always set)
+constexpr int kFastSlices = 4;  // uniform-width layers up to 4 slices take the tcgen05 / slice-plane paths
+constexpr int kMaxBuckets = 1 << (kFastSlices - 1);  // 8 masks (slice-1 bit always set)
 constexpr int kDecMaxT = 32;                     // decode path (decode.cu): up to 32 tokens per call
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -83,11 +84,24 @@ struct MaskTable {
 
 }  // namespace mobi
 
+namespace mobi {
+// Bit layout of the merged code INT = ((c1 << b2 | c2) << b3 | c3) ... (slicer.hpp:150-161) for any
+// widths: slice e (0-based) occupies bits [off[e], off[e] + b[e]).
+struct SliceLayout {
+    int E;
+    int b[MOBI_MAX_SLICES];
+    int off[MOBI_MAX_SLICES];
+};
+}  // namespace mobi
+
 struct mobi_layer {
     int device = 0;
     int n_sm = 148;                          // SMs of `device` (grid sizing)
     int64_t out = 0, in = 0, gs = 0, G = 0;  // G = groups per row
-    int32_t E = 0, b = 0;                    // slices, bits per slice
+    int32_t E = 0, b = 0;                    // slices, bits per slice (0: non-uniform widths)
+    bool generic = false;                    // non-uniform widths or E > kFastSlices: per-slice CUDA-core path
+    mobi::SliceLayout sl{};
+    int32_t* hist256 = nullptr;              // generic layers: per-mask counts scratch (mobi_route)
     int32_t nr = 0;                          // routed slices = E-1
     int64_t h = 0;                           // router hidden
     int64_t out_pad = 0, in_pad = 0, kblocks = 0, h_pad = 0;
@@ -235,6 +249,13 @@ int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t
 int launch_gemm_tc(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st,
                    unsigned long long* trace = nullptr);
 int launch_gemm_simt(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st);
+// generic slice layouts (non-uniform widths, E > kFastSlices): per-slice CUDA-core GEMM on the
+// original token order, and the mask decision / stable permutation over all 2^E keys
+int launch_gemm_generic(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* masks, __nv_bfloat16* y,
+                        cudaStream_t st);
+int launch_bucket_generic(mobi_layer* L, int64_t T, float delta, const uint8_t* given_masks, float* scores_out,
+                          uint8_t* masks_out, int32_t* cperm_out, int32_t* inverse_out, int32_t* counts_out,
+                          cudaStream_t st, bool sanitize);
 int launch_gemm_tc2(mobi_layer* L, __nv_bfloat16* y, int64_t T, cudaStream_t st, unsigned long long* trace = nullptr,
                     bool pdl = false);  // gemm_tc2.cu (CTA pairs)
 // decode.cu (T <= kDecMaxT: router GEMV + stream-K decode GEMM, PDL-chained)

@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
             if (t < p.T) {
 #pragma unroll
-                for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
+                for (int k = 0; k < kFastSlices - 1; ++k)
                     if (k < p.nr) p.s_part[((int64_t)nt * p.T + t) * p.nr + k] = part[k];
             }
             // last hidden tile of token tile mt: scores and slice masks for its tokens
@@ -514,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
                                    part2 + s_pp[32 * q + lane][2]};
             if (t < p.T) {
 #pragma unroll
-                for (int k = 0; k < MOBI_MAX_SLICES - 1; ++k)
+                for (int k = 0; k < kFastSlices - 1; ++k)
                     if (k < p.nr) p.s_part[((int64_t)nt * p.T + t) * p.nr + k] = part[k];
             }
             // last hidden tile of token tile mt: scores and slice masks for its tokens
@@ -565,7 +565,7 @@ __global__ void __launch_bounds__(RN) router_reduce_kernel(const float* __restri
                                                            int64_t h, int64_t h_pad, const float* __restrict__ b1,
                                                            const float* __restrict__ w2, int nr,
                                                            float* __restrict__ s_part) {
-    __shared__ float red[MOBI_MAX_SLICES - 1][RN];
+    __shared__ float red[kFastSlices - 1][RN];
     const int64_t t = blockIdx.x;
     const int nt = blockIdx.y;
     const int64_t j = (int64_t)nt * RN + threadIdx.x;
@@ -591,7 +591,7 @@ __global__ void __launch_bounds__(RN) router_reduce_kernel(const float* __restri
 }  // namespace
 
 bool router_tc_supported(const mobi_layer* L, const void* x) {
-    return (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    return !L->generic && (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
 }
 
 // Launch with programmatic stream serialization (PDL) and, when cluster > 0, a runtime cluster size.

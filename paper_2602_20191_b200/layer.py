@@ -154,7 +154,7 @@ class MobiLayer:
 
     KERNEL_IDS = {0: None, 1: "router_dec", 2: "router_tc", 3: "router_tc_cluster", 4: "router_tc_splitk",
                   5: "router_pair128", 6: "router_pair256", 7: "router_simt", 11: "decode_planes",
-                  12: "decode_merged", 13: "gemm_splitk", 14: "gemm_pair", 15: "gemm_simt"}
+                  12: "decode_merged", 13: "gemm_splitk", 14: "gemm_pair", 15: "gemm_simt", 16: "gemm_generic"}
 
     def last_plan(self) -> dict:
         """Kernels the last call on this layer ran (mobi_layer_last_plan): router / GEMM kernel names,
@@ -219,7 +219,7 @@ class MobiLayer:
         m = torch.empty(T, dtype=torch.uint8, device=dev)
         perm = torch.empty(T, dtype=torch.int32, device=dev)
         inv = torch.empty(T, dtype=torch.int32, device=dev)
-        cnt = torch.zeros(16, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(1 << len(self.slice_bits), dtype=torch.int32, device=dev)  # bucket_count[m], m < 2^E
         check(lib().mobi_route(self._h, x.data_ptr(), T, float(delta), s.data_ptr(), m.data_ptr(), perm.data_ptr(),
                                inv.data_ptr(), cnt.data_ptr(), _stream_ptr(stream)))
         return s, m, perm, inv, cnt
