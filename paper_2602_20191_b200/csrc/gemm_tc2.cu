@@ -448,27 +448,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // the stage's data is in registers (consumed above): release the slot to the code warp
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&c_empty[(cbase + j) % NCS]);
-                if (j + 2 < ncs_u) load(j + 2);  // smem latency overlaps the TMEM store below
-                if (!valid) continue;
-                const uint32_t itk = base + kb;
-                const int s = (int)(itk % NSTAGE);
-                WAITX(&empty[s], ((itk / NSTAGE) & 1) ^ 1);
-                if (warp == 0) EV(4, kb, ui);
-                tc_fence_after();
-                if (!MOBI_X_NOST) {
-                    tmem_st32(tmem + lane_base + kACol0 + s * 32, v);
-                    tmem_st_wait();
+                if (valid) {
+                    const uint32_t itk = base + kb;
+                    const int s = (int)(itk % NSTAGE);
+                    WAITX(&empty[s], ((itk / NSTAGE) & 1) ^ 1);
+                    if (warp == 0) EV(4, kb, ui);
+                    tc_fence_after();
+                    if (!MOBI_X_NOST) {
+                        tmem_st32(tmem + lane_base + kACol0 + s * 32, v);
+                        tmem_st_wait();
+                    }
+                    tc_fence_before();
+                    __syncwarp();
+                    if (warp == 0) EV(5, kb, ui);
+                    if (warp == 3) EV(2, kb, ui);
+                    if (lane == 0) {
+                        if (rank == 0)
+                            mbar_arrive_relaxed(&full_a[s]);
+                        else
+                            mbar_arrive_relaxed_cluster(full_leader + s * 8);
+                    }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (warp == 0) EV(5, kb, ui);
-                if (warp == 3) EV(2, kb, ui);
-                if (lane == 0) {
-                    if (rank == 0)
-                        mbar_arrive_relaxed(&full_a[s]);
-                    else
-                        mbar_arrive_relaxed_cluster(full_leader + s * 8);
-                }
+                // the next code stage only after this k-block's A is in TMEM: a late code copy must not
+                // hold back the MMAs of the stage already dequantized
+                if (j + 2 < ncs_u) load(j + 2);
             }
             base += kb_n;
             cbase += ncs_u;
@@ -485,7 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int half = (warp - kWarpEpi0) / 4;      // 16-column chunks c with c % 2 == half
         const int et = threadIdx.x - 32 * kWarpEpi0;  // 0 .. 32*kEpiWarps-1
         const uint32_t lane_base = (uint32_t)(32 * q) << 16;
-        auto swz = [](int r) { return ((r >> 3) ^ ((r & 1) << 2)) & 7; };
+        auto swz = [](int r) { return (r ^ (r >> 3)) & 7; };
         const int my_r = 32 * q + lane;
         uint8_t* my_row = stage_y + my_r * (kTokTile * 2);
         const int my_g = swz(my_r);
@@ -529,16 +532,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 uint32_t(&cur)[16] = (i & 1) ? vb : va;
                 uint32_t(&nxt)[16] = (i & 1) ? va : vb;
                 if (c0 + 32 < tt.n) tmem_ld16(tmem + lane_base + c0 + 32, nxt);
+                // bf16 of the raw accumulator; the token's 2^e comes in the scatter (a power-of-two
+                // scale of a bf16 value is exact, so the result equals rounding acc * 2^e)
                 uint32_t w[8];
 #pragma unroll
-                for (int j4 = 0; j4 < 4; ++j4) {
-                    const float4 es = reinterpret_cast<const float4*>(tok_es + c0)[j4];  // broadcast
-                    const __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(cur[4 * j4]) * es.x,
-                                                                    __uint_as_float(cur[4 * j4 + 1]) * es.y);
-                    const __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(cur[4 * j4 + 2]) * es.z,
-                                                                    __uint_as_float(cur[4 * j4 + 3]) * es.w);
-                    w[2 * j4] = *reinterpret_cast<const uint32_t*>(&lo);
-                    w[2 * j4 + 1] = *reinterpret_cast<const uint32_t*>(&hi);
+                for (int j2 = 0; j2 < 8; ++j2) {
+                    const __nv_bfloat162 h2 =
+                        __floats2bfloat162_rn(__uint_as_float(cur[2 * j2]), __uint_as_float(cur[2 * j2 + 1]));
+                    w[j2] = *reinterpret_cast<const uint32_t*>(&h2);
                 }
                 const int ch = 2 * c;  // 16-byte chunk (8 tokens) index
                 *reinterpret_cast<uint4*>(my_row + ((ch ^ my_g) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
@@ -560,10 +561,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     wv[u] = *reinterpret_cast<const uint32_t*>(stage_y + r * (kTokTile * 2) +
                                                               (((t >> 3) ^ swz(r)) << 4) + (t & 7) * 2);
                 }
-                const uint4 y0 = make_uint4(__byte_perm(wv[0], wv[1], 0x5410), __byte_perm(wv[2], wv[3], 0x5410),
-                                            __byte_perm(wv[4], wv[5], 0x5410), __byte_perm(wv[6], wv[7], 0x5410));
-                const uint4 y1 = make_uint4(__byte_perm(wv[0], wv[1], 0x7632), __byte_perm(wv[2], wv[3], 0x7632),
-                                            __byte_perm(wv[4], wv[5], 0x7632), __byte_perm(wv[6], wv[7], 0x7632));
+                // token t: the low halves (x 2^e of t), token t+1: the high halves (x 2^e of t+1), in fp32
+                const float e0 = tok_es[t], e1 = tok_es[t + 1];
+                uint32_t o0[4], o1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t a = wv[2 * u], b = wv[2 * u + 1];  // rows 2u, 2u+1: (t, t+1) each
+                    const __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(a << 16) * e0,
+                                                                    __uint_as_float(b << 16) * e0);
+                    const __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(a & 0xffff0000u) * e1,
+                                                                    __uint_as_float(b & 0xffff0000u) * e1);
+                    o0[u] = *reinterpret_cast<const uint32_t*>(&lo);
+                    o1[u] = *reinterpret_cast<const uint32_t*>(&hi);
+                }
+                const uint4 y0 = make_uint4(o0[0], o0[1], o0[2], o0[3]);
+                const uint4 y1 = make_uint4(o1[0], o1[1], o1[2], o1[3]);
                 if (r0 >= p.out) continue;
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {

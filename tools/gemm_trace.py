@@ -26,7 +26,10 @@ def main():
     import os
     impl = int(os.environ.get("MOBI_TRACE_IMPL", "2"))
     layer.set_debug_impl(impl)
-    layer.forward(x, delta)
+    if os.environ.get("MOBI_TRACE_MASK1"):  # one bucket (every token slice 1 only): forward_masked
+        layer.forward_masked(x, torch.ones(x.shape[0], dtype=torch.uint8, device=dev))
+    else:
+        layer.forward(x, delta)
     torch.cuda.synchronize()
     layer.set_debug_impl(0)
     n = torch.cuda.get_device_properties(0).multi_processor_count
