@@ -13,7 +13,9 @@
 //
 // gather_kernel: one CTA per token copies X[t] (bf16) into xperm[pinv[t]] (fp16) scaled
 // by a per-row power of two 2^-e (max|x| lands in [2^14, 2^15)); the GEMM epilogue multiplies
-// by 2^e.  The scaling is exact, so fp16 operands lose nothing against the bf16 input.
+// by 2^e.  The scaling is exact for every element within 2^29 of the row's maximum (fp16's normal
+// range below 2^15); smaller elements become fp16 subnormals or zero, a perturbation below 2^-24 of the
+// row's largest term.
 #include "mobi_internal.cuh"
 #include "sm100.cuh"
 
