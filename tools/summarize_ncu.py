@@ -63,7 +63,17 @@ def launches(path):
         lines = [l for l in f if l.startswith('"')]
     for r in csv.DictReader(io.StringIO("".join(lines))):
         if r.get("Metric Name") == "gpu__time_duration.sum":
-            name = r["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "")
+            full = r["Kernel Name"].replace("<unnamed>", "").replace("(anonymous namespace)", "")
+            head = full.split("(")[0]
+            depth, base = 0, ""
+            for ch in head:  # drop template arguments, keep the last name component
+                if ch == "<":
+                    depth += 1
+                elif ch == ">":
+                    depth -= 1
+                elif depth == 0:
+                    base += ch
+            name = base.replace("void ", "").strip().split("::")[-1]
             per[name].append(float(r["Metric Value"]) * (1e-3 if r["Metric Unit"] == "ns" else 1.0))
     tot = sum(sum(v) for v in per.values()) or 1.0
     return {k: {"launches": len(v), "us_total": round(sum(v), 2), "us_mean": round(sum(v) / len(v), 2),
