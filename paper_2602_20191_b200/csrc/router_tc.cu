@@ -350,7 +350,9 @@ __global__ void __launch_bounds__(kRThreads, 1) router_tc_kernel(const __grid_co
 // tiles sit at the measured ~71 B/cycle/SM L2->SMEM limit.  The leader's MMA thread issues for the
 // pair; both CTAs run the same fused SiLU.w2 / gate / histogram epilogue on their own tokens.
 // 8 epilogue warps (two per TMEM lane quarter, each taking half of the tile's hidden units), TMA, MMA
-constexpr int k2WarpTma = 8, k2WarpMma = 9, k2Threads = 320;
+// two TMA warps (X and w1): one thread issues a TMA about every 250-430 cycles, the pair's MMAs for a
+// k-block take 256 (N = 128)
+constexpr int k2WarpTma = 8, k2WarpMma = 9, k2WarpTmaB = 10, k2Threads = 352;
 template <int PN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
     router_tc2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -407,7 +409,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
         mp = pair % n_mp;
         nt = pair / n_mp;
     };
-    if (warp == k2WarpTma) {
+    if (warp == k2WarpTma || warp == k2WarpTmaB) {
+        // X rows (warp k2WarpTma, which also posts the stage's expected bytes) and w1 rows (k2WarpTmaB)
+        // of every stage; a w1 box may land before the expect_tx (the tx-count goes transiently negative)
+        const bool xw = warp == k2WarpTma;
         const uint32_t full_leader = mapa_shared(smem_u32(full), 0);
         uint32_t it = 0;
         for (int pair = cid; pair < total; pair += ncl) {
@@ -418,10 +423,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(k2Threads, 1)
                 mbar_wait(&empty[s], ((it / NS) & 1) ^ 1);
                 if (elect_one_sync()) {
                     uint8_t* a = smem + s * kStg;
-                    if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * kStg);
-                    tma_load_2d_2sm(a, &tmap_a, full_leader + s * 8, kb * kKBlock, (2 * mp + (int)rank) * RM);
-                    tma_load_2d_2sm(a + kAB, &tmap_b, full_leader + s * 8, kb * kKBlock,
-                                    nt * PN + (int)rank * (PN / 2));
+                    if (xw) {
+                        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * kStg);
+                        tma_load_2d_2sm(a, &tmap_a, full_leader + s * 8, kb * kKBlock, (2 * mp + (int)rank) * RM);
+                    } else {
+                        tma_load_2d_2sm(a + kAB, &tmap_b, full_leader + s * 8, kb * kKBlock,
+                                        nt * PN + (int)rank * (PN / 2));
+                    }
                 }
                 __syncwarp();
             }
