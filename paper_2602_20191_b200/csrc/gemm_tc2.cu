@@ -136,7 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * kStageBytes);
     // one full barrier per stage, in the leader: both halves' TMA bytes (one expect_tx arrival) and the
     // 8 + 8 dequant warps of the pair (the peer's arrive remotely)
-    uint64_t* full_b = bars;                 // [NSTAGE] leader: B of the stage landed in both CTAs' smem (TMA)
+    uint64_t* full_b = bars;                 // [NSTAGE] leader: B in both CTAs' smem (TMA bytes) + A in both TMEMs
     uint64_t* empty = bars + NSTAGE;         // [NSTAGE] each CTA: pair MMAs done with the stage
     uint64_t* acc_full = bars + 2 * NSTAGE;  // each CTA
     uint64_t* acc_empty = acc_full + 1;      // leader: both CTAs drained TMEM
@@ -150,7 +150,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* stage_c = smem + NSTAGE * kStageBytes + 512 + kYStageBytes + 2 * kTokTile * 4;  // [NCS][kCodeStage]
     uint64_t* c_full = u_empty + kURing;   // [NCS] each CTA: the stage's codes + constants landed
     uint64_t* c_empty = c_full + NCS;      // [NCS] each CTA: the 8 dequant warps of its two k-blocks read them
-    uint64_t* full_a = c_empty + NCS;      // [NSTAGE] leader: A of the stage stored in both CTAs' TMEM
+    uint64_t* full_a = full_b;             // one full barrier per stage: the A stores join the B bytes
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); };
 
     const int warp = warp_idx_uniform(), lane = threadIdx.x % 32;
@@ -158,8 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023) __trap();  // SW128 B stages need 1024-byte alignment
         for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full_b[s], 1);             // the leader's TMA expect_tx (both CTAs' bytes)
-            mbar_init(&full_a[s], kDqWarps / 2);  // 4 dequant warps per CTA x 2
+            mbar_init(&full_b[s], 1 + kDqWarps / 2);  // the leader's TMA expect_tx + 4 dequant warps per CTA x 2
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
@@ -297,8 +296,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 for (int kb = 0; kb < kb_n; ++kb, ++it) {
                     const uint32_t s = it % NSTAGE;
-                    WAITX(&full_a[s], (it / NSTAGE) & 1);
-                    EV(7, kb, tc);
                     WAITX(&full_b[s], (it / NSTAGE) & 1);
                     EV(1, kb, tc);
                     tc_fence_after();

@@ -21,10 +21,11 @@ from gpu_helpers import make_layer, make_x  # noqa: E402
 from paper_2602_20191_b200 import calibrate_threshold, permute_by_slice  # noqa: E402
 from paper_2602_20191_b200.layer import decompose  # noqa: E402
 
+GENERIC = [((4, 2, 2), 300), ((1, 1, 1, 1, 1, 1, 1, 1), 40)]  # per-slice CUDA-core path
 CASES = [  # (out, in, h, T, what)
     (256, 512, 128, 1, "decode router + slice planes"),
     (256, 512, 128, 16, "slice planes, two 8-token groups"),
-    (2048, 4096, 128, 12, "stream-K merged-code decode (planes do not fit)"),
+    (8192, 1024, 64, 8, "stream-K merged-code decode (planes do not fit)"),
     (256, 1024, 256, 40, "1-CTA router cluster K-split + split-K GEMM"),
     (256, 512, 2048, 1024, "pair router N=128 + pair GEMM"),
     (256, 256, 4096, 1280, "pair router N=256 + pair GEMM"),
@@ -49,6 +50,21 @@ def main():
         d = (y.float() - y_ref.float()).norm() / y_ref.float().norm()
         print(f"{what:52s} {out}x{inn} h={h} T={T}: plan {plan} rel vs simt {d:.2e}", flush=True)
         assert d < 1e-2, what
+        layer.close()
+    from paper_2602_20191_b200 import MobiLayer
+    from oracle import oracle as O
+    for sb, T in GENERIC:
+        if only and only != "generic":
+            continue
+        L = O.synthetic_layer(192, 320, seed=4, group_size=64, slice_bits=sb)
+        layer = MobiLayer.from_stack(L["codes"], L["slice_bits"], L["scale"], L["zero"], 64, L["w1"], L["b1"],
+                                     L["w2"], L["b2"], device=0)
+        xb, _ = make_x(T, 320, seed=T)
+        delta = calibrate_threshold(layer.score(xb), 1 / 6)
+        y, m = layer.forward(xb, delta, return_masks=True)
+        layer.route(xb, delta)
+        torch.cuda.synchronize()
+        print(f"generic {sb} T={T}: plan {layer.last_plan()}", flush=True)
         layer.close()
     masks = torch.randint(0, 8, (333,), dtype=torch.uint8, device="cuda") * 2 + 1
     perm, inv, groups = permute_by_slice(masks)
