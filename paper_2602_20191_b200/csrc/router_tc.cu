@@ -626,7 +626,7 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-// development switch (MOBI_ROUTER_PAIR): 0 = never use the CTA-pair router
+// development switch (MOBI_ROUTER_PAIR): 0 = never use the CTA-pair router, 2 = N = 256 tiles whenever h allows
 int g_router_pair = [] {
     const char* e = std::getenv("MOBI_ROUTER_PAIR");
     return e ? std::atoi(e) : 1;
@@ -689,7 +689,8 @@ int launch_router_tc(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float del
     const int n_mp = (int)cdiv(T, 2 * RM);
     const int n_mp_plan = (int)cdiv(Tp, 2 * RM);
     int pn = 0;
-    if (g_router_pair && Tp > 64 && L->h % 256 == 0 && n_mp_plan * (int)(L->h / 256) * 2 >= L->n_sm)
+    if (g_router_pair && Tp > 64 && L->h % 256 == 0 &&
+        (n_mp_plan * (int)(L->h / 256) * 2 >= L->n_sm || g_router_pair == 2))
         pn = 256;
     else if (g_router_pair && Tp > 64 && L->h % 128 == 0 && n_mp_plan * (int)(L->h / 128) * 2 >= L->n_sm * 3 / 4)
         pn = 128;
