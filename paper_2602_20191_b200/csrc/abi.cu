@@ -459,7 +459,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
               "mobi_out_desc: columns [" << od->col0 << "," << od->col0 + L->out << ") exceed ldy " << od->ldy);
     for (int k = 0; k < od->n_dst; ++k) CHECK_ARG(od->dst[k], "mobi_out_desc: null destination " << k);
     const int64_t Tp = std::max(T, L->plan_T);
-    const bool pair = L->impl == 0 && !L->generic && !decode_supported(L, x, Tp) && Tp > 64;
+    const bool pair = L->impl == 0 && !L->generic && !decode_supported(L, x, Tp) && Tp > 32;
     if (pair) {
         L->od = *od;
         const int rc = run_layer_y(L, x, T, delta, given_masks, nullptr, masks_out, st);
@@ -559,9 +559,9 @@ int run_layer_y(mobi_layer* L, const void* x, int64_t T, float delta, const uint
     }
     if (L->impl == 3) return launch_gemm_tc2(L, yb, T, st);  // CTA-pair kernel
     if (L->impl == 5) return launch_gemm_tc(L, yb, T, st);   // 1-CTA kernel (comparison)
-    // production: the CTA-pair kernel (B split across the pair: half the smem operand traffic per SM);
-    // the 1-CTA kernel for batches small enough to need split-K
-    if (Tp <= 64) return launch_gemm_tc(L, yb, T, st);
+    // production: the CTA-pair kernel (B split across the pair: half the smem operand traffic per SM) for
+    // every batch above the decode sizes; at 33..64 tokens it beats the 1-CTA split-K kernel too
+    // (56 vs 72-74 us at q/o 4096x4096, tools/small_t_probe.py), which stays as a comparison path
     return launch_gemm_tc2(L, yb, T, st, nullptr, !L->prof);
 }
 

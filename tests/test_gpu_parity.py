@@ -302,3 +302,23 @@ def test_chained_layers_under_pdl_equal_synchronized(orc, T):
         b = l2.forward(a, d2)  # back to back on one stream
     torch.cuda.synchronize()
     assert torch.equal(a, y1) and torch.equal(b, ref2)
+
+
+@pytest.mark.parametrize("T", [40, 64, 300])
+def test_one_cta_splitk_gemm_matches_oracle(orc, T):
+    """The 1-CTA split-K tcgen05 GEMM (gemm_tc.cu, debug impl 5: a comparison path since the CTA-pair
+    kernel took over 33..64 tokens) still computes forward_elastic within the stated tolerance."""
+    L, layer = make_layer(512, 384, gs=128, seed=T + 77)
+    xb, x64 = make_x(T, 384, seed=T + 78)
+    rng = np.random.default_rng(T)
+    masks = (rng.integers(0, 8, T) * 2 + 1).astype(np.uint8)
+    layer.set_debug_impl(5)
+    try:
+        y = layer.forward_masked(xb, torch.from_numpy(masks).cuda())
+    finally:
+        layer.set_debug_impl(0)
+    y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 128, gates_from_masks(masks, 3))
+    assert_y_close(y, y_ref, f"1-CTA split-K T={T}")
+    y_pair = layer.forward_masked(xb, torch.from_numpy(masks).cuda())
+    assert layer.last_plan()["gemm"] == "gemm_pair"
+    assert_y_close(y_pair, y_ref, f"CTA-pair T={T}")
