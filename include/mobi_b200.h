@@ -236,6 +236,7 @@ MOBI_API const char* mobi_last_error(void);
 
 /* Test hook (not part of the drop-in surface), per layer: impl 1 routes the GEMM through the
  * CUDA-core reference kernel (gemm_simt.cu) so the test-suite can cross-check the tcgen05 kernel;
+ * 5 = the 1-CTA split-K GEMM, 10 = the decode kernels for every batch they support (T <= 32);
  * other values select traced / alternative kernels for development tools.  0 = production. */
 MOBI_API int mobi_layer_debug_impl(mobi_layer_t layer, int impl);
 MOBI_API const char* mobi_version(void);

@@ -448,6 +448,17 @@ struct ProfScope {
 int run_layer_y(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_t* given_masks, void* y,
                 uint8_t* masks_out, cudaStream_t st);
 
+// Decode kernels (router GEMV + slice-plane / stream-K GEMV) for batches up to kDecodePreferT tokens (one
+// slice-plane launch); above, the prefill path (tcgen05 router + gather + CTA-pair GEMM) is faster (q/o
+// 4096x4096, graph-replayed steps: 41.8 vs 45.0 us at T=16, 73.4 vs 52.7 at 32; eager: 53.0 vs 42.9 at
+// T=20, tools/small_t_probe.py).  Debug impls 6 (no PDL), 9 (traced) and 10 run the decode kernels
+// whenever they support the batch (T <= 32).
+constexpr int64_t kDecodePreferT = 16;
+bool uses_decode(const mobi_layer* L, const void* x, int64_t Tp) {
+    if (!decode_supported(L, x, Tp)) return false;
+    return (L->impl == 0 && Tp <= kDecodePreferT) || L->impl == 6 || L->impl == 9 || L->impl == 10;
+}
+
 // the layer forward with an output descriptor: the CTA-pair GEMM places Y itself (every destination,
 // from its epilogue); the small-T paths compute into a staging buffer and scatter it
 int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_t* given_masks, void* y,
@@ -459,7 +470,7 @@ int run_layer(mobi_layer* L, const void* x, int64_t T, float delta, const uint8_
               "mobi_out_desc: columns [" << od->col0 << "," << od->col0 + L->out << ") exceed ldy " << od->ldy);
     for (int k = 0; k < od->n_dst; ++k) CHECK_ARG(od->dst[k], "mobi_out_desc: null destination " << k);
     const int64_t Tp = std::max(T, L->plan_T);
-    const bool pair = L->impl == 0 && !L->generic && !decode_supported(L, x, Tp) && Tp > 32;
+    const bool pair = L->impl == 0 && !L->generic && !uses_decode(L, x, Tp);
     if (pair) {
         L->od = *od;
         const int rc = run_layer_y(L, x, T, delta, given_masks, nullptr, masks_out, st);
@@ -505,7 +516,7 @@ int run_layer_y(mobi_layer* L, const void* x, int64_t T, float delta, const uint
     }
     // kernel choices follow the plan size (the whole batch when mobi_forward_host runs it in chunks)
     const int64_t Tp = std::max(T, L->plan_T);
-    if ((L->impl == 0 || L->impl == 6 || L->impl == 9) && decode_supported(L, x, Tp)) {
+    if (uses_decode(L, x, Tp)) {
         // decode-size batch: router GEMV -> (PDL) stream-K decode GEMM, no bucketing
         unsigned long long* tbuf = nullptr;
         if (L->impl == 9) {  // traced (development hook): per-CTA globaltimer marks

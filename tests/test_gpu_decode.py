@@ -28,6 +28,9 @@ def _impl(layer, n):
     layer.set_debug_impl(n)
 
 
+DECODE = 10  # debug impl: the decode kernels for every batch they support (production: T <= 16)
+
+
 def _masks(T, seed):
     rng = np.random.default_rng(seed)
     m = (rng.integers(0, 8, T) * 2 + 1).astype(np.uint8)
@@ -58,7 +61,9 @@ def test_decode_masked_matches_oracle_and_bucketed(orc, out, inn, gs, h, T):
     xb, x64 = make_x(T, inn, seed=T + 7)
     masks = _masks(T, T)
     md = torch.from_numpy(masks).cuda()
+    _impl(layer, DECODE)
     y = layer.forward_masked(xb, md)
+    assert layer.last_plan()["gemm"] in ("decode_planes", "decode_merged")
     y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], gs,
                                 gates_from_masks(masks, 3))
     assert_y_close(y, y_ref, f"decode {out}x{inn} T={T}")
@@ -74,6 +79,7 @@ def test_decode_masked_matches_oracle_and_bucketed(orc, out, inn, gs, h, T):
                                             (300, 136, 136, 24, 32), (1024, 4096, 128, 0, 7)])
 def test_decode_forward_routes_like_oracle(orc, out, inn, gs, h, T):
     L, layer = make_layer(out, inn, gs=gs, hidden=h, seed=out + 2 * T)
+    _impl(layer, DECODE)
     xb, x64 = make_x(T, inn, seed=T + 9)
     s_ref = oracle_scores(orc, layer, x64)
     for rho in (0.0, 1 / 6, 1 / 3, 1.0):
@@ -95,6 +101,7 @@ def test_decode_forward_routes_like_oracle(orc, out, inn, gs, h, T):
 def test_decode_deterministic_repeat_pdl_and_graph():
     L, layer = make_layer(2048, 2048, gs=128, hidden=0, seed=4)
     delta = 0.0
+    _impl(layer, DECODE)
     for T in (1, 6, 16, 29):
         xb, _ = make_x(T, 2048, seed=T)
         y0 = layer.forward(xb, delta).clone()
@@ -104,7 +111,7 @@ def test_decode_deterministic_repeat_pdl_and_graph():
         try:
             assert torch.equal(layer.forward(xb, delta), y0)
         finally:
-            _impl(layer, 0)
+            _impl(layer, DECODE)
         # CUDA-graph capture of the whole forward (router + decode GEMM), replayed on new inputs
         xg = xb.clone()
         yg = torch.empty_like(y0)
@@ -132,3 +139,17 @@ def test_decode_path_skipped_when_unsupported(orc):
     y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 32,
                                 gates_from_masks(masks, 3))
     assert_y_close(y, y_ref, "gs=32")
+
+
+def test_production_prefers_prefill_path_above_16_tokens(orc):
+    """Production kernel choice: decode kernels up to 16 tokens, the tcgen05 prefill path above (both
+    within the stated tolerance of the oracle)."""
+    L, layer = make_layer(1024, 1024, gs=128, hidden=0, seed=31)
+    for T, kind in ((16, ("decode_planes", "decode_merged")), (17, ("gemm_pair",)), (32, ("gemm_pair",))):
+        xb, x64 = make_x(T, 1024, seed=T)
+        masks = _masks(T, T)
+        y = layer.forward_masked(xb, torch.from_numpy(masks).cuda())
+        assert layer.last_plan()["gemm"] in kind, (T, layer.last_plan())
+        y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 128,
+                                    gates_from_masks(masks, 3))
+        assert_y_close(y, y_ref, f"T={T}")

@@ -1,5 +1,8 @@
-"""Development tool: forward() step time at 33..128 tokens with the 1-CTA split-K GEMM (debug impl 5)
-vs the CTA-pair GEMM (debug impl 3), q/o 4096x4096, 3 bits (CUDA events over 50 calls)."""
+"""Development tool: forward() step time at small batches with the production kernel choice (debug impl 0),
+the 1-CTA split-K GEMM (impl 5) and the CTA-pair GEMM path (impl 3: router + gather + pair GEMM, never the
+decode kernels), q/o 4096x4096, 3 bits, CUDA events over 50 calls.  MOBI_PROBE_T="16,24,32" picks the
+token counts."""
+import os
 import sys
 from pathlib import Path
 
@@ -18,7 +21,8 @@ def main():
     args.tokens = 4096
     xcal = bench.make_x(args, dev, 5)
     delta = calibrate_threshold(layer.score(xcal), 1 / 6)
-    for T in (33, 48, 64, 96, 128):
+    Ts = [int(t) for t in os.environ.get("MOBI_PROBE_T", "33,48,64,96,128").split(",")]
+    for T in Ts:
         x = xcal[:T].contiguous()
         res = {}
         for impl in (5, 3, 0):
@@ -34,7 +38,8 @@ def main():
             torch.cuda.synchronize()
             res[impl] = e0.elapsed_time(e1) / 50 * 1e3
         layer.set_debug_impl(0)
-        print(f"T={T:4d}: split-K 1-CTA {res[5]:6.1f} us, CTA-pair {res[3]:6.1f} us, production {res[0]:6.1f} us")
+        print(f"T={T:4d}: split-K 1-CTA {res[5]:6.1f} us, CTA-pair path {res[3]:6.1f} us, production {res[0]:6.1f} us "
+              f"({layer.last_plan()['gemm']})")
 
 
 if __name__ == "__main__":
