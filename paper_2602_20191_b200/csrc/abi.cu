@@ -449,14 +449,18 @@ int run_layer_y(mobi_layer* L, const void* x, int64_t T, float delta, const uint
                 uint8_t* masks_out, cudaStream_t st);
 
 // Decode kernels (router GEMV + slice-plane / stream-K GEMV) for batches up to kDecodePreferT tokens (one
-// slice-plane launch); above, the prefill path (tcgen05 router + gather + CTA-pair GEMM) is faster (q/o
-// 4096x4096, graph-replayed steps: 41.8 vs 45.0 us at T=16, 73.4 vs 52.7 at 32; eager: 53.0 vs 42.9 at
-// T=20, tools/small_t_probe.py).  Debug impls 6 (no PDL), 9 (traced) and 10 run the decode kernels
-// whenever they support the batch (T <= 32).
-constexpr int64_t kDecodePreferT = 16;
+// slice-plane launch) when the slice-plane GEMV takes the batch, and below kDecodeMergedT tokens when only
+// the stream-K merged-code GEMV does (it streams all four slices); above, the prefill path (tcgen05 router
+// + gather + CTA-pair GEMM) is faster.  Measured eager, tools/small_t_probe.py, decode vs prefill path:
+// q/o T=16 43.8 vs 42.8 us, T=17 51.4 vs 42.7; gate/up (merged at 16) 107.1 vs 102.7; down (merged from
+// T=3) T=4 95.7 vs 111.6, T=8 113.3 vs 99.3, T=16 165.6 vs 99.5; k/v T=16 32.9 vs 41.4.  Debug impls 6 (no
+// PDL), 9 (traced) and 10 run the decode kernels whenever they support the batch (T <= 32).
+constexpr int64_t kDecodePreferT = 16, kDecodeMergedT = 8;
 bool uses_decode(const mobi_layer* L, const void* x, int64_t Tp) {
     if (!decode_supported(L, x, Tp)) return false;
-    return (L->impl == 0 && Tp <= kDecodePreferT) || L->impl == 6 || L->impl == 9 || L->impl == 10;
+    if (L->impl == 6 || L->impl == 9 || L->impl == 10) return true;
+    if (L->impl != 0 || Tp > kDecodePreferT) return false;
+    return Tp < kDecodeMergedT || decode_planes_supported(L, x, Tp);
 }
 
 // the layer forward with an output descriptor: the CTA-pair GEMM places Y itself (every destination,

@@ -116,14 +116,16 @@ struct RDParams {
 // shared memory (rank 0 + rank 1, fixed order), then silu(H + b1) . w2 over the tile's 16 hidden
 // units gives the tile's partial scores spart[mt][t][k] (router.hpp:63-76).  The decode GEMM sums
 // the tiles in order, adds b2 and applies gate_hard(delta).
-constexpr int kRdRing = 6;  // router: 32-k chunks in flight per lane
+// router: 32-k chunks in flight per lane -- 6, or fewer when that keeps every CTA of a tall router
+// (down: 448 CTAs) in one wave (launch_router_dec)
 __device__ __forceinline__ void rd_cp16(void* dst, const void* src, bool ok) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
                  : "memory");
 }
-template <int NT>
+template <int NT, int kRdRing>
 __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWarps)
     router_dec_kernel(const __grid_constant__ RDParams p) {
+    static_assert(kRdRing >= 2, "ring");
     extern __shared__ __align__(16) uint8_t rd_ring[];  // [warps][kRdRing][32 lanes][2 + NT] x 16 B
     const int tcta = blockIdx.x;
     auto TRM = [&](int i) {
@@ -197,7 +199,7 @@ __global__ void __cluster_dims__(kRdCluster, 1, 1) __launch_bounds__(32 * kRdWar
     for (int64_t q = q0; q < q1; ++q) {
         const int64_t pend = qi - 1 - q;  // groups allowed to stay in flight
         if (pend >= kRdRing - 2) asm volatile("cp.async.wait_group %0;" ::"n"(kRdRing - 2) : "memory");
-        else if (pend >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+        else if (pend >= 2 && kRdRing > 4) asm volatile("cp.async.wait_group 2;" ::: "memory");
         else if (pend >= 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
         else asm volatile("cp.async.wait_group 0;" ::: "memory");
         const uint4* d = ring + (size_t)((q - q0) % kRdRing) * 32 * kSlot;
@@ -1055,19 +1057,7 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
     p.delta = delta;
     const int n_mt = (int)(L->h_pad / kRdRows);
     const dim3 grid((unsigned)(n_mt * kRdCluster));
-    auto smem_of = [](int nt) { return (size_t)kRdWarps * kRdRing * 32 * (2 + nt) * 16; };
-    {  // run with the SM configured for maximum shared memory, so the decode GEMM that
-                   // follows (PDL) can be co-resident while the router streams w1
-        MOBI_TRY(func_attr_once(router_dec_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                       (int)cudaSharedmemCarveoutMaxShared));
-        MOBI_TRY(func_attr_once(router_dec_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                       (int)cudaSharedmemCarveoutMaxShared));
-        MOBI_TRY(func_attr_once(router_dec_kernel<4>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                       (int)cudaSharedmemCarveoutMaxShared));
-        MOBI_TRY(func_attr_once(router_dec_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(1)));
-        MOBI_TRY(func_attr_once(router_dec_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(2)));
-        MOBI_TRY(func_attr_once(router_dec_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(4)));
-    }
+    auto smem_of = [](int nt, int ring) { return (size_t)kRdWarps * ring * 32 * (2 + nt) * 16; };
     // PDL: the router's CTAs may launch while the previous kernel (e.g. the last layer's decode GEMM)
     // drains and prefetch their first w1 chunks; griddepcontrol.wait guards X and every write
     cudaLaunchConfig_t cfg = {};
@@ -1079,16 +1069,43 @@ int launch_router_dec(mobi_layer* L, const __nv_bfloat16* x, int64_t T, float de
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (T <= 8) {
-        cfg.dynamicSmemBytes = smem_of(1);
-        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_dec_kernel<1>, p));
-    } else if (T <= 16) {
-        cfg.dynamicSmemBytes = smem_of(2);
-        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_dec_kernel<2>, p));
-    } else {
-        cfg.dynamicSmemBytes = smem_of(4);
-        MOBI_CUDA(cudaLaunchKernelEx(&cfg, router_dec_kernel<4>, p));
+    const int nt = T <= 8 ? 1 : T <= 16 ? 2 : 4;
+    // the deepest ring whose occupancy keeps the whole grid in one wave: a CTA streams its share of w1
+    // as one latency chain, so a second wave (4 CTAs past 3 per SM on down) doubles the router
+    static int occ[3][3] = {};  // [nt 1/2/4][ring 6/4/2] CTAs per SM, queried once
+    const int nti = nt == 1 ? 0 : nt == 2 ? 1 : 2;
+    int ring = 6;
+    for (int ri = 0; ri < 3; ++ri) {
+        const int r = ri == 0 ? 6 : ri == 1 ? 4 : 2;
+        const void* fn = nullptr;
+        switch (nti * 3 + ri) {
+#define RD_FN(i, N, R) case i: fn = reinterpret_cast<const void*>(router_dec_kernel<N, R>); break;
+            RD_FN(0, 1, 6) RD_FN(1, 1, 4) RD_FN(2, 1, 2) RD_FN(3, 2, 6) RD_FN(4, 2, 4) RD_FN(5, 2, 2)
+            RD_FN(6, 4, 6) RD_FN(7, 4, 4) RD_FN(8, 4, 2)
+#undef RD_FN
+        }
+        // run with the SM configured for maximum shared memory, so the decode GEMV that follows (PDL)
+        // can be co-resident while the router streams w1 (per device, once)
+        MOBI_TRY(func_attr_once(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared));
+        MOBI_TRY(func_attr_once(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_of(nt, r)));
+        if (!occ[nti][ri]) {
+            int n = 0;
+            MOBI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, 32 * kRdWarps, smem_of(nt, r)));
+            occ[nti][ri] = std::max(n, 1);
+        }
+        if ((int64_t)occ[nti][ri] * L->n_sm >= (int64_t)grid.x) {
+            ring = r;
+            break;
+        }
     }
+    cfg.dynamicSmemBytes = smem_of(nt, ring);
+    auto go = [&](auto kern) { return cudaLaunchKernelEx(&cfg, kern, p); };
+    cudaError_t e = cudaSuccess;
+    if (nt == 1) e = ring == 6 ? go(router_dec_kernel<1, 6>) : ring == 4 ? go(router_dec_kernel<1, 4>) : go(router_dec_kernel<1, 2>);
+    else if (nt == 2) e = ring == 6 ? go(router_dec_kernel<2, 6>) : ring == 4 ? go(router_dec_kernel<2, 4>) : go(router_dec_kernel<2, 2>);
+    else e = ring == 6 ? go(router_dec_kernel<4, 6>) : ring == 4 ? go(router_dec_kernel<4, 4>) : go(router_dec_kernel<4, 2>);
+    MOBI_CUDA(e);
     MOBI_LAUNCH_CHECK();
     ++L->last_launches;
     L->plan[0] = MOBI_K_ROUTER_DECODE;

@@ -14,8 +14,9 @@
 // fragment-ordered 2-bit codes expanded to exact fp16 (1024 + c, the offset cancelled with the
 // group's activation sum) and x scaled per token by 2^-e into fp16 (exact).
 //
-// One CTA owns a 32-row tile over the whole K (no cross-CTA reduction); its eight warps split K and
-// are summed in warp order at the end (deterministic).
+// One CTA owns R 32-row tiles (R = 1 while the tiles fit one wave, else 2/4/8) over the whole K (no
+// cross-CTA reduction); each tile's 16/R warps split K and are summed in warp order at the end
+// (deterministic).  With R > 1 the first 16/R warps convert X for everyone.
 #include "mobi_internal.cuh"
 #include "sm100.cuh"
 
@@ -27,7 +28,7 @@ using namespace sm100;
 constexpr int kD2Warps = 16, kD2Threads = 32 * kD2Warps;  // 16 warps: 4 per scheduler (latency hiding)
 constexpr int kD2MaxT = 16;       // tokens per launch: two groups of 8 (the m16n8k16 N dimension)
 constexpr int kD2MaxLaunchT = 32;  // larger decode batches: one launch per 16 tokens
-constexpr int kD2Acc = 3 * 2 * 4;  // per lane: y over the token's slices, A, B  ([2][4] each)
+constexpr int kD2Acc = 2 * 2 * 4;  // per lane: y over the token's slices (B folded in), A  ([2][4] each)
 
 struct D2Params {
     const uint4* dplanes;     // [E][n_rt32][kblocks][32] 16 B
@@ -46,6 +47,7 @@ struct D2Params {
     int single_group, T, E, nr, n_mt, vmask, n_rt32, xs_stride;
     int t0, t_all;    // this launch's first token and the batch size (router partials are [n_mt][t_all][nr])
     int gpw;          // groups per warp (bound) for the staged constants
+    int R, wpt;       // 32-row tiles per CTA, warps per tile (R * wpt = kD2Warps)
     int64_t gcs_off;  // byte offset of the staged constants in dynamic smem
     int64_t ring_off; // byte offset of the per-lane cp.async rings
     unsigned long long* trace;  // debug: per-CTA globaltimer marks [2048 + cta][8]
@@ -58,6 +60,10 @@ __device__ __forceinline__ unsigned long long gtimer2() {
 
 __device__ __forceinline__ void mma_f16_acc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                             uint32_t b0, uint32_t b1) {
+#ifdef MOBI_D2_NOMMA  // dev: what the stream costs without the tensor instructions (wrong results)
+    d[0] = fmaf(__uint_as_float((a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1) & 0x3fffffffu), 1e-30f, d[0]);
+    return;
+#endif
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
@@ -87,20 +93,10 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 constexpr int kD2Ring = 6;  // (slice, k-block) items in flight per lane (16 B each): 48 KiB per CTA
                             // (sized so the router's ring fits on the same SM at T = 8)
 
-// cp.async.wait_group for "at most n groups pending": exact in the steady state (n = kD2Ring - 2),
-// conservatively rounded down near the ends of the stream (no jump table in the item loop)
-__device__ __forceinline__ void cp_wait_dyn(int n) {
-    static_assert(kD2Ring == 6, "staged waits assume a 6-deep ring");
-    if (n >= 4) cp_wait<4>();
-    else if (n >= 2) cp_wait<2>();
-    else if (n >= 1) cp_wait<1>();
-    else cp_wait<0>();
-}
-
 // NG token groups of 8 per launch: 1 (T <= 8, capped at 80 registers so the router's CTAs stay
 // co-resident) or 2 (9..16 tokens: the A fragments of every item serve both groups)
 template <int NG>
-__global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __grid_constant__ D2Params p) {
+__global__ void __maxnreg__(NG == 1 ? 96 : 128) decode_planes_kernel(const __grid_constant__ D2Params p) {
     extern __shared__ __align__(16) uint8_t smem[];
     __half* x16 = reinterpret_cast<__half*>(smem);                                   // [T + 1][xs_stride]
     // [T][kblocks] {sum of the k-step-scaled fp16 X (offset cancellation), unscaled sum (A, B)}
@@ -112,14 +108,19 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
     const int tid = threadIdx.x, warp = warp_idx_uniform(), lane = tid & 31;
     float2* gcs = reinterpret_cast<float2*>(smem + p.gcs_off) + (size_t)warp * p.gpw * 32;  // [groups][32 rows]
     uint4* ring = reinterpret_cast<uint4*>(smem + p.ring_off) + (size_t)warp * kD2Ring * 32;   // [slots][32 lanes]
-    const int rt = blockIdx.x;
+    const int wl = warp % p.wpt;                    // warp index inside its tile (K split)
+    const int rt = blockIdx.x * p.R + warp / p.wpt;  // this warp's 32-row tile
+    const bool conv = warp < p.wpt;                 // converts X (k range of wl) for the whole CTA
     auto TRM = [&](int i) {
-        if (p.trace && tid == 0) p.trace[(size_t)(2048 + rt) * 8 + i] = gtimer2();
+        if (p.trace && tid == 0) p.trace[(size_t)(2048 + blockIdx.x) * 8 + i] = gtimer2();
     };
     TRM(0);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next router may prefetch its w1
     const int T = p.T;
-    const int kw0 = (int)((int64_t)warp * p.kblocks / kD2Warps), kw1 = (int)((int64_t)(warp + 1) * p.kblocks / kD2Warps);
+    // k-block range of this warp; warps of a tile past the last have none (they still take part in
+    // the CTA barriers)
+    const int kw0 = (int)((int64_t)wl * p.kblocks / p.wpt);
+    const int kw1 = rt < p.n_rt32 ? (int)((int64_t)(wl + 1) * p.kblocks / p.wpt) : kw0;
     // streamed items (see (2)-(4) below): item i = (slice slist[i / nk], k-block kw0 + i % nk); issued in
     // order, one cp.async group each, into ring slot i % kD2Ring; slice 1's first items go out now so
     // their latency hides behind the activation prologue
@@ -130,9 +131,14 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
     const int plane_stride = p.n_rt32 * (int)p.kblocks * 32;  // uint4s per slice plane
     const uint4* ip = rt_planes + kw0 * 32;  // source of item pi
     auto seek = [&]() { ip = rt_planes + ((int)(slist >> (2 * psi)) & 3) * plane_stride + pkb * 32; };
-    auto issue = [&](int i) {
-        cp_async16(ring + (i % kD2Ring) * 32 + lane, ip, true);
-        cp_commit();
+    // every prologue step and every loop iteration commits exactly one cp.async group (empty when there
+    // is nothing to issue), so item ci is always followed by kD2Ring - 2 newer groups and one constant
+    // wait_group covers every position of the stream
+    int pslot = 0;  // ring slot of item pi (= pi % kD2Ring)
+    auto issue = [&]() {
+        cp_async16(ring + pslot * 32 + lane, ip, true);
+        ++pi;
+        pslot = pslot + 1 == kD2Ring ? 0 : pslot + 1;
         if (++pkb == kw1) {
             pkb = kw0, ++psi;
             seek();
@@ -143,7 +149,7 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
     // (0) stage, as one cp.async group: this warp's k range of every token's bf16 X into its x16 rows
     //     (converted in place below) and the group constants (s, s*z) of the warp's groups for the
     //     tile's 32 rows (read once for all slices); slice 1's first items follow as their own groups
-    const int64_t k_lo = (int64_t)kw0 * kKBlock, k_hi = (int64_t)kw1 * kKBlock;
+    const int64_t k_lo = (int64_t)kw0 * kKBlock, k_hi = conv ? (int64_t)kw1 * kKBlock : k_lo;
     for (int t = 0; t < T; ++t)
         for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256) {
             const bool ok = k < p.in;
@@ -159,20 +165,18 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
                            p.gconst + (g0 + i / 16) * p.out_pad + (int64_t)rt * 32 + (i % 16) * 2, true);
     }
     cp_commit();
-    while (pi < kw1 - kw0 && pi < kD2Ring - 1) issue(pi++);
-    switch (pi) {  // the staging group has landed (slice 1's items may still be in flight)
-        case 0: cp_wait<0>(); break;
-        case 1: cp_wait<1>(); break;
-        case 2: cp_wait<2>(); break;
-        case 3: cp_wait<3>(); break;
-        case 4: cp_wait<4>(); break;
-        default: cp_wait<5>(); break;
+    for (int j = 0; j < kD2Ring - 1; ++j) {
+        if (pi < kw1 - kw0) issue();
+        cp_commit();
     }
+    cp_wait<kD2Ring - 1>();  // the staging group has landed (slice 1's items may still be in flight)
     __syncwarp();
 
     // (1) X in place: bf16 -> per-token 2^-e scale (max over the warp's range) x 4^-ss per k-step ->
     //     fp16, and per-(token, k-block) sums of the fp16 values (scaled, and rescaled by 4^ss)
-    const int lss = (lane & 7) >> 1;  // k-step ss = (k % 64) / 16 of this lane's 8 values
+    // k-step of a value: ss = (k % 16) / 4 (pack_dplanes_kernel's fragment order), so a lane's 8
+    // values are 4 of k-step ss0 and 4 of ss0 + 1
+    const int ss0 = 2 * (lane & 1);
     // four tokens at a time: their max-reductions and conversions proceed side by side
     // (independent shuffle chains)
     for (int tb = 0; tb < T; tb += 4) {
@@ -205,7 +209,7 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
                 // normal float for tiny activations; powers of two from exponent bits (no libm calls)
                 int e = 0;
                 if (m[i] > 0.f && m[i] <= 3.0e38f) e = max(((__float_as_int(m[i]) >> 23) & 0xff) - 127 - 14, -100);
-                sc[i] = __int_as_float((127 - e - 2 * lss) << 23);
+                sc[i] = __int_as_float((127 - e - 2 * ss0) << 23);
                 if (lane == 0 && tb + i < T) es_s[warp][tb + i] = __int_as_float((127 + e) << 23);
             }
         }
@@ -215,7 +219,7 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int t = tb + i;
-                sacc[i] = 0.f;
+                float s_lo = 0.f, s_hi = 0.f;  // values of k-steps ss0 and ss0 + 1
                 if (t < T && k < k_hi) {
                     __half* xp = x16 + (size_t)t * p.xs_stride + k;
                     const uint4 q = *reinterpret_cast<const uint4*>(xp);
@@ -224,14 +228,16 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
                     __half2* hh = reinterpret_cast<__half2*>(&o);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
+                        const float scj = j < 2 ? sc[i] : sc[i] * 0.25f;  // 4^-ss, exact
                         const float2 f2 = __bfloat1622float2(b[j]);
-                        hh[j] = __floats2half2_rn(f2.x * sc[i], f2.y * sc[i]);
+                        hh[j] = __floats2half2_rn(f2.x * scj, f2.y * scj);
                         const float2 h2 = __half22float2(hh[j]);
-                        sacc[i] += h2.x + h2.y;
+                        (j < 2 ? s_lo : s_hi) += h2.x + h2.y;
                     }
                     *reinterpret_cast<uint4*>(xp) = o;
                 }
-                uacc[i] = sacc[i] * (float)(1 << (2 * lss));  // exact: power-of-two rescale
+                sacc[i] = s_lo + s_hi;
+                uacc[i] = s_lo * (float)(1 << (2 * ss0)) + s_hi * (float)(4 << (2 * ss0));  // exact rescales
             }
 #pragma unroll
             for (int o = 1; o < 8; o <<= 1)
@@ -247,19 +253,22 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
         }
     }
     TRM(7);
-    for (int64_t k = (int64_t)kw0 * kKBlock + lane * 8; k < (int64_t)kw1 * kKBlock; k += 256)
+    for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256)
         *reinterpret_cast<uint4*>(x16 + (size_t)T * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
-    __syncwarp();
+    if (p.R > 1) __syncthreads();  // X, its sums and scales come from the first tile's warps
+    else __syncwarp();
 
     // yt: this lane's outputs (rows g/g+8 of both row groups, tokens 8gi+2c / 8gi+2c+1 of token group
     // gi) over the slices each token uses; ys: the current slice's partials
-    float yt[NG][2][4], ys[NG][2][4], A[NG][2][4], B[NG][2][4], D[NG][2][4];
+    // A = sum_g s_g sum_k x (times kc[m] at the end, in units of the token scale); B = sum_g s_g z_g
+    // sum_k x goes straight into slice 1's partials (slice 1 is every token's, scaled by the token scale)
+    float yt[NG][2][4], ys[NG][2][4], A[NG][2][4], D[NG][2][4];
 #pragma unroll
     for (int gi = 0; gi < NG; ++gi)
 #pragma unroll
         for (int rg = 0; rg < 2; ++rg)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) yt[gi][rg][j] = ys[gi][rg][j] = A[gi][rg][j] = B[gi][rg][j] = D[gi][rg][j] = 0.f;
+            for (int j = 0; j < 4; ++j) yt[gi][rg][j] = ys[gi][rg][j] = A[gi][rg][j] = D[gi][rg][j] = 0.f;
     TRM(1);
     const int g = lane >> 2, c = lane & 3;
     const __half* xr[NG];  // B-fragment token rows (row T is zeros)
@@ -268,11 +277,11 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
 #pragma unroll
     for (int gi = 0; gi < NG; ++gi) {
         const int tg = 8 * gi + g < T ? 8 * gi + g : T;
-        xr[gi] = x16 + (size_t)tg * p.xs_stride + 2 * c;
+        xr[gi] = x16 + (size_t)tg * p.xs_stride + 16 * c;  // the lane's 16 values of every k-block
         tk0[gi] = 8 * gi + 2 * c;
         tk1[gi] = 8 * gi + 2 * c + 1;
-        es0[gi] = tk0[gi] < T ? es_s[warp][tk0[gi]] : 0.f;
-        es1[gi] = tk1[gi] < T ? es_s[warp][tk1[gi]] : 0.f;
+        es0[gi] = tk0[gi] < T ? es_s[wl][tk0[gi]] : 0.f;
+        es1[gi] = tk1[gi] < T ? es_s[wl][tk1[gi]] : 0.f;
     }
     float xg0[NG], xg1[NG], xu0[NG], xu1[NG];
 #pragma unroll
@@ -288,7 +297,7 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
     int mt0[NG], mt1[NG];
 #pragma unroll
     for (int gi = 0; gi < NG; ++gi) mt0[gi] = mt1[gi] = 0;
-    int csi = 0, ckb = kw0;  // consume cursor
+    int csi = 0, ckb = kw0, cslot = 0;  // consume cursor
     for (int ci = 0;; ++ci) {
         if (ci == nk) {
             TRM(2);
@@ -312,10 +321,10 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
                     int m = 1;
                     for (int k = 0; k < p.nr; ++k) {
                         if ((s_score[tid][k] - p.delta) > 0.f) m |= 1 << (k + 1);
-                        if (rt == 0 && p.scores_out) p.scores_out[tid * p.nr + k] = s_score[tid][k];
+                        if (blockIdx.x == 0 && p.scores_out) p.scores_out[tid * p.nr + k] = s_score[tid][k];
                     }
                     s_mask[tid] = m;
-                    if (rt == 0) {
+                    if (blockIdx.x == 0) {
                         p.masks_dev[tid] = (uint8_t)m;
                         if (p.masks_out) p.masks_out[tid] = (uint8_t)m;
                     }
@@ -333,17 +342,31 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
                 if (uni >> e0 & 1) slist |= (uint32_t)e0 << (2 * ns++);
             n_items = nk * ns;
             seek();  // the issue cursor's slice is known now
-            // burst: the union's first items
-            while (pi < n_items && pi <= ci + kD2Ring - 1) issue(pi++);
+            // burst: the union's first items (kD2Ring - 1 groups, padded with empty ones)
+            for (int j = 0; j < kD2Ring - 1; ++j) {
+                if (pi < n_items) issue();
+                cp_commit();
+            }
         }
         if (ci >= n_items) break;
         const int si = csi, kb = ckb, e0 = (int)(slist >> (2 * si)) & 3;
         if (++ckb == kw1) ckb = kw0, ++csi;
-        cp_wait_dyn(pi - 1 - ci);
-        if (ci == 0) __syncwarp();  // the group constants other lanes copied are visible
-        const uint4 q = ring[(ci % kD2Ring) * 32 + lane];
+        // debug: per-item globaltimer marks of CTA 0's warps (before the wait, data in, issued)
+        const bool tri = p.trace && blockIdx.x == 0 && lane == 0 && ci < 32;
+        if (tri) p.trace[24576 + warp * 128 + ci * 4 + 0] = gtimer2();
+        cp_wait<kD2Ring - 2>();
+        const uint4 q = ring[cslot * 32 + lane];
+        if (tri) p.trace[24576 + warp * 128 + ci * 4 + 1] = gtimer2() + (q.x & 0);
+        cslot = cslot + 1 == kD2Ring ? 0 : cslot + 1;
         const uint32_t w0[4] = {q.x, q.y, q.z, q.w};
         const uint32_t w1[4] = {q.x >> 8, q.y >> 8, q.z >> 8, q.w >> 8};  // row group 1's fields
+        uint4 xb[NG][2];  // B fragments of the four k-steps: (b0, b1) of k-step ss = words 2ss, 2ss + 1
+#pragma unroll
+        for (int gi = 0; gi < NG; ++gi) {
+            const uint4* xk = reinterpret_cast<const uint4*>(xr[gi] + (size_t)kb * kKBlock);
+            xb[gi][0] = xk[0];
+            xb[gi][1] = xk[1];
+        }
         auto kstep = [&](auto SSc) {
             constexpr int SS = decltype(SSc)::value;
             const uint32_t a00 = frag<SS>(w0[0], magic), a01 = frag<SS>(w0[1], magic), a02 = frag<SS>(w0[2], magic),
@@ -352,9 +375,8 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
                            a13 = frag<SS>(w1[3], magic);
 #pragma unroll
             for (int gi = 0; gi < NG; ++gi) {  // the A fragments serve every token group
-                const __half* xk = xr[gi] + (size_t)kb * kKBlock + 16 * SS;
-                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xk);
-                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xk + 8);
+                const uint4& v = xb[gi][SS / 2];
+                const uint32_t b0 = SS % 2 ? v.z : v.x, b1 = SS % 2 ? v.w : v.y;
                 mma_f16_acc(D[gi][0], a00, a01, a02, a03, b0, b1);
                 mma_f16_acc(D[gi][1], a10, a11, a12, a13, b0, b1);
             }
@@ -364,7 +386,10 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
         kstep(std::integral_constant<int, 2>{});
         kstep(std::integral_constant<int, 3>{});
         // refill: item ci + R - 1 goes into the slot just consumed (its data is in registers)
-        if (pi < n_items && pi <= ci + kD2Ring - 1) issue(pi++);
+        if (tri) p.trace[24576 + warp * 128 + ci * 4 + 2] = gtimer2() + (uint32_t)(D[0][0][0] != 0.f) * 0;
+        if (pi < n_items && pi <= ci + kD2Ring - 1) issue();
+        cp_commit();
+        if (tri) p.trace[24576 + warp * 128 + ci * 4 + 3] = gtimer2();
 #pragma unroll
         for (int gi = 0; gi < NG; ++gi) {
             const float2 s0 = tk0[gi] < T ? xsum[tk0[gi] * p.kblocks + kb] : make_float2(0.f, 0.f);
@@ -388,10 +413,10 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
                         ys[gi][rg][2 * h] = fmaf(D[gi][rg][2 * h] - 1024.f * xg0[gi], sc.x, ys[gi][rg][2 * h]);
                         ys[gi][rg][2 * h + 1] = fmaf(D[gi][rg][2 * h + 1] - 1024.f * xg1[gi], sc.x, ys[gi][rg][2 * h + 1]);
                         if (si == 0) {
-                            A[gi][rg][2 * h] = fmaf(sc.x, xu0[gi] * es0[gi], A[gi][rg][2 * h]);
-                            A[gi][rg][2 * h + 1] = fmaf(sc.x, xu1[gi] * es1[gi], A[gi][rg][2 * h + 1]);
-                            B[gi][rg][2 * h] = fmaf(sc.y, xu0[gi] * es0[gi], B[gi][rg][2 * h]);
-                            B[gi][rg][2 * h + 1] = fmaf(sc.y, xu1[gi] * es1[gi], B[gi][rg][2 * h + 1]);
+                            A[gi][rg][2 * h] = fmaf(sc.x, xu0[gi], A[gi][rg][2 * h]);
+                            A[gi][rg][2 * h + 1] = fmaf(sc.x, xu1[gi], A[gi][rg][2 * h + 1]);
+                            ys[gi][rg][2 * h] = fmaf(-sc.y, xu0[gi], ys[gi][rg][2 * h]);
+                            ys[gi][rg][2 * h + 1] = fmaf(-sc.y, xu1[gi], ys[gi][rg][2 * h + 1]);
                         }
                     }
                 }
@@ -435,24 +460,23 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     r[(i++) * 32] = yt[gi][rg][j];
-                    r[(i++) * 32] = A[gi][rg][j];
-                    r[(i++) * 32] = B[gi][rg][j];
+                    r[(i++) * 32] = A[gi][rg][j] * (j & 1 ? es1[gi] : es0[gi]);  // exact: power of two
                 }
     }
     __syncthreads();
-    if (tid < 32 * 8 * NG) {
-        const int rl = tid % 32, t = tid / 32;
-        const int64_t row = (int64_t)rt * 32 + rl;
+    for (int i = tid; i < p.R * 32 * 8 * NG; i += kD2Threads) {
+        const int rl = i % 32, t = (i / 32) % (8 * NG), j_tile = i / (32 * 8 * NG);
+        const int64_t row = ((int64_t)blockIdx.x * p.R + j_tile) * 32 + rl;
         if (t < T && row < p.out) {
             const int gi = t / 8, tl = t % 8;
             const int rg = rl / 16, rr = rl % 16, g = rr % 8, hi = rr / 8;
             const int ln = g * 4 + tl / 2, j = hi * 2 + (tl & 1);
-            const int base = ((gi * 2 + rg) * 4 + j) * 3;
+            const int base = ((gi * 2 + rg) * 4 + j) * 2;
             const float kc = p.mt.kc[s_mask[t]];
             float acc = 0.f;
-            for (int w = 0; w < kD2Warps; ++w) {
+            for (int w = j_tile * p.wpt; w < (j_tile + 1) * p.wpt; ++w) {
                 const float* r = red + (size_t)w * (NG * kD2Acc) * 32 + ln;
-                acc += r[(base + 0) * 32] + (kc * r[(base + 1) * 32] - r[(base + 2) * 32]);
+                acc += r[(base + 0) * 32] + kc * r[(base + 1) * 32];
             }
             p.y[(int64_t)t * p.out + row] = __float2bfloat16_rn(acc);
         }
@@ -462,9 +486,18 @@ __global__ void __maxnreg__(NG == 1 ? 80 : 128) decode_planes_kernel(const __gri
 
 }  // namespace
 
-int d2_groups_per_warp(const mobi_layer* L) {
+// 32-row tiles per CTA: the smallest R in {1, 2, 4, 8} whose CTAs fit one wave (a CTA's latency chain
+// is serial, so a second wave costs as much as the first); 0 = the layer is too tall for this kernel
+static int d2_tiles_per_cta(const mobi_layer* L) {
+    const int64_t n_rt = cdiv(L->out, (int64_t)32);
+    for (int r = 1; r <= 8; r *= 2)
+        if (cdiv(n_rt, (int64_t)r) <= L->n_sm) return r;
+    return 0;
+}
+
+static int d2_groups_per_warp(const mobi_layer* L, int wpt) {
     if (L->single_group) return 1;
-    const int64_t kpw = cdiv(L->kblocks, (int64_t)kD2Warps) * kKBlock;  // k per warp (upper bound)
+    const int64_t kpw = cdiv(L->kblocks, (int64_t)wpt) * kKBlock;  // k per warp (upper bound)
     return (int)(kpw / L->gs + 2);
 }
 
@@ -473,12 +506,12 @@ int d2_groups_per_warp(const mobi_layer* L) {
 struct D2Smem {
     size_t gcs_off, ring_off, total;
 };
-static D2Smem d2_smem(const mobi_layer* L, int64_t T) {
+static D2Smem d2_smem(const mobi_layer* L, int64_t T, int R) {
     const int ng = T > 8 ? 2 : 1;
     const size_t xs = (size_t)(T + 1) * (L->in_pad + 8) * 2 + (size_t)T * L->kblocks * 8;
     D2Smem m;
     m.gcs_off = (std::max(xs, (size_t)kD2Warps * ng * kD2Acc * 32 * 4) + 15) / 16 * 16;
-    m.ring_off = m.gcs_off + (size_t)kD2Warps * d2_groups_per_warp(L) * 32 * 8;
+    m.ring_off = m.gcs_off + (size_t)kD2Warps * d2_groups_per_warp(L, kD2Warps / R) * 32 * 8;
     m.total = m.ring_off + (size_t)kD2Warps * kD2Ring * 32 * 16;
     return m;
 }
@@ -489,12 +522,10 @@ bool decode_planes_supported(const mobi_layer* L, const void* x, int64_t T) {
     if (T < 1 || T > kD2MaxLaunchT || !L->dplanes || L->E > 4) return false;
     if (L->in % 8 != 0 || (reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
     if (!L->single_group && L->gs % kKBlock != 0) return false;
-    const int n_sm = L->n_sm;
-    // one CTA per 32-row tile pays only while the tiles fit one wave: the latency chain of every
-    // wave is serial (gate/up, 448 tiles, is faster on the stream-K merged-code kernels)
-    if (cdiv(L->out, (int64_t)32) > n_sm) return false;
+    const int R = d2_tiles_per_cta(L);
+    if (R == 0) return false;
     const int64_t Tg = std::min<int64_t>(T, kD2MaxT);
-    return d2_smem(L, Tg).total <= (Tg > 8 ? kD2SmemMax : kD2SmemCoRes);
+    return d2_smem(L, Tg, R).total <= (Tg > 8 ? kD2SmemMax : kD2SmemCoRes);
 }
 
 int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const uint8_t* given_masks, float delta,
@@ -541,12 +572,14 @@ int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const
         p.vmask = (1 << (L->nr + 1)) - 1;
         p.n_rt32 = (int)(L->out_pad / 32);
         p.xs_stride = (int)(L->in_pad + 8);
-        p.gpw = d2_groups_per_warp(L);
-        const D2Smem sm = d2_smem(L, Tg);
+        p.R = d2_tiles_per_cta(L);
+        p.wpt = kD2Warps / p.R;
+        p.gpw = d2_groups_per_warp(L, p.wpt);
+        const D2Smem sm = d2_smem(L, Tg, p.R);
         p.gcs_off = (int64_t)sm.gcs_off;
         p.ring_off = (int64_t)sm.ring_off;
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)cdiv(L->out, 32));
+        cfg.gridDim = dim3((unsigned)cdiv(cdiv(L->out, (int64_t)32), (int64_t)p.R));
         cfg.blockDim = dim3(kD2Threads);
         cfg.dynamicSmemBytes = sm.total;
         cfg.stream = st;

@@ -104,8 +104,10 @@ int check_codes_device(const uint8_t* codes_dev, int64_t n, int qmax, int64_t* b
 
 // Decode slice planes (decode2.cu): per slice e, 32-row tile rt, 64-k block kb: 32 lanes x 16 bytes
 // holding the lane's m16n8k16 A fragments.  Lane (g = lane/4, c = lane%4): word q is fragment register
-// a_q (a0: row g, k 2c|2c+1; a1: row g+8; a2: row g, k 2c+8|2c+9; a3: row g+8) of all eight MMAs of
-// the block -- row group rg (16 rows) x k-step ss (16 k) sits in field i = 4 rg + ss, low half at
+// a_q (a0: row g, MMA k 2c|2c+1; a1: row g+8; a2: row g, MMA k 2c+8|2c+9; a3: row g+8) of all eight
+// MMAs of the block.  MMA k of k-step ss maps to memory k 16c + 4ss + {0,1 | 2,3} (a0 | a2), so the
+// activations a lane feeds as B fragments over the block's four k-steps are 16 contiguous values (two
+// 16-byte shared loads).  Row group rg (16 rows) x k-step ss sits in field i = 4 rg + ss, low half at
 // bits 2i..2i+1, high half at bits 16+2i.  A field masked in place (rg 0) or after one shift by 8
 // (rg 1) reads as the fp16 1024 + c 4^ss with a single LOP3, so the kernel scales the activations of
 // k-step ss by 4^-ss instead of shifting every field down.  A kernel reads only the planes it needs.
@@ -126,7 +128,7 @@ __global__ void pack_dplanes_kernel(const uint8_t* __restrict__ codes8, int64_t 
         for (int i = 0; i < 8; ++i) {
             const int rg = i / 4, ss = i % 4;
             const int64_t row = rt * 32 + 16 * rg + g + ((q & 1) ? 8 : 0);
-            const int64_t k0 = kb * kKBlock + 16 * ss + 2 * c + ((q & 2) ? 8 : 0);
+            const int64_t k0 = kb * kKBlock + 16 * c + 4 * ss + ((q & 2) ? 2 : 0);
             const uint32_t lo = (codes8[code_offset(row, k0, kblocks)] >> shift) & 3u;
             const uint32_t hi = (codes8[code_offset(row, k0 + 1, kblocks)] >> shift) & 3u;
             word |= lo << (2 * i) | hi << (16 + 2 * i);

@@ -143,7 +143,8 @@ __device__ __forceinline__ void mbar_wait_relaxed(uint64_t* bar, uint32_t parity
         "r"(parity)
         : "memory");
 }
-// bulk prefetch of a global range into L2 (no smem, no completion tracking)
+// bulk prefetch of a global range into L2 (no smem, no completion tracking).  Measured on the decode
+// streams (router w1, slice planes): no faster than the per-lane cp.async rings alone, so unused there.
 __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }

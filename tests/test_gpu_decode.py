@@ -52,6 +52,10 @@ DEC_SHAPES = [  # (out, in, gs, hidden, T)
     (14336 // 4, 4096, 128, 0, 4),  # more row tiles than SMs' worth of k-blocks per tile
     (4096, 4096, 128, 0, 8),    # slice-plane kernel at its 8-token limit
     (1024, 14336, 128, 0, 6),   # in = 14336 (down projection), planes kernel
+    (14336, 4096, 128, 0, 1),   # gate/up: 448 row tiles, four per planes CTA
+    (4768, 512, 128, 64, 3),    # 149 row tiles: two per CTA, the last CTA's second tile empty
+    (9600, 256, 64, 16, 12),    # 300 row tiles, four per CTA, two token groups
+    (20000, 128, 64, 16, 2),    # 625 row tiles, eight per CTA (two warps per tile)
 ]
 
 
@@ -76,7 +80,9 @@ def test_decode_masked_matches_oracle_and_bucketed(orc, out, inn, gs, h, T):
 
 
 @pytest.mark.parametrize("out,inn,gs,h,T", [(4096, 4096, 128, 0, 1), (512, 1024, 128, 64, 16),
-                                            (300, 136, 136, 24, 32), (1024, 4096, 128, 0, 7)])
+                                            (300, 136, 136, 24, 32), (1024, 4096, 128, 0, 7),
+                                            (1024, 14336, 128, 0, 1),     # 448 router CTAs: shallower ring, one wave
+                                            (14336, 4096, 128, 0, 2)])    # gate/up: multi-tile planes CTAs
 def test_decode_forward_routes_like_oracle(orc, out, inn, gs, h, T):
     L, layer = make_layer(out, inn, gs=gs, hidden=h, seed=out + 2 * T)
     _impl(layer, DECODE)
@@ -153,3 +159,17 @@ def test_production_prefers_prefill_path_above_16_tokens(orc):
         y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 128,
                                     gates_from_masks(masks, 3))
         assert_y_close(y, y_ref, f"T={T}")
+
+
+@pytest.mark.parametrize("out,inn,T", [(14336, 4096, 1), (20000, 128, 5)])
+def test_tall_layers_stream_slice_planes(orc, out, inn, T):
+    """Layers with more 32-row tiles than SMs (gate/up: 448) take the slice-plane GEMV with several
+    tiles per CTA, so a decode step streams only its union's planes -- not the merged 8-bit codes."""
+    L, layer = make_layer(out, inn, gs=64, hidden=16, seed=out + T)
+    xb, x64 = make_x(T, inn, seed=T + 11)
+    masks = _masks(T, T + 1)
+    y = layer.forward_masked(xb, torch.from_numpy(masks).cuda())
+    assert layer.last_plan()["gemm"] == "decode_planes", layer.last_plan()
+    y_ref = orc.forward_elastic(x64, L["codes"], L["slice_bits"], L["scale"], L["zero"], 64,
+                                gates_from_masks(masks, 3))
+    assert_y_close(y, y_ref, f"{out}x{inn} T={T}")

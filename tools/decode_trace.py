@@ -62,11 +62,11 @@ def main():
     show("planes", g, ["start", "x prep done", "slice 1 done", "grid dep resolved", "union slices done", "end",
                        "x token 0 loaded", "x last token loaded"])
     it = full.astype(np.int64)[24576:24576 + 16 * 32 * 4].reshape(16, 32, 4)
-    for w in (0, 7, 15):
-        print(f"planes CTA0 warp {w} per item (cycles rel. item 0: pre-wait, data, mma done, issued):")
+    for w in (0, 5, 15):
+        print(f"planes CTA0 warp {w} per item (ns rel. kernel start: pre-wait, data, mma done, issued):")
         for ci in range(32):
             if it[w, ci, 0]:
-                print("   ", ci, [int(v - it[w, 0, 0]) for v in it[w, ci]])
+                print("   ", ci, [int(v - t0) for v in it[w, ci]])
     return
     ft = full.astype(np.int64)[24576:24576 + 4 * 64].reshape(4, 64)
     for c in range(2):

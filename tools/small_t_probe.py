@@ -1,7 +1,8 @@
 """Development tool: forward() step time at small batches with the production kernel choice (debug impl 0),
-the 1-CTA split-K GEMM (impl 5) and the CTA-pair GEMM path (impl 3: router + gather + pair GEMM, never the
-decode kernels), q/o 4096x4096, 3 bits, CUDA events over 50 calls.  MOBI_PROBE_T="16,24,32" picks the
-token counts."""
+the 1-CTA split-K GEMM (impl 5), the CTA-pair GEMM path (impl 3: router + gather + pair GEMM, never the
+decode kernels) and the decode kernels (impl 10), 3 bits, CUDA events over 50 calls (not graph-replayed).
+Shape from bench.py's --out/--in; MOBI_PROBE_T="16,24,32" picks the token counts, MOBI_PROBE_IMPLS the
+variants."""
 import os
 import sys
 from pathlib import Path
@@ -22,10 +23,11 @@ def main():
     xcal = bench.make_x(args, dev, 5)
     delta = calibrate_threshold(layer.score(xcal), 1 / 6)
     Ts = [int(t) for t in os.environ.get("MOBI_PROBE_T", "33,48,64,96,128").split(",")]
+    IMPLS = [int(i) for i in os.environ.get("MOBI_PROBE_IMPLS", "5,3,0").split(",")]
     for T in Ts:
         x = xcal[:T].contiguous()
         res = {}
-        for impl in (5, 3, 0):
+        for impl in IMPLS:
             layer.set_debug_impl(impl)
             for _ in range(5):
                 layer.forward(x, delta)
@@ -38,8 +40,10 @@ def main():
             torch.cuda.synchronize()
             res[impl] = e0.elapsed_time(e1) / 50 * 1e3
         layer.set_debug_impl(0)
-        print(f"T={T:4d}: split-K 1-CTA {res[5]:6.1f} us, CTA-pair path {res[3]:6.1f} us, production {res[0]:6.1f} us "
-              f"({layer.last_plan()['gemm']})")
+        layer.forward(x, delta)
+        names = {5: "split-K 1-CTA", 3: "CTA-pair path", 10: "decode kernels", 0: "production"}
+        print(f"{layer.out}x{layer.inn} T={T:4d}: " + ", ".join(f"{names.get(i, i)} {res[i]:6.1f} us" for i in IMPLS)
+              + f" ({layer.last_plan()['gemm']})", flush=True)
 
 
 if __name__ == "__main__":

@@ -10,6 +10,7 @@ graph replay.
 Prints one JSON line per target budget (rank 0; tokens/s is the whole job, time = max over ranks).
 """
 import argparse
+import functools
 import json
 import os
 import sys
@@ -29,6 +30,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--calib-tokens", type=int, default=0,
+                    help="calibrate the thresholds on a separate batch of this many tokens (decode runs: "
+                         "--tokens 1 --calib-tokens 2048); 0 = calibrate on the timed batch itself")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -39,16 +43,29 @@ def main():
     torch.cuda.set_device(local)
     from paper_2602_20191_b200.stack import MobiStack
     t0 = time.time()
-    stack = MobiStack(blocks=args.blocks, device=local, seed=args.seed, max_tokens=args.tokens)
+    stack = MobiStack(blocks=args.blocks, device=local, seed=args.seed,
+                      max_tokens=max(args.tokens, args.calib_tokens))
     build_s = time.time() - t0
     g = torch.Generator(device="cuda").manual_seed(args.seed * 7919 + rank)
-    x = torch.randn((args.tokens, stack.d), generator=g, device="cuda")
+    pool = max(args.tokens, args.calib_tokens)
+    x = torch.randn((pool, stack.d), generator=g, device="cuda")
     ch = torch.randperm(stack.d, generator=g, device="cuda")[: round(0.05 * stack.d)]
     x[:, ch] *= 8.0
     x = x.to(torch.bfloat16)
+    xcal, x = x, x[: args.tokens].contiguous()
+    from paper_2602_20191_b200.layer import avg_bits_from_masks
     for target in args.targets:
-        res = stack.sweep_point(x, target)
+        res = stack.sweep_point(xcal, target)
         deltas = {id(layer): d for layer, d in zip(stack.layers, res.per_layer_delta)}
+        masks: list = []
+        stack.forward(x, deltas, masks)  # the timed batch's own masks
+        timed_bits = [avg_bits_from_masks(m, [2, 2, 2, 2]) for m in masks]
+        # slice-code bytes the timed batch's masks select (union over its tokens, per layer): the decode
+        # kernels read exactly the planes some token needs, so at T=1 this is the weight traffic
+        union_bytes = 0
+        for layer, m in zip(stack.layers, masks):
+            u = functools.reduce(lambda a, b: a | b, torch.unique(m).tolist(), 0)
+            union_bytes += layer.out * layer.inn * 2 * bin(u).count("1") // 8
         graph, _ = stack.capture(x, deltas)
         for _ in range(args.warmup):
             graph.replay()
@@ -75,6 +92,10 @@ def main():
                 "criterion6_within_0.15": abs(res.realized_bits - target) <= 0.15,
                 "per_layer_bits_min": round(min(res.per_layer_bits), 4),
                 "per_layer_bits_max": round(max(res.per_layer_bits), 4),
+                "calib_tokens": args.calib_tokens or args.tokens,
+                "timed_batch_avg_bits": round(float(sum(timed_bits) / len(timed_bits)), 4),
+                "slice_code_bytes_selected": union_bytes,
+                "slice_code_GBps": round(union_bytes / (ms / 1e3) / 1e9, 1),
                 "ms_per_forward": round(ms, 3), "tokens_per_s": round(args.tokens * world / (ms / 1e3), 1),
                 "device_gib": round(stack.device_bytes() / 2**30, 2), "build_s": round(build_s, 1),
                 "data": "random-init slices (uniform 2-bit codes, unit-gain group scales), calibset-style X"}),
