@@ -50,6 +50,7 @@ struct D2Params {
     int R, wpt;       // 32-row tiles per CTA, warps per tile (R * wpt = kD2Warps)
     int64_t gcs_off;  // byte offset of the staged constants in dynamic smem
     int64_t ring_off; // byte offset of the per-lane cp.async rings
+    int64_t xgs_off;  // byte offset of the per-(k range, token, group) activation sums
     unsigned long long* trace;  // debug: per-CTA globaltimer marks [2048 + cta][8]
 };
 __device__ __forceinline__ unsigned long long gtimer2() {
@@ -255,6 +256,24 @@ __global__ void __maxnreg__(NG == 1 ? 96 : 128) decode_planes_kernel(const __gri
     TRM(7);
     for (int64_t k = k_lo + lane * 8; k < k_hi; k += 256)
         *reinterpret_cast<uint4*>(x16 + (size_t)T * p.xs_stride + k) = make_uint4(0, 0, 0, 0);
+    // per (token, group of this warp's k range) sums of the k-block sums, read once per group fold
+    // instead of once per item: xgs[(wl * T + t) * gpw + lg], lg = local group (the first may be partial)
+    const int kpg = p.single_group ? (1 << 30) : (int)(p.gs / kKBlock);  // k-blocks per group
+    float2* xgs = reinterpret_cast<float2*>(smem + p.xgs_off);
+    if (conv && kw1 > kw0) {
+        __syncwarp();
+        const int g_first = kw0 / kpg, n_lg = (kw1 - 1) / kpg - g_first + 1;
+        for (int i = lane; i < T * n_lg; i += 32) {
+            const int t = i / n_lg, lg = i % n_lg;
+            const int b0 = max(kw0, (g_first + lg) * kpg), b1 = min(kw1, (g_first + lg + 1) * kpg);
+            float sx = 0.f, su = 0.f;
+            for (int b = b0; b < b1; ++b) {
+                const float2 v = xsum[t * p.kblocks + b];
+                sx += v.x, su += v.y;
+            }
+            xgs[(wl * T + t) * p.gpw + lg] = make_float2(sx, su);
+        }
+    }
     if (p.R > 1) __syncthreads();  // X, its sums and scales come from the first tile's warps
     else __syncwarp();
 
@@ -283,11 +302,7 @@ __global__ void __maxnreg__(NG == 1 ? 96 : 128) decode_planes_kernel(const __gri
         es0[gi] = tk0[gi] < T ? es_s[wl][tk0[gi]] : 0.f;
         es1[gi] = tk1[gi] < T ? es_s[wl][tk1[gi]] : 0.f;
     }
-    float xg0[NG], xg1[NG], xu0[NG], xu1[NG];
-#pragma unroll
-    for (int gi = 0; gi < NG; ++gi) xg0[gi] = xg1[gi] = xu0[gi] = xu1[gi] = 0.f;
     int grp = 0, gleft = 0;
-    const int kpg = p.single_group ? (1 << 30) : (int)(p.gs / kKBlock);  // k-blocks per group
     // (2)-(4) one stream of (slice, k-block) items: slice 1's k-blocks (already in flight since the
     // prologue), then -- once the masks are known -- those of every other slice in the batch's union
     const int nk = kw1 - kw0;
@@ -390,19 +405,20 @@ __global__ void __maxnreg__(NG == 1 ? 96 : 128) decode_planes_kernel(const __gri
         if (pi < n_items && pi <= ci + kD2Ring - 1) issue();
         cp_commit();
         if (tri) p.trace[24576 + warp * 128 + ci * 4 + 3] = gtimer2();
-#pragma unroll
-        for (int gi = 0; gi < NG; ++gi) {
-            const float2 s0 = tk0[gi] < T ? xsum[tk0[gi] * p.kblocks + kb] : make_float2(0.f, 0.f);
-            const float2 s1 = tk1[gi] < T ? xsum[tk1[gi] * p.kblocks + kb] : make_float2(0.f, 0.f);
-            xg0[gi] += s0.x, xu0[gi] += s0.y;
-            xg1[gi] += s1.x, xu1[gi] += s1.y;
-        }
         if (kb == kw0) {  // a slice starts: its group cursor
             grp = 0;
             gleft = gleft0;
         }
         const bool slice_end = kb + 1 == kw1;
         if (slice_end || --gleft == 0) {
+            float xg0[NG], xg1[NG], xu0[NG], xu1[NG];  // the group's activation sums of the lane's tokens
+#pragma unroll
+            for (int gi = 0; gi < NG; ++gi) {
+                const float2 s0 = tk0[gi] < T ? xgs[(wl * T + tk0[gi]) * p.gpw + grp] : make_float2(0.f, 0.f);
+                const float2 s1 = tk1[gi] < T ? xgs[(wl * T + tk1[gi]) * p.gpw + grp] : make_float2(0.f, 0.f);
+                xg0[gi] = s0.x, xu0[gi] = s0.y;
+                xg1[gi] = s1.x, xu1[gi] = s1.y;
+            }
 #pragma unroll
             for (int rg = 0; rg < 2; ++rg) {
 #pragma unroll
@@ -423,8 +439,6 @@ __global__ void __maxnreg__(NG == 1 ? 96 : 128) decode_planes_kernel(const __gri
 #pragma unroll
                 for (int gi = 0; gi < NG; ++gi) D[gi][rg][0] = D[gi][rg][1] = D[gi][rg][2] = D[gi][rg][3] = 0.f;
             }
-#pragma unroll
-            for (int gi = 0; gi < NG; ++gi) xg0[gi] = xg1[gi] = xu0[gi] = xu1[gi] = 0.f;
             ++grp;
             gleft = kpg;
         }
@@ -504,7 +518,7 @@ static int d2_groups_per_warp(const mobi_layer* L, int wpt) {
 // dynamic shared memory: x16 rows 0..T (row T zeros) + per-(token, k-block) sums, aliased after the
 // item loop by the warps' reduction buffer; then the staged group constants and the per-lane rings
 struct D2Smem {
-    size_t gcs_off, ring_off, total;
+    size_t gcs_off, ring_off, xgs_off, total;
 };
 static D2Smem d2_smem(const mobi_layer* L, int64_t T, int R) {
     const int ng = T > 8 ? 2 : 1;
@@ -512,7 +526,8 @@ static D2Smem d2_smem(const mobi_layer* L, int64_t T, int R) {
     D2Smem m;
     m.gcs_off = (std::max(xs, (size_t)kD2Warps * ng * kD2Acc * 32 * 4) + 15) / 16 * 16;
     m.ring_off = m.gcs_off + (size_t)kD2Warps * d2_groups_per_warp(L, kD2Warps / R) * 32 * 8;
-    m.total = m.ring_off + (size_t)kD2Warps * kD2Ring * 32 * 16;
+    m.xgs_off = m.ring_off + (size_t)kD2Warps * kD2Ring * 32 * 16;
+    m.total = m.xgs_off + (size_t)(kD2Warps / R) * T * d2_groups_per_warp(L, kD2Warps / R) * 8;
     return m;
 }
 // up to 8 tokens the kernel must leave room for the router's CTAs (co-residency under PDL)
@@ -578,6 +593,7 @@ int launch_decode_planes(mobi_layer* L, const __nv_bfloat16* x, int64_t T, const
         const D2Smem sm = d2_smem(L, Tg, p.R);
         p.gcs_off = (int64_t)sm.gcs_off;
         p.ring_off = (int64_t)sm.ring_off;
+        p.xgs_off = (int64_t)sm.xgs_off;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)cdiv(cdiv(L->out, (int64_t)32), (int64_t)p.R));
         cfg.blockDim = dim3(kD2Threads);
