@@ -214,7 +214,7 @@ __device__ void build_tiles(const int* hist, TokTile* tiles, int32_t* meta) {
     meta[33] = 1;  // GEMM split count
 }
 
-__global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __restrict__ x, int64_t in,
+__global__ void __launch_bounds__(128, 16) gather_kernel(const __nv_bfloat16* __restrict__ x, int64_t in,
                                                      int64_t in_pad, int64_t tpad, int32_t* __restrict__ pinv,
                                                      __half* __restrict__ xperm, float* __restrict__ escale,
                                                      bool vec, const uint8_t* __restrict__ masks,
@@ -223,35 +223,36 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
                                                      int32_t* __restrict__ meta) {
     __shared__ float red[4];
     __shared__ int s_row;
+    __shared__ uint64_t s_bar;
+    // vec: the row (bf16, in % 8 == 0) lands in shared memory with one bulk copy issued before the grid
+    // dependency resolves (an input, not a router output).  Staging in shared memory instead of registers
+    // keeps the kernel at ~30 registers, so the whole batch's CTAs are resident in one wave (2048 tokens:
+    // 14 per SM) and every row read is in flight at once.
+    extern __shared__ __align__(16) uint8_t g_row[];
     const int64_t src = blockIdx.x;
     sm100::pdl_trigger();
-    // the row (an input, not a router output) is loaded before the grid dependency resolves; its
-    // vectors stay in registers between the max and the conversion (in <= 8192)
-    constexpr int kRV = 8;
     const __nv_bfloat16* row = x + (int64_t)src * in;
-    uint4 rv[kRV];
-    if (vec) {
-#pragma unroll
-        for (int j = 0; j < kRV; ++j) {
-            const int64_t k = (int64_t)(threadIdx.x + 128 * j) * 8;
-            rv[j] = k < in ? __ldg(reinterpret_cast<const uint4*>(row + k)) : make_uint4(0, 0, 0, 0);
-        }
-    }
-    // the row's max (and so its 2^-e scale) does not depend on the router either
+    const __nv_bfloat16* srow = reinterpret_cast<const __nv_bfloat16*>(g_row);
     float m = 0.f;
-    auto vmax = [&](uint4 q) {  // by value: rv stays in registers
-        const __nv_bfloat162* pp = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            float2 f = __bfloat1622float2(pp[j]);
-            m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
-        }
-    };
     if (vec) {
+        if (threadIdx.x == 0) {
+            sm100::mbar_init(&s_bar, 1);
+            sm100::fence_barrier_init();
+            sm100::mbar_arrive_expect_tx(&s_bar, (uint32_t)(in * 2));
+            sm100::bulk_g2s(g_row, row, (uint32_t)(in * 2), &s_bar);
+        }
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        sm100::mbar_wait(&s_bar, 0);
+        // the row's max (and so its 2^-e scale) does not depend on the router either
+        for (int64_t k = (int64_t)threadIdx.x * 8; k < in; k += 128 * 8) {
+            const uint4 q = *reinterpret_cast<const uint4*>(srow + k);
+            const __nv_bfloat162* pp = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-        for (int j = 0; j < kRV; ++j) vmax(rv[j]);
-        for (int64_t k = (int64_t)(threadIdx.x + 128 * kRV) * 8; k < in; k += 128 * 8)
-            vmax(__ldg(reinterpret_cast<const uint4*>(row + k)));
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(pp[j]);
+                m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+            }
+        }
     } else {
         for (int64_t k = threadIdx.x; k < in; k += 128) m = fmaxf(m, fabsf(__bfloat162float(row[k])));
     }
@@ -284,25 +285,17 @@ __global__ void __launch_bounds__(128) gather_kernel(const __nv_bfloat16* __rest
     const float sc = ldexpf(1.f, -e);
     if (threadIdx.x == 0) escale[i] = ldexpf(1.f, e);
     if (vec) {
-        auto conv = [&](uint4 q) {
+        for (int64_t k = (int64_t)threadIdx.x * 8; k < in_pad; k += 128 * 8) {  // the in..in_pad tail: zeros
+            const uint4 q = k < in ? *reinterpret_cast<const uint4*>(srow + k) : make_uint4(0, 0, 0, 0);
             uint4 o;
             const __nv_bfloat162* pp = reinterpret_cast<const __nv_bfloat162*>(&q);
             __half2* h = reinterpret_cast<__half2*>(&o);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                float2 f = __bfloat1622float2(pp[j]);
+                const float2 f = __bfloat1622float2(pp[j]);
                 h[j] = __floats2half2_rn(f.x * sc, f.y * sc);
             }
-            return o;
-        };
-#pragma unroll
-        for (int j = 0; j < kRV; ++j) {  // rv[j] is zero past `in`: the in..in_pad tail is written as zeros
-            const int64_t k = (int64_t)(threadIdx.x + 128 * j) * 8;
-            if (k < in_pad) *reinterpret_cast<uint4*>(at(k)) = conv(rv[j]);
-        }
-        for (int64_t k = (int64_t)(threadIdx.x + 128 * kRV) * 8; k < in_pad; k += 128 * 8) {
-            const uint4 q = k < in ? __ldg(reinterpret_cast<const uint4*>(row + k)) : make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(at(k)) = conv(q);
+            *reinterpret_cast<uint4*>(at(k)) = o;
         }
     } else {
         for (int64_t k = threadIdx.x; k < in_pad; k += 128)
@@ -355,11 +348,14 @@ int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* 
 }
 
 int launch_gather(mobi_layer* L, const __nv_bfloat16* x, int64_t T, cudaStream_t st, bool claim, bool pdl) {
-    const bool vec = (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    const bool vec = (L->in % 8 == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && L->in * 2 <= 200 * 1024;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)T);
     cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = vec ? (size_t)L->in * 2 : 0;
     cfg.stream = st;
+    if (vec && cfg.dynamicSmemBytes > 48 * 1024)
+        MOBI_TRY(func_attr_once(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
