@@ -159,9 +159,10 @@ def test_per_slice_isolation(orc, T):
 
 
 def test_routing_is_batch_size_invariant_outside_margin(orc):
-    """The same tokens routed inside batches of 8, 16, 40, 300 and 2048 (decode GEMV router up to 16
-    tokens / 1-CTA cluster K-split / CTA-pair router) get identical masks except within the stated margin
-    (test_router.cpp:62-75 pins batch == row-wise for the fp64 reference)."""
+    """The same tokens routed inside batches of 1, 8, 16, 40, 64, 300 and 2048 (decode GEMV router up to
+    16 tokens / 1-CTA cluster K-split / CTA-pair router), through score() and through forward()'s masks,
+    get the oracle's masks except within the stated margin (test_router.cpp:62-75 pins batch ==
+    row-wise for the fp64 reference)."""
     L, layer = random_layer(4096, 4096, seed=3)
     xb, x64 = make_x(2048, 4096, seed=4)
     n = 16
@@ -169,7 +170,7 @@ def test_routing_is_batch_size_invariant_outside_margin(orc):
     delta = float(np.quantile(s_ref, 0.8))
     near = np.any(np.abs(s_ref - delta) <= MASK_MARGIN, axis=1)
     m_ref = O.masks_from_gates(orc.gate_hard(s_ref, delta))
-    for T in (8, 16, 40, 300, 2048):
+    for T in (1, 8, 16, 40, 64, 300, 2048):
         k = min(n, T)
         s = layer.score(xb[:T].contiguous()).cpu().numpy()[:k].astype(np.float64)
         assert np.all(np.abs(s - s_ref[:k]) <= SCORE_ATOL + SCORE_RTOL * np.abs(s_ref[:k])), f"T={T}"
