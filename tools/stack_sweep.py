@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--concurrent", action="store_true",
+                    help="run q/k/v and gate/up as parallel graph branches (side streams)")
     ap.add_argument("--calib-tokens", type=int, default=0,
                     help="calibrate the thresholds on a separate batch of this many tokens (decode runs: "
                          "--tokens 1 --calib-tokens 2048); 0 = calibrate on the timed batch itself")
@@ -44,7 +46,7 @@ def main():
     from paper_2602_20191_b200.stack import MobiStack
     t0 = time.time()
     stack = MobiStack(blocks=args.blocks, device=local, seed=args.seed,
-                      max_tokens=max(args.tokens, args.calib_tokens))
+                      max_tokens=max(args.tokens, args.calib_tokens), concurrent=args.concurrent)
     build_s = time.time() - t0
     g = torch.Generator(device="cuda").manual_seed(args.seed * 7919 + rank)
     pool = max(args.tokens, args.calib_tokens)
@@ -93,6 +95,7 @@ def main():
                 "per_layer_bits_min": round(min(res.per_layer_bits), 4),
                 "per_layer_bits_max": round(max(res.per_layer_bits), 4),
                 "calib_tokens": args.calib_tokens or args.tokens,
+                "branches": "q/k/v and gate/up as parallel graph branches" if args.concurrent else "serial",
                 "timed_batch_avg_bits": round(float(sum(timed_bits) / len(timed_bits)), 4),
                 "slice_code_bytes_selected": union_bytes,
                 "slice_code_GBps": round(union_bytes / (ms / 1e3) / 1e9, 1),
