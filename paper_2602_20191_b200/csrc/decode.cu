@@ -354,6 +354,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_gemm_kernel(const __gri
     auto issue = [&](int sidx) {
         const int64_t grp = p.single_group ? 0 : ((int64_t)pkb * kKBlock) / p.gs;
         uint8_t* dst = ring + (size_t)sidx * kDecStageBytes;
+        fence_proxy_async_smem();  // the MMA warps' reads of a recycled stage precede the copy into it
         mbar_arrive_expect_tx(&full[sidx], kDecStageBytes);
         bulk_load(dst, p.codes8 + pu * kBlockBytes, kBlockBytes, &full[sidx], pol);
         bulk_load(dst + kBlockBytes, p.gconst + grp * p.out_pad + prt * kRowTile, kRowTile * 8, &full[sidx], pol);
@@ -753,6 +754,7 @@ __global__ void __launch_bounds__(kFmaThreads, kFmaCps) decode_fma_kernel(const 
     int pkb = (int)(u0 - prt * kbn);
     auto issue = [&](int sidx, int nb) {  // nb consecutive blocks: one code copy + one constants copy each
         uint8_t* dst = ring + (size_t)sidx * kFmaStageBytes;
+        fence_proxy_async_smem();  // the FMA warps' reads of a recycled stage precede the copy into it
         mbar_arrive_expect_tx(&full[sidx], nb * kDecStageBytes);
         bulk_load(dst, p.codes8 + pu * kBlockBytes, nb * kBlockBytes, &full[sidx], pol);
         for (int j = 0; j < nb; ++j) {

@@ -149,7 +149,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int32_t* tok_src = reinterpret_cast<int32_t*>(tok_es + kTokTile);                               // [kTokTile]
     uint8_t* stage_c = smem + NSTAGE * kStageBytes + 512 + kYStageBytes + 2 * kTokTile * 4;  // [NCS][kCodeStage]
     uint64_t* c_full = u_empty + kURing;   // [NCS] each CTA: the stage's codes + constants landed
-    uint64_t* c_empty = c_full + NCS;      // [NCS] each CTA: the 8 dequant warps of its two k-blocks read them
+    uint64_t* c_empty = c_full + NCS;      // [NCS] each CTA: the 256 lanes of its two k-blocks' 8 dequant warps read them
     uint64_t* full_a = full_b;             // one full barrier per stage: the A stores join the B bytes
     auto epi_bar_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); };
 
@@ -169,7 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int s = 0; s < NCS; ++s) {
             mbar_init(&c_full[s], 1);
-            mbar_init(&c_empty[s], kDqWarps / 2);
+            mbar_init(&c_empty[s], kDqWarps / 2 * 32);  // every lane of the stage's 8 dequant warps
         }
         fence_barrier_init();
         prefetch_tmap(&tmap16);
@@ -331,6 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 if ((int)(it % kCodeWarps) != warp - kWarpCode) continue;
                 const int s = (int)(it % NCS);
                 WAITX(&c_empty[s], ((it / NCS) & 1) ^ 1);
+                fence_proxy_async_smem();  // the dequantizers' reads of the slot precede the next copy into it
                 EV(6, kb0, ui);
 #ifndef MOBI_LANE_ISSUE
 #define MOBI_LANE_ISSUE 1
@@ -442,9 +443,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         }
                     }
                 }
-                // the stage's data is in registers (consumed above): release the slot to the code warp
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&c_empty[(cbase + j) % NCS]);
+                // the stage's data is in registers (consumed above): release the slot to the code warp,
+                // every lane for its own reads (the next bulk copy into the slot is an async-proxy write)
+                mbar_arrive(&c_empty[(cbase + j) % NCS]);
                 if (valid) {
                     const uint32_t itk = base + kb;
                     const int s = (int)(itk % NSTAGE);

@@ -3,12 +3,12 @@ compute-sanitizer (racecheck / synccheck / memcheck) on the B200:
 
   compute-sanitizer --tool racecheck python tools/sanitize_paths.py
 
-Covers the decode router + slice-plane GEMV (T=1, 16), the merged-code stream-K decode GEMV,
-the 1-CTA tcgen05 router with the cluster K-split and the split-K GEMM (T=40), the CTA-pair router
-(N=128 and N=256) and the CTA-pair GEMM (T=300..1300), gather, the stable permutation, the device
-radix-select for delta and the GPU decompose.  Each forward is also compared with the CUDA-core
-reference GEMM (debug impl 1) on the same masks, so a sanitizer-perturbed schedule that corrupts
-results fails loudly.
+Covers the decode router (6- and 4-deep rings) + slice-plane GEMV (T=1, 16; 1, 2 and 8 row tiles per
+CTA), the merged-code stream-K decode GEMV, the 1-CTA tcgen05 router with the cluster K-split and the
+split-K GEMM (T=40), the CTA-pair router (N=128 and N=256) and the CTA-pair GEMM (T=300..1300), the
+bulk-copy gather, the stable permutation, the device radix-select for delta and the GPU decompose.
+Each forward is also compared with the CUDA-core reference GEMM (debug impl 1) on the same masks, so a
+sanitizer-perturbed schedule that corrupts results fails loudly.
 """
 import sys
 from pathlib import Path
@@ -25,7 +25,11 @@ GENERIC = [((4, 2, 2), 300), ((1, 1, 1, 1, 1, 1, 1, 1), 40)]  # per-slice CUDA-c
 CASES = [  # (out, in, h, T, what)
     (256, 512, 128, 1, "decode router + slice planes"),
     (256, 512, 128, 16, "slice planes, two 8-token groups"),
-    (8192, 1024, 64, 8, "stream-K merged-code decode (planes do not fit)"),
+    (8192, 1024, 64, 8, "slice planes, 2 row tiles per CTA"),
+    (4768, 512, 64, 1, "slice planes, 2 row tiles per CTA, last CTA half empty"),
+    (20000, 128, 16, 2, "slice planes, 8 row tiles per CTA"),
+    (1024, 14336, 3584, 1, "down-size decode router: 448 CTAs, 4-deep ring"),
+    (1024, 14336, 3584, 4, "stream-K merged-code decode (planes' activations do not fit)"),
     (256, 1024, 256, 40, "1-CTA router cluster K-split + split-K GEMM"),
     (256, 512, 2048, 1024, "pair router N=128 + pair GEMM"),
     (256, 256, 4096, 1280, "pair router N=256 + pair GEMM"),
