@@ -158,7 +158,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         if (smem_u32(smem_raw) & 1023) __trap();  // SW128 B stages need 1024-byte alignment
         for (int s = 0; s < NSTAGE; ++s) {
-            mbar_init(&full_b[s], 1 + kDqWarps / 2);  // the leader's TMA expect_tx + 4 dequant warps per CTA x 2
+            // the leader's TMA expect_tx + its 4 dequant warps' lanes (each after its own TMEM store) + the
+            // peer's 4 dequant warps (one remote arrival each)
+            mbar_init(&full_b[s], 1 + kDqWarps / 4 * 32 + kDqWarps / 4);
             mbar_init(&empty[s], 1);
         }
         mbar_init(acc_full, 1);
@@ -457,14 +459,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         tmem_st_wait();
                     }
                     tc_fence_before();
-                    __syncwarp();
                     if (warp == 0) EV(5, kb, ui);
                     if (warp == 3) EV(2, kb, ui);
-                    if (lane == 0) {
-                        if (rank == 0)
-                            mbar_arrive_relaxed(&full_a[s]);
-                        else
-                            mbar_arrive_relaxed_cluster(full_leader + s * 8);
+                    if (rank == 0) {
+                        mbar_arrive_relaxed(&full_a[s]);  // every lane, after its own wait::st
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_relaxed_cluster(full_leader + s * 8);
                     }
                 }
                 // the next code stage only after this k-block's A is in TMEM: a late code copy must not
