@@ -25,6 +25,8 @@
  *                            (bitplane.hpp:75-84), read back from the device layout (bit-exact check)
  *   mobi_decompose           slicer::decompose (slicer.hpp:69-113) + qcore::params_from_clip
  *                            (qcore.hpp:122-146), on the GPU
+ *   mobi_joint_step          trainer::joint_forward (trainer.hpp:203-263) + trainer::joint_backward
+ *                            (trainer.hpp:341-396): one stage-2 calibration step, fp64, on the GPU
  *
  * Error convention (mirrors MOBI_CHECK, common.hpp:13-24): every entry point returns
  * MOBI_OK, MOBI_EINVAL (the reference would throw std::invalid_argument; message names the
@@ -198,6 +200,40 @@ MOBI_API int mobi_avg_bits(const uint8_t* masks, int64_t T, const int32_t* slice
 MOBI_API int mobi_decompose(const double* w, int64_t out, int64_t in, int64_t group_size,
                    const int32_t* slice_bits, int32_t n_slices, double gamma, uint8_t* codes,
                    double* scale, double* zero, int64_t* clamp_counts, void* stream);
+
+/* Stage-2 calibration step (offline PTQ).  BudgetSchedule (trainer.hpp:45-51):
+ * shape 0 log / 1 linear / 2 cosine / 3 exp. */
+typedef struct mobi_budget_schedule {
+    double b_init;
+    double b_target;
+    int64_t total_steps;
+    int32_t shape;
+    double reg_weight;
+} mobi_budget_schedule;
+
+/* JointForward's scalars (trainer.hpp:186-199) */
+typedef struct mobi_joint_scalars {
+    double data_term;
+    double reg_term; /* unweighted (AvgBits - b(t)) * ||G||_1 */
+    double avg_bits;
+    double sched_b;
+    double loss;
+    double tau; /* 0 at t = L (indicator gate) and with force_gates_on */
+} mobi_joint_scalars;
+
+/* trainer::joint_forward (+ joint_backward when d_gamma_lo is non-null) of one QuantLayer, fp64:
+ *   w [out][in], x [T][in], y_fp [T][out], router w1 [in][h], b1 [h], w2 [h][n_slices-1], b2 [n_slices-1],
+ *   y_hat [T][out] (nullable) and the router gradients (same shapes) are DEVICE memory;
+ *   slice_bits, the per-group clip gammas gamma_lo / gamma_hi [out*ceil(in/gs)] and their gradients are
+ *   HOST memory (the clip squash runs on the host with the reference's libm; groups are few).
+ * Synchronous on `stream`.  Errors as the reference's MOBI_CHECKs (shape mismatch, t outside [1, L]). */
+MOBI_API int mobi_joint_step(const double* w, int64_t out, int64_t in, int64_t group_size, const int32_t* slice_bits,
+                             int32_t n_slices, const double* gamma_lo, const double* gamma_hi, const double* w1,
+                             const double* b1, const double* w2, const double* b2, int64_t hidden, const double* x,
+                             const double* y_fp, int64_t T, const mobi_budget_schedule* sched, int64_t t,
+                             int32_t force_gates_on, double* y_hat, mobi_joint_scalars* scalars, double* d_gamma_lo,
+                             double* d_gamma_hi, double* d_w1, double* d_b1, double* d_w2, double* d_b2,
+                             void* stream);
 
 /* Per-kernel device timing (CUDA events recorded on the launch stream around every kernel the
  * layer launches).  enable=1 starts a fresh accumulation; mobi_layer_profile_read synchronises

@@ -224,6 +224,36 @@ class _Backend:
         return permuted, perm, inv, groups
 
 
+    # ---- trainer.hpp (stage-2 calibration step; the reference backend only) ----
+    def joint_step(self, w, group_size, slice_bits, gamma_lo, gamma_hi, w1, b1, w2, b2, x, y_fp, sched, t,
+                   force_gates_on=False, backward=True):
+        """trainer.hpp:203-263 joint_forward (+ 341-396 joint_backward).  sched = (b_init, b_target,
+        total_steps, shape 0 log / 1 linear / 2 cosine / 3 exp, reg_weight)."""
+        w, x, y_fp, w1, b1, w2, b2 = map(_f64, (w, x, y_fp, w1, b1, w2, b2))
+        sb = _i32a(slice_bits)
+        out, inn = w.shape
+        T = x.shape[0]
+        h = w1.shape[1]
+        ng = out * ((inn + group_size - 1) // group_size)
+        glo, ghi = _f64(gamma_lo), _f64(gamma_hi)
+        y_hat = np.zeros((T, out))
+        sc = np.zeros(6)
+        g = dict(d_gamma_lo=np.zeros(ng), d_gamma_hi=np.zeros(ng), d_w1=np.zeros_like(w1), d_b1=np.zeros(h),
+                 d_w2=np.zeros_like(w2), d_b2=np.zeros(w2.shape[1]))
+        bi, bt, L, shape, rw = sched
+        gp = (lambda k: _ptr(g[k])) if backward else (lambda k: None)
+        self._call("joint_step", _ptr(w), _i64(out), _i64(inn), _i64(group_size), _ptr(sb), _i32(sb.size),
+                   _ptr(glo), _ptr(ghi), _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), _i64(h), _ptr(x), _ptr(y_fp),
+                   _i64(T), _dbl(bi), _dbl(bt), _i64(L), _i32(shape), _dbl(rw), _i64(t), _i32(int(force_gates_on)),
+                   _ptr(y_hat), _ptr(sc), gp("d_gamma_lo"), gp("d_gamma_hi"), gp("d_w1"), gp("d_b1"), gp("d_w2"),
+                   gp("d_b2"))
+        r = dict(zip(("data_term", "reg_term", "avg_bits", "sched_b", "loss", "tau"), sc.tolist()))
+        r["y_hat"] = y_hat
+        if backward:
+            r.update(g)
+        return r
+
+
 def restatement() -> _Backend:
     return _Backend(LIB_ORACLE, "orc_")
 
@@ -311,3 +341,135 @@ def synthetic_layer(out_dim, in_dim, *, seed=1, group_size=128, slice_bits=(2, 2
     b2 = rng.normal(b2.size, b2_sd)
     return dict(w=w, scale=scale, zero=zero, codes=codes, clamp_counts=counts, slice_bits=list(slice_bits),
                 group_size=group_size, w1=w1, b1=b1, w2=w2, b2=b2)
+
+
+# ---------------------------------------------------------------------------------------------
+# Stage-2 calibration step, restated in numpy: trainer.hpp:203-263 joint_forward
+# and trainer.hpp:341-396 joint_backward, with the bit-exact C restatement for params_from_clip /
+# decompose (qcore.hpp:122-146, slicer.hpp:69-113).  Matrix products use numpy's summation order,
+# so this is pinned to the reference within fp64 rounding (tests/test_oracle.py), not bit-for-bit.
+# ---------------------------------------------------------------------------------------------
+
+def _sigmoid(v):
+    v = np.asarray(v, np.float64)
+    e = np.exp(-np.abs(v))
+    return np.where(v >= 0.0, 1.0 / (1.0 + e), e / (1.0 + e))  # common.hpp:125-131
+
+
+def schedule_value(sched, t):
+    """trainer.hpp:52-73."""
+    bi, bt, L, shape, _ = sched
+    if not 1 <= t <= L:
+        raise OracleError(f"schedule_value: step {t} outside [1,{L}]")
+    frac = t / L
+    if shape == 0:
+        return bt if t == L else bi - (bi - bt) * np.log(t) / np.log(L)
+    if shape == 1:
+        return bi - (bi - bt) * frac
+    if shape == 2:
+        return bt + (bi - bt) * (1.0 + np.cos(np.pi * frac)) / 2.0
+    return bi * (bt / bi) ** frac
+
+
+def group_stats(w, group_size):
+    """qcore.hpp:75-111 GroupStats::from_weights: per (row, group) min, max, ref = clamp(0, min, max)."""
+    out, inn = w.shape
+    G = (inn + group_size - 1) // group_size
+    pad = np.full((out, G * group_size), np.nan)
+    pad[:, :inn] = w
+    blk = pad.reshape(out, G, group_size)
+    mn = np.nanmin(blk, axis=2).reshape(-1)
+    mx = np.nanmax(blk, axis=2).reshape(-1)
+    ref = np.minimum(np.maximum(0.0, mn), mx)
+    return mn, mx, ref
+
+
+def joint_step_np(w, group_size, slice_bits, gamma_lo, gamma_hi, w1, b1, w2, b2, x, y_fp, sched, t,
+                  force_gates_on=False, backward=True):
+    orc = restatement()
+    w, x, y_fp = _f64(w), _f64(x), _f64(y_fp)
+    sb = [int(b) for b in slice_bits]
+    E, nr = len(sb), len(sb) - 1
+    out, inn = w.shape
+    T = x.shape[0]
+    G = (inn + group_size - 1) // group_size
+    glo, ghi = _f64(gamma_lo), _f64(gamma_hi)
+    scale, zero = orc.params_from_clip(w, group_size, sb[0], glo, ghi)
+    codes, _, _ = orc.decompose(w, group_size, scale, zero, sb)
+    gidx = (np.arange(out)[:, None] * G + np.arange(inn)[None, :] // group_size)
+    P, frames = [], []
+    before = 0
+    for e in range(1, E + 1):
+        unit = np.ldexp(1.0, -before)
+        mid = 0.0 if e == 1 else np.ldexp(1.0, sb[e - 1] - 1)
+        s_e = scale[gidx] * unit
+        z_e = zero[gidx] if e == 1 else mid
+        We = s_e * (codes[e - 1].astype(np.float64) - z_e + 0.5)  # qcore.hpp:180-197 with slice_params(e)
+        P.append(x @ We.T)
+        frames.append((codes[e - 1].astype(np.float64) - mid + 0.5) * unit)
+        before += sb[e - 1]
+    L = sched[2]
+    hard = False
+    tau = 0.0
+    if force_gates_on:
+        gates = np.ones((T, nr))
+        hpre = hact = np.zeros((T, w1.shape[1]))
+        hard = True
+    else:
+        hpre = x @ _f64(w1) + _f64(b1)[None, :]
+        hact = hpre * _sigmoid(hpre)
+        scores = hact @ _f64(w2) + _f64(b2)[None, :]
+        hard = t == L
+        if hard:
+            gates = (scores > 0.0).astype(np.float64)
+        else:
+            ll = np.log(L)
+            tau = ll / (ll - np.log(t))
+            gates = _sigmoid(tau * scores)
+    y_hat = P[0].copy()
+    for e in range(2, E + 1):
+        y_hat += gates[:, e - 2:e - 1] * P[e - 1]
+    data_term = float(np.mean((y_hat - y_fp) ** 2))
+    bits = sb[0] + ((gates > 0.5) * np.asarray(sb[1:], np.float64)[None, :]).sum(axis=1)
+    avg_bits = float(bits.mean())
+    sched_b = float(schedule_value(sched, t))
+    reg_term = (avg_bits - sched_b) * float(gates.sum())
+    r = dict(data_term=data_term, reg_term=reg_term, avg_bits=avg_bits, sched_b=sched_b,
+             loss=data_term + sched[4] * reg_term, tau=tau, y_hat=y_hat)
+    if not backward:
+        return r
+    resid = 2.0 / y_hat.size * (y_hat - y_fp)
+    qmax1 = float((1 << sb[0]) - 1)
+    d_lo = np.zeros(out * G)
+    d_hi = np.zeros(out * G)
+    d1 = None
+    for e in range(1, E + 1):
+        dm = resid.T @ x if e == 1 else (resid * gates[:, e - 2:e - 1]).T @ x
+        if e == 1:
+            d1 = dm
+        fr = dm * frames[e - 1] / qmax1
+        np.add.at(d_hi, gidx, fr)
+        np.add.at(d_lo, gidx, (dm - fr) if e == 1 else -fr)
+    mn, mx, ref = group_stats(w, group_size)
+    lo = ref + _sigmoid(glo) * (mn - ref)
+    hi = ref + _sigmoid(ghi) * (mx - ref)
+    floored = ~((hi - lo) / qmax1 > 1e-8)
+    sg_lo = _sigmoid(glo) * (1.0 - _sigmoid(glo))
+    sg_hi = _sigmoid(ghi) * (1.0 - _sigmoid(ghi))
+    dg_lo = d_lo * sg_lo * (mn - ref)
+    dg_hi = np.where(floored, 0.0, d_hi * sg_hi * (mx - ref))
+    if floored.any():
+        s1 = np.zeros(out * G)
+        np.add.at(s1, gidx, d1)
+        dg_lo = np.where(floored, s1 * sg_lo * (mn - ref), dg_lo)
+    r.update(d_gamma_lo=dg_lo, d_gamma_hi=dg_hi)
+    h = _f64(w1).shape[1]
+    if hard:
+        r.update(d_w1=np.zeros_like(_f64(w1)), d_b1=np.zeros(h), d_w2=np.zeros_like(_f64(w2)), d_b2=np.zeros(nr))
+        return r
+    reg_coeff = sched[4] * (avg_bits - sched_b)
+    d_gate = np.stack([(resid * P[e + 1]).sum(axis=1) for e in range(nr)], axis=1) + reg_coeff
+    d_score = d_gate * tau * gates * (1.0 - gates)
+    d_act = (d_score @ _f64(w2).T) * (_sigmoid(hpre) * (1.0 + hpre * (1.0 - _sigmoid(hpre))))
+    r.update(d_w2=hact.T @ d_score, d_b2=d_score.sum(axis=0), d_w1=x.T @ d_act, d_b1=d_act.sum(axis=0))
+    return r

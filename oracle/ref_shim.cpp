@@ -20,6 +20,7 @@
 #include "mobi/qcore.hpp"
 #include "mobi/router.hpp"
 #include "mobi/slicer.hpp"
+#include "mobi/trainer.hpp"
 
 using namespace mobi;
 
@@ -379,6 +380,50 @@ int ref_layer_forward_rowsharded(const double* x, int64_t T, int64_t in, const u
         for (auto& t : pool) t.join();
         for (auto& e : errs)
             if (!e.empty()) throw std::invalid_argument(e);
+    });
+}
+
+// trainer.hpp:203-263 joint_forward + 341-396 joint_backward (one stage-2 calibration step).
+// scalars[6] = data_term, reg_term, avg_bits, sched_b, loss, tau.  Gradients are written only when
+// d_gamma_lo is non-null.
+int ref_joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* slice_bits,
+                   int32_t n_slices, const double* gamma_lo, const double* gamma_hi, const double* w1,
+                   const double* b1, const double* w2, const double* b2, int64_t h, const double* x,
+                   const double* y_fp, int64_t T, double b_init, double b_target, int64_t total_steps,
+                   int32_t shape, double reg_weight, int64_t t, int32_t force_gates_on, double* y_hat,
+                   double* scalars, double* d_gamma_lo, double* d_gamma_hi, double* d_w1, double* d_b1,
+                   double* d_w2, double* d_b2) {
+    return guard([&] {
+        trainer::QuantLayer L;
+        L.w = mat(w, out, in);
+        L.group_size = static_cast<std::size_t>(gs);
+        L.slice_bits.assign(slice_bits, slice_bits + n_slices);
+        L.stats = qcore::GroupStats::from_weights(L.w, L.group_size);
+        const std::size_t ng = L.stats.min.size();
+        L.clip.gamma_lo.assign(gamma_lo, gamma_lo + ng);
+        L.clip.gamma_hi.assign(gamma_hi, gamma_hi + ng);
+        L.rs = router_of(in, h, n_slices - 1, w1, b1, w2, b2);
+        trainer::BudgetSchedule sc;
+        sc.b_init = b_init;
+        sc.b_target = b_target;
+        sc.total_steps = static_cast<std::size_t>(total_steps);
+        sc.shape = static_cast<trainer::ScheduleShape>(shape);
+        sc.reg_weight = reg_weight;
+        trainer::JointOptions opt;
+        opt.force_gates_on = force_gates_on != 0;
+        const Matrix X = mat(x, T, in), Y = mat(y_fp, T, out);
+        trainer::JointForward f = trainer::joint_forward(L, X, Y, sc, static_cast<std::size_t>(t), opt);
+        if (y_hat) put(f.y_hat, y_hat);
+        const double sv[6] = {f.data_term, f.reg_term, f.avg_bits, f.sched_b, f.loss, f.tau};
+        std::copy(sv, sv + 6, scalars);
+        if (!d_gamma_lo) return;
+        trainer::JointGrads g = trainer::joint_backward(L, f, X, Y, sc);
+        std::copy(g.d_gamma_lo.begin(), g.d_gamma_lo.end(), d_gamma_lo);
+        std::copy(g.d_gamma_hi.begin(), g.d_gamma_hi.end(), d_gamma_hi);
+        put(g.d_w1, d_w1);
+        std::copy(g.d_b1.begin(), g.d_b1.end(), d_b1);
+        put(g.d_w2, d_w2);
+        std::copy(g.d_b2.begin(), g.d_b2.end(), d_b2);
     });
 }
 

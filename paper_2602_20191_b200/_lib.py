@@ -64,6 +64,8 @@ _SIGS = {
     "mobi_calibrate_threshold": [_p, _i64, _f64, C.POINTER(_f64), _p],
     "mobi_avg_bits": [_p, _i64, _p, _i32, C.POINTER(_f64), _p],
     "mobi_decompose": [_p, _i64, _i64, _i64, _p, _i32, _f64, _p, _p, _p, _p, _p],
+    "mobi_joint_step": [_p, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _i64, _p, _i64, _i32,
+                        _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "mobi_layer_last_launches": [_p, C.POINTER(_i32)],
     "mobi_layer_debug_impl": [_p, C.c_int],
     "mobi_layer_last_plan": [_p, C.POINTER(_i32)],

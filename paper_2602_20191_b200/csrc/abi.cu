@@ -36,6 +36,12 @@ int func_attr_once_impl(const void* fn, cudaFuncAttribute attr, int value) {
     return MOBI_OK;
 }
 
+int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* slice_bits, int32_t E,
+               const double* gamma_lo, const double* gamma_hi, const double* w1, const double* b1, const double* w2,
+               const double* b2, int64_t h, const double* x, const double* y_fp, int64_t T,
+               const mobi_budget_schedule* sched, int64_t t, int32_t force_on, double* y_hat_out,
+               mobi_joint_scalars* res, double* d_gamma_lo, double* d_gamma_hi, double* d_w1, double* d_b1,
+               double* d_w2, double* d_b2, cudaStream_t st);
 int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* cperm, int32_t* inverse,
                    int32_t* hist256, cudaStream_t st);
 
@@ -1096,6 +1102,33 @@ int mobi_decompose(const double* w, int64_t out, int64_t in, int64_t group_size,
     CHECK_ARG(w && codes && scale && zero && slice_bits, "decompose: null argument");
     return launch_decompose(w, out, in, group_size, slice_bits, n_slices, gamma, codes, scale, zero, clamp_counts,
                             S(stream));
+}
+
+int mobi_joint_step(const double* w, int64_t out, int64_t in, int64_t group_size, const int32_t* slice_bits,
+                    int32_t n_slices, const double* gamma_lo, const double* gamma_hi, const double* w1, const double* b1,
+                    const double* w2, const double* b2, int64_t hidden, const double* x, const double* y_fp, int64_t T,
+                    const mobi_budget_schedule* sched, int64_t t, int32_t force_gates_on, double* y_hat,
+                    mobi_joint_scalars* scalars, double* d_gamma_lo, double* d_gamma_hi, double* d_w1, double* d_b1,
+                    double* d_w2, double* d_b2, void* stream) {
+    CHECK_ARG(w && slice_bits && gamma_lo && gamma_hi && x && y_fp && sched && scalars, "joint_step: null argument");
+    CHECK_ARG(force_gates_on || (w1 && b1 && w2 && b2), "joint_step: null router argument");
+    CHECK_ARG(!d_gamma_lo || (d_gamma_hi && d_w1 && d_b1 && d_w2 && d_b2), "joint_step: null gradient argument");
+    CHECK_ARG(out > 0 && in > 0 && group_size > 0 && T > 0 && hidden > 0, "joint_step: empty dimension");
+    CHECK_ARG(n_slices >= 2 && n_slices <= MOBI_MAX_SLICES, "joint_step: need 2.." << MOBI_MAX_SLICES << " slices");
+    int total = 0;
+    for (int e = 0; e < n_slices; ++e) {
+        CHECK_ARG(slice_bits[e] >= 1 && slice_bits[e] <= 8, "joint_step: slice bit width " << slice_bits[e]);
+        total += slice_bits[e];
+    }
+    CHECK_ARG(total <= 8, "joint_step: total bits " << total << " exceed the 8-bit code budget");
+    CHECK_ARG(sched->total_steps >= 1 && sched->shape >= 0 && sched->shape <= 3, "joint_step: bad schedule");
+    CHECK_ARG(t >= 1 && t <= sched->total_steps,
+              "schedule_value: step " << t << " outside [1," << sched->total_steps << "]");
+    CHECK_ARG(sched->shape != 3 || (sched->b_init > 0.0 && sched->b_target > 0.0),
+              "schedule_value: exponential shape needs positive bits");
+    return joint_step(w, out, in, group_size, slice_bits, n_slices, gamma_lo, gamma_hi, w1, b1, w2, b2, hidden, x,
+                      y_fp, T, sched, t, force_gates_on, y_hat, scalars, d_gamma_lo, d_gamma_hi, d_w1, d_b1, d_w2,
+                      d_b2, S(stream));
 }
 
 int mobi_layer_profile(mobi_layer_t L, int enable) {

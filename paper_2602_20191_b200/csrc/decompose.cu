@@ -16,8 +16,10 @@ namespace {
 // one thread per (row, group): stats -> params -> all slices of the group's elements
 __global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int64_t in, int64_t gs,
                                  int64_t G, const int32_t* __restrict__ bits_dev, int E, double sq_lo,
-                                 double sq_hi, uint8_t* __restrict__ codes, double* __restrict__ scale,
-                                 double* __restrict__ zero, unsigned long long* __restrict__ clamp_counts) {
+                                 double sq_hi, const double* __restrict__ sq_lo_g,
+                                 const double* __restrict__ sq_hi_g, uint8_t* __restrict__ codes,
+                                 double* __restrict__ scale, double* __restrict__ zero,
+                                 double* __restrict__ stats, unsigned long long* __restrict__ clamp_counts) {
     const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= out * G) return;
     const int64_t r = gi / G, g = gi % G;
@@ -32,6 +34,15 @@ __global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int6
     // GroupStats::ref = min(max(0, min), max); clip_lo/hi; params_from_clip
     const double lo0 = mn > 0.0 ? mn : 0.0;
     const double ref = mx < lo0 ? mx : lo0;
+    if (sq_lo_g) {  // per-group clip (a calibration step's gammas)
+        sq_lo = sq_lo_g[gi];
+        sq_hi = sq_hi_g[gi];
+    }
+    if (stats) {  // GroupStats min / max / ref, [3][out*G]
+        stats[gi] = mn;
+        stats[out * G + gi] = mx;
+        stats[2 * out * G + gi] = ref;
+    }
     const double lo = __dadd_rn(ref, __dmul_rn(sq_lo, __dsub_rn(mn, ref)));
     const double hi = __dadd_rn(ref, __dmul_rn(sq_hi, __dsub_rn(mx, ref)));
     const int b1 = bits_dev[0];
@@ -87,8 +98,8 @@ int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const
     MOBI_CUDA(cudaMallocAsync(&cc, sizeof(unsigned long long) * MOBI_MAX_SLICES, st));
     MOBI_CUDA(cudaMemcpyAsync(bits_dev, bits, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st));
     MOBI_CUDA(cudaMemsetAsync(cc, 0, sizeof(unsigned long long) * MOBI_MAX_SLICES, st));
-    decompose_kernel<<<(unsigned)cdiv(out * G, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, sq, sq, codes,
-                                                                   scale, zero, cc);
+    decompose_kernel<<<(unsigned)cdiv(out * G, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, sq, sq, nullptr,
+                                                                   nullptr, codes, scale, zero, nullptr, cc);
     MOBI_LAUNCH_CHECK();
     unsigned long long h[MOBI_MAX_SLICES];
     MOBI_CUDA(cudaMemcpyAsync(h, cc, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -97,6 +108,19 @@ int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const
         for (int e = 0; e < E; ++e) clamp_counts_host[e] = (int64_t)h[e];
     cudaFreeAsync(bits_dev, st);
     cudaFreeAsync(cc, st);
+    return MOBI_OK;
+}
+
+// The calibration step's decomposition (trainer.hpp:166-168 QuantLayer::decompose): per-group clip
+// squashes sq_lo_g / sq_hi_g (device, evaluated on the host with the reference's libm), the group
+// statistics written to stats [3][out*G].  bits_dev is device memory; asynchronous.
+int launch_decompose_clip(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* bits_dev, int32_t E,
+                          const double* sq_lo_g, const double* sq_hi_g, uint8_t* codes, double* scale, double* zero,
+                          double* stats, unsigned long long* clamp_counts, cudaStream_t st) {
+    const int64_t G = cdiv(in, gs);
+    decompose_kernel<<<(unsigned)cdiv(out * G, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, 0.0, 0.0, sq_lo_g,
+                                                                   sq_hi_g, codes, scale, zero, stats, clamp_counts);
+    MOBI_LAUNCH_CHECK();
     return MOBI_OK;
 }
 

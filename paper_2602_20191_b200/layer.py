@@ -356,3 +356,67 @@ def decompose(w: torch.Tensor, group_size: int, slice_bits: Sequence[int], gamma
                                _stream_ptr(stream)))
     return codes, scale, zero, cc
 
+
+
+class BudgetSchedule(C.Structure):
+    """trainer::BudgetSchedule (trainer.hpp:45-51); shape 0 log / 1 linear / 2 cosine / 3 exp."""
+    _fields_ = [("b_init", C.c_double), ("b_target", C.c_double), ("total_steps", C.c_int64),
+                ("shape", C.c_int32), ("reg_weight", C.c_double)]
+
+
+class _JointScalars(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("data_term", "reg_term", "avg_bits", "sched_b", "loss", "tau")]
+
+
+_SHAPES = {"log": 0, "logarithmic": 0, "linear": 1, "cosine": 2, "exp": 3, "exponential": 3}
+
+
+def joint_step(w: torch.Tensor, group_size: int, slice_bits: Sequence[int], gamma_lo, gamma_hi,
+               w1: Optional[torch.Tensor], b1, w2, b2, x: torch.Tensor, y_fp: torch.Tensor, sched, t: int,
+               force_gates_on: bool = False, backward: bool = True, stream=None) -> dict:
+    """One stage-2 calibration step on the GPU (fp64): trainer::joint_forward (trainer.hpp:203-263)
+    and, with backward=True, trainer::joint_backward (trainer.hpp:341-396).
+
+    w [out, in], x [T, in], y_fp [T, out] and the router (w1 [in, h], b1 [h], w2 [h, E-1], b2 [E-1]) are
+    CUDA fp64 tensors; gamma_lo / gamma_hi are the per-group clip parameters (host arrays,
+    out*ceil(in/group_size)); sched = (b_init, b_target, total_steps, shape, reg_weight) with shape an
+    int or "log" / "linear" / "cosine" / "exp".  Returns the JointForward scalars, y_hat and (backward)
+    d_gamma_lo / d_gamma_hi (numpy) and d_w1 / d_b1 / d_w2 / d_b2 (CUDA tensors).
+    """
+    dev = x.device
+    f64 = lambda a: a.to(device=dev, dtype=torch.float64).contiguous()  # noqa: E731
+    w, x, y_fp = f64(w), f64(x), f64(y_fp)
+    out, inn = w.shape
+    T = x.shape[0]
+    sb = _arr(slice_bits, np.int32)
+    nr = sb.size - 1
+    G = (inn + group_size - 1) // group_size
+    glo = _arr(np.broadcast_to(np.asarray(gamma_lo, np.float64), (out * G,)), np.float64)
+    ghi = _arr(np.broadcast_to(np.asarray(gamma_hi, np.float64), (out * G,)), np.float64)
+    if w1 is None:
+        w1 = torch.zeros((inn, 1), dtype=torch.float64, device=dev)
+        b1 = torch.zeros(1, dtype=torch.float64, device=dev)
+        w2 = torch.zeros((1, max(nr, 1)), dtype=torch.float64, device=dev)
+        b2 = torch.zeros(max(nr, 1), dtype=torch.float64, device=dev)
+    w1, b1, w2, b2 = f64(w1), f64(b1), f64(w2), f64(b2)
+    h = w1.shape[1]
+    bi, bt, L, shape, rw = sched
+    sc = BudgetSchedule(float(bi), float(bt), int(L), int(_SHAPES.get(shape, shape)), float(rw))
+    res = _JointScalars()
+    y_hat = torch.empty((T, out), dtype=torch.float64, device=dev)
+    g = {}
+    if backward:
+        g = dict(d_gamma_lo=np.zeros(out * G), d_gamma_hi=np.zeros(out * G), d_w1=torch.empty_like(w1),
+                 d_b1=torch.empty_like(b1), d_w2=torch.empty_like(w2), d_b2=torch.empty_like(b2))
+    gp = (lambda k: g[k].ctypes.data if isinstance(g[k], np.ndarray) else g[k].data_ptr()) if backward \
+        else (lambda k: None)
+    with torch.cuda.device(dev):
+        check(lib().mobi_joint_step(w.data_ptr(), out, inn, group_size, sb.ctypes.data, sb.size, glo.ctypes.data,
+                                    ghi.ctypes.data, w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(), h,
+                                    x.data_ptr(), y_fp.data_ptr(), T, C.byref(sc), int(t), int(bool(force_gates_on)),
+                                    y_hat.data_ptr(), C.byref(res), gp("d_gamma_lo"), gp("d_gamma_hi"), gp("d_w1"),
+                                    gp("d_b1"), gp("d_w2"), gp("d_b2"), _stream_ptr(stream)))
+    r = {k: getattr(res, k) for k, _ in _JointScalars._fields_}
+    r["y_hat"] = y_hat
+    r.update(g)
+    return r

@@ -74,3 +74,24 @@ def test_ratio_from_target_bits_mirror(orc):
         assert ratio_from_target_bits(t, [2, 2, 2, 2]) == orc.ratio_from_target_bits(t, [2, 2, 2, 2])
     with pytest.raises(ValueError, match="outside"):
         ratio_from_target_bits(1.5, [2, 2, 2, 2])
+
+
+def test_joint_step_validates_like_the_reference(lib):
+    """mobi_joint_step rejects bad schedules / slice layouts before touching a device (the reference's
+    MOBI_CHECKs in schedule_value / gate_soft, trainer.hpp:52-56, router.hpp:79-81)."""
+    import ctypes as C
+    import numpy as np
+    from paper_2602_20191_b200.layer import BudgetSchedule, _JointScalars
+    sb = np.array([2, 2, 2, 2], np.int32)
+    g = np.zeros(4)
+    res = _JointScalars()
+    dummy = C.c_void_p(16)  # never dereferenced: validation fails first
+    for sched, t, bits, msg in [(BudgetSchedule(8, 3, 10, 0, 1e-3), 0, sb, b"outside [1,10]"),
+                                (BudgetSchedule(8, 3, 10, 0, 1e-3), 11, sb, b"outside [1,10]"),
+                                (BudgetSchedule(8, 0, 10, 3, 1e-3), 2, sb, b"exponential"),
+                                (BudgetSchedule(8, 3, 10, 0, 1e-3), 2, np.array([4, 4, 2], np.int32), b"exceed"),
+                                (BudgetSchedule(8, 3, 10, 0, 1e-3), 2, np.array([8], np.int32), b"slices")]:
+        rc = lib.mobi_joint_step(dummy, 4, 8, 8, bits.ctypes.data, bits.size, g.ctypes.data, g.ctypes.data, dummy,
+                                 dummy, dummy, dummy, 2, dummy, dummy, 3, C.byref(sched), t, 0, None, C.byref(res),
+                                 None, None, None, None, None, None, None)
+        assert rc == 1 and msg in lib.mobi_last_error(), (rc, lib.mobi_last_error())

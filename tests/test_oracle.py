@@ -238,3 +238,60 @@ def test_golden_qo_T4(orc):
     assert np.array_equal(g, z["g"])
     y = orc.forward_elastic(z["x"], L["codes"], L["slice_bits"], L["scale"], L["zero"], 128, g)
     assert np.array_equal(y, z["y"])
+
+
+# ---- stage-2 calibration step (trainer.hpp:203-263, 341-396) ----
+
+def joint_case(out=48, inn=160, T=24, h=16, gs=64, slice_bits=(2, 2, 2, 2), seed=5):
+    """Small calibration-step inputs: partial groups (160 = 2.5 x 64), one constant group (the
+    epsilon-floored scale branch, trainer.hpp:323-337), random clip gammas and a non-zero w2."""
+    rng = np.random.default_rng(seed)
+    w = rng.normal(0, 0.02, (out, inn))
+    w[3, 64:128] = 0.01  # constant group -> floored scale
+    G = (inn + gs - 1) // gs
+    glo = rng.uniform(1.0, 5.0, out * G)
+    ghi = rng.uniform(1.0, 5.0, out * G)
+    nr = len(slice_bits) - 1
+    w1 = rng.normal(0, 1 / np.sqrt(inn), (inn, h))
+    b1 = rng.normal(0, 0.1, h)
+    w2 = rng.normal(0, 0.5, (h, nr))
+    b2 = rng.normal(0, 0.1, nr)
+    x = rng.normal(0, 1.0, (T, inn))
+    y_fp = x @ w.T
+    return dict(w=w, group_size=gs, slice_bits=slice_bits, gamma_lo=glo, gamma_hi=ghi, w1=w1, b1=b1, w2=w2,
+                b2=b2, x=x, y_fp=y_fp)
+
+
+JOINT_KEYS = ("y_hat", "d_gamma_lo", "d_gamma_hi", "d_w1", "d_b1", "d_w2", "d_b2")
+
+
+def assert_joint_close(a, b, rtol=1e-9):
+    for k in ("data_term", "reg_term", "avg_bits", "sched_b", "loss", "tau"):
+        assert abs(a[k] - b[k]) <= rtol * max(1.0, abs(b[k])), (k, a[k], b[k])
+    for k in JOINT_KEYS:
+        if k not in b:
+            continue
+        scale = max(np.abs(b[k]).max(), 1e-300)
+        err = np.abs(np.asarray(a[k]) - b[k]).max() / scale
+        assert err <= rtol, (k, err)
+
+
+@pytest.mark.skipif(not O.LIB_REF.exists(), reason="reference library not built")
+@pytest.mark.parametrize("sched,t,force", [((8.0, 3.0, 10, 0, 1e-3), 4, False),   # soft gates, log schedule
+                                          ((8.0, 3.0, 10, 0, 1e-3), 10, False),  # t = L: indicator gates
+                                          ((6.0, 2.5, 7, 2, 1e-2), 3, False),    # cosine schedule
+                                          ((6.0, 2.5, 7, 3, 1e-2), 5, False),    # exponential
+                                          ((8.0, 3.0, 10, 1, 1e-3), 2, True)])   # force_gates_on ablation
+def test_joint_step_restatement_matches_reference(sched, t, force):
+    c = joint_case()
+    ref = O.reference().joint_step(**c, sched=sched, t=t, force_gates_on=force)
+    port = O.joint_step_np(**c, sched=sched, t=t, force_gates_on=force)
+    assert_joint_close(port, ref)
+    assert np.abs(ref["d_gamma_lo"]).max() > 0 and (force or t == 10 or np.abs(ref["d_w1"]).max() > 0)
+
+
+@pytest.mark.skipif(not O.LIB_REF.exists(), reason="reference library not built")
+def test_joint_step_non_uniform_slices():
+    c = joint_case(slice_bits=(4, 2, 2), seed=9)
+    sched = (8.0, 3.0, 12, 1, 1e-3)
+    assert_joint_close(O.joint_step_np(**c, sched=sched, t=5), O.reference().joint_step(**c, sched=sched, t=5))
