@@ -5,8 +5,8 @@
 // gradients through gate_soft / SiLU).
 //
 // This is offline calibration, not the inference hot path: it runs once per layer per optimiser
-// step.  The matrix products are a shared-memory tiled fp64 GEMM (64x64 tiles, 4x4 outputs per
-// thread, k-ordered sums -> deterministic); the reductions the reference performs in a fixed order
+// step.  The matrix products are a shared-memory tiled fp64 tensor-core GEMM (DMMA m8n8k4, 128x64
+// CTA tiles; a fixed k order -> deterministic); the reductions the reference performs in a fixed order
 // (per-group clip sums, column sums of the bias gradients) keep that order (one thread per group /
 // column), every other reduction is a fixed two-level tree, so repeated steps are bit-identical.
 // The per-group sigmoid of the clip gammas is evaluated on the host with the reference's libm
@@ -24,7 +24,7 @@ int launch_decompose_clip(const double* w, int64_t out, int64_t in, int64_t gs, 
 
 namespace {
 
-constexpr int kTile = 64, kTk = 16, kGemmThreads = 256, kRedThreads = 256;
+constexpr int kBM = 128, kBN = 64, kTk = 16, kGemmThreads = 256, kRedThreads = 256;
 
 __device__ __forceinline__ double sigmoid_d(double v) {  // common.hpp:125-131
     if (v >= 0.0) return 1.0 / (1.0 + exp(-v));
@@ -33,59 +33,76 @@ __device__ __forceinline__ double sigmoid_d(double v) {  // common.hpp:125-131
 }
 
 // C[i][j] = Σ_k A(i,k)·s(k)·B(k,j) (+ bias[j]); A(i,k) = A[i·sai + k·sak], B(k,j) = B[k·sbk + j·sbj],
-// s(k) = ascale[k·sas] when given (the gate scaling of dP_e, trainer.hpp:351-357).  Each thread owns
-// rows ty + 16r and columns tx + 16c of the 64x64 tile (conflict-free shared reads, coalesced stores).
-__global__ void __launch_bounds__(kGemmThreads) dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A,
+// s(k) = ascale[k·sas] when given (the gate scaling of dP_e, trainer.hpp:351-357).  fp64 tensor cores:
+// mma.sync m8n8k4 (DMMA), 128x64 CTA tile, 8 warps of 32x32 (4x4 MMA tiles each), k staged 16 at a
+// time through shared memory (the unit-stride dimension walked by consecutive threads on load).
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 2) dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A,
                                                              int64_t sai, int64_t sak, const double* __restrict__ B,
                                                              int64_t sbk, int64_t sbj, const double* __restrict__ ascale,
                                                              int64_t sas, const double* __restrict__ bias,
                                                              double* __restrict__ C, int64_t ldc) {
-    __shared__ double As[kTk][kTile + 1];
-    __shared__ double Bs[kTk][kTile + 1];
-    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int64_t i0 = (int64_t)blockIdx.y * kTile, j0 = (int64_t)blockIdx.x * kTile;
-    double acc[4][4] = {};
+    // +8 doubles per row: a fragment load's four k rows take two bank halves (two wavefronts, the
+    // minimum for 32 doubles); the column index is XOR-swizzled by (k >> 1) & 7 inside each 8-column
+    // group so the k-fast stores of a k-contiguous operand also spread over all banks
+    __shared__ double As[kTk][kBM + 8];
+    __shared__ double Bs[kTk][kBN + 8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int64_t i0 = (int64_t)blockIdx.y * kBM, j0 = (int64_t)blockIdx.x * kBN;
+    double acc[4][4][2] = {};
     for (int64_t k0 = 0; k0 < K; k0 += kTk) {
 #pragma unroll
-        for (int l = 0; l < kTile * kTk / kGemmThreads; ++l) {
+        for (int l = 0; l < kBM * kTk / kGemmThreads; ++l) {
             const int idx = tid + l * kGemmThreads;
-            // walk the unit-stride dimension with consecutive threads
-            const int ii = sak == 1 ? idx / kTk : idx % kTile, kk = sak == 1 ? idx % kTk : idx / kTile;
+            const int ii = sak == 1 ? idx / kTk : idx % kBM, kk = sak == 1 ? idx % kTk : idx / kBM;
             const int64_t i = i0 + ii, k = k0 + kk;
             double a = 0.0;
             if (i < M && k < K) {
                 a = A[i * sai + k * sak];
                 if (ascale) a *= ascale[k * sas];
             }
-            As[kk][ii] = a;
-            const int jj = sbj == 1 ? idx % kTile : idx / kTk, kb = sbj == 1 ? idx / kTile : idx % kTk;
-            const int64_t j = j0 + jj, kbk = k0 + kb;
-            Bs[kb][jj] = (j < N && kbk < K) ? B[kbk * sbk + j * sbj] : 0.0;
+            As[kk][ii ^ ((kk >> 1) & 7)] = a;
+        }
+#pragma unroll
+        for (int l = 0; l < kBN * kTk / kGemmThreads; ++l) {
+            const int idx = tid + l * kGemmThreads;
+            const int jj = sbj == 1 ? idx % kBN : idx / kTk, kb = sbj == 1 ? idx / kBN : idx % kTk;
+            const int64_t j = j0 + jj, k = k0 + kb;
+            Bs[kb][jj ^ ((kb >> 1) & 7)] = (j < N && k < K) ? B[k * sbk + j * sbj] : 0.0;
         }
         __syncthreads();
 #pragma unroll
-        for (int kk = 0; kk < kTk; ++kk) {
+        for (int ks = 0; ks < kTk; ks += 4) {
             double a[4], b[4];
+            const int sw = ((ks + q) >> 1) & 7;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+            for (int m = 0; m < 4; ++m) a[m] = As[ks + q][(wm + m * 8 + g) ^ sw];  // A frag: row g, col q
 #pragma unroll
-            for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
+            for (int n = 0; n < 4; ++n) b[n] = Bs[ks + q][(wn + n * 8 + g) ^ sw];  // B frag: row q, col g
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
+            for (int m = 0; m < 4; ++m)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+                for (int n = 0; n < 4; ++n) dmma(acc[m][n], a[m], b[n]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t i = i0 + ty + 16 * r;
+    for (int m = 0; m < 4; ++m) {
+        const int64_t i = i0 + wm + m * 8 + g;
         if (i >= M) continue;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            const int64_t j = j0 + tx + 16 * c;
-            if (j < N) C[i * ldc + j] = bias ? acc[r][c] + bias[j] : acc[r][c];
-        }
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // C frag: row g, cols 2q, 2q+1
+                const int64_t j = j0 + wn + n * 8 + 2 * q + h;
+                if (j < N) C[i * ldc + j] = bias ? acc[m][n][h] + bias[j] : acc[m][n][h];
+            }
     }
 }
 
@@ -267,7 +284,7 @@ inline unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>(cdiv(n,
 int dgemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t sai, int64_t sak, const double* B, int64_t sbk,
           int64_t sbj, const double* ascale, int64_t sas, const double* bias, double* C, int64_t ldc, cudaStream_t st) {
     if (M <= 0 || N <= 0) return MOBI_OK;
-    dim3 grid((unsigned)cdiv(N, kTile), (unsigned)cdiv(M, kTile));
+    dim3 grid((unsigned)cdiv(N, kBN), (unsigned)cdiv(M, kBM));
     dgemm_kernel<<<grid, kGemmThreads, 0, st>>>(M, N, K, A, sai, sak, B, sbk, sbj, ascale, sas, bias, C, ldc);
     MOBI_LAUNCH_CHECK();
     return MOBI_OK;
@@ -319,6 +336,15 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
                double* d_w2, double* d_b2, cudaStream_t st) {
     const int nr = E - 1;
     const int64_t G = cdiv(in, gs), NG = out * G, TO = T * out;
+    {  // keep the stream-ordered scratch (hundreds of MB at LLaMA shapes) mapped between steps: the
+       // default pool would otherwise return it to the OS at every synchronize and re-map it next step
+        int dev = 0;
+        cudaMemPool_t pool;
+        MOBI_CUDA(cudaGetDevice(&dev));
+        MOBI_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t keep = UINT64_MAX;
+        MOBI_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     DevBuf buf{st, {}};
     // host side: per-group squash / squash' with the reference's libm; schedule, temperature
     std::vector<double> hq(4 * NG);
