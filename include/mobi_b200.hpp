@@ -15,6 +15,8 @@
 //   router::avg_bits(gates, slice_bits)         ->    mobi_b200::avg_bits(gates, slice_bits)
 //   bitplane::permute_by_slice(tokens, masks)   ->    mobi_b200::permute_by_slice(tokens, masks)
 //   (multi-GPU)                    ->    mobi_b200::ShardedLayer(stack, rs, comm, rank, P, mode)
+//   trainer::joint_forward + joint_backward     ->    mobi_b200::joint_step(layer, x, y_fp, sched, t, opt)
+//   (trainer.hpp:203-263, 341-396)                    (one stage-2 calibration step, fp64, on the GPU)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -265,6 +267,63 @@ double avg_bits(const Matrix& gates, const std::vector<int>& slice_bits) {
     double out = 0.0;
     check(mobi_avg_bits(dm.p, static_cast<int64_t>(m.size()), b.data(), static_cast<int32_t>(b.size()), &out, nullptr));
     return out;
+}
+
+// trainer::joint_forward + trainer::joint_backward (trainer.hpp:203-263, 341-396) on the GPU, fp64.
+// QuantLayer / BudgetSchedule / JointOptions are the reference's types (trainer.hpp:45-51, 136-169,
+// 182-184); the result carries JointForward's scalars and y_hat and JointGrads' fields.
+template <class Matrix>
+struct JointStep {
+    double data_term = 0, reg_term = 0, avg_bits = 0, sched_b = 0, loss = 0, tau = 0;
+    bool hard = false;
+    Matrix y_hat;
+    std::vector<double> d_gamma_lo, d_gamma_hi, d_b1, d_b2;
+    Matrix d_w1, d_w2;
+};
+
+template <class QuantLayer, class Matrix, class Schedule, class Options>
+JointStep<Matrix> joint_step(const QuantLayer& L, const Matrix& x, const Matrix& y_fp, const Schedule& sc, size_t t,
+                             const Options& opt, bool backward = true) {
+    const int64_t out = (int64_t)L.w.rows(), in = (int64_t)L.w.cols(), T = (int64_t)x.rows();
+    if (x.cols() != L.w.cols()) throw std::invalid_argument("joint_forward: input dim mismatch");
+    if (y_fp.rows() != x.rows() || y_fp.cols() != L.w.rows())
+        throw std::invalid_argument("joint_forward: reference output shape mismatch");
+    const int64_t h = (int64_t)L.rs.w1.cols(), nr = (int64_t)L.rs.w2.cols();
+    std::vector<int32_t> bits(L.slice_bits.begin(), L.slice_bits.end());
+    auto vec = [](const Matrix& m) { return std::vector<double>(m.data(), m.data() + m.size()); };
+    detail::DevBuf<double> w(vec(L.w)), dx(vec(x)), dy(vec(y_fp)), w1(vec(L.rs.w1)), b1(L.rs.b1), w2(vec(L.rs.w2)),
+        b2(L.rs.b2), yh(static_cast<size_t>(T * out)), gw1(static_cast<size_t>(in * h)), gb1(static_cast<size_t>(h)),
+        gw2(static_cast<size_t>(h * nr)), gb2(static_cast<size_t>(nr));
+    mobi_budget_schedule bs{sc.b_init, sc.b_target, (int64_t)sc.total_steps, (int32_t)sc.shape, sc.reg_weight};
+    mobi_joint_scalars r{};
+    JointStep<Matrix> o;
+    const size_t ng = L.clip.gamma_lo.size();
+    o.d_gamma_lo.assign(ng, 0.0);
+    o.d_gamma_hi.assign(ng, 0.0);
+    check(mobi_joint_step(w.p, out, in, (int64_t)L.group_size, bits.data(), (int32_t)bits.size(), L.clip.gamma_lo.data(),
+                          L.clip.gamma_hi.data(), w1.p, b1.p, w2.p, b2.p, h, dx.p, dy.p, T, &bs, (int64_t)t,
+                          opt.force_gates_on ? 1 : 0, yh.p, &r, backward ? o.d_gamma_lo.data() : nullptr,
+                          o.d_gamma_hi.data(), gw1.p, gb1.p, gw2.p, gb2.p, nullptr));
+    o.data_term = r.data_term;
+    o.reg_term = r.reg_term;
+    o.avg_bits = r.avg_bits;
+    o.sched_b = r.sched_b;
+    o.loss = r.loss;
+    o.tau = r.tau;
+    o.hard = opt.force_gates_on || t == sc.total_steps;
+    auto mat = [](const std::vector<double>& v, size_t rows, size_t cols) {
+        Matrix m(rows, cols);
+        std::copy(v.begin(), v.end(), m.data());
+        return m;
+    };
+    o.y_hat = mat(yh.download(), (size_t)T, (size_t)out);
+    if (backward) {
+        o.d_w1 = mat(gw1.download(), (size_t)in, (size_t)h);
+        o.d_w2 = mat(gw2.download(), (size_t)h, (size_t)nr);
+        o.d_b1 = gb1.download();
+        o.d_b2 = gb2.download();
+    }
+    return o;
 }
 
 // bitplane::permute_by_slice (bitplane.hpp:178-201): stable sort of tokens by mask

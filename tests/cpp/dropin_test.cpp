@@ -12,6 +12,7 @@
 #include "mobi/bitplane.hpp"
 #include "mobi/router.hpp"
 #include "mobi/slicer.hpp"
+#include "mobi/trainer.hpp"
 #include "mobi_b200.hpp"
 
 using namespace mobi;
@@ -139,10 +140,54 @@ int run_case(size_t out, size_t in, size_t gs, size_t T, unsigned seed) {
     return 0;
 }
 
+// trainer::joint_forward / joint_backward (the stage-2 calibration step) next to mobi_b200::joint_step
+int run_joint(size_t out, size_t in, size_t T, unsigned seed) {
+    Rng rng(seed);
+    Matrix w(out, in);
+    for (size_t i = 0; i < w.size(); ++i) w[i] = 0.02 * rng.normal();
+    trainer::QuantLayer L = trainer::QuantLayer::init(w, {2, 2, 2, 2}, 128, 10, rng, 4.0);
+    for (auto& v : L.rs.w2.vec()) v = 0.5 * rng.normal();
+    for (size_t g = 0; g < L.clip.gamma_lo.size(); ++g) {
+        L.clip.gamma_lo[g] = 1.0 + 4.0 * rng.uniform();
+        L.clip.gamma_hi[g] = 1.0 + 4.0 * rng.uniform();
+    }
+    Matrix x(T, in);
+    for (size_t i = 0; i < x.size(); ++i) x[i] = rng.normal();
+    Matrix y = matmul_nt(x, w);
+    trainer::BudgetSchedule sc;
+    sc.total_steps = 10;
+    sc.reg_weight = 1e-3;
+    trainer::JointOptions opt;
+    for (size_t t : {3u, 10u}) {
+        trainer::JointForward f = trainer::joint_forward(L, x, y, sc, t, opt);
+        trainer::JointGrads g = trainer::joint_backward(L, f, x, y, sc);
+        auto r = mobi_b200::joint_step(L, x, y, sc, t, opt);
+        auto rel = [](const double* a, const double* b, size_t n) {
+            double m = 0, d = 0;
+            for (size_t i = 0; i < n; ++i) {
+                m = std::max(m, std::fabs(b[i]));
+                d = std::max(d, std::fabs(a[i] - b[i]));
+            }
+            return m > 0 ? d / m : d;
+        };
+        EXPECT(std::fabs(r.loss - f.loss) <= 1e-9 * std::fabs(f.loss), "joint loss t=%zu", t);
+        EXPECT(r.avg_bits == f.avg_bits && r.sched_b == f.sched_b && r.tau == f.tau, "joint scalars t=%zu", t);
+        EXPECT(rel(r.y_hat.data(), f.y_hat.data(), f.y_hat.size()) <= 1e-9, "joint y_hat t=%zu", t);
+        EXPECT(rel(r.d_gamma_lo.data(), g.d_gamma_lo.data(), g.d_gamma_lo.size()) <= 1e-9, "d_gamma_lo t=%zu", t);
+        EXPECT(rel(r.d_gamma_hi.data(), g.d_gamma_hi.data(), g.d_gamma_hi.size()) <= 1e-9, "d_gamma_hi t=%zu", t);
+        EXPECT(rel(r.d_w1.data(), g.d_w1.data(), g.d_w1.size()) <= 1e-9, "d_w1 t=%zu", t);
+        EXPECT(rel(r.d_w2.data(), g.d_w2.data(), g.d_w2.size()) <= 1e-9, "d_w2 t=%zu", t);
+        EXPECT(rel(r.d_b1.data(), g.d_b1.data(), g.d_b1.size()) <= 1e-9, "d_b1 t=%zu", t);
+        std::printf("joint step %zux%zu T=%zu t=%zu: loss %.6e (ref %.6e)\n", out, in, T, t, r.loss, f.loss);
+    }
+    return 0;
+}
+
 int main() {
     run_case(256, 512, 128, 64, 3);
     run_case(130, 96, 32, 37, 5);
     run_case(32, 32, 128, 128, 1);
+    run_joint(192, 320, 48, 7);
     std::printf(fails ? "DROPIN FAIL (%d)\n" : "DROPIN OK\n", fails);
     return fails ? 1 : 0;
 }
