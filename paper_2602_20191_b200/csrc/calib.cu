@@ -6,7 +6,7 @@
 //
 // This is offline calibration, not the inference hot path: it runs once per layer per optimiser
 // step.  The matrix products are a shared-memory tiled fp64 tensor-core GEMM (DMMA m8n8k4, 128x64
-// CTA tiles; a fixed k order -> deterministic); the reductions the reference performs in a fixed order
+// CTA tiles, 3-stage cp.async ring; a fixed k order -> deterministic); the reductions the reference performs in a fixed order
 // (per-group clip sums, column sums of the bias gradients) keep that order (one thread per group /
 // column), every other reduction is a fixed two-level tree, so repeated steps are bit-identical.
 // The per-group sigmoid of the clip gammas is evaluated on the host with the reference's libm
@@ -24,7 +24,7 @@ int launch_decompose_clip(const double* w, int64_t out, int64_t in, int64_t gs, 
 
 namespace {
 
-constexpr int kBM = 128, kBN = 64, kTk = 16, kGemmThreads = 256, kRedThreads = 256;
+constexpr int kBM = 128, kBN = 64, kTk = 16, kStages = 3, kGemmThreads = 256, kRedThreads = 256;
 
 __device__ __forceinline__ double sigmoid_d(double v) {  // common.hpp:125-131
     if (v >= 0.0) return 1.0 / (1.0 + exp(-v));
@@ -32,66 +32,91 @@ __device__ __forceinline__ double sigmoid_d(double v) {  // common.hpp:125-131
     return e / (1.0 + e);
 }
 
-// C[i][j] = Σ_k A(i,k)·s(k)·B(k,j) (+ bias[j]); A(i,k) = A[i·sai + k·sak], B(k,j) = B[k·sbk + j·sbj],
-// s(k) = ascale[k·sas] when given (the gate scaling of dP_e, trainer.hpp:351-357).  fp64 tensor cores:
-// mma.sync m8n8k4 (DMMA), 128x64 CTA tile, 8 warps of 32x32 (4x4 MMA tiles each), k staged 16 at a
-// time through shared memory (the unit-stride dimension walked by consecutive threads on load).
+// C[i][j] = Σ_k A(i,k)·B(k,j) (+ bias[j]); A(i,k) = A[i·sai + k·sak], B(k,j) = B[k·sbk + j·sbj].
+// fp64 tensor cores: mma.sync m8n8k4 (DMMA), 128x64 CTA tile, 8 warps of 32x32 (4x4 MMA tiles each);
+// k staged 16 at a time through a kStages-deep cp.async ring (8-byte element copies, so any operand
+// stride lands in the same k-major tile; out-of-range elements are zero-filled by the copy).
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c[0]), "+d"(c[1])
                  : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 2) dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A,
-                                                             int64_t sai, int64_t sak, const double* __restrict__ B,
-                                                             int64_t sbk, int64_t sbj, const double* __restrict__ ascale,
-                                                             int64_t sas, const double* __restrict__ bias,
-                                                             double* __restrict__ C, int64_t ldc) {
-    // +8 doubles per row: a fragment load's four k rows take two bank halves (two wavefronts, the
-    // minimum for 32 doubles); the column index is XOR-swizzled by (k >> 1) & 7 inside each 8-column
-    // group so the k-fast stores of a k-contiguous operand also spread over all banks
-    __shared__ double As[kTk][kBM + 8];
-    __shared__ double Bs[kTk][kBN + 8];
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+    const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+
+// +8 doubles per row: a fragment load's four k rows take two bank halves (two wavefronts, the minimum
+// for 32 doubles); the column index is XOR-swizzled by (k >> 1) & 7 inside each 8-column group so the
+// k-fast copies of a k-contiguous operand also spread over all banks
+constexpr int kAStride = kBM + 8, kBStride = kBN + 8;
+constexpr int kStageDoubles = kTk * (kAStride + kBStride);
+constexpr size_t kGemmSmem = (size_t)kStages * kStageDoubles * sizeof(double);
+
+__global__ void __launch_bounds__(kGemmThreads, 1) dgemm_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A,
+                                                                int64_t sai, int64_t sak, const double* __restrict__ B,
+                                                                int64_t sbk, int64_t sbj, const double* __restrict__ bias,
+                                                                double* __restrict__ C, int64_t ldc) {
+    extern __shared__ double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
     const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
     const int64_t i0 = (int64_t)blockIdx.y * kBM, j0 = (int64_t)blockIdx.x * kBN;
-    double acc[4][4][2] = {};
-    for (int64_t k0 = 0; k0 < K; k0 += kTk) {
+    const int64_t nkt = (K + kTk - 1) / kTk;
+    // a thread's copies in one stage differ by a fixed step along one dimension: (row, k) of copy l is
+    // (r0 + l·dr, k0 + c0 + l·dc), with the unit-stride dimension walked by consecutive threads
+    const bool a_kf = sak == 1, b_kf = sbk == 1 && sbj != 1;
+    const int a_r0 = a_kf ? tid / kTk : tid % kBM, a_c0 = a_kf ? tid % kTk : tid / kBM;
+    const int a_dr = a_kf ? kGemmThreads / kTk : 0, a_dc = a_kf ? 0 : kGemmThreads / kBM;
+    const int b_r0 = b_kf ? tid / kTk : tid % kBN, b_c0 = b_kf ? tid % kTk : tid / kBN;
+    const int b_dr = b_kf ? kGemmThreads / kTk : 0, b_dc = b_kf ? 0 : kGemmThreads / kBN;
+    auto load = [&](int64_t kt) {
+        double* As = smem + (kt % kStages) * kStageDoubles;
+        double* Bs = As + kTk * kAStride;
+        const int64_t k0 = kt * kTk;
 #pragma unroll
         for (int l = 0; l < kBM * kTk / kGemmThreads; ++l) {
-            const int idx = tid + l * kGemmThreads;
-            const int ii = sak == 1 ? idx / kTk : idx % kBM, kk = sak == 1 ? idx % kTk : idx / kBM;
+            const int ii = a_r0 + l * a_dr, kk = a_c0 + l * a_dc;
             const int64_t i = i0 + ii, k = k0 + kk;
-            double a = 0.0;
-            if (i < M && k < K) {
-                a = A[i * sai + k * sak];
-                if (ascale) a *= ascale[k * sas];
-            }
-            As[kk][ii ^ ((kk >> 1) & 7)] = a;
+            const bool ok = i < M && k < K;
+            cp_async8(As + kk * kAStride + (ii ^ ((kk >> 1) & 7)), ok ? A + i * sai + k * sak : A, ok);
         }
 #pragma unroll
         for (int l = 0; l < kBN * kTk / kGemmThreads; ++l) {
-            const int idx = tid + l * kGemmThreads;
-            const int jj = sbj == 1 ? idx % kBN : idx / kTk, kb = sbj == 1 ? idx / kBN : idx % kTk;
+            const int jj = b_r0 + l * b_dr, kb = b_c0 + l * b_dc;
             const int64_t j = j0 + jj, k = k0 + kb;
-            Bs[kb][jj ^ ((kb >> 1) & 7)] = (j < N && k < K) ? B[k * sbk + j * sbj] : 0.0;
+            const bool ok = j < N && k < K;
+            cp_async8(Bs + kb * kBStride + (jj ^ ((kb >> 1) & 7)), ok ? B + k * sbk + j * sbj : B, ok);
         }
-        __syncthreads();
+    };
+    double acc[4][4][2] = {};
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+        if (s < nkt) load(s);
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    for (int64_t kt = 0; kt < nkt; ++kt) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kStages - 2));
+        __syncthreads();  // stage kt landed for every thread; stage kt-1 is free to refill
+        if (kt + kStages - 1 < nkt) load(kt + kStages - 1);
+        asm volatile("cp.async.commit_group;\n" ::);
+        const double* As = smem + (kt % kStages) * kStageDoubles;
+        const double* Bs = As + kTk * kAStride;
 #pragma unroll
         for (int ks = 0; ks < kTk; ks += 4) {
             double a[4], b[4];
             const int sw = ((ks + q) >> 1) & 7;
 #pragma unroll
-            for (int m = 0; m < 4; ++m) a[m] = As[ks + q][(wm + m * 8 + g) ^ sw];  // A frag: row g, col q
+            for (int m = 0; m < 4; ++m) a[m] = As[(ks + q) * kAStride + ((wm + m * 8 + g) ^ sw)];  // A: row g, col q
 #pragma unroll
-            for (int n = 0; n < 4; ++n) b[n] = Bs[ks + q][(wn + n * 8 + g) ^ sw];  // B frag: row q, col g
+            for (int n = 0; n < 4; ++n) b[n] = Bs[(ks + q) * kBStride + ((wn + n * 8 + g) ^ sw)];  // B: row q, col g
 #pragma unroll
             for (int m = 0; m < 4; ++m)
 #pragma unroll
                 for (int n = 0; n < 4; ++n) dmma(acc[m][n], a[m], b[n]);
         }
-        __syncthreads();
     }
+    asm volatile("cp.async.wait_group 0;\n" ::);
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         const int64_t i = i0 + wm + m * 8 + g;
@@ -104,6 +129,14 @@ __global__ void __launch_bounds__(kGemmThreads, 2) dgemm_kernel(int64_t M, int64
                 if (j < N) C[i * ldc + j] = bias ? acc[m][n][h] + bias[j] : acc[m][n][h];
             }
     }
+}
+
+// dP_e = diag(g_e)·resid (trainer.hpp:351-357): the gate-scaled operand of dL/dW_e
+__global__ void row_scale_kernel(const double* __restrict__ resid, const double* __restrict__ gates, int nr, int col,
+                                 int64_t T, int64_t out, double* __restrict__ dst) {
+    const int64_t n = T * out;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = resid[i] * gates[(i / out) * nr + col];
 }
 
 // W_e = slice_params(e) dequantize_centered: s·2^{-before}·(code − z + ½), z = zero[g] for e = 1,
@@ -282,10 +315,14 @@ __global__ void silu_grad_mul_kernel(double* __restrict__ d_act, const double* _
 inline unsigned grid_for(int64_t n) { return (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 16); }
 
 int dgemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t sai, int64_t sak, const double* B, int64_t sbk,
-          int64_t sbj, const double* ascale, int64_t sas, const double* bias, double* C, int64_t ldc, cudaStream_t st) {
+          int64_t sbj, const double* bias, double* C, int64_t ldc, cudaStream_t st) {
     if (M <= 0 || N <= 0) return MOBI_OK;
+    // per device, cached (mobi_internal.cuh): 3 stages x 26 KB of dynamic shared memory
+    const int rc = func_attr_once_impl(reinterpret_cast<const void*>(dgemm_kernel),
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+    if (rc) return rc;
     dim3 grid((unsigned)cdiv(N, kBN), (unsigned)cdiv(M, kBM));
-    dgemm_kernel<<<grid, kGemmThreads, 0, st>>>(M, N, K, A, sai, sak, B, sbk, sbj, ascale, sas, bias, C, ldc);
+    dgemm_kernel<<<grid, kGemmThreads, kGemmSmem, st>>>(M, N, K, A, sai, sak, B, sbk, sbj, bias, C, ldc);
     MOBI_LAUNCH_CHECK();
     return MOBI_OK;
 }
@@ -396,17 +433,17 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
         dequant_slice_kernel<<<grid_for(out * in), 256, 0, st>>>(codes + (int64_t)e * out * in, scale, zero, out, in,
                                                                  gs, G, unit[e], mid[e], e == 0, W);
         MOBI_LAUNCH_CHECK();
-        TRY(dgemm(T, out, in, x, in, 1, W, 1, in, nullptr, 0, nullptr, P + (int64_t)e * TO, out, st));
+        TRY(dgemm(T, out, in, x, in, 1, W, 1, in, nullptr, P + (int64_t)e * TO, out, st));
     }
     // router MLP + gate_soft (trainer.hpp:220-243)
     if (!force_on) {
         TRY(buf.get(&hpre, T * h));
         TRY(buf.get(&hact, T * h));
         TRY(buf.get(&S, T * nr));
-        TRY(dgemm(T, h, in, x, in, 1, w1, h, 1, nullptr, 0, b1, hpre, h, st));
+        TRY(dgemm(T, h, in, x, in, 1, w1, h, 1, b1, hpre, h, st));
         silu_kernel<<<grid_for(T * h), 256, 0, st>>>(hpre, hact, T * h);
         MOBI_LAUNCH_CHECK();
-        TRY(dgemm(T, nr, h, hact, h, 1, w2, nr, 1, nullptr, 0, b2, S, nr, st));
+        TRY(dgemm(T, nr, h, hact, h, 1, w2, nr, 1, b2, S, nr, st));
     }
     gates_kernel<<<grid_for(T * nr), 256, 0, st>>>(S, gates, T * nr, tau, force_on ? 2 : (hard ? 1 : 0));
     MOBI_LAUNCH_CHECK();
@@ -426,8 +463,9 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
     if (!d_gamma_lo) return MOBI_OK;
 
     // ---- joint_backward (trainer.hpp:341-396) ----
-    double *resid, *d_lo, *d_hi, *s1;
+    double *resid, *dpe, *d_lo, *d_hi, *s1;
     TRY(buf.get(&resid, TO));
+    TRY(buf.get(&dpe, TO));
     TRY(buf.get(&d_lo, NG));
     TRY(buf.get(&d_hi, NG));
     TRY(buf.get(&s1, NG));
@@ -438,7 +476,13 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
     const double qmax1 = (double)((1 << slice_bits[0]) - 1);
     for (int e = 0; e < E; ++e) {
         // dL/dW_e = (g_e ⊙ resid)ᵀ X  [out][in]   (W's buffer is free after the forward)
-        TRY(dgemm(out, in, T, resid, 1, out, x, in, 1, e == 0 ? nullptr : gates + (e - 1), nr, nullptr, W, in, st));
+        const double* dp = resid;
+        if (e > 0) {  // the reference materialises dpe = resid * gate, then multiplies (trainer.hpp:351-358)
+            row_scale_kernel<<<grid_for(TO), 256, 0, st>>>(resid, gates, nr, e - 1, T, out, dpe);
+            MOBI_LAUNCH_CHECK();
+            dp = dpe;
+        }
+        TRY(dgemm(out, in, T, dp, 1, out, x, in, 1, nullptr, W, in, st));
         clip_accum_kernel<<<(unsigned)cdiv(NG, 128), 128, 0, st>>>(W, codes + (int64_t)e * out * in, out, in, gs, G,
                                                                    unit[e], mid[e], qmax1, e == 0, d_lo, d_hi, s1);
         MOBI_LAUNCH_CHECK();
@@ -462,13 +506,13 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
         const double reg_coeff = sched->reg_weight * (res->avg_bits - res->sched_b);
         dscore_kernel<<<(unsigned)T, kRedThreads, 0, st>>>(resid, P, TO, out, nr, gates, reg_coeff, tau, d_score);
         MOBI_LAUNCH_CHECK();
-        TRY(dgemm(h, nr, T, hact, 1, h, d_score, nr, 1, nullptr, 0, nullptr, d_w2, nr, st));  // hactᵀ d_score
+        TRY(dgemm(h, nr, T, hact, 1, h, d_score, nr, 1, nullptr, d_w2, nr, st));  // hactᵀ d_score
         colsum_kernel<<<1, 32, 0, st>>>(d_score, T, nr, d_b2);
         MOBI_LAUNCH_CHECK();
-        TRY(dgemm(T, h, nr, d_score, nr, 1, w2, 1, nr, nullptr, 0, nullptr, d_act, h, st));  // d_score w2ᵀ
+        TRY(dgemm(T, h, nr, d_score, nr, 1, w2, 1, nr, nullptr, d_act, h, st));  // d_score w2ᵀ
         silu_grad_mul_kernel<<<grid_for(T * h), 256, 0, st>>>(d_act, hpre, T * h);
         MOBI_LAUNCH_CHECK();
-        TRY(dgemm(in, h, T, x, 1, in, d_act, h, 1, nullptr, 0, nullptr, d_w1, h, st));  // Xᵀ d_act
+        TRY(dgemm(in, h, T, x, 1, in, d_act, h, 1, nullptr, d_w1, h, st));  // Xᵀ d_act
         colsum_kernel<<<(unsigned)cdiv(h, 128), 128, 0, st>>>(d_act, T, h, d_b1);
         MOBI_LAUNCH_CHECK();
     }

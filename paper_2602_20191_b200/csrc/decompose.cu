@@ -13,23 +13,29 @@
 namespace mobi {
 namespace {
 
-// one thread per (row, group): stats -> params -> all slices of the group's elements
+// one warp per (row, group): stats (warp min / max) -> params -> all slices of the group's elements,
+// lanes striding the group (coalesced); per-element arithmetic is the reference's, in its order
 __global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int64_t in, int64_t gs,
                                  int64_t G, const int32_t* __restrict__ bits_dev, int E, double sq_lo,
                                  double sq_hi, const double* __restrict__ sq_lo_g,
                                  const double* __restrict__ sq_hi_g, uint8_t* __restrict__ codes,
                                  double* __restrict__ scale, double* __restrict__ zero,
                                  double* __restrict__ stats, unsigned long long* __restrict__ clamp_counts) {
-    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // warp-uniform
     if (gi >= out * G) return;
     const int64_t r = gi / G, g = gi % G;
     const int64_t c0 = g * gs, c1 = min(in, c0 + gs);
     const double* row = w + r * in;
     double mn = row[c0], mx = row[c0];
-    for (int64_t c = c0 + 1; c < c1; ++c) {
+    for (int64_t c = c0 + lane; c < c1; c += 32) {
         const double v = row[c];
         mn = fmin(mn, v);
         mx = fmax(mx, v);
+    }
+    for (int o = 16; o; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
     // GroupStats::ref = min(max(0, min), max); clip_lo/hi; params_from_clip
     const double lo0 = mn > 0.0 ? mn : 0.0;
@@ -38,7 +44,7 @@ __global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int6
         sq_lo = sq_lo_g[gi];
         sq_hi = sq_hi_g[gi];
     }
-    if (stats) {  // GroupStats min / max / ref, [3][out*G]
+    if (stats && lane == 0) {  // GroupStats min / max / ref, [3][out*G]
         stats[gi] = mn;
         stats[out * G + gi] = mx;
         stats[2 * out * G + gi] = ref;
@@ -49,10 +55,12 @@ __global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int6
     double s = __ddiv_rn(__dsub_rn(hi, lo), (double)((1 << b1) - 1));
     if (!(s > 1e-8)) s = 1e-8;
     const double z1 = __ddiv_rn(-lo, s);
-    scale[gi] = s;
-    zero[gi] = z1;
-    unsigned long long cl[MOBI_MAX_SLICES] = {};
-    for (int64_t c = c0; c < c1; ++c) {
+    if (lane == 0) {
+        scale[gi] = s;
+        zero[gi] = z1;
+    }
+    unsigned cl[MOBI_MAX_SLICES] = {};
+    for (int64_t c = c0 + lane; c < c1; c += 32) {
         double v = row[c];
         int bb = 0;
         for (int e = 0; e < E; ++e) {
@@ -70,8 +78,11 @@ __global__ void decompose_kernel(const double* __restrict__ w, int64_t out, int6
             bb += be;
         }
     }
-    for (int e = 0; e < E; ++e)
-        if (cl[e]) atomicAdd(&clamp_counts[e], cl[e]);
+    for (int e = 0; e < E; ++e) {
+        unsigned n = cl[e];
+        for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        if (lane == 0 && n) atomicAdd(&clamp_counts[e], (unsigned long long)n);
+    }
 }
 
 }  // namespace
@@ -98,7 +109,7 @@ int launch_decompose(const double* w, int64_t out, int64_t in, int64_t gs, const
     MOBI_CUDA(cudaMallocAsync(&cc, sizeof(unsigned long long) * MOBI_MAX_SLICES, st));
     MOBI_CUDA(cudaMemcpyAsync(bits_dev, bits, sizeof(int32_t) * E, cudaMemcpyHostToDevice, st));
     MOBI_CUDA(cudaMemsetAsync(cc, 0, sizeof(unsigned long long) * MOBI_MAX_SLICES, st));
-    decompose_kernel<<<(unsigned)cdiv(out * G, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, sq, sq, nullptr,
+    decompose_kernel<<<(unsigned)cdiv(out * G * 32, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, sq, sq, nullptr,
                                                                    nullptr, codes, scale, zero, nullptr, cc);
     MOBI_LAUNCH_CHECK();
     unsigned long long h[MOBI_MAX_SLICES];
@@ -118,7 +129,7 @@ int launch_decompose_clip(const double* w, int64_t out, int64_t in, int64_t gs, 
                           const double* sq_lo_g, const double* sq_hi_g, uint8_t* codes, double* scale, double* zero,
                           double* stats, unsigned long long* clamp_counts, cudaStream_t st) {
     const int64_t G = cdiv(in, gs);
-    decompose_kernel<<<(unsigned)cdiv(out * G, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, 0.0, 0.0, sq_lo_g,
+    decompose_kernel<<<(unsigned)cdiv(out * G * 32, 128), 128, 0, st>>>(w, out, in, gs, G, bits_dev, E, 0.0, 0.0, sq_lo_g,
                                                                    sq_hi_g, codes, scale, zero, stats, clamp_counts);
     MOBI_LAUNCH_CHECK();
     return MOBI_OK;
