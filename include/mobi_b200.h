@@ -27,6 +27,7 @@
  *                            (qcore.hpp:122-146), on the GPU
  *   mobi_joint_step          trainer::joint_forward (trainer.hpp:203-263) + trainer::joint_backward
  *                            (trainer.hpp:341-396): one stage-2 calibration step, fp64, on the GPU
+ *   mobi_msb_step            trainer::msb_forward + msb_backward (trainer.hpp:404-426): the stage-1 step
  *
  * Error convention (mirrors MOBI_CHECK, common.hpp:13-24): every entry point returns
  * MOBI_OK, MOBI_EINVAL (the reference would throw std::invalid_argument; message names the
@@ -234,6 +235,14 @@ MOBI_API int mobi_joint_step(const double* w, int64_t out, int64_t in, int64_t g
                              int32_t force_gates_on, double* y_hat, mobi_joint_scalars* scalars, double* d_gamma_lo,
                              double* d_gamma_hi, double* d_w1, double* d_b1, double* d_w2, double* d_b2,
                              void* stream);
+
+/* Stage-1 calibration step: trainer::msb_forward + msb_backward (trainer.hpp:404-426), fp64 -- slice 1
+ * alone (quantize_floor with the clip's base params), y_msb = X·W_1ᵀ, loss = MSE, clip gradients.
+ * Same memory conventions as mobi_joint_step; y_msb and the gradients are nullable. */
+MOBI_API int mobi_msb_step(const double* w, int64_t out, int64_t in, int64_t group_size, int32_t msb_bits,
+                           const double* gamma_lo, const double* gamma_hi, const double* x, const double* y_fp,
+                           int64_t T, double* y_msb, double* loss, double* d_gamma_lo, double* d_gamma_hi,
+                           void* stream);
 
 /* Per-kernel device timing (CUDA events recorded on the launch stream around every kernel the
  * layer launches).  enable=1 starts a fresh accumulation; mobi_layer_profile_read synchronises

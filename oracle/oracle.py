@@ -253,6 +253,20 @@ class _Backend:
             r.update(g)
         return r
 
+    def msb_step(self, w, group_size, slice_bits, gamma_lo, gamma_hi, x, y_fp):
+        """trainer.hpp:404-426 msb_forward + msb_backward."""
+        w, x, y_fp, glo, ghi = map(_f64, (w, x, y_fp, gamma_lo, gamma_hi))
+        sb = _i32a(slice_bits)
+        out, inn = w.shape
+        T = x.shape[0]
+        ng = out * ((inn + group_size - 1) // group_size)
+        y = np.zeros((T, out))
+        loss = _dbl()
+        dlo, dhi = np.zeros(ng), np.zeros(ng)
+        self._call("msb_step", _ptr(w), _i64(out), _i64(inn), _i64(group_size), _ptr(sb), _i32(sb.size), _ptr(glo),
+                   _ptr(ghi), _ptr(x), _ptr(y_fp), _i64(T), _ptr(y), C.byref(loss), _ptr(dlo), _ptr(dhi))
+        return dict(y_msb=y, loss=loss.value, d_gamma_lo=dlo, d_gamma_hi=dhi)
+
 
 def restatement() -> _Backend:
     return _Backend(LIB_ORACLE, "orc_")
@@ -385,7 +399,7 @@ def group_stats(w, group_size):
 
 
 def joint_step_np(w, group_size, slice_bits, gamma_lo, gamma_hi, w1, b1, w2, b2, x, y_fp, sched, t,
-                  force_gates_on=False, backward=True):
+                  force_gates_on=False, backward=True, slice1_only=False):
     orc = restatement()
     w, x, y_fp = _f64(w), _f64(x), _f64(y_fp)
     sb = [int(b) for b in slice_bits]
@@ -396,6 +410,8 @@ def joint_step_np(w, group_size, slice_bits, gamma_lo, gamma_hi, w1, b1, w2, b2,
     glo, ghi = _f64(gamma_lo), _f64(gamma_hi)
     scale, zero = orc.params_from_clip(w, group_size, sb[0], glo, ghi)
     codes, _, _ = orc.decompose(w, group_size, scale, zero, sb)
+    if slice1_only:  # msb_forward: slice 1 alone
+        sb, E, nr, codes = sb[:1], 1, 0, codes[:1]
     gidx = (np.arange(out)[:, None] * G + np.arange(inn)[None, :] // group_size)
     P, frames = [], []
     before = 0
@@ -473,3 +489,12 @@ def joint_step_np(w, group_size, slice_bits, gamma_lo, gamma_hi, w1, b1, w2, b2,
     d_act = (d_score @ _f64(w2).T) * (_sigmoid(hpre) * (1.0 + hpre * (1.0 - _sigmoid(hpre))))
     r.update(d_w2=hact.T @ d_score, d_b2=d_score.sum(axis=0), d_w1=x.T @ d_act, d_b1=d_act.sum(axis=0))
     return r
+
+
+def msb_step_np(w, group_size, slice_bits, gamma_lo, gamma_hi, x, y_fp):
+    """trainer.hpp:404-426: the stage-1 step is the joint step's slice-1 part (quantize_floor with the
+    clip's base params is decompose's first slice), without router or regulariser."""
+    r = joint_step_np(w, group_size, [slice_bits[0], 1], gamma_lo, gamma_hi, np.zeros((w.shape[1], 1)), np.zeros(1),
+                      np.zeros((1, 1)), np.zeros(1), x, y_fp, (0.0, 0.0, 1, 0, 0.0), 1, force_gates_on=True,
+                      slice1_only=True)
+    return dict(y_msb=r["y_hat"], loss=r["data_term"], d_gamma_lo=r["d_gamma_lo"], d_gamma_hi=r["d_gamma_hi"])

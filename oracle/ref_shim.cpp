@@ -427,4 +427,28 @@ int ref_joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const i
     });
 }
 
+// trainer.hpp:404-426 msb_forward + msb_backward (the stage-1 step)
+int ref_msb_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32_t* slice_bits, int32_t n_slices,
+                 const double* gamma_lo, const double* gamma_hi, const double* x, const double* y_fp, int64_t T,
+                 double* y_msb, double* loss, double* d_gamma_lo, double* d_gamma_hi) {
+    return guard([&] {
+        trainer::QuantLayer L;
+        L.w = mat(w, out, in);
+        L.group_size = static_cast<std::size_t>(gs);
+        L.slice_bits.assign(slice_bits, slice_bits + n_slices);
+        L.stats = qcore::GroupStats::from_weights(L.w, L.group_size);
+        const std::size_t ng = L.stats.min.size();
+        L.clip.gamma_lo.assign(gamma_lo, gamma_lo + ng);
+        L.clip.gamma_hi.assign(gamma_hi, gamma_hi + ng);
+        const Matrix X = mat(x, T, in), Y = mat(y_fp, T, out);
+        trainer::MsbForward f = trainer::msb_forward(L, X, Y);
+        put(f.y_msb, y_msb);
+        *loss = f.loss;
+        std::vector<double> lo, hi;
+        trainer::msb_backward(L, f, X, Y, lo, hi);
+        std::copy(lo.begin(), lo.end(), d_gamma_lo);
+        std::copy(hi.begin(), hi.end(), d_gamma_hi);
+    });
+}
+
 }  // extern "C"

@@ -41,7 +41,7 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
                const double* b2, int64_t h, const double* x, const double* y_fp, int64_t T,
                const mobi_budget_schedule* sched, int64_t t, int32_t force_on, double* y_hat_out,
                mobi_joint_scalars* res, double* d_gamma_lo, double* d_gamma_hi, double* d_w1, double* d_b1,
-               double* d_w2, double* d_b2, cudaStream_t st);
+               double* d_w2, double* d_b2, cudaStream_t st, bool msb = false);
 int launch_permute(const uint8_t* masks, int64_t T, uint8_t* keys_tmp, int32_t* cperm, int32_t* inverse,
                    int32_t* hist256, cudaStream_t st);
 
@@ -1129,6 +1129,24 @@ int mobi_joint_step(const double* w, int64_t out, int64_t in, int64_t group_size
     return joint_step(w, out, in, group_size, slice_bits, n_slices, gamma_lo, gamma_hi, w1, b1, w2, b2, hidden, x,
                       y_fp, T, sched, t, force_gates_on, y_hat, scalars, d_gamma_lo, d_gamma_hi, d_w1, d_b1, d_w2,
                       d_b2, S(stream));
+}
+
+int mobi_msb_step(const double* w, int64_t out, int64_t in, int64_t group_size, int32_t msb_bits,
+                  const double* gamma_lo, const double* gamma_hi, const double* x, const double* y_fp, int64_t T,
+                  double* y_msb, double* loss, double* d_gamma_lo, double* d_gamma_hi, void* stream) {
+    CHECK_ARG(w && gamma_lo && gamma_hi && x && y_fp && loss, "msb_step: null argument");
+    CHECK_ARG(!d_gamma_lo == !d_gamma_hi, "msb_step: null gradient argument");
+    CHECK_ARG(out > 0 && in > 0 && group_size > 0 && T > 0, "msb_step: empty dimension");
+    CHECK_ARG(msb_bits >= 1 && msb_bits <= 8, "msb_step: slice bit width " << msb_bits);
+    // stage 1 = the joint step's machinery on slice 1 alone: decompose's first slice is
+    // quantize_floor(w, base) (slicer.hpp:86-100 vs qcore.hpp:157-176), no router, loss = MSE
+    const mobi_budget_schedule one{0.0, 0.0, 1, 0, 0.0};
+    mobi_joint_scalars r{};
+    const int rc = joint_step(w, out, in, group_size, &msb_bits, 1, gamma_lo, gamma_hi, nullptr, nullptr, nullptr,
+                              nullptr, 1, x, y_fp, T, &one, 1, 1, y_msb, &r, d_gamma_lo, d_gamma_hi, nullptr, nullptr,
+                              nullptr, nullptr, S(stream), true);
+    *loss = r.data_term;
+    return rc;
 }
 
 int mobi_layer_profile(mobi_layer_t L, int enable) {

@@ -370,8 +370,8 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
                const double* b2, int64_t h, const double* x, const double* y_fp, int64_t T,
                const mobi_budget_schedule* sched, int64_t t, int32_t force_on, double* y_hat_out,
                mobi_joint_scalars* res, double* d_gamma_lo, double* d_gamma_hi, double* d_w1, double* d_b1,
-               double* d_w2, double* d_b2, cudaStream_t st) {
-    const int nr = E - 1;
+               double* d_w2, double* d_b2, cudaStream_t st, bool msb) {
+    const int nr = E - 1;  // 0 for the stage-1 MSB step (slice 1 alone, no router)
     const int64_t G = cdiv(in, gs), NG = out * G, TO = T * out;
     {  // keep the stream-ordered scratch (hundreds of MB at LLaMA shapes) mapped between steps: the
        // default pool would otherwise return it to the OS at every synchronize and re-map it next step
@@ -445,8 +445,10 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
         MOBI_LAUNCH_CHECK();
         TRY(dgemm(T, nr, h, hact, h, 1, w2, nr, 1, b2, S, nr, st));
     }
-    gates_kernel<<<grid_for(T * nr), 256, 0, st>>>(S, gates, T * nr, tau, force_on ? 2 : (hard ? 1 : 0));
-    MOBI_LAUNCH_CHECK();
+    if (nr > 0) {
+        gates_kernel<<<grid_for(T * nr), 256, 0, st>>>(S, gates, T * nr, tau, force_on ? 2 : (hard ? 1 : 0));
+        MOBI_LAUNCH_CHECK();
+    }
     combine_kernel<<<(unsigned)T, kRedThreads, 0, st>>>(P, TO, E, gates, nr, out, y_fp, y_hat, partial);
     MOBI_LAUNCH_CHECK();
     scalars_kernel<<<1, kRedThreads, 0, st>>>(partial, T, gates, nr, bits_dev, sc3);
@@ -494,7 +496,8 @@ int joint_step(const double* w, int64_t out, int64_t in, int64_t gs, const int32
     MOBI_LAUNCH_CHECK();
     MOBI_CUDA(cudaMemcpyAsync(d_gamma_lo, dg, sizeof(double) * NG, cudaMemcpyDeviceToHost, st));
     MOBI_CUDA(cudaMemcpyAsync(d_gamma_hi, dg + NG, sizeof(double) * NG, cudaMemcpyDeviceToHost, st));
-    if (hard) {  // indicator gate: zero router gradient (trainer.hpp:364)
+    if (msb) {  // msb_backward (trainer.hpp:417-426): clip gradients only
+    } else if (hard) {  // indicator gate: zero router gradient (trainer.hpp:364)
         MOBI_CUDA(cudaMemsetAsync(d_w1, 0, sizeof(double) * in * h, st));
         MOBI_CUDA(cudaMemsetAsync(d_b1, 0, sizeof(double) * h, st));
         MOBI_CUDA(cudaMemsetAsync(d_w2, 0, sizeof(double) * h * nr, st));

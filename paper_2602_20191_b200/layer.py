@@ -420,3 +420,28 @@ def joint_step(w: torch.Tensor, group_size: int, slice_bits: Sequence[int], gamm
     r["y_hat"] = y_hat
     r.update(g)
     return r
+
+
+def msb_step(w: torch.Tensor, group_size: int, msb_bits: int, gamma_lo, gamma_hi, x: torch.Tensor,
+             y_fp: torch.Tensor, backward: bool = True, stream=None) -> dict:
+    """The stage-1 calibration step on the GPU (fp64): trainer::msb_forward + msb_backward
+    (trainer.hpp:404-426) -- slice 1 alone, y_msb = X·W_1ᵀ, loss = MSE and the clip gradients."""
+    dev = x.device
+    f64 = lambda a: a.to(device=dev, dtype=torch.float64).contiguous()  # noqa: E731
+    w, x, y_fp = f64(w), f64(x), f64(y_fp)
+    out, inn = w.shape
+    G = (inn + group_size - 1) // group_size
+    glo = _arr(np.broadcast_to(np.asarray(gamma_lo, np.float64), (out * G,)), np.float64)
+    ghi = _arr(np.broadcast_to(np.asarray(gamma_hi, np.float64), (out * G,)), np.float64)
+    y = torch.empty((x.shape[0], out), dtype=torch.float64, device=dev)
+    loss = C.c_double()
+    dlo, dhi = np.zeros(out * G), np.zeros(out * G)
+    with torch.cuda.device(dev):
+        check(lib().mobi_msb_step(w.data_ptr(), out, inn, group_size, int(msb_bits), glo.ctypes.data, ghi.ctypes.data,
+                                  x.data_ptr(), y_fp.data_ptr(), x.shape[0], y.data_ptr(), C.byref(loss),
+                                  dlo.ctypes.data if backward else None, dhi.ctypes.data if backward else None,
+                                  _stream_ptr(stream)))
+    r = dict(y_msb=y, loss=loss.value)
+    if backward:
+        r.update(d_gamma_lo=dlo, d_gamma_hi=dhi)
+    return r

@@ -64,3 +64,19 @@ def test_joint_step_errors_like_reference():
         run_gpu(c, (8.0, 3.0, 10, 0, 1e-3), 0)
     with pytest.raises(O.OracleError, match=r"outside \[1,10\]"):
         O.reference().joint_step(**c, sched=(8.0, 3.0, 10, 0, 1e-3), t=0)
+
+
+@pytest.mark.parametrize("bits", [(2, 2, 2, 2), (4, 2, 2), (3, 5)])
+def test_msb_step_matches_oracle(bits):
+    """Stage 1 (trainer.hpp:404-426): mobi_msb_step against the oracle."""
+    from paper_2602_20191_b200 import msb_step
+    c = joint_case(out=150, inn=330, T=70, slice_bits=bits, seed=13)
+    cuda = {k: torch.from_numpy(c[k]).cuda() for k in ("w", "x", "y_fp")}
+    r = msb_step(cuda["w"], c["group_size"], bits[0], c["gamma_lo"], c["gamma_hi"], cuda["x"], cuda["y_fp"])
+    ref = O.msb_step_np(w=c["w"], group_size=c["group_size"], slice_bits=bits, gamma_lo=c["gamma_lo"],
+                        gamma_hi=c["gamma_hi"], x=c["x"], y_fp=c["y_fp"])
+    assert abs(r["loss"] - ref["loss"]) <= 1e-9 * ref["loss"]
+    y = r["y_msb"].cpu().numpy()
+    assert np.abs(y - ref["y_msb"]).max() <= 1e-9 * np.abs(ref["y_msb"]).max()
+    for k in ("d_gamma_lo", "d_gamma_hi"):
+        assert np.abs(r[k] - ref[k]).max() <= 1e-9 * np.abs(ref[k]).max(), k

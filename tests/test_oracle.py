@@ -295,3 +295,17 @@ def test_joint_step_non_uniform_slices():
     c = joint_case(slice_bits=(4, 2, 2), seed=9)
     sched = (8.0, 3.0, 12, 1, 1e-3)
     assert_joint_close(O.joint_step_np(**c, sched=sched, t=5), O.reference().joint_step(**c, sched=sched, t=5))
+
+
+@pytest.mark.skipif(not O.LIB_REF.exists(), reason="reference library not built")
+@pytest.mark.parametrize("bits", [(2, 2, 2, 2), (4, 2, 2), (3, 5)])
+def test_msb_step_restatement_matches_reference(bits):
+    """trainer.hpp:404-426 (stage 1): slice 1 alone, with the epsilon-floored group of joint_case."""
+    c = joint_case(slice_bits=bits, seed=13)
+    args = dict(w=c["w"], group_size=c["group_size"], slice_bits=bits, gamma_lo=c["gamma_lo"],
+                gamma_hi=c["gamma_hi"], x=c["x"], y_fp=c["y_fp"])
+    ref = O.reference().msb_step(**args)
+    port = O.msb_step_np(**args)
+    assert abs(port["loss"] - ref["loss"]) <= 1e-9 * ref["loss"]
+    for k in ("y_msb", "d_gamma_lo", "d_gamma_hi"):
+        assert np.abs(port[k] - ref[k]).max() <= 1e-9 * np.abs(ref[k]).max(), k
