@@ -80,3 +80,20 @@ def test_msb_step_matches_oracle(bits):
     assert np.abs(y - ref["y_msb"]).max() <= 1e-9 * np.abs(ref["y_msb"]).max()
     for k in ("d_gamma_lo", "d_gamma_hi"):
         assert np.abs(r[k] - ref[k]).max() <= 1e-9 * np.abs(ref[k]).max(), k
+
+
+@pytest.mark.parametrize("out,inn,T,h,gs,bits", [(5, 7, 1, 1, 128, (4, 4)),      # gs > in, one token, h = 1
+                                                 (9, 130, 3, 2, 64, (2, 2, 2, 2)),  # partial group, tiny tiles
+                                                 (129, 65, 17, 65, 32, (3, 3, 2))])  # tile edges + 1
+def test_joint_and_msb_step_edge_shapes(out, inn, T, h, gs, bits):
+    c = joint_case(out=out, inn=inn, T=T, h=h, gs=gs, slice_bits=bits, seed=21)
+    sched = (8.0, 3.0, 10, 0, 1e-3)
+    assert_joint_close(run_gpu(c, sched, 4), O.joint_step_np(**c, sched=sched, t=4))
+    from paper_2602_20191_b200 import msb_step
+    r = msb_step(torch.from_numpy(c["w"]).cuda(), gs, bits[0], c["gamma_lo"], c["gamma_hi"],
+                 torch.from_numpy(c["x"]).cuda(), torch.from_numpy(c["y_fp"]).cuda())
+    ref = O.msb_step_np(w=c["w"], group_size=gs, slice_bits=bits, gamma_lo=c["gamma_lo"], gamma_hi=c["gamma_hi"],
+                        x=c["x"], y_fp=c["y_fp"])
+    assert abs(r["loss"] - ref["loss"]) <= 1e-9 * ref["loss"]
+    for k in ("d_gamma_lo", "d_gamma_hi"):
+        assert np.abs(r[k] - ref[k]).max() <= 1e-9 * max(np.abs(ref[k]).max(), 1e-300), k
