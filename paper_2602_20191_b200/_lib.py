@@ -67,6 +67,7 @@ _SIGS = {
     "mobi_joint_step": [_p, _i64, _i64, _i64, _p, _i32, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _i64, _p, _i64, _i32,
                         _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "mobi_msb_step": [_p, _i64, _i64, _i64, _i32, _p, _p, _p, _p, _i64, _p, C.POINTER(_f64), _p, _p, _p],
+    "mobi_layers_share_activations": [_p, _i32],
     "mobi_layer_last_launches": [_p, C.POINTER(_i32)],
     "mobi_layer_debug_impl": [_p, C.c_int],
     "mobi_layer_last_plan": [_p, C.POINTER(_i32)],

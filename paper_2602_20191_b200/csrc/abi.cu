@@ -98,7 +98,12 @@ void free_ws(mobi_layer* L) {
     dfree(L->inverse);
     dfree(L->cperm);
     dfree(L->escale);
-    dfree(L->xperm);
+    if (L->xperm_shared) {
+        L->xperm_shared.reset();
+        L->xperm = nullptr;
+    } else {
+        dfree(L->xperm);
+    }
     dfree(L->tiles);
     dfree(L->meta);
     dfree(L->rt_cnt);
@@ -763,6 +768,37 @@ int mobi_layer_reserve(mobi_layer_t L, int64_t max_tokens) {
     for (mobi_layer* c : L->ctxs)
         if (!rc) rc = ensure_ws(c, max_tokens);
     return rc;
+}
+
+int mobi_layers_share_activations(mobi_layer_t* layers, int32_t n) {
+    CHECK_ARG(layers && n >= 1, "mobi_layers_share_activations: no layers");
+    size_t bytes = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        CHECK_ARG(layers[i], "mobi_layers_share_activations: null layer " << i);
+        CHECK_ARG(layers[i]->device == layers[0]->device, "mobi_layers_share_activations: layers on different devices");
+        CHECK_ARG(layers[i]->ws_T > 0, "mobi_layers_share_activations: layer " << i << " not reserved");
+        bytes = std::max(bytes, (size_t)(layers[i]->tpad_max * layers[i]->in_pad) * sizeof(__half));
+    }
+    DeviceGuard g(layers[0]->device);
+    MOBI_CUDA(cudaDeviceSynchronize());  // queued work may still use the buffers being replaced
+    void* p = nullptr;
+    MOBI_CUDA(cudaMalloc(&p, bytes));
+    std::shared_ptr<void> blk(p, [](void* q) { cudaFree(q); });
+    for (int32_t i = 0; i < n; ++i) {
+        mobi_layer* L = layers[i];
+        std::lock_guard<std::mutex> lk(*L->ctx_mu);
+        if (L->xperm_shared)
+            L->xperm_shared.reset();
+        else
+            dfree(L->xperm);
+        L->xperm = reinterpret_cast<__half*>(p);
+        L->xperm_shared = blk;
+        if (L->tmap_x) delete L->tmap_x;  // tensor maps encode the old address
+        L->tmap_x = nullptr;
+        if (L->tmap_x2) delete[] L->tmap_x2;
+        L->tmap_x2 = nullptr;
+    }
+    return MOBI_OK;
 }
 
 int mobi_layer_info(mobi_layer_t L, int64_t* out, int64_t* in, int32_t* n_slices, int64_t* router_hidden,

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <memory>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -131,6 +132,8 @@ struct mobi_layer {
     float* escale = nullptr;   // [tpad_max] per-row power-of-two scale
     __half* xperm = nullptr;   // [kblocks][tpad_max][64] fp16 permuted, scaled activations: k-block slabs,
                                // so a TMA box of consecutive permuted rows is one contiguous span
+    std::shared_ptr<void> xperm_shared;  // set: xperm is a block shared with other handles
+                                         // (mobi_layers_share_activations), freed with its last user
     mobi::TokTile* tiles = nullptr;  // [max_tiles]
     float* gpart = nullptr;    // [8][64][out] split-K partials (decode-size T)
     float* hpart = nullptr;    // [16][64][h_pad] router split-K partials

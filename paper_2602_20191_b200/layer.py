@@ -445,3 +445,10 @@ def msb_step(w: torch.Tensor, group_size: int, msb_bits: int, gamma_lo, gamma_hi
     if backward:
         r.update(d_gamma_lo=dlo, d_gamma_hi=dhi)
     return r
+
+
+def share_activations(layers: Sequence["MobiLayer"]) -> None:
+    """mobi_layers_share_activations: layers that run one after another on one stream (a model stack)
+    share one permuted-activation buffer instead of one each.  Reserve every layer first."""
+    arr = (C.c_void_p * len(layers))(*[ly._h.value for ly in layers])
+    check(lib().mobi_layers_share_activations(arr, len(layers)))

@@ -90,6 +90,9 @@ class MobiStack:
                 layer.reserve(max_tokens)
             self.blocks.append(blk)
         self.layers = [blk[n] for blk in self.blocks for n in LINEARS]
+        if not concurrent:  # serial layers: one permuted-activation buffer for the whole stack
+            from .layer import share_activations
+            share_activations(self.layers)
 
     def device_bytes(self) -> int:
         return sum(layer.device_bytes() for layer in self.layers)

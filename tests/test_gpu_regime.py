@@ -235,3 +235,28 @@ def test_concurrent_forwards_on_distinct_streams():
 def test_tolerances_are_tight():
     """Stated tolerances (tests/gpu_helpers.py): a 5% error in one slice's scale must fail them."""
     assert Y_REL_L2 <= 4e-3 and Y_MAX_ABS <= 3e-2
+
+
+def test_shared_activation_buffer_bit_identical_and_smaller():
+    """mobi_layers_share_activations: serial layers on one stream share one permuted-activation buffer;
+    outputs are bit-identical to private buffers and the device frees the others."""
+    import torch
+    from gpu_helpers import make_layer, make_x
+    from paper_2602_20191_b200 import calibrate_threshold, share_activations
+    dims = [(256, 512), (512, 2048), (256, 1024)]
+    layers = [make_layer(o, i, seed=k + 1)[1] for k, (o, i) in enumerate(dims)]
+    T = 1536
+    xs = [make_x(T, i, seed=5 + k)[0] for k, (_, i) in enumerate(dims)]
+    deltas = [calibrate_threshold(ly.score(x), 1 / 6) for ly, x in zip(layers, xs)]
+    for ly in layers:
+        ly.reserve(T)
+    ref = [ly.forward(x, d).clone() for ly, x, d in zip(layers, xs, deltas)]
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    share_activations(layers)
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    for _ in range(2):  # interleaved: each layer overwrites the shared buffer the previous one used
+        for ly, x, d, r in zip(layers, xs, deltas, ref):
+            assert torch.equal(ly.forward(x, d), r)
+    assert free1 > free0, (free0, free1)
