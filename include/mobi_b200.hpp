@@ -17,6 +17,7 @@
 //   (multi-GPU)                    ->    mobi_b200::ShardedLayer(stack, rs, comm, rank, P, mode)
 //   trainer::joint_forward + joint_backward     ->    mobi_b200::joint_step(layer, x, y_fp, sched, t, opt)
 //   (trainer.hpp:203-263, 341-396)                    (one stage-2 calibration step, fp64, on the GPU)
+//   trainer::msb_forward + msb_backward         ->    mobi_b200::msb_step(layer, x, y_fp)  (stage 1)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -323,6 +324,31 @@ JointStep<Matrix> joint_step(const QuantLayer& L, const Matrix& x, const Matrix&
         o.d_b1 = gb1.download();
         o.d_b2 = gb2.download();
     }
+    return o;
+}
+
+// trainer::msb_forward + trainer::msb_backward (trainer.hpp:404-426) on the GPU, fp64: loss, y_msb and
+// the clip gradients of the stage-1 step
+template <class Matrix>
+struct MsbStep {
+    double loss = 0;
+    Matrix y_msb;
+    std::vector<double> d_lo, d_hi;
+};
+
+template <class QuantLayer, class Matrix>
+MsbStep<Matrix> msb_step(const QuantLayer& L, const Matrix& x, const Matrix& y_fp) {
+    const int64_t out = (int64_t)L.w.rows(), in = (int64_t)L.w.cols(), T = (int64_t)x.rows();
+    auto vec = [](const Matrix& m) { return std::vector<double>(m.data(), m.data() + m.size()); };
+    detail::DevBuf<double> w(vec(L.w)), dx(vec(x)), dy(vec(y_fp)), y(static_cast<size_t>(T * out));
+    MsbStep<Matrix> o;
+    o.d_lo.assign(L.clip.gamma_lo.size(), 0.0);
+    o.d_hi.assign(L.clip.gamma_hi.size(), 0.0);
+    check(mobi_msb_step(w.p, out, in, (int64_t)L.group_size, (int32_t)L.slice_bits[0], L.clip.gamma_lo.data(),
+                        L.clip.gamma_hi.data(), dx.p, dy.p, T, y.p, &o.loss, o.d_lo.data(), o.d_hi.data(), nullptr));
+    const std::vector<double> h = y.download();
+    o.y_msb = Matrix((size_t)T, (size_t)out);
+    std::copy(h.begin(), h.end(), o.y_msb.data());
     return o;
 }
 

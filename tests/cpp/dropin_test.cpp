@@ -180,6 +180,20 @@ int run_joint(size_t out, size_t in, size_t T, unsigned seed) {
         EXPECT(rel(r.d_b1.data(), g.d_b1.data(), g.d_b1.size()) <= 1e-9, "d_b1 t=%zu", t);
         std::printf("joint step %zux%zu T=%zu t=%zu: loss %.6e (ref %.6e)\n", out, in, T, t, r.loss, f.loss);
     }
+    {  // stage 1
+        trainer::MsbForward f = trainer::msb_forward(L, x, y);
+        std::vector<double> lo, hi;
+        trainer::msb_backward(L, f, x, y, lo, hi);
+        auto r = mobi_b200::msb_step(L, x, y);
+        double dl = 0, ml = 0;
+        for (size_t g = 0; g < lo.size(); ++g) {
+            dl = std::max(dl, std::max(std::fabs(r.d_lo[g] - lo[g]), std::fabs(r.d_hi[g] - hi[g])));
+            ml = std::max(ml, std::max(std::fabs(lo[g]), std::fabs(hi[g])));
+        }
+        EXPECT(std::fabs(r.loss - f.loss) <= 1e-9 * f.loss, "msb loss");
+        EXPECT(dl <= 1e-9 * ml, "msb clip gradients");
+        std::printf("msb step %zux%zu T=%zu: loss %.6e (ref %.6e)\n", out, in, T, r.loss, f.loss);
+    }
     return 0;
 }
 
