@@ -113,7 +113,8 @@ MOBI_API int mobi_layer_reserve(mobi_layer_t layer, int64_t max_tokens);
  * buffer (the largest workspace part, T_pad x in_pad fp16 per layer -- ~5 GiB over a 224-layer
  * LLaMA3-8B stack at 2048 tokens).  Each layer must be reserved (mobi_layer_reserve) first; the block
  * is sized for the largest and freed with its last user.  Shares the handles' primary workspace only;
- * layers whose calls can overlap in time (different streams) must not share.  Synchronises the device. */
+ * layers whose calls can overlap in time (different streams) must not share.  A later reserve or call
+ * beyond a layer's reserved size gives that layer a private buffer again.  Synchronises the device. */
 MOBI_API int mobi_layers_share_activations(mobi_layer_t* layers, int32_t n);
 MOBI_API int mobi_layer_info(mobi_layer_t layer, int64_t* out, int64_t* in, int32_t* n_slices,
                     int64_t* router_hidden, int64_t* device_bytes);
